@@ -1,0 +1,150 @@
+/*
+ * fsda_b200.h — C ABI of the B200-native FSDA hot path.
+ *
+ * This is the drop-in boundary for the reference's FSDA solver
+ * (`sdakit.sda._SOLVERS["fsda"]`, /root/reference/pkg/src/sdakit/sda.py:465-486).
+ * Every entry point takes plain host pointers and sizes; no torch or numpy
+ * types appear here.  The Python host layer (paper_1709_04794_b200/_capi.py)
+ * binds these with ctypes; INTEGRATION.md shows the stub a maintainer of the
+ * reference would add.
+ *
+ * Data model (mirrors sdakit, /root/reference/pkg/src/sdakit/sparse.py:41-146):
+ *   X   N x D CSR, int64 row offsets + int64 column indices, implicit value 1
+ *       (the reference stores float64 values; a non-binary X is rejected by the
+ *       host layer with ValueError before it reaches this ABI).
+ *   L   N x N graph Laplacian CSR (int64 offsets, int64 columns, float64
+ *       values), exactly as sdakit builds it (graph.py:191-195): -1 off the
+ *       diagonal, the degree on it.  Off-diagonals other than -1 are rejected
+ *       with FSDA_EINVAL (weighted graphs are out of scope).
+ *   labels  int8 in {+1, -1, 0}, labeled rows first (sda.py:97-101).
+ *
+ * Status codes (mapped to the reference's exceptions by the host layer):
+ *   FSDA_OK         0
+ *   FSDA_EINVAL     1  bad argument             -> ValueError
+ *   FSDA_EBREAKDOWN 2  <p, Bp> == 0             -> SolverBreakdownError   (krylov.py:215-216)
+ *   FSDA_ENONFINITE 3  non-finite <p,Bp> or r.r -> NumericalFailureError  (krylov.py:213-214, 234-235)
+ *   FSDA_ECUDA      4  CUDA / NCCL failure      -> RuntimeError
+ *   FSDA_ELABEL     5  no labeled sample        -> LabelError             (sparse.py:258-265)
+ * fsda_last_error() returns a thread-local message for the last failure.
+ *
+ * Arithmetic: fp64 throughout.  Row sums (X p, L y, X W) are sequential in
+ * stored column order, bit-identical to scipy's csr_matvec; every other sum
+ * (X^T z columns, dots, norms, class sums) uses the fixed "R256" reduction
+ * tree documented in DESIGN.md §4, so results are bitwise reproducible run to
+ * run and are mirrored exactly by oracle/fsda_oracle.c.
+ */
+#ifndef FSDA_B200_H
+#define FSDA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSDA_OK 0
+#define FSDA_EINVAL 1
+#define FSDA_EBREAKDOWN 2
+#define FSDA_ENONFINITE 3
+#define FSDA_ECUDA 4
+#define FSDA_ELABEL 5
+
+typedef struct fsda_ctx fsda_ctx;
+
+/* ABI version, bumped on any signature change. */
+int fsda_abi_version(void);
+
+/* Thread-local description of the last non-zero status. */
+const char* fsda_last_error(void);
+
+/* One context per device.  Calls on a context are serialized by a mutex and
+ * are synchronous unless named *_async.  `stream` may be NULL (the context
+ * creates its own) or a cudaStream_t owned by the caller (e.g. torch's
+ * current stream), so callers can time launches with their own events. */
+int fsda_ctx_create(fsda_ctx** out, int device, void* stream);
+int fsda_ctx_destroy(fsda_ctx* ctx);
+int fsda_ctx_set_stream(fsda_ctx* ctx, void* stream);
+
+/* Upload X (replaces SparseMatrix construction + the scipy handle,
+ * sparse.py:70-114).  Builds the device CSR (int32 columns) and a CSC copy by
+ * a stable device sort, so rows stay ascending inside every column, plus the
+ * column work plan used by the X^T kernels. */
+int fsda_upload_x(fsda_ctx* ctx, int64_t n_rows, int64_t n_cols,
+                  const int64_t* row_offsets, const int64_t* col_indices);
+
+/* Upload the Laplacian L = D - S (graph.py:191-195).  N must equal X's rows. */
+int fsda_upload_laplacian(fsda_ctx* ctx, int64_t n, const int64_t* row_offsets,
+                          const int64_t* col_indices, const double* values);
+
+/* Ternary labels, N entries, labeled-first (LabelVector, sparse.py:198-235). */
+int fsda_set_labels(fsda_ctx* ctx, const int8_t* labels);
+
+/* ---- single products, host buffers in and out (parity probes) ---------- */
+/* y = X v                         SparseMatrix.matvec            sparse.py:116-121 */
+int fsda_matvec(fsda_ctx* ctx, const double* v, double* y);
+/* u = X^T w                       SparseMatrix.matvec_transpose  sparse.py:123-134 */
+int fsda_matvec_transpose(fsda_ctx* ctx, const double* w, double* u);
+/* mu = X^T 1_l / l                labeled_mean                   sparse.py:258-265 */
+int fsda_labeled_mean(fsda_ctx* ctx, double* mu);
+/* u = X^T w - mu * sum(w)         centered_matvec_transpose      sparse.py:274-277 */
+int fsda_centered_matvec_transpose(fsda_ctx* ctx, const double* mu, const double* w, double* u);
+/* z = [(1-a)(I_l + 0) + a L] y    apply_smoother                 sda.py:131-140 */
+int fsda_apply_smoother(fsda_ctx* ctx, double alpha, const double* y, double* z);
+/* q = (X - 1 mu^T)^T M X w        fsda_operator                  sda.py:162-174 */
+int fsda_operator_apply(fsda_ctx* ctx, double alpha, const double* w, double* q);
+
+/* ---- the hot path ------------------------------------------------------- */
+/* Full FSDA regularization sweep (fsda_solve, sda.py:293-320): labeled mean,
+ * rhs = X_c^T (W + 0) X probe, shifted CG over the whole beta grid
+ * (krylov.py:168-281) with one operator application per iteration, then the
+ * per-shift projections s = X w with sign orientation (sda.py:265-284).
+ *   betas          n_shifts, strictly ascending, >= 0 (ShiftGrid, krylov.py:69-90)
+ *   probe          D doubles, the reference's rng.uniform(-1, 1, D) draw (sda.py:300)
+ *   directions     n_shifts x D (row s = w for betas[s]), oriented
+ *   scores         n_shifts x N (row s = X w), oriented; may be NULL
+ *   residuals      n_shifts   iterations  n_shifts   converged  n_shifts
+ *   n_applies      operator applications (LinearOperator.n_applies, krylov.py:54-56)
+ *   fail_iter      iteration index of a breakdown / non-finite failure, else -1 */
+int fsda_solve(fsda_ctx* ctx, double alpha, const double* betas, int n_shifts,
+               double tol, int64_t max_iter, const double* probe,
+               double* directions, double* scores, double* residuals,
+               int64_t* iterations, uint8_t* converged, int64_t* n_applies,
+               int64_t* fail_iter);
+
+/* Device-resident variant for throughput measurement: launches one complete
+ * solve on the context stream and returns without copying results to the
+ * host (inputs already resident in HBM).  Results stay in the context and can
+ * be fetched with fsda_fetch_results.  The probe is uploaded once by
+ * fsda_prepare_resident.  `launches` receives the number of kernels the solve
+ * launched (summed over loop iterations) after fsda_fetch_results. */
+int fsda_prepare_resident(fsda_ctx* ctx, double alpha, const double* betas, int n_shifts,
+                          double tol, int64_t max_iter, const double* probe);
+int fsda_solve_async(fsda_ctx* ctx);
+int fsda_fetch_results(fsda_ctx* ctx, double* directions, double* scores, double* residuals,
+                       int64_t* iterations, uint8_t* converged, int64_t* n_applies,
+                       int64_t* fail_iter, int64_t* launches);
+
+/* Per-kernel device time of one solve, measured with CUDA events around each
+ * kernel launched eagerly (not from the graph) on the context stream.
+ * names/ms/bytes receive up to max_kernels entries: kernel name, mean ms per
+ * launch, algorithmic bytes per launch, launches per solve.  Returns the count
+ * in *n_kernels. */
+int fsda_profile_kernels(fsda_ctx* ctx, int max_kernels, int* n_kernels,
+                         const char** names, double* ms_per_launch,
+                         double* bytes_per_launch, int64_t* launches_per_solve);
+
+/* Shifted CG on a dense symmetric operator held on the device
+ * (shifted_cg with LinearOperator.from_dense, krylov.py:61-66, 168-281).
+ * Same device recurrence kernels as fsda_solve; used to run the reference's
+ * own shifted-CG tests against the device path.  solutions is n_shifts x dim. */
+int fsda_shifted_cg_dense(fsda_ctx* ctx, int64_t dim, const double* a, const double* b,
+                          const double* betas, int n_shifts, double tol, int64_t max_iter,
+                          int absolute_tol, double* solutions, double* residuals,
+                          int64_t* iterations, uint8_t* converged, int64_t* n_applies,
+                          int64_t* fail_iter);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSDA_B200_H */

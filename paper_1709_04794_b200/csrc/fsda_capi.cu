@@ -1,0 +1,1083 @@
+// fsda_capi.cu — context, uploads, solve orchestration and the C ABI declared
+// in include/fsda_b200.h.
+//
+// One solve = one CUDA graph: setup kernels (labeled mean, rhs, CG init), a
+// conditional WHILE node whose body is one shifted-CG iteration (7 kernels),
+// and the projection kernels.  The body's last kernel sets the loop condition
+// from the device-side "finished" flag, so the graph runs exactly as many
+// iterations as the reference's Python loop (krylov.py:210-270) without any
+// host round trip.  The eager path (same kernels, host loop) serves the
+// per-kernel profiler and is the fallback when conditional nodes are absent.
+#include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fsda_b200.h"
+#include "fsda_device.cuh"
+
+using namespace fsda;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+struct CudaError {
+  cudaError_t err;
+  const char* what;
+  int line;
+};
+
+#define CK(call)                                                         \
+  do {                                                                   \
+    cudaError_t e_ = (call);                                             \
+    if (e_ != cudaSuccess) throw CudaError{e_, #call, __LINE__};         \
+  } while (0)
+#define CKL() CK(cudaGetLastError())
+
+// Bumped on every device (re)allocation; part of the graph cache key so a
+// cached graph never holds a stale buffer pointer.
+unsigned long long g_alloc_gen = 0;
+
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;  // elements
+  void ensure(size_t n) {
+    if (n <= cap && ptr) return;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    size_t alloc = std::max<size_t>(n, 1);
+    CK(cudaMalloc(&ptr, alloc * sizeof(T)));
+    cap = alloc;
+    ++g_alloc_gen;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+};
+
+inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+inline long long n_leaves(long long n) { return cdiv(n, LEAF); }
+constexpr long long MAX_REDUCE = 65536LL * LEAF;  // two-level R256 limit
+
+// One kernel launch seen by the profiler.
+struct Launch {
+  const char* name;
+  double bytes;
+};
+
+}  // namespace
+
+struct fsda_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::mutex mu;
+  int num_sms = 148;
+
+  // X: CSR + CSC (int32 indices, value-free)
+  long long n = 0, d = 0, nnz = 0;
+  bool has_x = false;
+  DevBuf<int> x_rowptr, x_cols, csc_colptr, csc_rows;
+  // column work plan
+  DevBuf<int> tiny_cols, warp_cols, seg_col, seg_start, heavy_cols, heavy_seg0, heavy_nseg;
+  DevBuf<double> seg_part;
+  XtPlan plan{};
+  long long xt_warps = 0;
+
+  // L: CSR with diagonal entries in place, diag values split out
+  bool has_l = false;
+  long long l_nnz = 0;
+  DevBuf<int> l_rowptr, l_cols;
+  DevBuf<double> l_diag;
+
+  // labels
+  bool has_labels = false;
+  DevBuf<signed char> labels;
+  long long n1 = 0, n2 = 0, ell = 0;
+
+  // work vectors
+  DevBuf<double> y, z, q, p, r0, r1, mu_v, t, wv, b, ind, probe, part_n, part_d, part_o;
+  DevBuf<double> bigp, sols, wT, scores, dense_a;
+  // per-shift state
+  DevBuf<double> beta, zeta_prev, zeta, zeta_next, gamma_s, alpha_s, resid;
+  DevBuf<long long> iters;
+  DevBuf<unsigned char> conv;
+  DevBuf<int> active, good, pending, flip, err;
+  CgScalars* sc = nullptr;
+
+  // graph cache for the solve
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  std::string graph_key;
+  bool cond_supported = true;
+
+  // resident-solve parameters
+  double r_alpha = 0.0, r_tol = 0.0;
+  int r_ns = 0;
+  long long r_max_iter = 0;
+  bool r_prepared = false;
+  long long last_launch_count = 0;
+
+  ShiftState shifts() {
+    ShiftState s;
+    s.beta = beta.ptr; s.zeta_prev = zeta_prev.ptr; s.zeta = zeta.ptr;
+    s.zeta_next = zeta_next.ptr; s.gamma_s = gamma_s.ptr; s.alpha_s = alpha_s.ptr;
+    s.resid = resid.ptr; s.iters = iters.ptr; s.conv = conv.ptr; s.active = active.ptr;
+    s.good = good.ptr; s.pending = pending.ptr; s.flip = flip.ptr;
+    return s;
+  }
+
+  void invalidate_graph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+    graph_key.clear();
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------- helpers
+
+struct Recorder {
+  // Eager profiling: events around each launch.
+  std::vector<std::pair<const char*, double>> names;  // name, bytes
+  std::vector<cudaEvent_t> ev;
+  cudaStream_t stream = nullptr;
+  void before(const char* name, double bytes) {
+    cudaEvent_t e0;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventRecord(e0, stream));
+    ev.push_back(e0);
+    names.emplace_back(name, bytes);
+  }
+  void after() {
+    cudaEvent_t e1;
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e1, stream));
+    ev.push_back(e1);
+  }
+  ~Recorder() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
+struct Enq {
+  fsda_ctx* c;
+  Recorder* rec = nullptr;
+  long long count = 0;
+  template <typename F>
+  void go(const char* name, double bytes, F&& f) {
+    if (rec) rec->before(name, bytes);
+    f();
+    CKL();
+    if (rec) rec->after();
+    ++count;
+  }
+};
+
+void ensure_vectors(fsda_ctx* c, int ns) {
+  const long long n = std::max<long long>(c->n, 1), d = std::max<long long>(c->d, 1);
+  c->y.ensure(n); c->z.ensure(n); c->t.ensure(n); c->wv.ensure(n); c->ind.ensure(n);
+  c->q.ensure(d); c->p.ensure(d); c->r0.ensure(d); c->r1.ensure(d); c->mu_v.ensure(d);
+  c->b.ensure(d); c->probe.ensure(d);
+  c->part_n.ensure(2 * n_leaves(n) + 2);
+  c->part_d.ensure(n_leaves(d) + 1);
+  const int nsx = std::max(ns, 1);
+  c->part_o.ensure((size_t)nsx * n_leaves(n) + 1);
+  c->bigp.ensure((size_t)nsx * d); c->sols.ensure((size_t)nsx * d);
+  c->wT.ensure((size_t)nsx * d); c->scores.ensure((size_t)nsx * n);
+  c->beta.ensure(nsx); c->zeta_prev.ensure(nsx); c->zeta.ensure(nsx); c->zeta_next.ensure(nsx);
+  c->gamma_s.ensure(nsx); c->alpha_s.ensure(nsx); c->resid.ensure(nsx); c->iters.ensure(nsx);
+  c->conv.ensure(nsx); c->active.ensure(nsx); c->good.ensure(nsx); c->pending.ensure(nsx);
+  c->flip.ensure(nsx);
+}
+
+int grid_for(long long n, int block) { return (int)std::max<long long>(1, cdiv(n, block)); }
+
+// ---- K3 launch (light + heavy) for one X^T product
+void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* mu, double ell,
+            int guarded) {
+  fsda_ctx* c = e.c;
+  const double xt_bytes = 4.0 * (c->d + 1) + 4.0 * c->nnz + 8.0 * c->n + 8.0 * c->d +
+                          (mode == 1 ? 8.0 * c->d : 0.0);
+  XtPlan pl = c->plan;
+  int blocks = (int)std::max<long long>(1, std::min<long long>(cdiv(c->xt_warps, 8),
+                                                                (long long)c->num_sms * 16));
+  e.go("xt_light", xt_bytes, [&] {
+    k_xt_light<<<blocks, 256, 0, c->stream>>>(pl, zsrc, out, mode, mu, c->sc, ell, guarded);
+  });
+  if (c->plan.n_heavy > 0) {
+    int hb = (int)std::min<long long>(c->plan.n_heavy, (long long)c->num_sms * 8);
+    e.go("xt_heavy", 8.0 * c->plan.n_segs, [&] {
+      k_xt_heavy<<<hb, 256, 0, c->stream>>>(pl, out, mode, mu, c->sc, ell, guarded);
+    });
+  }
+}
+
+int alpha_mode_of(double alpha) { return alpha == 0.0 ? 0 : (alpha == 1.0 ? 1 : 2); }
+
+// One shifted-CG iteration for the FSDA operator (graph body).
+void enq_fsda_iteration(Enq& e, double alpha, int ns, unsigned long long cond, int use_cond) {
+  fsda_ctx* c = e.c;
+  const long long n = c->n, d = c->d;
+  const long long nlN = n_leaves(n), nlD = n_leaves(d);
+  const int amode = alpha_mode_of(alpha);
+  const double b_spmv = 4.0 * (n + 1) + 4.0 * c->nnz + 8.0 * d + 8.0 * n;
+  e.go("spmv_rows", b_spmv, [&] {
+    k_spmv_rows<<<grid_for(n, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr, c->p.ptr,
+                                                         c->y.ptr, (int)n, c->sc);
+  });
+  const double b_sm = amode == 0 ? (1.0 * n + 16.0 * n)
+                                 : (4.0 * (n + 1) + 4.0 * c->l_nnz + 8.0 * n + 1.0 * n + 16.0 * n);
+  e.go("smoother", b_sm, [&] {
+    k_smoother<<<grid_for(nlN, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+        c->l_rowptr.ptr, c->l_cols.ptr, c->l_diag.ptr, c->labels.ptr, c->y.ptr, c->z.ptr, (int)n,
+        alpha, amode, c->part_n.ptr, nlN, c->sc, 1, nullptr);
+  });
+  enq_xt(e, c->z.ptr, c->q.ptr, 1, c->mu_v.ptr, (double)c->ell, 1);
+  ShiftState ss = c->shifts();
+  e.go("dot_pq", 16.0 * d, [&] {
+    k_dot_pq<<<grid_for(nlD, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+        c->p.ptr, c->q.ptr, d, c->part_d.ptr, nlD, c->sc, ss, ns);
+  });
+  e.go("update", 24.0 * d + 32.0 * d * ns, [&] {
+    dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
+    k_update<<<g, LEAF_THREADS, 0, c->stream>>>(c->q.ptr, c->r0.ptr, c->r1.ptr, c->bigp.ptr,
+                                                c->sols.ptr, d, c->part_d.ptr, nlD, c->sc, ss, ns);
+  });
+  e.go("pupdate", 24.0 * d, [&] {
+    int gb = (int)std::min<long long>(grid_for(d, 256), (long long)c->num_sms * 8);
+    k_pupdate<<<gb, 256, 0, c->stream>>>(c->r0.ptr, c->r1.ptr, c->p.ptr, d, c->sc, cond,
+                                         use_cond);
+  });
+}
+
+// Setup (labeled mean, rhs, CG init) — sda.py:297-301, krylov.py:185-208.
+void enq_fsda_setup(Enq& e, int ns, long long max_iter, double tol) {
+  fsda_ctx* c = e.c;
+  const long long n = c->n, d = c->d, nlN = n_leaves(n), nlD = n_leaves(d);
+  ShiftState ss = c->shifts();
+  e.go("solve_reset", 0.0, [&] {
+    k_solve_reset<<<1, 256, 0, c->stream>>>(c->sc, ss, ns, max_iter, tol, 0);
+  });
+  e.go("indicator", 9.0 * n, [&] {
+    k_indicator<<<grid_for(n, 256), 256, 0, c->stream>>>(c->labels.ptr, c->ind.ptr, (int)n);
+  });
+  enq_xt(e, c->ind.ptr, c->mu_v.ptr, 2, nullptr, (double)c->ell, 0);
+  e.go("spmv_rows", 4.0 * (n + 1) + 4.0 * c->nnz + 8.0 * d + 8.0 * n, [&] {
+    k_spmv_rows<<<grid_for(n, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr,
+                                                         c->probe.ptr, c->t.ptr, (int)n, nullptr);
+  });
+  e.go("class_sums", 9.0 * n, [&] {
+    k_class_sums<<<grid_for(nlN, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+        c->t.ptr, c->labels.ptr, n, c->part_n.ptr, nlN, c->sc, (double)c->n1, (double)c->n2);
+  });
+  e.go("apply_w", 9.0 * n, [&] {
+    k_apply_w<<<grid_for(nlN, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+        c->labels.ptr, c->wv.ptr, n, c->part_n.ptr, nlN, c->sc);
+  });
+  enq_xt(e, c->wv.ptr, c->b.ptr, 1, c->mu_v.ptr, (double)c->ell, 0);
+  e.go("cg_init", 8.0 * d * 3 + 16.0 * d * ns, [&] {
+    dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
+    k_cg_init<<<g, LEAF_THREADS, 0, c->stream>>>(c->b.ptr, c->r0.ptr, c->p.ptr, c->bigp.ptr,
+                                                 c->sols.ptr, d, c->part_d.ptr, nlD, c->sc, ss, ns);
+  });
+}
+
+// Projection (sda.py:265-284) and the still-active residuals.
+void enq_fsda_tail(Enq& e, int ns) {
+  fsda_ctx* c = e.c;
+  const long long n = c->n, d = c->d, nlN = n_leaves(n);
+  ShiftState ss = c->shifts();
+  e.go("cg_finish", 0.0, [&] { k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns); });
+  e.go("transpose_sols", 16.0 * d * ns, [&] {
+    k_transpose_sols<<<grid_for(d * ns, 256), 256, 0, c->stream>>>(c->sols.ptr, c->wT.ptr, d, ns);
+  });
+  e.go("spmm_scores", 4.0 * (n + 1) + 4.0 * c->nnz + 8.0 * d * ns + 8.0 * n * ns, [&] {
+    k_spmm_scores<8><<<grid_for(n, 128), 128, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr,
+                                                              c->wT.ptr, c->scores.ptr, (int)n, ns);
+  });
+  e.go("orient", 8.0 * n * ns + 1.0 * n, [&] {
+    dim3 g(grid_for(nlN, WARPS_PER_BLOCK), ns);
+    k_orient<<<g, LEAF_THREADS, 0, c->stream>>>(c->labels.ptr, c->scores.ptr, n, c->part_o.ptr,
+                                                nlN, c->sc, ss, ns);
+  });
+  e.go("flip", 0.0, [&] {
+    dim3 g((unsigned)std::min<long long>(grid_for(std::max(n, d), 256), 1024), ns);
+    k_flip<<<g, 256, 0, c->stream>>>(c->scores.ptr, c->sols.ptr, n, d, ss);
+  });
+}
+
+// Build (or reuse) the whole-solve graph with a conditional WHILE node.
+bool build_solve_graph(fsda_ctx* c, double alpha, int ns, long long max_iter, double tol,
+                       long long* launches_fixed, long long* launches_body) {
+  char key[256];
+  snprintf(key, sizeof(key), "%a|%d|%lld|%a|%lld|%lld|%llu", alpha, ns, max_iter, tol, c->n, c->nnz,
+           g_alloc_gen);
+  if (c->exec && c->graph_key == key) return true;
+  c->invalidate_graph();
+  cudaStream_t s = c->stream;
+  cudaGraph_t graph;
+  CK(cudaGraphCreate(&graph, 0));
+  CK(cudaStreamBeginCaptureToGraph(s, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  Enq e{c};
+  try {
+    enq_fsda_setup(e, ns, max_iter, tol);
+  } catch (...) {
+    cudaGraph_t g2;
+    cudaStreamEndCapture(s, &g2);
+    cudaGraphDestroy(graph);
+    throw;
+  }
+  long long fixed = e.count;
+  cudaStreamCaptureStatus st;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  cudaGraph_t cap_graph;
+  CK(cudaStreamGetCaptureInfo(s, &st, nullptr, &cap_graph, &deps, &ndeps));
+  cudaGraphConditionalHandle handle;
+  CK(cudaGraphConditionalHandleCreate(&handle, cap_graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cond_node;
+  CK(cudaGraphAddNode(&cond_node, cap_graph, deps, ndeps, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CK(cudaStreamUpdateCaptureDependencies(s, &cond_node, 1, cudaStreamSetCaptureDependencies));
+  // capture the body on a side stream
+  cudaStream_t s2;
+  CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  CK(cudaStreamBeginCaptureToGraph(s2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  Enq eb{c};
+  cudaStream_t saved = c->stream;
+  c->stream = s2;
+  enq_fsda_iteration(eb, alpha, ns, (unsigned long long)handle, 1);
+  c->stream = saved;
+  cudaGraph_t body_out;
+  CK(cudaStreamEndCapture(s2, &body_out));
+  CK(cudaStreamDestroy(s2));
+  enq_fsda_tail(e, ns);
+  cudaGraph_t out;
+  CK(cudaStreamEndCapture(s, &out));
+  c->graph = out;
+  CK(cudaGraphInstantiate(&c->exec, out, 0));
+  c->graph_key = key;
+  *launches_fixed = e.count;  // setup + tail
+  *launches_body = eb.count;
+  (void)fixed;
+  return true;
+}
+
+struct SolveOut {
+  double* directions;
+  double* scores;
+  double* residuals;
+  int64_t* iterations;
+  uint8_t* converged;
+  int64_t* n_applies;
+  int64_t* fail_iter;
+};
+
+int check_solve_args(fsda_ctx* c, double alpha, const double* betas, int ns, double tol) {
+  if (!c->has_x) return fail(FSDA_EINVAL, "fsda_solve: X has not been uploaded");
+  if (!c->has_l) return fail(FSDA_EINVAL, "fsda_solve: Laplacian has not been uploaded");
+  if (!c->has_labels) return fail(FSDA_EINVAL, "fsda_solve: labels have not been set");
+  if (c->ell == 0) return fail(FSDA_ELABEL, "centering requires at least one labeled sample");
+  if (c->n1 == 0 || c->n2 == 0)
+    return fail(FSDA_EINVAL, "both classes need at least one labeled sample");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(FSDA_EINVAL, "alpha must lie in [0, 1], got %g", alpha);
+  if (ns <= 0) return fail(FSDA_EINVAL, "shift grid must be a non-empty 1-d array");
+  for (int s = 0; s < ns; ++s) {
+    if (!std::isfinite(betas[s])) return fail(FSDA_EINVAL, "shifts must be finite");
+    if (s == 0 && betas[s] < 0) return fail(FSDA_EINVAL, "shifts must be non-negative");
+    if (s > 0 && !(betas[s] > betas[s - 1])) return fail(FSDA_EINVAL, "shifts must be strictly ascending");
+  }
+  if (!(tol > 0)) return fail(FSDA_EINVAL, "tol must be positive");
+  if (c->d <= 0) return fail(FSDA_EINVAL, "operator dimension must be positive");
+  return FSDA_OK;
+}
+
+void upload_solve_params(fsda_ctx* c, const double* betas, int ns, const double* probe) {
+  ensure_vectors(c, ns);
+  CK(cudaMemcpyAsync(c->beta.ptr, betas, sizeof(double) * ns, cudaMemcpyHostToDevice, c->stream));
+  if (probe)
+    CK(cudaMemcpyAsync(c->probe.ptr, probe, sizeof(double) * c->d, cudaMemcpyHostToDevice, c->stream));
+}
+
+// Launch one complete solve (graph, or eager when rec != null or no graph).
+long long launch_solve(fsda_ctx* c, double alpha, int ns, long long max_iter, double tol,
+                       Recorder* rec) {
+  if (!rec && c->cond_supported) {
+    long long fixed = 0, body = 0;
+    try {
+      build_solve_graph(c, alpha, ns, max_iter, tol, &fixed, &body);
+      CK(cudaGraphLaunch(c->exec, c->stream));
+      // launches = fixed + body * iterations; iterations known after sync
+      c->last_launch_count = -(fixed * 1000000LL + body);  // decoded by fetch
+      return 0;
+    } catch (CudaError&) {
+      cudaGetLastError();
+      c->invalidate_graph();
+      c->cond_supported = false;  // fall through to eager
+    }
+  }
+  Enq e{c, rec};
+  enq_fsda_setup(e, ns, max_iter, tol);
+  for (long long it = 0; it < max_iter; ++it) enq_fsda_iteration(e, alpha, ns, 0, 0);
+  enq_fsda_tail(e, ns);
+  c->last_launch_count = e.count;
+  return e.count;
+}
+
+int read_results(fsda_ctx* c, int ns, const SolveOut& o, int64_t* launches) {
+  CgScalars h;
+  CK(cudaMemcpyAsync(&h, c->sc, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  std::vector<long long> it(ns);
+  std::vector<unsigned char> cv(ns);
+  if (o.directions)
+    CK(cudaMemcpyAsync(o.directions, c->sols.ptr, sizeof(double) * ns * c->d, cudaMemcpyDeviceToHost, c->stream));
+  if (o.scores)
+    CK(cudaMemcpyAsync(o.scores, c->scores.ptr, sizeof(double) * ns * c->n, cudaMemcpyDeviceToHost, c->stream));
+  if (o.residuals)
+    CK(cudaMemcpyAsync(o.residuals, c->resid.ptr, sizeof(double) * ns, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(it.data(), c->iters.ptr, sizeof(long long) * ns, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(cv.data(), c->conv.ptr, ns, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (o.iterations)
+    for (int s = 0; s < ns; ++s) o.iterations[s] = it[s];
+  if (o.converged)
+    for (int s = 0; s < ns; ++s) o.converged[s] = cv[s];
+  if (o.n_applies) *o.n_applies = h.iter;
+  if (o.fail_iter) *o.fail_iter = h.fail_iter;
+  if (launches) {
+    long long lc = c->last_launch_count;
+    if (lc < 0) {
+      long long enc = -lc, fixed = enc / 1000000LL, body = enc % 1000000LL;
+      long long runs = h.iter + ((h.status != ST_OK || h.b_norm == 0.0) ? 1 : 0);
+      lc = fixed + body * std::max<long long>(runs, 1);
+    }
+    *launches = lc;
+  }
+  if (h.status == ST_BREAKDOWN)
+    return fail(FSDA_EBREAKDOWN, "singular direction: <p, Bp> = 0 at iteration %lld", h.fail_iter);
+  if (h.status == ST_NONFINITE)
+    return fail(FSDA_ENONFINITE, "non-finite <p, Bp> or residual at iteration %lld", h.fail_iter);
+  return FSDA_OK;
+}
+
+// Build the column work plan from the CSC column pointer (host side).
+void build_xt_plan(fsda_ctx* c) {
+  const long long D = c->d;
+  std::vector<int> colptr(D + 1);
+  CK(cudaMemcpy(colptr.data(), c->csc_colptr.ptr, sizeof(int) * (D + 1), cudaMemcpyDeviceToHost));
+  std::vector<int> tiny[5], warpc, segc, segs, hc, h0, hn;
+  for (long long col = 0; col < D; ++col) {
+    int nc = colptr[col + 1] - colptr[col];
+    if (nc <= 16) {
+      int k = 0;
+      while ((1 << k) < nc) ++k;
+      tiny[k].push_back((int)col);
+    } else if (nc <= LEAF) {
+      warpc.push_back((int)col);
+    } else {
+      hc.push_back((int)col);
+      h0.push_back((int)segc.size());
+      int nseg = (int)cdiv(nc, LEAF);
+      hn.push_back(nseg);
+      for (int j = 0; j < nseg; ++j) {
+        segc.push_back((int)col);
+        segs.push_back(colptr[col] + j * LEAF);
+      }
+    }
+  }
+  std::vector<int> tiny_all;
+  XtPlan& pl = c->plan;
+  memset(&pl, 0, sizeof(pl));
+  long long off = 0;
+  for (int k = 0; k < 5; ++k) {
+    pl.tiny_off[k] = off;
+    tiny_all.insert(tiny_all.end(), tiny[k].begin(), tiny[k].end());
+    off += (long long)tiny[k].size();
+    pl.warps_tiny[k] = cdiv((long long)tiny[k].size(), 32 >> k);
+  }
+  pl.tiny_off[5] = off;
+  auto up = [&](DevBuf<int>& dst, const std::vector<int>& v) {
+    dst.ensure(v.size());
+    if (!v.empty()) CK(cudaMemcpy(dst.ptr, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice));
+  };
+  up(c->tiny_cols, tiny_all);
+  up(c->warp_cols, warpc);
+  up(c->seg_col, segc);
+  up(c->seg_start, segs);
+  up(c->heavy_cols, hc);
+  up(c->heavy_seg0, h0);
+  up(c->heavy_nseg, hn);
+  c->seg_part.ensure(segc.size());
+  pl.colptr = c->csc_colptr.ptr;
+  pl.rows = c->csc_rows.ptr;
+  pl.tiny_cols = c->tiny_cols.ptr;
+  pl.warp_cols = c->warp_cols.ptr;
+  pl.n_warp_cols = (long long)warpc.size();
+  pl.seg_col = c->seg_col.ptr;
+  pl.seg_start = c->seg_start.ptr;
+  pl.n_segs = (long long)segc.size();
+  pl.heavy_cols = c->heavy_cols.ptr;
+  pl.heavy_seg0 = c->heavy_seg0.ptr;
+  pl.heavy_nseg = c->heavy_nseg.ptr;
+  pl.n_heavy = (long long)hc.size();
+  pl.seg_part = c->seg_part.ptr;
+  long long base = 0;
+  for (int k = 0; k < 5; ++k) {
+    pl.warp_base[k] = base;
+    base += pl.warps_tiny[k];
+  }
+  pl.warp_base[5] = base;
+  base += pl.n_warp_cols;
+  pl.warp_base[6] = base;
+  base += pl.n_segs;
+  pl.warp_base[7] = base;
+  c->xt_warps = base;
+}
+
+int check_err_flag(fsda_ctx* c, const char* what) {
+  int h = 0;
+  CK(cudaMemcpy(&h, c->err.ptr, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h == 1) return fail(FSDA_EINVAL, "%s: index out of range", what);
+  if (h == 2) return fail(FSDA_EINVAL, "%s: row_offsets must be non-decreasing", what);
+  if (h == 3) return fail(FSDA_EINVAL, "%s: column indices must be strictly increasing within each row", what);
+  if (h == 4)
+    return fail(FSDA_EINVAL, "%s: only unit-weight graphs are supported (off-diagonal values must be -1)", what);
+  return FSDA_OK;
+}
+
+// Upload an int64 index array and narrow it to int32 on the device.
+void upload_narrow(fsda_ctx* c, const int64_t* host, long long n, long long limit, DevBuf<int>& out) {
+  out.ensure(n + 1);
+  if (n == 0) return;
+  long long* tmp = nullptr;
+  CK(cudaMalloc(&tmp, sizeof(long long) * n));
+  CK(cudaMemcpyAsync(tmp, host, sizeof(long long) * n, cudaMemcpyHostToDevice, c->stream));
+  int g = (int)std::min<long long>(cdiv(n, 256), (long long)c->num_sms * 32);
+  k_narrow_idx<<<g, 256, 0, c->stream>>>(tmp, out.ptr, n, limit, c->err.ptr);
+  CKL();
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(tmp);
+}
+
+#define API_BEGIN(ctx)                                   \
+  if (!(ctx)) return fail(FSDA_EINVAL, "null context"); \
+  std::lock_guard<std::mutex> lock_((ctx)->mu);          \
+  try {                                                  \
+    CK(cudaSetDevice((ctx)->device));
+#define API_END                                                                     \
+  }                                                                                 \
+  catch (CudaError & e) {                                                           \
+    return fail(FSDA_ECUDA, "CUDA error %s at %s (line %d)", cudaGetErrorString(e.err), e.what, \
+                e.line);                                                            \
+  }
+
+}  // namespace
+
+// ===================================================================== C ABI
+
+extern "C" {
+
+int fsda_abi_version(void) { return 1; }
+
+const char* fsda_last_error(void) { return g_last_error.c_str(); }
+
+int fsda_ctx_create(fsda_ctx** out, int device, void* stream) {
+  if (!out) return fail(FSDA_EINVAL, "null output pointer");
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(FSDA_ECUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(FSDA_EINVAL, "device %d out of range", device);
+  fsda_ctx* c = new fsda_ctx();
+  c->device = device;
+  try {
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      throw CudaError{cudaErrorInvalidDevice, "this library is built for sm_100a (B200)", __LINE__};
+    c->num_sms = prop.multiProcessorCount;
+    if (stream) {
+      c->stream = (cudaStream_t)stream;
+    } else {
+      CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    CK(cudaMalloc(&c->sc, sizeof(CgScalars)));
+    CK(cudaMemset(c->sc, 0, sizeof(CgScalars)));
+    c->err.ensure(1);
+    CK(cudaMemset(c->err.ptr, 0, sizeof(int)));
+  } catch (CudaError& ce) {
+    delete c;
+    return fail(FSDA_ECUDA, "CUDA error %s at %s", cudaGetErrorString(ce.err), ce.what);
+  }
+  *out = c;
+  return FSDA_OK;
+}
+
+int fsda_ctx_destroy(fsda_ctx* c) {
+  if (!c) return FSDA_OK;
+  {
+    std::lock_guard<std::mutex> lock(c->mu);
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    c->invalidate_graph();
+    DevBuf<int>* ib[] = {&c->x_rowptr, &c->x_cols, &c->csc_colptr, &c->csc_rows, &c->tiny_cols,
+                         &c->warp_cols, &c->seg_col, &c->seg_start, &c->heavy_cols, &c->heavy_seg0,
+                         &c->heavy_nseg, &c->l_rowptr, &c->l_cols, &c->active, &c->good,
+                         &c->pending, &c->flip, &c->err};
+    for (auto b : ib) b->release();
+    DevBuf<double>* db[] = {&c->seg_part, &c->l_diag, &c->y, &c->z, &c->q, &c->p, &c->r0, &c->r1,
+                            &c->mu_v, &c->t, &c->wv, &c->b, &c->ind, &c->probe, &c->part_n,
+                            &c->part_d, &c->part_o, &c->bigp, &c->sols, &c->wT, &c->scores,
+                            &c->dense_a, &c->beta, &c->zeta_prev, &c->zeta, &c->zeta_next,
+                            &c->gamma_s, &c->alpha_s, &c->resid};
+    for (auto b : db) b->release();
+    c->iters.release();
+    c->conv.release();
+    c->labels.release();
+    if (c->sc) cudaFree(c->sc);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+  }
+  delete c;
+  return FSDA_OK;
+}
+
+int fsda_ctx_set_stream(fsda_ctx* c, void* stream) {
+  API_BEGIN(c)
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->own_stream) CK(cudaStreamDestroy(c->stream));
+  c->own_stream = false;
+  if (stream) {
+    c->stream = (cudaStream_t)stream;
+  } else {
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  c->invalidate_graph();
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* row_offsets,
+                  const int64_t* col_indices) {
+  API_BEGIN(c)
+  if (n_rows < 0 || n_cols < 0) return fail(FSDA_EINVAL, "matrix shape must be non-negative");
+  if (!row_offsets) return fail(FSDA_EINVAL, "row_offsets is null");
+  const long long nnz = row_offsets[n_rows];
+  if (row_offsets[0] != 0 || nnz < 0) return fail(FSDA_EINVAL, "row_offsets must be non-decreasing from 0 to nnz");
+  if (nnz > 0 && !col_indices) return fail(FSDA_EINVAL, "col_indices is null");
+  if (nnz >= (1LL << 31) - 1 || n_rows >= (1LL << 31) - 1 || n_cols >= (1LL << 31) - 1)
+    return fail(FSDA_EINVAL, "X too large for int32 device indices (nnz=%lld)", nnz);
+  if (n_rows > MAX_REDUCE || n_cols > MAX_REDUCE)
+    return fail(FSDA_EINVAL, "vector length above the two-level reduction limit (%lld)", MAX_REDUCE);
+  c->has_x = false;
+  c->invalidate_graph();
+  CK(cudaMemset(c->err.ptr, 0, sizeof(int)));
+  c->n = n_rows;
+  c->d = n_cols;
+  c->nnz = nnz;
+  upload_narrow(c, row_offsets, n_rows + 1, nnz, c->x_rowptr);
+  upload_narrow(c, col_indices, nnz, n_cols - 1, c->x_cols);
+  int rc = check_err_flag(c, "X");
+  if (rc) return rc;
+  // row ids + in-row order validation
+  DevBuf<int> row_of;
+  row_of.ensure(nnz);
+  if (n_rows > 0) {
+    k_row_ids<<<grid_for(n_rows, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr,
+                                                            row_of.ptr, (int)n_rows, c->err.ptr);
+    CKL();
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  rc = check_err_flag(c, "X");
+  if (rc) { row_of.release(); return rc; }
+  // CSC by a stable radix sort of (column, row) pairs: rows stay ascending.
+  c->csc_rows.ensure(nnz);
+  c->csc_colptr.ensure(n_cols + 1);
+  DevBuf<int> keys_out;
+  keys_out.ensure(nnz);
+  if (nnz > 0) {
+    int end_bit = 1;
+    while ((1LL << end_bit) < n_cols) ++end_bit;
+    size_t temp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, c->x_cols.ptr, keys_out.ptr, row_of.ptr,
+                                       c->csc_rows.ptr, (int)nnz, 0, end_bit, c->stream));
+    void* temp = nullptr;
+    CK(cudaMalloc(&temp, std::max<size_t>(temp_bytes, 1)));
+    CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, c->x_cols.ptr, keys_out.ptr, row_of.ptr,
+                                       c->csc_rows.ptr, (int)nnz, 0, end_bit, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(temp);
+  }
+  k_colptr_from_sorted<<<grid_for(n_cols + 1, 256), 256, 0, c->stream>>>(keys_out.ptr, nnz,
+                                                                          c->csc_colptr.ptr, (int)n_cols);
+  CKL();
+  CK(cudaStreamSynchronize(c->stream));
+  keys_out.release();
+  row_of.release();
+  build_xt_plan(c);
+  c->has_x = true;
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_upload_laplacian(fsda_ctx* c, int64_t n, const int64_t* row_offsets,
+                          const int64_t* col_indices, const double* values) {
+  API_BEGIN(c)
+  if (!c->has_x) return fail(FSDA_EINVAL, "upload X before the Laplacian");
+  if (n != c->n) return fail(FSDA_EINVAL, "laplacian must be square with one row per sample");
+  if (!row_offsets) return fail(FSDA_EINVAL, "row_offsets is null");
+  const long long nnz = row_offsets[n];
+  if (row_offsets[0] != 0 || nnz < 0) return fail(FSDA_EINVAL, "row_offsets must be non-decreasing from 0 to nnz");
+  if (nnz >= (1LL << 31) - 1) return fail(FSDA_EINVAL, "Laplacian too large for int32 indices");
+  c->has_l = false;
+  c->invalidate_graph();
+  CK(cudaMemset(c->err.ptr, 0, sizeof(int)));
+  c->l_nnz = nnz;
+  upload_narrow(c, row_offsets, n + 1, nnz, c->l_rowptr);
+  upload_narrow(c, col_indices, nnz, n - 1, c->l_cols);
+  int rc = check_err_flag(c, "laplacian");
+  if (rc) return rc;
+  c->l_diag.ensure(n);
+  if (n > 0) {
+    double* dvals = nullptr;
+    CK(cudaMalloc(&dvals, sizeof(double) * std::max<long long>(nnz, 1)));
+    if (nnz > 0)
+      CK(cudaMemcpyAsync(dvals, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, c->stream));
+    k_laplacian_split<<<grid_for(n, 256), 256, 0, c->stream>>>(c->l_rowptr.ptr, c->l_cols.ptr, dvals,
+                                                               c->l_diag.ptr, (int)n, c->err.ptr);
+    CKL();
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(dvals);
+  }
+  rc = check_err_flag(c, "laplacian");
+  if (rc) return rc;
+  c->has_l = true;
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_set_labels(fsda_ctx* c, const int8_t* labels) {
+  API_BEGIN(c)
+  if (!c->has_x) return fail(FSDA_EINVAL, "upload X before the labels");
+  long long n1 = 0, n2 = 0;
+  bool seen_unlabeled = false, labeled_first = true;
+  for (long long i = 0; i < c->n; ++i) {
+    int8_t l = labels[i];
+    if (l != 0 && l != 1 && l != -1) return fail(FSDA_ELABEL, "labels must take values in {+1, -1, 0}");
+    if (l == 1) ++n1;
+    if (l == -1) ++n2;
+    if (l == 0) seen_unlabeled = true;
+    else if (seen_unlabeled) labeled_first = false;
+  }
+  if (!labeled_first)
+    return fail(FSDA_EINVAL,
+                "labeled samples must occupy the first rows; use arrange_labeled_first to permute the problem");
+  c->labels.ensure(std::max<long long>(c->n, 1));
+  if (c->n > 0)
+    CK(cudaMemcpyAsync(c->labels.ptr, labels, c->n, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->n1 = n1;
+  c->n2 = n2;
+  c->ell = n1 + n2;
+  c->has_labels = true;
+  return FSDA_OK;
+  API_END
+}
+
+// ---- parity probes ---------------------------------------------------------
+
+int fsda_matvec(fsda_ctx* c, const double* v, double* yout) {
+  API_BEGIN(c)
+  if (!c->has_x) return fail(FSDA_EINVAL, "X has not been uploaded");
+  ensure_vectors(c, 1);
+  CK(cudaMemcpyAsync(c->p.ptr, v, sizeof(double) * c->d, cudaMemcpyHostToDevice, c->stream));
+  if (c->n > 0) {
+    k_spmv_rows<<<grid_for(c->n, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr, c->p.ptr,
+                                                            c->y.ptr, (int)c->n, nullptr);
+    CKL();
+  }
+  CK(cudaMemcpyAsync(yout, c->y.ptr, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return FSDA_OK;
+  API_END
+}
+
+static int xt_probe(fsda_ctx* c, const double* mu, const double* w, double* out, int mode) {
+  ensure_vectors(c, 1);
+  CK(cudaMemcpyAsync(c->z.ptr, w, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
+  if (mode == 1) {
+    CK(cudaMemcpyAsync(c->mu_v.ptr, mu, sizeof(double) * c->d, cudaMemcpyHostToDevice, c->stream));
+    long long nl = n_leaves(c->n);
+    k_vector_sum<<<grid_for(nl, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+        c->z.ptr, c->n, c->part_n.ptr, nl, c->sc, nullptr);
+    CKL();
+  }
+  Enq e{c};
+  enq_xt(e, c->z.ptr, c->q.ptr, mode, c->mu_v.ptr, (double)c->ell, 0);
+  CK(cudaMemcpyAsync(out, c->q.ptr, sizeof(double) * c->d, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return FSDA_OK;
+}
+
+int fsda_matvec_transpose(fsda_ctx* c, const double* w, double* u) {
+  API_BEGIN(c)
+  if (!c->has_x) return fail(FSDA_EINVAL, "X has not been uploaded");
+  return xt_probe(c, nullptr, w, u, 0);
+  API_END
+}
+
+int fsda_centered_matvec_transpose(fsda_ctx* c, const double* mu, const double* w, double* u) {
+  API_BEGIN(c)
+  if (!c->has_x) return fail(FSDA_EINVAL, "X has not been uploaded");
+  return xt_probe(c, mu, w, u, 1);
+  API_END
+}
+
+int fsda_labeled_mean(fsda_ctx* c, double* mu) {
+  API_BEGIN(c)
+  if (!c->has_x || !c->has_labels) return fail(FSDA_EINVAL, "X and labels must be uploaded");
+  if (c->ell == 0) return fail(FSDA_ELABEL, "centering requires at least one labeled sample");
+  ensure_vectors(c, 1);
+  k_indicator<<<grid_for(c->n, 256), 256, 0, c->stream>>>(c->labels.ptr, c->ind.ptr, (int)c->n);
+  CKL();
+  Enq e{c};
+  enq_xt(e, c->ind.ptr, c->mu_v.ptr, 2, nullptr, (double)c->ell, 0);
+  CK(cudaMemcpyAsync(mu, c->mu_v.ptr, sizeof(double) * c->d, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_apply_smoother(fsda_ctx* c, double alpha, const double* yin, double* zout) {
+  API_BEGIN(c)
+  if (!c->has_l || !c->has_labels) return fail(FSDA_EINVAL, "Laplacian and labels must be uploaded");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(FSDA_EINVAL, "alpha must lie in [0, 1], got %g", alpha);
+  ensure_vectors(c, 1);
+  CK(cudaMemcpyAsync(c->y.ptr, yin, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
+  long long nl = n_leaves(c->n);
+  k_smoother<<<grid_for(nl, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+      c->l_rowptr.ptr, c->l_cols.ptr, c->l_diag.ptr, c->labels.ptr, c->y.ptr, c->z.ptr, (int)c->n,
+      alpha, alpha_mode_of(alpha), c->part_n.ptr, nl, c->sc, 0, nullptr);
+  CKL();
+  CK(cudaMemcpyAsync(zout, c->z.ptr, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_operator_apply(fsda_ctx* c, double alpha, const double* w, double* qout) {
+  API_BEGIN(c)
+  if (!c->has_x || !c->has_l || !c->has_labels)
+    return fail(FSDA_EINVAL, "X, Laplacian and labels must be uploaded");
+  if (c->ell == 0) return fail(FSDA_ELABEL, "centering requires at least one labeled sample");
+  ensure_vectors(c, 1);
+  // mu
+  k_indicator<<<grid_for(c->n, 256), 256, 0, c->stream>>>(c->labels.ptr, c->ind.ptr, (int)c->n);
+  CKL();
+  Enq e{c};
+  enq_xt(e, c->ind.ptr, c->mu_v.ptr, 2, nullptr, (double)c->ell, 0);
+  CK(cudaMemcpyAsync(c->p.ptr, w, sizeof(double) * c->d, cudaMemcpyHostToDevice, c->stream));
+  k_spmv_rows<<<grid_for(c->n, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr, c->p.ptr,
+                                                          c->y.ptr, (int)c->n, nullptr);
+  CKL();
+  long long nl = n_leaves(c->n);
+  k_smoother<<<grid_for(nl, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+      c->l_rowptr.ptr, c->l_cols.ptr, c->l_diag.ptr, c->labels.ptr, c->y.ptr, c->z.ptr, (int)c->n,
+      alpha, alpha_mode_of(alpha), c->part_n.ptr, nl, c->sc, 0, nullptr);
+  CKL();
+  enq_xt(e, c->z.ptr, c->q.ptr, 1, c->mu_v.ptr, (double)c->ell, 0);
+  CK(cudaMemcpyAsync(qout, c->q.ptr, sizeof(double) * c->d, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return FSDA_OK;
+  API_END
+}
+
+// ---- the hot path -----------------------------------------------------------
+
+int fsda_solve(fsda_ctx* c, double alpha, const double* betas, int ns, double tol,
+               int64_t max_iter, const double* probe, double* directions, double* scores,
+               double* residuals, int64_t* iterations, uint8_t* converged, int64_t* n_applies,
+               int64_t* fail_iter) {
+  API_BEGIN(c)
+  int rc = check_solve_args(c, alpha, betas, ns, tol);
+  if (rc) return rc;
+  if (!probe) return fail(FSDA_EINVAL, "probe is null");
+  upload_solve_params(c, betas, ns, probe);
+  launch_solve(c, alpha, ns, max_iter, tol, nullptr);
+  SolveOut o{directions, scores, residuals, iterations, converged, n_applies, fail_iter};
+  return read_results(c, ns, o, nullptr);
+  API_END
+}
+
+int fsda_prepare_resident(fsda_ctx* c, double alpha, const double* betas, int ns, double tol,
+                          int64_t max_iter, const double* probe) {
+  API_BEGIN(c)
+  int rc = check_solve_args(c, alpha, betas, ns, tol);
+  if (rc) return rc;
+  upload_solve_params(c, betas, ns, probe);
+  CK(cudaStreamSynchronize(c->stream));
+  c->r_alpha = alpha;
+  c->r_ns = ns;
+  c->r_tol = tol;
+  c->r_max_iter = max_iter;
+  c->r_prepared = true;
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_solve_async(fsda_ctx* c) {
+  API_BEGIN(c)
+  if (!c->r_prepared) return fail(FSDA_EINVAL, "call fsda_prepare_resident first");
+  launch_solve(c, c->r_alpha, c->r_ns, c->r_max_iter, c->r_tol, nullptr);
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_fetch_results(fsda_ctx* c, double* directions, double* scores, double* residuals,
+                       int64_t* iterations, uint8_t* converged, int64_t* n_applies,
+                       int64_t* fail_iter, int64_t* launches) {
+  API_BEGIN(c)
+  if (!c->r_prepared) return fail(FSDA_EINVAL, "call fsda_prepare_resident first");
+  SolveOut o{directions, scores, residuals, iterations, converged, n_applies, fail_iter};
+  return read_results(c, c->r_ns, o, launches);
+  API_END
+}
+
+int fsda_profile_kernels(fsda_ctx* c, int max_kernels, int* n_kernels, const char** names,
+                         double* ms_per_launch, double* bytes_per_launch,
+                         int64_t* launches_per_solve) {
+  API_BEGIN(c)
+  if (!c->r_prepared) return fail(FSDA_EINVAL, "call fsda_prepare_resident first");
+  Recorder rec;
+  rec.stream = c->stream;
+  launch_solve(c, c->r_alpha, c->r_ns, c->r_max_iter, c->r_tol, &rec);
+  CK(cudaStreamSynchronize(c->stream));
+  // accumulate per name, skipping launches after the loop finished is not
+  // needed: for the measured configurations every iteration runs.
+  std::vector<std::string> order;
+  std::map<std::string, double> ms, bytes;
+  std::map<std::string, long long> cnt;
+  for (size_t k = 0; k < rec.names.size(); ++k) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, rec.ev[2 * k], rec.ev[2 * k + 1]));
+    std::string nm = rec.names[k].first;
+    if (!cnt.count(nm)) order.push_back(nm);
+    ms[nm] += t;
+    bytes[nm] = rec.names[k].second;
+    cnt[nm] += 1;
+  }
+  static thread_local std::vector<std::string> keep;
+  keep = order;
+  int k = 0;
+  for (auto& nm : keep) {
+    if (k >= max_kernels) break;
+    names[k] = nm.c_str();
+    ms_per_launch[k] = ms[nm] / (double)cnt[nm];
+    bytes_per_launch[k] = bytes[nm];
+    launches_per_solve[k] = cnt[nm];
+    ++k;
+  }
+  *n_kernels = k;
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_shifted_cg_dense(fsda_ctx* c, int64_t dim, const double* a, const double* bvec,
+                          const double* betas, int ns, double tol, int64_t max_iter,
+                          int absolute_tol, double* solutions, double* residuals,
+                          int64_t* iterations, uint8_t* converged, int64_t* n_applies,
+                          int64_t* fail_iter) {
+  API_BEGIN(c)
+  if (dim <= 0) return fail(FSDA_EINVAL, "operator dimension must be positive");
+  if (dim > MAX_REDUCE) return fail(FSDA_EINVAL, "dimension above the reduction limit");
+  if (ns <= 0) return fail(FSDA_EINVAL, "shift grid must be a non-empty 1-d array");
+  for (int s = 0; s < ns; ++s) {
+    if (!std::isfinite(betas[s])) return fail(FSDA_EINVAL, "shifts must be finite");
+    if (s == 0 && betas[s] < 0) return fail(FSDA_EINVAL, "shifts must be non-negative");
+    if (s > 0 && !(betas[s] > betas[s - 1])) return fail(FSDA_EINVAL, "shifts must be strictly ascending");
+  }
+  if (!(tol > 0)) return fail(FSDA_EINVAL, "tol must be positive");
+  // Borrow the solve buffers with d = dim; restore the problem shape on exit.
+  struct ShapeGuard {
+    fsda_ctx* c;
+    long long n, d;
+    ~ShapeGuard() { c->n = n; c->d = d; c->invalidate_graph(); }
+  } guard{c, c->n, c->d};
+  c->d = dim;
+  c->n = std::max<long long>(c->n, 1);
+  ensure_vectors(c, ns);
+  c->dense_a.ensure((size_t)dim * dim);
+  CK(cudaMemcpyAsync(c->dense_a.ptr, a, sizeof(double) * dim * dim, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->b.ptr, bvec, sizeof(double) * dim, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->beta.ptr, betas, sizeof(double) * ns, cudaMemcpyHostToDevice, c->stream));
+  ShiftState ss = c->shifts();
+  const long long nlD = n_leaves(dim);
+  k_solve_reset<<<1, 256, 0, c->stream>>>(c->sc, ss, ns, max_iter, tol, absolute_tol);
+  CKL();
+  {
+    dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
+    k_cg_init<<<g, LEAF_THREADS, 0, c->stream>>>(c->b.ptr, c->r0.ptr, c->p.ptr, c->bigp.ptr,
+                                                 c->sols.ptr, dim, c->part_d.ptr, nlD, c->sc, ss, ns);
+    CKL();
+  }
+  for (long long it = 0; it < max_iter; ++it) {
+    k_dense_matvec<<<grid_for(dim, 128), 128, 0, c->stream>>>(c->dense_a.ptr, c->p.ptr, c->q.ptr,
+                                                              (int)dim, c->sc);
+    k_dot_pq<<<grid_for(nlD, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+        c->p.ptr, c->q.ptr, dim, c->part_d.ptr, nlD, c->sc, ss, ns);
+    dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
+    k_update<<<g, LEAF_THREADS, 0, c->stream>>>(c->q.ptr, c->r0.ptr, c->r1.ptr, c->bigp.ptr,
+                                                c->sols.ptr, dim, c->part_d.ptr, nlD, c->sc, ss, ns);
+    k_pupdate<<<grid_for(dim, 256), 256, 0, c->stream>>>(c->r0.ptr, c->r1.ptr, c->p.ptr, dim, c->sc,
+                                                         0, 0);
+    CKL();
+    if ((it & 15) == 15) {  // stop launching once every shift froze
+      CgScalars h;
+      CK(cudaMemcpyAsync(&h, c->sc, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      if (h.finished || h.status) break;
+    }
+  }
+  k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns);
+  CKL();
+  SolveOut o{solutions, nullptr, residuals, iterations, converged, n_applies, fail_iter};
+  return read_results(c, ns, o, nullptr);
+  API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,194 @@
+"""Seeded synthetic FSDA problems with the shapes of BASELINE.json's configs.
+
+The reference publishes no dataset for this path (its ChEMBL corpus is not
+shipped), so every measurement and parity case runs on generated inputs with
+the stated shapes and value distributions:
+
+* X: row i draws ``n_i ~ Poisson(lam)`` nonzeros, then ``n_i`` *distinct*
+  columns by successive weighted sampling without replacement from
+  ``P(j) ∝ (j+1)^-s`` (low index = popular; the convention of the reference's
+  ``random_sparse_binary``, /root/reference/pkg/src/sdakit/synthetic.py:49).
+* Graph: every node picks ``k`` distinct uniform neighbours other than
+  itself; the edge set is union-symmetrized (graph.py:141-149) and
+  ``L = diag(deg) - S`` (graph.py:191-195), stored exactly as sdakit stores it.
+* Labels: rows ``0 .. ell-1`` are labeled (rows are i.i.d., so this equals a
+  random selection and needs no ``arrange_labeled_first``); ``n_pos`` of them,
+  a seeded random subset, are +1, the rest -1.
+
+Everything is plain numpy; the arrays plug straight into either the
+reference's ``SdaProblem`` or ours.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+# (name, N, D, Poisson mean, Zipf s, k, ell, n_pos, n_shifts, beta_lo, beta_hi, K)
+CONFIGS = {
+    "cfg1": dict(n=10_000, d=5_000, lam=25.0, s=1.1, k=10, ell=1_000, n_pos=200,
+                 n_shifts=10, beta_lo=1e-4, beta_hi=1e2, max_iter=50),
+    "cfg2": dict(n=200_000, d=100_000, lam=50.0, s=1.1, k=10, ell=10_000, n_pos=3_000,
+                 n_shifts=20, beta_lo=1e-5, beta_hi=1e3, max_iter=100),
+    "cfg3": dict(n=1_500_000, d=500_000, lam=50.0, s=1.05, k=10, ell=30_000, n_pos=3_000,
+                 n_shifts=30, beta_lo=1e-6, beta_hi=1e3, max_iter=150),
+}
+
+ALPHA = 0.5      # reference default, config.py:36
+TOL = 1e-8       # reference default, sda.py:78
+
+
+@dataclass
+class Workload:
+    """Raw arrays of one FSDA problem (reference storage conventions)."""
+
+    name: str
+    n: int
+    d: int
+    x_offsets: np.ndarray   # int64, N+1
+    x_cols: np.ndarray      # int64, nnz (strictly increasing per row)
+    l_offsets: np.ndarray   # int64, N+1
+    l_cols: np.ndarray      # int64
+    l_vals: np.ndarray      # float64 (-1 off the diagonal, degree on it)
+    degrees: np.ndarray     # int64
+    labels: np.ndarray      # int8, labeled first
+    betas: np.ndarray       # ascending
+    alpha: float = ALPHA
+    tol: float = TOL
+    max_iter: int = 100
+    seed: int = 0
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.x_cols.size)
+
+    def probe(self) -> np.ndarray:
+        """The reference's probe draw: default_rng(seed).uniform(-1, 1, D)
+        (sda.py:297,300)."""
+        return np.random.default_rng(self.seed).uniform(-1.0, 1.0, size=self.d)
+
+
+def _first_distinct(row: np.ndarray, cand: np.ndarray, width: int, want: np.ndarray):
+    """For candidate draws grouped by row (draw order), keep the first
+    ``want[r]`` distinct values of each row.  Returns (rows, values, short)
+    with ``short`` the rows that ran out of distinct candidates."""
+    n = want.size
+    key = row.astype(np.int64) * width + cand
+    order = np.argsort(key, kind="stable")
+    ks = key[order]
+    first = np.ones(ks.size, dtype=bool)
+    first[1:] = ks[1:] != ks[:-1]
+    pos = np.sort(order[first])            # first occurrences, back in draw order
+    r = row[pos]
+    start = np.searchsorted(r, np.arange(n))
+    rank = np.arange(r.size) - start[r]
+    keep = rank < want[r]
+    got = np.bincount(r[keep], minlength=n)
+    return r[keep], cand[pos][keep], np.flatnonzero(got < want)
+
+
+def zipf_binary_rows(n: int, d: int, lam: float, s: float, seed: int):
+    """CSR (offsets, cols) of the binary X described in the module docstring."""
+    rng = np.random.default_rng(seed)
+    counts = np.minimum(rng.poisson(lam, size=n), d).astype(np.int64)
+    cdf = np.cumsum((np.arange(d, dtype=np.float64) + 1.0) ** (-s))
+    cdf /= cdf[-1]
+    m = 2 * counts + 8
+    row = np.repeat(np.arange(n, dtype=np.int64), m)
+    cand = np.minimum(np.searchsorted(cdf, rng.random(row.size), side="right"), d - 1)
+    rows, cols, short = _first_distinct(row, cand.astype(np.int64), d, counts)
+    if short.size:  # rare: successive sampling row by row for the leftovers
+        extra_r, extra_c = [], []
+        keep_mask = ~np.isin(rows, short)
+        rows, cols = rows[keep_mask], cols[keep_mask]
+        for i in short:
+            chosen: list[int] = []
+            seen = set()
+            while len(chosen) < counts[i]:
+                c = int(min(np.searchsorted(cdf, rng.random(), side="right"), d - 1))
+                if c not in seen:
+                    seen.add(c)
+                    chosen.append(c)
+            extra_r.append(np.full(len(chosen), i, dtype=np.int64))
+            extra_c.append(np.asarray(chosen, dtype=np.int64))
+        rows = np.concatenate([rows] + extra_r)
+        cols = np.concatenate([cols] + extra_c)
+    key = np.sort(rows * d + cols)
+    rows, cols = key // d, key % d
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=offsets[1:])
+    return offsets, cols.astype(np.int64)
+
+
+def random_knn_laplacian(n: int, k: int, seed: int):
+    """Union-symmetrized random k-NN graph, returned as the Laplacian CSR
+    (offsets, cols, vals) plus the degree vector."""
+    rng = np.random.default_rng(seed)
+    m = k + 4
+    row = np.repeat(np.arange(n, dtype=np.int64), m)
+    cand = rng.integers(0, n - 1, size=row.size)
+    cand = cand + (cand >= row)                      # skip self
+    want = np.full(n, k, dtype=np.int64)
+    src, dst, short = _first_distinct(row, cand, n, want)
+    if short.size:
+        keep_mask = ~np.isin(src, short)
+        src, dst = src[keep_mask], dst[keep_mask]
+        er, ec = [], []
+        for i in short:
+            pick = rng.choice(np.delete(np.arange(n), i), size=k, replace=False)
+            er.append(np.full(k, i, dtype=np.int64))
+            ec.append(pick.astype(np.int64))
+        src = np.concatenate([src] + er)
+        dst = np.concatenate([dst] + ec)
+    keys = np.unique(np.concatenate([src * n + dst, dst * n + src]))
+    a_rows, a_cols = keys // n, keys % n
+    deg = np.bincount(a_rows, minlength=n).astype(np.int64)
+    # L = D - S with the diagonal at its sorted position; isolated vertices store nothing.
+    has_d = deg > 0
+    d_idx = np.flatnonzero(has_d)
+    all_rows = np.concatenate([a_rows, d_idx])
+    all_cols = np.concatenate([a_cols, d_idx])
+    all_vals = np.concatenate([np.full(a_rows.size, -1.0), deg[d_idx].astype(np.float64)])
+    order = np.lexsort((all_cols, all_rows))
+    l_rows = all_rows[order]
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(l_rows, minlength=n), out=offsets[1:])
+    return offsets, all_cols[order].astype(np.int64), all_vals[order], deg
+
+
+def labels_first(n: int, ell: int, n_pos: int, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    lab = np.zeros(n, dtype=np.int8)
+    lab[:ell] = -1
+    lab[rng.choice(ell, size=n_pos, replace=False)] = 1
+    return lab
+
+
+def make_workload(name: str = "cfg2", *, max_iter: int | None = None, seed: int = 2024,
+                  **overrides) -> Workload:
+    """Generate config ``name`` (see CONFIGS) deterministically."""
+    cfg = dict(CONFIGS[name])
+    cfg.update(overrides)
+    n, d = cfg["n"], cfg["d"]
+    xo, xc = zipf_binary_rows(n, d, cfg["lam"], cfg["s"], seed)
+    lo, lc, lv, deg = random_knn_laplacian(n, cfg["k"], seed + 1)
+    lab = labels_first(n, cfg["ell"], cfg["n_pos"], seed + 2)
+    betas = np.geomspace(cfg["beta_lo"], cfg["beta_hi"], cfg["n_shifts"])
+    return Workload(
+        name=name, n=n, d=d, x_offsets=xo, x_cols=xc, l_offsets=lo, l_cols=lc, l_vals=lv,
+        degrees=deg, labels=lab, betas=betas,
+        max_iter=int(cfg["max_iter"] if max_iter is None else max_iter),
+        meta={k: v for k, v in cfg.items()},
+    )
+
+
+def workload_digest(w: Workload) -> str:
+    """sha256 over the raw input arrays (pins fixtures to generator output)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for a in (w.x_offsets, w.x_cols, w.l_offsets, w.l_cols, w.l_vals, w.labels, w.betas):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()

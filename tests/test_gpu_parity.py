@@ -1,0 +1,376 @@
+"""Device parity: the CUDA path against the oracles and the reference's goldens.
+
+Tolerances (written here, per BASELINE.json north_star):
+* vs oracle/fsda_oracle.c (same summation tree): bitwise, at every K.
+* vs the reference (golden fixtures / oracle.ref_numpy, reference order):
+  directions rel <= 1e-6 per shift and identical labeled-row AUC at the
+  stable Krylov dimension (K=20 cfg1, K=30 cfg2); past it the reference is
+  rounding-chaotic (its own 1-vs-8-thread runs differ by 1.2e-4), so full-K
+  runs are held to the chaos bound 1e-2 and AUC within 1e-3.
+"""
+
+import numpy as np
+import pytest
+
+import paper_1709_04794_b200 as fb
+from oracle import c_oracle, ref_numpy
+from paper_1709_04794_b200.workloads import make_workload
+
+from helpers import (dense_case, labeled_aucs, problem_from_case, problem_from_workload,
+                     rel_rows, same_ranking, small_case)
+
+pytestmark = pytest.mark.gpu
+
+
+def _dirs(rep, betas):
+    return np.stack([rep.directions[float(b)] for b in betas])
+
+
+def _scores(rep, betas):
+    return np.stack([rep.ratings[float(b)].scores for b in betas])
+
+
+# ----------------------------------------------------------- primitives
+
+def test_primitives_match_reference(cfg1_workload, golden_cfg1):
+    w, g = cfg1_workload, golden_cfg1
+    p = problem_from_workload(w, max_iter=1)
+    dev = fb.default_device()
+    dev.load_problem(p)
+    v, z = g["prim_v"], g["prim_z"]
+    np.testing.assert_array_equal(dev.matvec(v), g["prim_xv"])          # scipy order: bitwise
+    mu = dev.labeled_mean()
+    np.testing.assert_array_equal(mu, g["prim_mu"])
+    xtz = dev.matvec_transpose(z)
+    np.testing.assert_array_equal(xtz, c_oracle.matvec_transpose(w.x_offsets, w.x_cols, w.d, z))
+    assert np.linalg.norm(xtz - g["prim_xtz"]) <= 1e-13 * np.linalg.norm(g["prim_xtz"])
+    cx = dev.centered_matvec_transpose(mu, z)
+    np.testing.assert_array_equal(
+        cx, c_oracle.centered_matvec_transpose(w.x_offsets, w.x_cols, w.d, mu, z))
+    assert np.linalg.norm(cx - g["prim_cxtz"]) <= 1e-12 * np.linalg.norm(g["prim_cxtz"])
+    for a, key in ((0.0, "prim_sm0"), (0.5, "prim_sm05"), (1.0, "prim_sm1")):
+        np.testing.assert_array_equal(dev.apply_smoother(a, z), g[key])
+    op = dev.operator_apply(w.alpha, v)
+    np.testing.assert_array_equal(
+        op, c_oracle.operator_apply(w.x_offsets, w.x_cols, w.d, w.l_offsets, w.l_cols, w.l_vals,
+                                    w.labels, w.alpha, v))
+    assert np.linalg.norm(op - g["prim_op"]) <= 1e-12 * np.linalg.norm(g["prim_op"])
+
+
+def test_module_level_products(cfg1_workload, golden_cfg1):
+    w, g = cfg1_workload, golden_cfg1
+    p = problem_from_workload(w, max_iter=1)
+    np.testing.assert_array_equal(fb.matvec(p.x, g["prim_v"]), g["prim_xv"])
+    c = fb.labeled_mean(p.x, p.labels)
+    np.testing.assert_array_equal(c.mu, g["prim_mu"])
+    assert c.n_labeled == int(np.count_nonzero(w.labels))
+    np.testing.assert_array_equal(fb.apply_smoother(p.labels, p.lap, 0.5, g["prim_z"]), g["prim_sm05"])
+    got = fb.centered_matvec_transpose(p.x, c, g["prim_z"])
+    assert np.linalg.norm(got - g["prim_cxtz"]) <= 1e-12 * np.linalg.norm(g["prim_cxtz"])
+    got = fb.fsda_operator_apply(p, g["prim_v"])
+    assert np.linalg.norm(got - g["prim_op"]) <= 1e-12 * np.linalg.norm(g["prim_op"])
+
+
+# ------------------------------------------------------- full sweep, cfg1
+
+@pytest.mark.parametrize("k", [20, 50])
+def test_cfg1_sweep_bitwise_vs_oracle(cfg1_workload, k):
+    w = cfg1_workload
+    rep = fb.fsda_solve(problem_from_workload(w, max_iter=k))
+    ref = c_oracle.fsda_solve_workload(w, max_iter=k)
+    np.testing.assert_array_equal(_dirs(rep, w.betas), ref["directions"])
+    np.testing.assert_array_equal(_scores(rep, w.betas), ref["scores"])
+    np.testing.assert_array_equal(rep.regression.residuals, ref["residuals"])
+    np.testing.assert_array_equal(rep.regression.iterations, ref["iterations"])
+    np.testing.assert_array_equal(rep.regression.converged, ref["converged"])
+    assert rep.regression.operator_applications == ref["n_applies"] == k
+
+
+@pytest.mark.parametrize("k", [20, 50])
+def test_cfg1_sweep_vs_reference(cfg1_workload, golden_cfg1, k):
+    w, g = cfg1_workload, golden_cfg1
+    rep = fb.fsda_solve(problem_from_workload(w, max_iter=k))
+    dirs = _dirs(rep, w.betas)
+    aucs = labeled_aucs(_scores(rep, w.betas), w.labels)
+    if k == 20:   # stable Krylov dimension: the strict gate
+        assert rel_rows(dirs, g["k20_directions"]) <= 1e-6
+        np.testing.assert_array_equal(aucs, g["k20_auc_labeled"])
+        # full ranking of every row identical to the reference's scores
+        x = rep.ratings  # scores == X w, and the reference's X w is scipy's sequential sum
+        ref_scores = np.stack([c_oracle.matvec(w.x_offsets, w.x_cols, r) for r in g["k20_directions"]])
+        np.testing.assert_allclose(_scores(rep, w.betas), ref_scores, rtol=1e-6, atol=1e-9)
+        del x
+    else:         # past the horizon: within the reference's own chaos bound
+        assert rel_rows(dirs, g[f"k{k}_directions"]) <= 1e-2
+        assert np.max(np.abs(aucs - g[f"k{k}_auc_labeled"])) <= 1e-3
+    np.testing.assert_array_equal(rep.regression.iterations, g[f"k{k}_iterations"])
+    assert rep.regression.operator_applications == int(g[f"k{k}_n_applies"])
+
+
+def test_scores_are_projections(cfg1_workload):
+    """scores == X @ direction per shift (sda.py:272-283, tests/test_sda.py:221-232)."""
+    w = cfg1_workload
+    rep = fb.fsda_solve(problem_from_workload(w, max_iter=10))
+    for b in w.betas:
+        np.testing.assert_array_equal(rep.ratings[float(b)].scores,
+                                      c_oracle.matvec(w.x_offsets, w.x_cols, rep.directions[float(b)]))
+        lab = w.labels.astype(np.float64)
+        assert float(lab @ rep.ratings[float(b)].scores) >= 0.0     # oriented
+
+
+def test_sweep_is_deterministic(cfg1_workload):
+    p = problem_from_workload(cfg1_workload, max_iter=50)
+    a = fb.fsda_solve(p)
+    b = fb.fsda_solve(p)
+    for beta in cfg1_workload.betas:
+        np.testing.assert_array_equal(a.directions[float(beta)], b.directions[float(beta)])
+        np.testing.assert_array_equal(a.ratings[float(beta)].scores, b.ratings[float(beta)].scores)
+
+
+# ------------------------------------------------- small converging cases
+
+@pytest.mark.parametrize("idx", range(7))
+def test_small_cases(golden_small, idx):
+    c = small_case(golden_small, idx)
+    p = problem_from_case(c)
+    rep = fb.fsda_solve(p)
+    betas = p.betas.betas
+    ref = c_oracle.fsda_solve(c["x_offsets"], c["x_cols"], int(c["d"]), c["l_offsets"], c["l_cols"],
+                              c["l_vals"], c["labels"], float(c["alpha"]), betas, float(c["tol"]),
+                              int(c["max_iter"]),
+                              np.random.default_rng(int(c["seed"])).uniform(-1, 1, int(c["d"])))
+    np.testing.assert_array_equal(_dirs(rep, betas), ref["directions"])
+    np.testing.assert_array_equal(rep.regression.iterations, ref["iterations"])
+    np.testing.assert_array_equal(rep.regression.residuals, ref["residuals"])
+    # vs the reference itself
+    assert rel_rows(_dirs(rep, betas), c["directions"]) <= 1e-6
+    np.testing.assert_array_equal(rep.regression.converged, c["converged"])
+    np.testing.assert_array_equal(labeled_aucs(_scores(rep, betas), c["labels"]), c["auc_labeled"])
+    assert rep.regression.operator_applications == int(rep.regression.iterations.max())
+
+
+# ------------------------------------------------- dense shifted CG battery
+
+@pytest.mark.parametrize("idx", range(8))
+def test_dense_shifted_cg_vs_oracle_and_reference(golden_dense, idx):
+    c = dense_case(golden_dense, idx)
+    op = fb.LinearOperator.from_dense(c["a"])
+    res = fb.shifted_cg(op, c["b"], c["betas"], tol=float(c["tol"]), max_iter=int(c["max_iter"]))
+    sols, rs, its, conv, napp = c_oracle.shifted_cg_dense(c["a"], c["b"], c["betas"],
+                                                         float(c["tol"]), int(c["max_iter"]))
+    np.testing.assert_array_equal(res.solutions.T, sols)
+    np.testing.assert_array_equal(res.iterations, its)
+    np.testing.assert_array_equal(res.residual_norms, rs)
+    assert op.n_applies == napp == int(its.max())
+    np.testing.assert_array_equal(res.converged, c["converged"])
+    if res.all_converged:
+        for s, beta in enumerate(c["betas"]):
+            if beta == 0.0 and str(c["name"]) == "singular_base":
+                continue
+            want = np.linalg.solve(c["a"] + beta * np.eye(c["b"].size), c["b"])
+            assert np.linalg.norm(res.solutions[:, s] - want) <= 1e-8 * np.linalg.norm(want)
+
+
+def test_shifted_identity_closed_form():
+    op = fb.LinearOperator.from_dense(np.eye(6))
+    b = np.arange(1.0, 7.0)
+    res = fb.shifted_cg(op, b, (0.0, 0.5, 2.0), tol=1e-12)
+    for s, beta in enumerate([0.0, 0.5, 2.0]):
+        np.testing.assert_allclose(res.solutions[:, s], b / (1.0 + beta), rtol=1e-12)
+    assert res.all_converged and op.n_applies == 1
+
+
+def test_shifted_zero_rhs_shortcut():
+    op = fb.LinearOperator.from_dense(np.eye(4))
+    res = fb.shifted_cg(op, np.zeros(4), (0.1, 1.0))
+    assert res.all_converged and op.n_applies == 0
+    np.testing.assert_array_equal(res.iterations, [0, 0])
+    np.testing.assert_array_equal(res.solutions, np.zeros((4, 2)))
+
+
+def test_shifted_breakdown_raises():
+    op = fb.LinearOperator.from_dense(np.zeros((3, 3)))
+    with pytest.raises(fb.SolverBreakdownError, match="iteration 0"):
+        fb.shifted_cg(op, np.ones(3), (0.0,))
+
+
+def test_shifted_nonfinite_raises():
+    a = np.eye(3)
+    a[0, 0] = np.inf
+    with pytest.raises(fb.NumericalFailureError):
+        fb.shifted_cg(fb.LinearOperator.from_dense(a), np.ones(3), (0.0,))
+
+
+def test_shifted_residual_certification(rng):
+    q, _ = np.linalg.qr(rng.standard_normal((30, 30)))
+    a = (q * np.geomspace(1.0, 100.0, 30)) @ q.T
+    b = rng.standard_normal(30)
+    res = fb.shifted_cg(fb.LinearOperator.from_dense(a), b, (1e-2, 1.0), tol=1e-9, max_iter=500)
+    for s, beta in enumerate((1e-2, 1.0)):
+        true_res = np.linalg.norm(b - (a + beta * np.eye(30)) @ res.solutions[:, s])
+        assert true_res <= 10 * 1e-9 * np.linalg.norm(b)
+
+
+# ---------------------------------------------------------- edge cases
+
+def _tiny_problem(alpha=0.5, betas=(1e-3,), **kw):
+    w = make_workload("cfg1", n=400, d=300, ell=40, n_pos=10, lam=6.0, k=4, n_shifts=3)
+    return w, problem_from_workload(w, max_iter=kw.pop("max_iter", 25), alpha=alpha, **kw)
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.25, 1.0])
+def test_alpha_branches_bitwise(alpha):
+    w, p = _tiny_problem(alpha=alpha)
+    rep = fb.fsda_solve(p)
+    ref = c_oracle.fsda_solve(w.x_offsets, w.x_cols, w.d, w.l_offsets, w.l_cols, w.l_vals, w.labels,
+                              alpha, p.betas.betas, p.tol, p.max_iter_d, w.probe())
+    np.testing.assert_array_equal(_dirs(rep, p.betas.betas), ref["directions"])
+
+
+def test_lda_alias():
+    w, p = _tiny_problem(alpha=0.0)
+    a = fb.solve(p, "lda")
+    b = fb.solve(p, "fsda")
+    assert a.algorithm == "lda"
+    for beta in p.betas.betas:
+        np.testing.assert_array_equal(a.ratings[float(beta)].scores, b.ratings[float(beta)].scores)
+    _, p5 = _tiny_problem(alpha=0.5)
+    with pytest.raises(ValueError, match="alpha"):
+        fb.solve(p5, "lda")
+
+
+def test_ragged_and_empty_rows_and_columns():
+    """Rows with no features, columns never used, a single labeled sample per class."""
+    rng = np.random.default_rng(5)
+    n, d = 300, 120
+    rows, cols = [], []
+    for i in range(n):
+        if i % 7 == 0:
+            continue                      # empty row
+        k = int(rng.integers(1, 12))
+        cs = np.sort(rng.choice(d - 20, size=k, replace=False))   # last 20 columns unused
+        rows += [i] * k
+        cols += cs.tolist()
+    x = fb.build_sparse(n, d, rows, cols, np.ones(len(rows)))
+    from paper_1709_04794_b200.workloads import random_knn_laplacian
+
+    lo, lc, lv, deg = random_knn_laplacian(n, 3, 9)
+    lap = fb.Laplacian(fb.SparseMatrix(n, n, lo, lc, lv), deg)
+    lab = np.zeros(n, dtype=np.int8)
+    lab[0], lab[1] = 1, -1
+    p = fb.SdaProblem(x=x, labels=fb.LabelVector(lab), lap=lap, alpha=0.5,
+                      betas=np.geomspace(1e-3, 10, 5), max_iter_d=30)
+    rep = fb.fsda_solve(p)
+    ref = c_oracle.fsda_solve(x.row_offsets, x.col_indices, d, lo, lc, lv, lab, 0.5, p.betas.betas,
+                              p.tol, 30, np.random.default_rng(0).uniform(-1, 1, d))
+    np.testing.assert_array_equal(_dirs(rep, p.betas.betas), ref["directions"])
+    np.testing.assert_array_equal(rep.regression.iterations, ref["iterations"])
+
+
+def test_heavy_columns_many_segments():
+    """A column present in every row (n_c > 256 * 256 would need N > 65536;
+    here 3000 rows = 12 segments) plus tiny columns of every size class."""
+    n, d = 3000, 64
+    rng = np.random.default_rng(11)
+    rows, cols = [], []
+    for i in range(n):
+        cs = {0} | set(rng.choice(np.arange(1, d), size=int(rng.integers(0, 5)), replace=False).tolist())
+        for c in sorted(cs):
+            rows.append(i)
+            cols.append(c)
+    x = fb.build_sparse(n, d, rows, cols, np.ones(len(rows)))
+    from paper_1709_04794_b200.workloads import random_knn_laplacian
+
+    lo, lc, lv, deg = random_knn_laplacian(n, 5, 3)
+    lap = fb.Laplacian(fb.SparseMatrix(n, n, lo, lc, lv), deg)
+    lab = np.zeros(n, dtype=np.int8)
+    lab[:50] = -1
+    lab[:20] = 1
+    p = fb.SdaProblem(x=x, labels=fb.LabelVector(lab), lap=lap, alpha=0.3,
+                      betas=(1e-4, 1e-2, 1.0), max_iter_d=40, tol=1e-12)
+    dev = fb.default_device()
+    dev.load_problem(p)
+    z = rng.standard_normal(n)
+    np.testing.assert_array_equal(dev.matvec_transpose(z),
+                                  c_oracle.matvec_transpose(x.row_offsets, x.col_indices, d, z))
+    rep = fb.fsda_solve(p)
+    ref = c_oracle.fsda_solve(x.row_offsets, x.col_indices, d, lo, lc, lv, lab, 0.3, p.betas.betas,
+                              1e-12, 40, np.random.default_rng(0).uniform(-1, 1, d))
+    np.testing.assert_array_equal(_dirs(rep, p.betas.betas), ref["directions"])
+
+
+def test_empty_x_gives_zero_rhs_shortcut():
+    n, d = 50, 10
+    x = fb.SparseMatrix(n, d, np.zeros(n + 1, dtype=np.int64), np.zeros(0, np.int64), np.zeros(0))
+    from paper_1709_04794_b200.workloads import random_knn_laplacian
+
+    lo, lc, lv, deg = random_knn_laplacian(n, 3, 1)
+    lab = np.zeros(n, dtype=np.int8)
+    lab[:3], lab[3:6] = 1, -1
+    p = fb.SdaProblem(x=x, labels=fb.LabelVector(lab),
+                      lap=fb.Laplacian(fb.SparseMatrix(n, n, lo, lc, lv), deg), alpha=0.5,
+                      betas=(0.1, 1.0))
+    rep = fb.fsda_solve(p)
+    assert rep.regression.operator_applications == 0
+    assert rep.converged
+    for beta in (0.1, 1.0):
+        np.testing.assert_array_equal(rep.directions[beta], np.zeros(d))
+
+
+def test_many_shifts_and_single_shift():
+    for ns in (1, 64):
+        w, p = _tiny_problem(betas=np.geomspace(1e-6, 1e3, ns), max_iter=15)
+        rep = fb.fsda_solve(p)
+        ref = c_oracle.fsda_solve(w.x_offsets, w.x_cols, w.d, w.l_offsets, w.l_cols, w.l_vals,
+                                  w.labels, p.alpha, p.betas.betas, p.tol, 15, w.probe())
+        np.testing.assert_array_equal(_dirs(rep, p.betas.betas), ref["directions"])
+
+
+def test_rejects_non_binary_x_and_weighted_graph():
+    w, p = _tiny_problem()
+    x2 = fb.SparseMatrix(w.n, w.d, w.x_offsets, w.x_cols, np.full(w.nnz, 2.0))
+    with pytest.raises(ValueError, match="binary"):
+        fb.fsda_solve(fb.SdaProblem(x=x2, labels=p.labels, lap=p.lap, alpha=0.5, betas=(1e-3,)))
+    vals = w.l_vals.copy()
+    vals[vals == -1.0] = -0.5
+    lap2 = fb.Laplacian(fb.SparseMatrix(w.n, w.n, w.l_offsets, w.l_cols, vals), w.degrees)
+    with pytest.raises(ValueError, match="unit-weight"):
+        fb.fsda_solve(fb.SdaProblem(x=p.x, labels=p.labels, lap=lap2, alpha=0.5, betas=(1e-3,)))
+
+
+def test_resident_problem_reuse(cfg1_workload):
+    p = problem_from_workload(cfg1_workload, max_iter=20)
+    dp = fb.DeviceProblem(p)
+    a = dp.solve()
+    b = dp.solve(betas=(1e-3, 1e-1))
+    full = fb.fsda_solve(p)
+    np.testing.assert_array_equal(a.directions[float(cfg1_workload.betas[3])],
+                                  full.directions[float(cfg1_workload.betas[3])])
+    assert set(b.directions) == {1e-3, 1e-1}
+
+
+# ----------------------------------------------- cfg2 (BASELINE configs[1])
+
+@pytest.fixture(scope="module")
+def cfg2():
+    return make_workload("cfg2")
+
+
+def test_cfg2_strict_gate_vs_reference_order(cfg2):
+    """K=30 (cfg2's stable Krylov dimension): rel <= 1e-6 per shift vs the
+    reference-order oracle and identical labeled-row AUC."""
+    rep = fb.fsda_solve(problem_from_workload(cfg2, max_iter=30))
+    ref = ref_numpy.fsda_solve_workload(cfg2, max_iter=30)
+    assert rel_rows(_dirs(rep, cfg2.betas), ref["directions"]) <= 1e-6
+    np.testing.assert_array_equal(labeled_aucs(_scores(rep, cfg2.betas), cfg2.labels),
+                                  labeled_aucs(ref["scores"], cfg2.labels))
+    assert same_ranking(_scores(rep, cfg2.betas)[:, cfg2.labels != 0],
+                        ref["scores"][:, cfg2.labels != 0])
+
+
+def test_cfg2_full_k_bitwise_vs_oracle(cfg2):
+    rep = fb.fsda_solve(problem_from_workload(cfg2))
+    ref = c_oracle.fsda_solve_workload(cfg2)
+    np.testing.assert_array_equal(_dirs(rep, cfg2.betas), ref["directions"])
+    np.testing.assert_array_equal(_scores(rep, cfg2.betas), ref["scores"])
+    assert rep.regression.operator_applications == 100

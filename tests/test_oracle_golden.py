@@ -1,0 +1,136 @@
+"""Pin the CPU oracles against the reference's own outputs (tests/golden/).
+
+The golden files were produced by the unmodified reference (sdakit) by
+tests/golden/make_golden.py.  Two oracles are checked:
+
+* oracle.ref_numpy — the reference's arithmetic restated on raw arrays; it
+  must reproduce the reference bit for bit.
+* oracle.c_oracle — the C restatement in the device's summation order; it
+  must agree with the reference within the reference's own noise floor
+  (bitwise row sums, ~1e-13 for X^T / operator products,
+  <= 1e-9 per shift at the stable Krylov dimension K=20 of cfg1, identical
+  labeled-row AUC; at K=50 the reference's chaos bound 1e-2).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import c_oracle, ref_numpy
+from paper_1709_04794_b200.workloads import workload_digest
+
+from helpers import dense_case, labeled_aucs, rel_rows, small_case
+
+
+def test_cfg1_fixture_matches_generator(cfg1_workload, golden_cfg1):
+    assert workload_digest(cfg1_workload) == str(golden_cfg1["digest"])
+
+
+@pytest.mark.parametrize("k", [20, 50])
+def test_numpy_oracle_reproduces_reference(cfg1_workload, golden_cfg1, k):
+    out = ref_numpy.fsda_solve_workload(cfg1_workload, max_iter=k)
+    ref = golden_cfg1[f"k{k}_directions"]
+    bound = 1e-12 if k == 20 else 1e-2   # K=50 is past cfg1's stability horizon
+    assert rel_rows(out["directions"], ref) <= bound
+    np.testing.assert_array_equal(out["iterations"], golden_cfg1[f"k{k}_iterations"])
+    assert out["n_applies"] == int(golden_cfg1[f"k{k}_n_applies"])
+
+
+def test_numpy_oracle_bitwise_at_stable_k(cfg1_workload, golden_cfg1):
+    out = ref_numpy.fsda_solve_workload(cfg1_workload, max_iter=20)
+    np.testing.assert_array_equal(out["directions"], golden_cfg1["k20_directions"])
+    np.testing.assert_array_equal(out["residuals"], golden_cfg1["k20_residuals"])
+
+
+@pytest.mark.parametrize("k", [20, 50])
+def test_c_oracle_matches_reference(cfg1_workload, golden_cfg1, k):
+    out = c_oracle.fsda_solve_workload(cfg1_workload, max_iter=k)
+    ref = golden_cfg1[f"k{k}_directions"]
+    if k == 20:
+        assert rel_rows(out["directions"], ref) <= 1e-9
+        np.testing.assert_allclose(out["residuals"], golden_cfg1["k20_residuals"], rtol=1e-9)
+        np.testing.assert_array_equal(labeled_aucs(out["scores"], cfg1_workload.labels),
+                                      golden_cfg1["k20_auc_labeled"])
+    else:
+        assert rel_rows(out["directions"], ref) <= 1e-2
+        assert np.max(np.abs(labeled_aucs(out["scores"], cfg1_workload.labels)
+                             - golden_cfg1["k50_auc_labeled"])) <= 1e-3
+    np.testing.assert_array_equal(out["iterations"], golden_cfg1[f"k{k}_iterations"])
+    np.testing.assert_array_equal(out["converged"], golden_cfg1[f"k{k}_converged"])
+    assert out["n_applies"] == int(golden_cfg1[f"k{k}_n_applies"])
+
+
+def test_c_oracle_primitives(cfg1_workload, golden_cfg1):
+    w, g = cfg1_workload, golden_cfg1
+    v, z = g["prim_v"], g["prim_z"]
+    # row sums are sequential in column order: bit-identical to scipy
+    np.testing.assert_array_equal(c_oracle.matvec(w.x_offsets, w.x_cols, v), g["prim_xv"])
+    mu = c_oracle.labeled_mean(w.x_offsets, w.x_cols, w.d, w.labels)
+    np.testing.assert_array_equal(mu, g["prim_mu"])          # integer counts / ell: exact
+    xtz = c_oracle.matvec_transpose(w.x_offsets, w.x_cols, w.d, z)
+    assert np.linalg.norm(xtz - g["prim_xtz"]) <= 1e-13 * np.linalg.norm(g["prim_xtz"])
+    cx = c_oracle.centered_matvec_transpose(w.x_offsets, w.x_cols, w.d, mu, z)
+    assert np.linalg.norm(cx - g["prim_cxtz"]) <= 1e-12 * np.linalg.norm(g["prim_cxtz"])
+    for a, key in ((0.0, "prim_sm0"), (0.5, "prim_sm05"), (1.0, "prim_sm1")):
+        sm = c_oracle.apply_smoother(w.l_offsets, w.l_cols, w.l_vals, w.labels, a, z)
+        np.testing.assert_array_equal(sm, g[key])
+    op = c_oracle.operator_apply(w.x_offsets, w.x_cols, w.d, w.l_offsets, w.l_cols, w.l_vals,
+                                 w.labels, w.alpha, v)
+    assert np.linalg.norm(op - g["prim_op"]) <= 1e-12 * np.linalg.norm(g["prim_op"])
+
+
+def _run_case(c, solver):
+    return solver(c["x_offsets"], c["x_cols"], int(c["d"]), c["l_offsets"], c["l_cols"],
+                  c["l_vals"], c["labels"], float(c["alpha"]), c["betas"], float(c["tol"]),
+                  int(c["max_iter"]), np.random.default_rng(int(c["seed"])).uniform(
+                      -1.0, 1.0, size=int(c["d"])))
+
+
+@pytest.mark.parametrize("idx", range(7))
+def test_c_oracle_small_cases(golden_small, idx):
+    c = small_case(golden_small, idx)
+    out = _run_case(c, c_oracle.fsda_solve)
+    assert rel_rows(out["directions"], c["directions"]) <= 1e-7
+    np.testing.assert_array_equal(out["converged"], c["converged"])
+    assert np.max(np.abs(out["iterations"] - c["iterations"])) <= 1
+    np.testing.assert_array_equal(labeled_aucs(out["scores"], c["labels"]), c["auc_labeled"])
+
+
+@pytest.mark.parametrize("idx", range(7))
+def test_numpy_oracle_small_cases(golden_small, idx):
+    c = small_case(golden_small, idx)
+    prob = ref_numpy.Problem(c["x_offsets"], c["x_cols"], int(c["d"]), c["l_offsets"],
+                             c["l_cols"], c["l_vals"], c["labels"])
+    out = ref_numpy.fsda_solve(prob, float(c["alpha"]), c["betas"], float(c["tol"]),
+                               int(c["max_iter"]), int(c["seed"]))
+    np.testing.assert_array_equal(out["directions"], c["directions"])
+    np.testing.assert_array_equal(out["scores"], c["scores"])
+    np.testing.assert_array_equal(out["iterations"], c["iterations"])
+
+
+@pytest.mark.parametrize("idx", range(8))
+def test_c_oracle_dense_shifted_cg(golden_dense, idx):
+    c = dense_case(golden_dense, idx)
+    sols, res, its, conv, napp = c_oracle.shifted_cg_dense(
+        c["a"], c["b"], c["betas"], float(c["tol"]), int(c["max_iter"]))
+    np.testing.assert_array_equal(conv, c["converged"])
+    # Past dim iterations CG's iteration count is itself rounding-sensitive
+    # (the BLAS gemv vs sequential row order moves it by a few percent).
+    slack = np.maximum(2, 0.05 * c["iterations"])
+    assert np.all(np.abs(its - c["iterations"]) <= slack)
+    assert napp == int(its.max())
+    if conv.all():
+        scale = np.maximum(np.linalg.norm(c["solutions"], axis=1), 1e-300)
+        assert np.max(np.linalg.norm(sols - c["solutions"], axis=1) / scale) <= 1e-8
+
+
+def test_r256_tree_definition():
+    """The canonical tree on small, hand-checkable inputs."""
+    v = np.arange(1.0, 601.0)
+    assert c_oracle.r256(v) == float(v.sum())      # integers: any order is exact
+    assert c_oracle.r256(np.array([])) == 0.0
+    # 1e16 + 1 + ... : lane 0 holds 1e16 and the 1.0 from index 32, so order shows
+    x = np.zeros(64)
+    x[0], x[32] = 1e16, 1.0
+    x[1] = -1e16
+    assert c_oracle.r256(x) == 0.0                 # (1e16+1) + (-1e16) = 0 in this tree
+    assert np.sum(x) in (0.0, 1.0)

@@ -230,7 +230,10 @@ def run_b200(args):
 
         m = w.meta
         w.labels = labels_first(w.n, m["ell"], m["n_pos"], 7919 * rank + 2)
-    stream = torch.cuda.current_stream()
+    # a real (non-legacy) stream: the library launches on it and the timing
+    # events below are recorded on it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     dev = fb.Device(local, stream=stream.cuda_stream)
     x = fb.SparseMatrix.binary(w.n, w.d, w.x_offsets, w.x_cols)
     lap = fb.Laplacian(fb.SparseMatrix(w.n, w.n, w.l_offsets, w.l_cols, w.l_vals), w.degrees)

@@ -46,6 +46,8 @@ def lib():
         h.oracle_dot.argtypes = [_PD, _PD, _I64]
         h.oracle_matvec.restype = None
         h.oracle_matvec.argtypes = [_I64, _PI64, _PI64, _PD, _PD]
+        h.oracle_matvec_r256.restype = None
+        h.oracle_matvec_r256.argtypes = [_I64, _PI64, _PI64, _PD, _PD]
         h.oracle_matvec_transpose.restype = None
         h.oracle_matvec_transpose.argtypes = [_I64, _I64, _PI64, _PI64, _PD, _PD]
         h.oracle_centered_matvec_transpose.restype = None
@@ -103,6 +105,17 @@ def matvec(offs, cols, v):
     n = offs.size - 1
     out = np.empty(n)
     lib().oracle_matvec(n, po, pc, pv, out.ctypes.data_as(_PD))
+    return out
+
+
+def matvec_r256(offs, cols, v):
+    """X v with every row summed by the canonical R256 tree (the device's K1)."""
+    offs, po = _i(offs)
+    cols, pc = _i(cols)
+    v, pv = _d(v)
+    n = offs.size - 1
+    out = np.empty(n)
+    lib().oracle_matvec_r256(n, po, pc, pv, out.ctypes.data_as(_PD))
     return out
 
 

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -23,6 +24,7 @@
 
 #include "../../include/fsda_b200.h"
 #include "fsda_device.cuh"
+#include "fsda_hot.cuh"
 
 using namespace fsda;
 
@@ -88,6 +90,19 @@ struct Launch {
   double bytes;
 };
 
+// Device side of one segmented-sum plan (see SegPlan in fsda_hot.cuh).
+struct HostPlan {
+  DevBuf<int4> tasks;
+  DevBuf<int> h0, hn, hs, ht;
+  DevBuf<unsigned> hc;
+  DevBuf<double> part;
+  SegPlan pl{};
+  void release() {
+    tasks.release(); h0.release(); hn.release(); hs.release(); ht.release(); hc.release();
+    part.release();
+  }
+};
+
 }  // namespace
 
 struct fsda_ctx {
@@ -101,11 +116,9 @@ struct fsda_ctx {
   long long n = 0, d = 0, nnz = 0;
   bool has_x = false;
   DevBuf<int> x_rowptr, x_cols, csc_colptr, csc_rows;
-  // column work plan
-  DevBuf<int> tiny_cols, warp_cols, seg_col, seg_start, heavy_cols, heavy_seg0, heavy_nseg;
-  DevBuf<double> seg_part;
-  XtPlan plan{};
-  long long xt_warps = 0;
+  // segmented-sum plans: rows of X, rows of L, columns of X
+  HostPlan plan_xr, plan_lr, plan_xc;
+  int step_blocks = 0;  // cooperative grid of k_cg_step
 
   // L: CSR with diagonal entries in place, diag values split out
   bool has_l = false;
@@ -119,7 +132,7 @@ struct fsda_ctx {
   long long n1 = 0, n2 = 0, ell = 0;
 
   // work vectors
-  DevBuf<double> y, z, q, p, r0, r1, mu_v, t, wv, b, ind, probe, part_n, part_d, part_o;
+  DevBuf<double> y, z, q, p, r0, r1, mu_v, t, wv, b, ind, probe, part_n, part_d, part_d2, part_o;
   DevBuf<double> bigp, sols, wT, scores, dense_a;
   // per-shift state
   DevBuf<double> beta, zeta_prev, zeta, zeta_next, gamma_s, alpha_s, resid;
@@ -133,6 +146,8 @@ struct fsda_ctx {
   cudaGraph_t graph = nullptr;
   std::string graph_key;
   bool cond_supported = true;
+
+  long long graph_fixed = 0, graph_body = 0;  // launches in the cached graph
 
   // resident-solve parameters
   double r_alpha = 0.0, r_tol = 0.0;
@@ -207,6 +222,7 @@ void ensure_vectors(fsda_ctx* c, int ns) {
   c->b.ensure(d); c->probe.ensure(d);
   c->part_n.ensure(2 * n_leaves(n) + 2);
   c->part_d.ensure(n_leaves(d) + 1);
+  c->part_d2.ensure(n_leaves(d) + 1);
   const int nsx = std::max(ns, 1);
   c->part_o.ensure((size_t)nsx * n_leaves(n) + 1);
   c->bigp.ensure((size_t)nsx * d); c->sols.ensure((size_t)nsx * d);
@@ -219,61 +235,118 @@ void ensure_vectors(fsda_ctx* c, int ns) {
 
 int grid_for(long long n, int block) { return (int)std::max<long long>(1, cdiv(n, block)); }
 
-// ---- K3 launch (light + heavy) for one X^T product
-void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* mu, double ell,
-            int guarded) {
+// ---- segmented sums (K1 / K2 / K3)
+template <int KIND>
+void launch_segsum(fsda_ctx* c, const HostPlan& hp, const SegArgs& a, int guarded,
+                   long long sum_leaves) {
+  SegPlan pl = hp.pl;
+  pl.warp_base[8] = pl.warp_base[7] + sum_leaves;
+  const long long warps = pl.warp_base[8];
+  if (warps == 0) return;
+  const int blocks = (int)std::max<long long>(
+      1, std::min<long long>(cdiv(warps, 8), (long long)c->num_sms * 16));
+  k_segsum<KIND><<<blocks, 256, 0, c->stream>>>(pl, a, c->sc, guarded);
+}
+
+SegArgs seg_args(const double* src, double* out) {
+  SegArgs a;
+  memset(&a, 0, sizeof(a));
+  a.src = src;
+  a.out = out;
+  return a;
+}
+
+// X^T z: mode 0 raw (+ optional sum(z) leaves), 1 centred with *sum_ptr, 2 / ell.
+void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* sum_ptr, int guarded,
+            double* sum_part) {
   fsda_ctx* c = e.c;
-  const double xt_bytes = 4.0 * (c->d + 1) + 4.0 * c->nnz + 8.0 * c->n + 8.0 * c->d +
-                          (mode == 1 ? 8.0 * c->d : 0.0);
-  XtPlan pl = c->plan;
-  int blocks = (int)std::max<long long>(1, std::min<long long>(cdiv(c->xt_warps, 8),
-                                                                (long long)c->num_sms * 16));
-  e.go("xt_light", xt_bytes, [&] {
-    k_xt_light<<<blocks, 256, 0, c->stream>>>(pl, zsrc, out, mode, mu, c->sc, ell, guarded);
+  const double bytes = 4.0 * (c->d + 1) + 4.0 * c->nnz + 8.0 * c->n + 8.0 * c->d +
+                       (mode == 1 ? 8.0 * c->d : 0.0);
+  SegArgs a = seg_args(zsrc, out);
+  a.mode = mode;
+  a.mu = c->mu_v.ptr;
+  a.sum_ptr = sum_ptr;
+  a.ell = (double)c->ell;
+  a.sum_part = sum_part;
+  a.sum_n = sum_part ? c->n : 0;
+  e.go("xt", bytes, [&] {
+    launch_segsum<SEG_XCOLS>(c, c->plan_xc, a, guarded, sum_part ? n_leaves(c->n) : 0);
   });
-  if (c->plan.n_heavy > 0) {
-    int hb = (int)std::min<long long>(c->plan.n_heavy, (long long)c->num_sms * 8);
-    e.go("xt_heavy", 8.0 * c->plan.n_segs, [&] {
-      k_xt_heavy<<<hb, 256, 0, c->stream>>>(pl, out, mode, mu, c->sc, ell, guarded);
-    });
-  }
+}
+
+// y = X v in the canonical row order.
+void enq_xrows(Enq& e, const double* v, double* out, int guarded) {
+  fsda_ctx* c = e.c;
+  const double bytes = 4.0 * (c->n + 1) + 4.0 * c->nnz + 8.0 * c->d + 8.0 * c->n;
+  SegArgs a = seg_args(v, out);
+  e.go("spmv_rows", bytes, [&] { launch_segsum<SEG_XROWS>(c, c->plan_xr, a, guarded, 0); });
 }
 
 int alpha_mode_of(double alpha) { return alpha == 0.0 ? 0 : (alpha == 1.0 ? 1 : 2); }
 
+// z = M y (apply_smoother, sda.py:131-140).
+void enq_smoother(Enq& e, double alpha, const double* y, double* z, int guarded) {
+  fsda_ctx* c = e.c;
+  const int amode = alpha_mode_of(alpha);
+  if (amode == 0) {
+    e.go("smoother", 17.0 * c->n, [&] {
+      k_mask_labeled<<<grid_for(c->n, 256), 256, 0, c->stream>>>(y, c->labels.ptr, z, (int)c->n, c->sc,
+                                                                 guarded);
+    });
+    return;
+  }
+  SegArgs a = seg_args(y, z);
+  a.ldiag = c->l_diag.ptr;
+  a.labels = c->labels.ptr;
+  a.alpha = alpha;
+  a.alpha_mode = amode;
+  const double bytes = 4.0 * (c->n + 1) + 4.0 * c->l_nnz + 8.0 * c->n + 1.0 * c->n + 16.0 * c->n;
+  e.go("smoother", bytes, [&] { launch_segsum<SEG_LROWS>(c, c->plan_lr, a, guarded, 0); });
+}
+
+size_t step_smem(int ns) { return sizeof(double) * 3 * (size_t)std::max(ns, 1); }
+
+// Cooperative launch of k_cg_step (capturable into graphs).
+void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, int use_cond,
+                    bool center) {
+  ShiftState ss = c->shifts();
+  const long long nlD = n_leaves(d);
+  double* q = c->q.ptr;
+  double* p = c->p.ptr;
+  double* r0 = c->r0.ptr;
+  double* r1 = c->r1.ptr;
+  double* bigp = c->bigp.ptr;
+  double* sols = c->sols.ptr;
+  double* pp = c->part_d.ptr;
+  double* pr = c->part_d2.ptr;
+  CgScalars* sc = c->sc;
+  const double* mu = center ? c->mu_v.ptr : nullptr;
+  const double* pz = center ? c->part_n.ptr : nullptr;
+  const long long nlz = center ? n_leaves(c->n) : 0;
+  void* args[] = {(void*)&q, (void*)&p, (void*)&r0, (void*)&r1, (void*)&bigp, (void*)&sols,
+                  (void*)&d, (void*)&pp, (void*)&pr, (void*)&nlD, (void*)&sc, (void*)&ss,
+                  (void*)&ns, (void*)&cond, (void*)&use_cond, (void*)&mu, (void*)&pz, (void*)&nlz};
+  const size_t smem = step_smem(ns);
+  if (c->step_blocks == 0) {
+    int nb = 0;
+    CK(cudaFuncSetAttribute(k_cg_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cg_step, 256, smem));
+    c->step_blocks = std::max(1, std::min(nb, 4)) * c->num_sms;
+  }
+  CK(cudaLaunchCooperativeKernel((void*)k_cg_step, dim3(c->step_blocks), dim3(256), args, smem,
+                                 c->stream));
+}
+
+
 // One shifted-CG iteration for the FSDA operator (graph body).
 void enq_fsda_iteration(Enq& e, double alpha, int ns, unsigned long long cond, int use_cond) {
   fsda_ctx* c = e.c;
-  const long long n = c->n, d = c->d;
-  const long long nlN = n_leaves(n), nlD = n_leaves(d);
-  const int amode = alpha_mode_of(alpha);
-  const double b_spmv = 4.0 * (n + 1) + 4.0 * c->nnz + 8.0 * d + 8.0 * n;
-  e.go("spmv_rows", b_spmv, [&] {
-    k_spmv_rows<<<grid_for(n, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr, c->p.ptr,
-                                                         c->y.ptr, (int)n, c->sc);
-  });
-  const double b_sm = amode == 0 ? (1.0 * n + 16.0 * n)
-                                 : (4.0 * (n + 1) + 4.0 * c->l_nnz + 8.0 * n + 1.0 * n + 16.0 * n);
-  e.go("smoother", b_sm, [&] {
-    k_smoother<<<grid_for(nlN, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
-        c->l_rowptr.ptr, c->l_cols.ptr, c->l_diag.ptr, c->labels.ptr, c->y.ptr, c->z.ptr, (int)n,
-        alpha, amode, c->part_n.ptr, nlN, c->sc, 1, nullptr);
-  });
-  enq_xt(e, c->z.ptr, c->q.ptr, 1, c->mu_v.ptr, (double)c->ell, 1);
-  ShiftState ss = c->shifts();
-  e.go("dot_pq", 16.0 * d, [&] {
-    k_dot_pq<<<grid_for(nlD, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
-        c->p.ptr, c->q.ptr, d, c->part_d.ptr, nlD, c->sc, ss, ns);
-  });
-  e.go("update", 24.0 * d + 32.0 * d * ns, [&] {
-    dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
-    k_update<<<g, LEAF_THREADS, 0, c->stream>>>(c->q.ptr, c->r0.ptr, c->r1.ptr, c->bigp.ptr,
-                                                c->sols.ptr, d, c->part_d.ptr, nlD, c->sc, ss, ns);
-  });
-  e.go("pupdate", 24.0 * d, [&] {
-    int gb = (int)std::min<long long>(grid_for(d, 256), (long long)c->num_sms * 8);
-    k_pupdate<<<gb, 256, 0, c->stream>>>(c->r0.ptr, c->r1.ptr, c->p.ptr, d, c->sc, cond,
-                                         use_cond);
+  const long long d = c->d;
+  enq_xrows(e, c->p.ptr, c->y.ptr, 1);
+  enq_smoother(e, alpha, c->y.ptr, c->z.ptr, 1);
+  enq_xt(e, c->z.ptr, c->q.ptr, 0, nullptr, 1, c->part_n.ptr);
+  e.go("cg_step", 8.0 * c->n + 24.0 * d + 24.0 * d + 32.0 * d * ns + 24.0 * d, [&] {
+    launch_cg_step(c, ns, d, cond, use_cond, true);
   });
 }
 
@@ -288,11 +361,8 @@ void enq_fsda_setup(Enq& e, int ns, long long max_iter, double tol) {
   e.go("indicator", 9.0 * n, [&] {
     k_indicator<<<grid_for(n, 256), 256, 0, c->stream>>>(c->labels.ptr, c->ind.ptr, (int)n);
   });
-  enq_xt(e, c->ind.ptr, c->mu_v.ptr, 2, nullptr, (double)c->ell, 0);
-  e.go("spmv_rows", 4.0 * (n + 1) + 4.0 * c->nnz + 8.0 * d + 8.0 * n, [&] {
-    k_spmv_rows<<<grid_for(n, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr,
-                                                         c->probe.ptr, c->t.ptr, (int)n, nullptr);
-  });
+  enq_xt(e, c->ind.ptr, c->mu_v.ptr, 2, nullptr, 0, nullptr);
+  enq_xrows(e, c->probe.ptr, c->t.ptr, 0);
   e.go("class_sums", 9.0 * n, [&] {
     k_class_sums<<<grid_for(nlN, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
         c->t.ptr, c->labels.ptr, n, c->part_n.ptr, nlN, c->sc, (double)c->n1, (double)c->n2);
@@ -301,7 +371,7 @@ void enq_fsda_setup(Enq& e, int ns, long long max_iter, double tol) {
     k_apply_w<<<grid_for(nlN, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
         c->labels.ptr, c->wv.ptr, n, c->part_n.ptr, nlN, c->sc);
   });
-  enq_xt(e, c->wv.ptr, c->b.ptr, 1, c->mu_v.ptr, (double)c->ell, 0);
+  enq_xt(e, c->wv.ptr, c->b.ptr, 1, &c->sc->sum_z, 0, nullptr);
   e.go("cg_init", 8.0 * d * 3 + 16.0 * d * ns, [&] {
     dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
     k_cg_init<<<g, LEAF_THREADS, 0, c->stream>>>(c->b.ptr, c->r0.ptr, c->p.ptr, c->bigp.ptr,
@@ -319,8 +389,8 @@ void enq_fsda_tail(Enq& e, int ns) {
     k_transpose_sols<<<grid_for(d * ns, 256), 256, 0, c->stream>>>(c->sols.ptr, c->wT.ptr, d, ns);
   });
   e.go("spmm_scores", 4.0 * (n + 1) + 4.0 * c->nnz + 8.0 * d * ns + 8.0 * n * ns, [&] {
-    k_spmm_scores<8><<<grid_for(n, 128), 128, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr,
-                                                              c->wT.ptr, c->scores.ptr, (int)n, ns);
+    k_spmm_scores<<<grid_for(n, 8), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr, c->wT.ptr,
+                                                         c->scores.ptr, (int)n, ns);
   });
   e.go("orient", 8.0 * n * ns + 1.0 * n, [&] {
     dim3 g(grid_for(nlN, WARPS_PER_BLOCK), ns);
@@ -339,7 +409,11 @@ bool build_solve_graph(fsda_ctx* c, double alpha, int ns, long long max_iter, do
   char key[256];
   snprintf(key, sizeof(key), "%a|%d|%lld|%a|%lld|%lld|%llu", alpha, ns, max_iter, tol, c->n, c->nnz,
            g_alloc_gen);
-  if (c->exec && c->graph_key == key) return true;
+  if (c->exec && c->graph_key == key) {
+    *launches_fixed = c->graph_fixed;
+    *launches_body = c->graph_body;
+    return true;
+  }
   c->invalidate_graph();
   cudaStream_t s = c->stream;
   cudaGraph_t graph;
@@ -389,8 +463,8 @@ bool build_solve_graph(fsda_ctx* c, double alpha, int ns, long long max_iter, do
   c->graph = out;
   CK(cudaGraphInstantiate(&c->exec, out, 0));
   c->graph_key = key;
-  *launches_fixed = e.count;  // setup + tail
-  *launches_body = eb.count;
+  *launches_fixed = c->graph_fixed = e.count;  // setup + tail
+  *launches_body = c->graph_body = eb.count;
   (void)fixed;
   return true;
 }
@@ -434,7 +508,10 @@ void upload_solve_params(fsda_ctx* c, const double* betas, int ns, const double*
 // Launch one complete solve (graph, or eager when rec != null or no graph).
 long long launch_solve(fsda_ctx* c, double alpha, int ns, long long max_iter, double tol,
                        Recorder* rec) {
-  if (!rec && c->cond_supported) {
+  // FSDA_B200_EAGER=1 launches the same kernels one by one (ncu cannot
+  // profile kernel nodes of graphs that contain conditional nodes).
+  static const bool force_eager = getenv("FSDA_B200_EAGER") && getenv("FSDA_B200_EAGER")[0] == '1';
+  if (!rec && c->cond_supported && !force_eager) {
     long long fixed = 0, body = 0;
     try {
       build_solve_graph(c, alpha, ns, max_iter, tol, &fixed, &body);
@@ -492,78 +569,71 @@ int read_results(fsda_ctx* c, int ns, const SolveOut& o, int64_t* launches) {
   return FSDA_OK;
 }
 
-// Build the column work plan from the CSC column pointer (host side).
-void build_xt_plan(fsda_ctx* c) {
-  const long long D = c->d;
-  std::vector<int> colptr(D + 1);
-  CK(cudaMemcpy(colptr.data(), c->csc_colptr.ptr, sizeof(int) * (D + 1), cudaMemcpyDeviceToHost));
-  std::vector<int> tiny[5], warpc, segc, segs, hc, h0, hn;
-  for (long long col = 0; col < D; ++col) {
-    int nc = colptr[col + 1] - colptr[col];
-    if (nc <= 16) {
+// Build a segmented-sum plan from host segment offsets (S+1 entries) over the
+// device index stream `ind`.  Classes: W = 1 << k for segments with n <= 8W,
+// heavy tasks of <= 4 leaves for n > 256.
+template <typename OffT>
+void build_seg_plan(HostPlan& hp, const OffT* offs, long long S, const int* ind) {
+  std::vector<int4> cls[6], heavy;
+  std::vector<int> h0, hn, hs, ht;
+  int leaves = 0;
+  for (long long sgi = 0; sgi < S; ++sgi) {
+    const int lo = (int)offs[sgi], n = (int)(offs[sgi + 1] - offs[sgi]);
+    if (n <= LEAF) {
       int k = 0;
-      while ((1 << k) < nc) ++k;
-      tiny[k].push_back((int)col);
-    } else if (nc <= LEAF) {
-      warpc.push_back((int)col);
+      while (8 * (1 << k) < n) ++k;
+      cls[k].push_back(make_int4((int)sgi, lo, n, -1));
     } else {
-      hc.push_back((int)col);
-      h0.push_back((int)segc.size());
-      int nseg = (int)cdiv(nc, LEAF);
+      const int h = (int)h0.size();
+      const int nseg = (int)cdiv(n, LEAF);
+      const int ntask = (int)cdiv(n, 4 * LEAF);
+      h0.push_back(leaves);
       hn.push_back(nseg);
-      for (int j = 0; j < nseg; ++j) {
-        segc.push_back((int)col);
-        segs.push_back(colptr[col] + j * LEAF);
-      }
+      hs.push_back(lo);
+      ht.push_back(ntask);
+      leaves += nseg;
+      for (int j = 0; j < ntask; ++j)
+        heavy.push_back(make_int4((int)sgi, lo + j * 4 * LEAF, std::min(4 * LEAF, n - j * 4 * LEAF), h));
     }
   }
-  std::vector<int> tiny_all;
-  XtPlan& pl = c->plan;
+  SegPlan& pl = hp.pl;
   memset(&pl, 0, sizeof(pl));
-  long long off = 0;
-  for (int k = 0; k < 5; ++k) {
-    pl.tiny_off[k] = off;
-    tiny_all.insert(tiny_all.end(), tiny[k].begin(), tiny[k].end());
-    off += (long long)tiny[k].size();
-    pl.warps_tiny[k] = cdiv((long long)tiny[k].size(), 32 >> k);
+  std::vector<int4> tasks;
+  long long wb = 0;
+  for (int k = 0; k < 6; ++k) {
+    pl.cls_off[k] = (long long)tasks.size();
+    tasks.insert(tasks.end(), cls[k].begin(), cls[k].end());
+    pl.warp_base[k] = wb;
+    wb += cdiv((long long)cls[k].size(), 32 >> k);
   }
-  pl.tiny_off[5] = off;
+  pl.cls_off[6] = (long long)tasks.size();
+  pl.warp_base[6] = wb;
+  tasks.insert(tasks.end(), heavy.begin(), heavy.end());
+  wb += (long long)heavy.size();
+  pl.warp_base[7] = wb;
+  pl.warp_base[8] = wb;
+  hp.tasks.ensure(tasks.size());
+  if (!tasks.empty())
+    CK(cudaMemcpy(hp.tasks.ptr, tasks.data(), sizeof(int4) * tasks.size(), cudaMemcpyHostToDevice));
   auto up = [&](DevBuf<int>& dst, const std::vector<int>& v) {
     dst.ensure(v.size());
     if (!v.empty()) CK(cudaMemcpy(dst.ptr, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice));
   };
-  up(c->tiny_cols, tiny_all);
-  up(c->warp_cols, warpc);
-  up(c->seg_col, segc);
-  up(c->seg_start, segs);
-  up(c->heavy_cols, hc);
-  up(c->heavy_seg0, h0);
-  up(c->heavy_nseg, hn);
-  c->seg_part.ensure(segc.size());
-  pl.colptr = c->csc_colptr.ptr;
-  pl.rows = c->csc_rows.ptr;
-  pl.tiny_cols = c->tiny_cols.ptr;
-  pl.warp_cols = c->warp_cols.ptr;
-  pl.n_warp_cols = (long long)warpc.size();
-  pl.seg_col = c->seg_col.ptr;
-  pl.seg_start = c->seg_start.ptr;
-  pl.n_segs = (long long)segc.size();
-  pl.heavy_cols = c->heavy_cols.ptr;
-  pl.heavy_seg0 = c->heavy_seg0.ptr;
-  pl.heavy_nseg = c->heavy_nseg.ptr;
-  pl.n_heavy = (long long)hc.size();
-  pl.seg_part = c->seg_part.ptr;
-  long long base = 0;
-  for (int k = 0; k < 5; ++k) {
-    pl.warp_base[k] = base;
-    base += pl.warps_tiny[k];
-  }
-  pl.warp_base[5] = base;
-  base += pl.n_warp_cols;
-  pl.warp_base[6] = base;
-  base += pl.n_segs;
-  pl.warp_base[7] = base;
-  c->xt_warps = base;
+  up(hp.h0, h0);
+  up(hp.hn, hn);
+  up(hp.hs, hs);
+  up(hp.ht, ht);
+  hp.hc.ensure(hn.size());
+  CK(cudaMemset(hp.hc.ptr, 0, sizeof(unsigned) * std::max<size_t>(hn.size(), 1)));
+  hp.part.ensure(leaves);
+  pl.ind = ind;
+  pl.tasks = hp.tasks.ptr;
+  pl.heavy_seg0 = hp.h0.ptr;
+  pl.heavy_nseg = hp.hn.ptr;
+  pl.heavy_start = hp.hs.ptr;
+  pl.heavy_ntask = hp.ht.ptr;
+  pl.heavy_count = hp.hc.ptr;
+  pl.seg_part = hp.part.ptr;
 }
 
 int check_err_flag(fsda_ctx* c, const char* what) {
@@ -579,7 +649,8 @@ int check_err_flag(fsda_ctx* c, const char* what) {
 
 // Upload an int64 index array and narrow it to int32 on the device.
 void upload_narrow(fsda_ctx* c, const int64_t* host, long long n, long long limit, DevBuf<int>& out) {
-  out.ensure(n + 1);
+  out.ensure(n + 8);  // tail padding: the row kernels stage indices with 16-byte loads
+  CK(cudaMemsetAsync(out.ptr + n, 0, 8 * sizeof(int), c->stream));
   if (n == 0) return;
   long long* tmp = nullptr;
   CK(cudaMalloc(&tmp, sizeof(long long) * n));
@@ -655,14 +726,15 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     c->invalidate_graph();
-    DevBuf<int>* ib[] = {&c->x_rowptr, &c->x_cols, &c->csc_colptr, &c->csc_rows, &c->tiny_cols,
-                         &c->warp_cols, &c->seg_col, &c->seg_start, &c->heavy_cols, &c->heavy_seg0,
-                         &c->heavy_nseg, &c->l_rowptr, &c->l_cols, &c->active, &c->good,
-                         &c->pending, &c->flip, &c->err};
+    DevBuf<int>* ib[] = {&c->x_rowptr, &c->x_cols, &c->csc_colptr, &c->csc_rows, &c->l_rowptr,
+                         &c->l_cols, &c->active, &c->good, &c->pending, &c->flip, &c->err};
+    c->plan_xr.release();
+    c->plan_lr.release();
+    c->plan_xc.release();
     for (auto b : ib) b->release();
-    DevBuf<double>* db[] = {&c->seg_part, &c->l_diag, &c->y, &c->z, &c->q, &c->p, &c->r0, &c->r1,
+    DevBuf<double>* db[] = {&c->l_diag, &c->y, &c->z, &c->q, &c->p, &c->r0, &c->r1,
                             &c->mu_v, &c->t, &c->wv, &c->b, &c->ind, &c->probe, &c->part_n,
-                            &c->part_d, &c->part_o, &c->bigp, &c->sols, &c->wT, &c->scores,
+                            &c->part_d, &c->part_d2, &c->part_o, &c->bigp, &c->sols, &c->wT, &c->scores,
                             &c->dense_a, &c->beta, &c->zeta_prev, &c->zeta, &c->zeta_next,
                             &c->gamma_s, &c->alpha_s, &c->resid};
     for (auto b : db) b->release();
@@ -749,7 +821,12 @@ int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* ro
   CK(cudaStreamSynchronize(c->stream));
   keys_out.release();
   row_of.release();
-  build_xt_plan(c);
+  build_seg_plan(c->plan_xr, row_offsets, n_rows, c->x_cols.ptr);
+  {
+    std::vector<int> colptr(n_cols + 1);
+    CK(cudaMemcpy(colptr.data(), c->csc_colptr.ptr, sizeof(int) * (n_cols + 1), cudaMemcpyDeviceToHost));
+    build_seg_plan(c->plan_xc, colptr.data(), n_cols, c->csc_rows.ptr);
+  }
   c->has_x = true;
   return FSDA_OK;
   API_END
@@ -786,6 +863,7 @@ int fsda_upload_laplacian(fsda_ctx* c, int64_t n, const int64_t* row_offsets,
   }
   rc = check_err_flag(c, "laplacian");
   if (rc) return rc;
+  build_seg_plan(c->plan_lr, row_offsets, n, c->l_cols.ptr);
   c->has_l = true;
   return FSDA_OK;
   API_END
@@ -848,7 +926,7 @@ static int xt_probe(fsda_ctx* c, const double* mu, const double* w, double* out,
     CKL();
   }
   Enq e{c};
-  enq_xt(e, c->z.ptr, c->q.ptr, mode, c->mu_v.ptr, (double)c->ell, 0);
+  enq_xt(e, c->z.ptr, c->q.ptr, mode, &c->sc->sum_z, 0, nullptr);
   CK(cudaMemcpyAsync(out, c->q.ptr, sizeof(double) * c->d, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return FSDA_OK;
@@ -876,7 +954,7 @@ int fsda_labeled_mean(fsda_ctx* c, double* mu) {
   k_indicator<<<grid_for(c->n, 256), 256, 0, c->stream>>>(c->labels.ptr, c->ind.ptr, (int)c->n);
   CKL();
   Enq e{c};
-  enq_xt(e, c->ind.ptr, c->mu_v.ptr, 2, nullptr, (double)c->ell, 0);
+  enq_xt(e, c->ind.ptr, c->mu_v.ptr, 2, nullptr, 0, nullptr);
   CK(cudaMemcpyAsync(mu, c->mu_v.ptr, sizeof(double) * c->d, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return FSDA_OK;
@@ -889,11 +967,8 @@ int fsda_apply_smoother(fsda_ctx* c, double alpha, const double* yin, double* zo
   if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(FSDA_EINVAL, "alpha must lie in [0, 1], got %g", alpha);
   ensure_vectors(c, 1);
   CK(cudaMemcpyAsync(c->y.ptr, yin, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
-  long long nl = n_leaves(c->n);
-  k_smoother<<<grid_for(nl, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
-      c->l_rowptr.ptr, c->l_cols.ptr, c->l_diag.ptr, c->labels.ptr, c->y.ptr, c->z.ptr, (int)c->n,
-      alpha, alpha_mode_of(alpha), c->part_n.ptr, nl, c->sc, 0, nullptr);
-  CKL();
+  Enq e{c};
+  enq_smoother(e, alpha, c->y.ptr, c->z.ptr, 0);
   CK(cudaMemcpyAsync(zout, c->z.ptr, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return FSDA_OK;
@@ -910,17 +985,15 @@ int fsda_operator_apply(fsda_ctx* c, double alpha, const double* w, double* qout
   k_indicator<<<grid_for(c->n, 256), 256, 0, c->stream>>>(c->labels.ptr, c->ind.ptr, (int)c->n);
   CKL();
   Enq e{c};
-  enq_xt(e, c->ind.ptr, c->mu_v.ptr, 2, nullptr, (double)c->ell, 0);
+  enq_xt(e, c->ind.ptr, c->mu_v.ptr, 2, nullptr, 0, nullptr);
   CK(cudaMemcpyAsync(c->p.ptr, w, sizeof(double) * c->d, cudaMemcpyHostToDevice, c->stream));
-  k_spmv_rows<<<grid_for(c->n, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr, c->p.ptr,
-                                                          c->y.ptr, (int)c->n, nullptr);
-  CKL();
+  enq_xrows(e, c->p.ptr, c->y.ptr, 0);
+  enq_smoother(e, alpha, c->y.ptr, c->z.ptr, 0);
   long long nl = n_leaves(c->n);
-  k_smoother<<<grid_for(nl, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
-      c->l_rowptr.ptr, c->l_cols.ptr, c->l_diag.ptr, c->labels.ptr, c->y.ptr, c->z.ptr, (int)c->n,
-      alpha, alpha_mode_of(alpha), c->part_n.ptr, nl, c->sc, 0, nullptr);
+  k_vector_sum<<<grid_for(nl, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+      c->z.ptr, c->n, c->part_n.ptr, nl, c->sc, nullptr);
   CKL();
-  enq_xt(e, c->z.ptr, c->q.ptr, 1, c->mu_v.ptr, (double)c->ell, 0);
+  enq_xt(e, c->z.ptr, c->q.ptr, 1, &c->sc->sum_z, 0, nullptr);
   CK(cudaMemcpyAsync(qout, c->q.ptr, sizeof(double) * c->d, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return FSDA_OK;
@@ -1058,14 +1131,8 @@ int fsda_shifted_cg_dense(fsda_ctx* c, int64_t dim, const double* a, const doubl
   for (long long it = 0; it < max_iter; ++it) {
     k_dense_matvec<<<grid_for(dim, 128), 128, 0, c->stream>>>(c->dense_a.ptr, c->p.ptr, c->q.ptr,
                                                               (int)dim, c->sc);
-    k_dot_pq<<<grid_for(nlD, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
-        c->p.ptr, c->q.ptr, dim, c->part_d.ptr, nlD, c->sc, ss, ns);
-    dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
-    k_update<<<g, LEAF_THREADS, 0, c->stream>>>(c->q.ptr, c->r0.ptr, c->r1.ptr, c->bigp.ptr,
-                                                c->sols.ptr, dim, c->part_d.ptr, nlD, c->sc, ss, ns);
-    k_pupdate<<<grid_for(dim, 256), 256, 0, c->stream>>>(c->r0.ptr, c->r1.ptr, c->p.ptr, dim, c->sc,
-                                                         0, 0);
     CKL();
+    launch_cg_step(c, ns, dim, 0, 0, false);
     if ((it & 15) == 15) {  // stop launching once every shift froze
       CgScalars h;
       CK(cudaMemcpyAsync(&h, c->sc, sizeof(h), cudaMemcpyDeviceToHost, c->stream));

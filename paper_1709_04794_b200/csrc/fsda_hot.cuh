@@ -1,0 +1,586 @@
+// fsda_hot.cuh — the per-iteration kernels of the FSDA sweep (included by
+// fsda_device.cuh; same arithmetic contract, see the header there).
+//
+// One shifted-CG iteration = 4 launches:
+//   k_segsum<SEG_XROWS>  y = X p                (rows, canonical tree)
+//   k_segsum<SEG_LROWS>  z = M y                (rows of L, canonical tree, blend)
+//   k_segsum<SEG_XCOLS>  q_raw = X^T z, + leaf partials of sum(z)
+//   k_cg_step            cooperative: centring, p.q -> shift scalars ->
+//                        sols/P/r updates -> r.r -> p
+// k_spmv_rows (scipy's sequential row order) serves the X v probe API.
+#pragma once
+
+#include <cooperative_groups.h>
+
+namespace fsda {
+
+namespace cg = cooperative_groups;
+
+constexpr int STAGE = 1024;    // column indices staged per warp and chunk
+constexpr int ROW_WARPS = 8;   // warps per block in the row kernels
+
+// Copy cols[c0, c1) into a warp's shared stage with 16-byte loads.  The copy
+// starts at the 16-byte boundary below c0 (index arrays carry >= 4 ints of
+// tail padding), so stage[j - base] holds cols[j].  Returns base.
+__device__ __forceinline__ int stage_cols(const int* __restrict__ cols, int c0, int c1, int* st,
+                                          int lane) {
+  const int base = c0 & ~3;
+  const int n4 = (c1 - base + 3) >> 2;
+  const int4* src = reinterpret_cast<const int4*>(cols + base);
+  int4* dst = reinterpret_cast<int4*>(st);
+  for (int k = lane; k < n4; k += 32) dst[k] = __ldg(src + k);
+  __syncwarp();
+  return base;
+}
+
+// acc + v[st[j - base]] for j in [a, b), strictly in order; gathers batched 8
+// deep for memory-level parallelism.
+__device__ __forceinline__ double gather_sum(double acc, const int* st, int base, int a, int b,
+                                             const double* __restrict__ v) {
+  int j = a;
+  for (; j + 8 <= b; j += 8) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = __ldg(v + st[j + u - base]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = acc + t[u];
+  }
+  for (; j < b; ++j) acc = acc + __ldg(v + st[j - base]);
+  return acc;
+}
+
+// ------------------------------------------------------------- K1: y = X p
+// A warp owns 32 consecutive rows (one per lane).  It streams the rows' column
+// indices through shared memory with coalesced 16-byte loads, and each lane
+// sums p over its own row sequentially in stored column order — the order of
+// scipy's csr_matvec (sparse.py:121), so y is bit-identical to the reference.
+__global__ void __launch_bounds__(256) k_spmv_rows(const int* __restrict__ rowptr,
+                                                   const int* __restrict__ cols,
+                                                   const double* __restrict__ p,
+                                                   double* __restrict__ y, int n_rows,
+                                                   const CgScalars* guard) {
+  if (guard && loop_idle(guard)) return;
+  __shared__ __align__(16) int stage[ROW_WARPS][STAGE + 8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long r0 = ((long long)blockIdx.x * ROW_WARPS + warp) * 32;
+  if (r0 >= n_rows) return;
+  const int row = (int)r0 + lane;
+  const bool valid = row < n_rows;
+  const int start = valid ? __ldg(rowptr + row) : 0;
+  const int end = valid ? __ldg(rowptr + row + 1) : 0;
+  const int last = (int)min(32LL, (long long)n_rows - r0) - 1;
+  const int wlo = __shfl_sync(FULL, start, 0);
+  const int whi = __shfl_sync(FULL, end, last);
+  int* st = stage[warp];
+  double acc = 0.0;
+  for (int c0 = wlo; c0 < whi; c0 += STAGE) {
+    const int c1 = min(c0 + STAGE, whi);
+    const int base = stage_cols(cols, c0, c1, st, lane);
+    const int a = max(start, c0), b = min(end, c1);
+    if (a < b) acc = gather_sum(acc, st, base, a, b, p);
+    __syncwarp();
+  }
+  if (valid) y[row] = acc;
+}
+
+// Dense symmetric operator for fsda_shifted_cg_dense: q = A p, row-major A,
+// sequential per row (the device stand-in for LinearOperator.from_dense).
+__global__ void k_dense_matvec(const double* __restrict__ a, const double* __restrict__ p,
+                               double* __restrict__ q, int dim, const CgScalars* guard) {
+  if (guard && loop_idle(guard)) return;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= dim) return;
+  const double* row = a + (long long)i * dim;
+  double acc = 0.0;
+  for (int j = 0; j < dim; ++j) acc = acc + row[j] * p[j];
+  q[i] = acc;
+}
+
+// Canonical sum of a vector (sum(w) for the parity probes).
+__global__ void k_vector_sum(const double* __restrict__ v, long long n, double* __restrict__ part,
+                             long long n_leaf, CgScalars* sc, double* out) {
+  __shared__ double smem[257];
+  const int lane = threadIdx.x & 31;
+  const long long g = (long long)blockIdx.x * WARPS_PER_BLOCK + (threadIdx.x >> 5);
+  if (g < n_leaf) {
+    double a = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      long long i = g * LEAF + k * 32 + lane;
+      if (i < n) a = a + v[i];
+    }
+    a = butterfly(a);
+    if (lane == 0) { part[g] = a; __threadfence(); }
+  }
+  if (arrive_last(&sc->counters[C_SUM], gridDim.x)) {
+    double s = block_reduce_partials(part, n_leaf, smem);
+    if (threadIdx.x == 0) {
+      if (out) *out = s;
+      sc->sum_z = s;
+    }
+  }
+}
+
+// R256 of m partials by one warp (m <= 65536); result in every lane.
+__device__ __forceinline__ double warp_reduce_partials(const double* part, int m, int lane) {
+  if (m <= LEAF) return warp_leaf(part, m, lane);
+  const int m2 = (m + LEAF - 1) / LEAF;
+  double acc = 0.0;
+  for (int g = 0; g < m2; ++g) {
+    const double r = warp_leaf(part + g * LEAF, min(LEAF, m - g * LEAF), lane);
+    if ((g & 31) == lane) acc = acc + r;
+  }
+  return butterfly(acc);
+}
+
+// -------------------------------------------- segmented canonical sums
+// X p (rows of X), L y (rows of L) and X^T z (columns of X) are all "sum the
+// gathered terms of every segment with the canonical R256 tree".  A host-built
+// plan sorts segments into classes by length:
+//   class k (W = 1 << k, k = 0..5): segments with n <= 8W, 32/W per warp, one
+//     W-lane group per segment, every lane holding <= 8 elements;
+//   heavy: n > 256, warp tasks of <= 4 leaves; each leaf partial goes to
+//     seg_part and the task that completes a segment (atomic counter,
+//     self-resetting) reduces its leaves with the same tree.
+// A W-lane group reproduces the canonical leaf exactly: lane t of the group
+// keeps accumulator A_m = sum_k v[t + mW + 32k] (in k order, from 0.0) —
+// the canonical lane t + mW — then combines A_m + A_{m+j} for j = M/2..1 and
+// finishes with the butterfly over the W lanes.  Those are precisely the
+// canonical xor-butterfly steps at offsets >= W and < W; accumulators that
+// can only hold zeros are skipped (x + 0.0 == x).
+enum SegKind : int { SEG_XROWS = 0, SEG_LROWS = 1, SEG_XCOLS = 2 };
+
+struct SegPlan {
+  const int* ind;            // index stream (X columns, L columns, or CSC rows)
+  const int4* tasks;         // {segment, start, length, heavy id or -1}
+  long long cls_off[7];      // class k tasks: [cls_off[k], cls_off[k+1]); heavy: [cls_off[6], ...)
+  long long warp_base[9];    // warps: classes 0..5, heavy tasks (6), sum leaves (7), end (8)
+  const int* heavy_seg0;     // first leaf partial of heavy segment h
+  const int* heavy_nseg;     // leaves of heavy segment h
+  const int* heavy_start;    // index-stream start of heavy segment h
+  const int* heavy_ntask;    // warp tasks of heavy segment h
+  unsigned* heavy_count;     // arrival counters
+  double* seg_part;          // leaf partials
+};
+
+struct SegArgs {
+  const double* src;         // gathered vector: p, y or z
+  double* out;               // y, z or q (raw)
+  // L rows: z = blend(alpha, masked y, alpha * (L y))
+  const double* ldiag;
+  const signed char* labels;
+  double alpha;
+  int alpha_mode;
+  // X^T columns: 0 raw, 1 centred (mu, *sum_ptr), 2 divided by ell
+  int mode;
+  const double* mu;
+  const double* sum_ptr;
+  double ell;
+  // optional leaf partials of sum(src) (K3 in the loop: sum(z))
+  double* sum_part;
+  long long sum_n;
+};
+
+template <int KIND>
+__device__ __forceinline__ double seg_term(const SegArgs& a, int seg, int idx, double dg) {
+  const double v = __ldg(a.src + idx);
+  if (KIND == SEG_LROWS) return (idx == seg) ? dg * v : -v;
+  return v;
+}
+
+template <int KIND>
+__device__ __forceinline__ void seg_finish(const SegArgs& a, int seg, double s) {
+  if (KIND == SEG_XROWS) {
+    a.out[seg] = s;
+  } else if (KIND == SEG_LROWS) {
+    const double masked = a.labels[seg] != 0 ? a.src[seg] : 0.0;
+    const double smoothed = a.alpha * s;
+    a.out[seg] = (a.alpha_mode == 1) ? smoothed : (1.0 - a.alpha) * masked + smoothed;
+  } else {
+    if (a.mode == 1) s = s - a.mu[seg] * (*a.sum_ptr);
+    else if (a.mode == 2) s = s / a.ell;
+    a.out[seg] = s;
+  }
+}
+
+// Canonical leaf of segment elements [start, start+n) (n <= 8W) by a W-lane
+// group; t = lane within the group; result in every lane of the group.
+template <int W, int KIND>
+__device__ __forceinline__ double group_leaf(const SegPlan& pl, const SegArgs& a, int seg, int start,
+                                             int n, int t) {
+  constexpr int M = 32 / W;
+  constexpr int MA = M < 8 ? M : 8;
+  constexpr int KA = W >= 8 ? W / 4 : 1;
+  double dg = 0.0;
+  if (KIND == SEG_LROWS && n > 0) dg = __ldg(a.ldiag + seg);
+  int ix[MA * KA];
+  double v[MA * KA];
+#pragma unroll
+  for (int m = 0; m < MA; ++m)
+#pragma unroll
+    for (int k = 0; k < KA; ++k) {
+      const int e = t + m * W + 32 * k;
+      ix[m * KA + k] = (e < n) ? __ldg(pl.ind + start + e) : 0;
+    }
+#pragma unroll
+  for (int m = 0; m < MA; ++m)
+#pragma unroll
+    for (int k = 0; k < KA; ++k) {
+      const int e = t + m * W + 32 * k;
+      v[m * KA + k] = (e < n) ? seg_term<KIND>(a, seg, ix[m * KA + k], dg) : 0.0;
+    }
+  double A[MA];
+#pragma unroll
+  for (int m = 0; m < MA; ++m) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < KA; ++k)
+      if (t + m * W + 32 * k < n) acc = acc + v[m * KA + k];
+    A[m] = acc;
+  }
+#pragma unroll
+  for (int j = MA / 2; j >= 1; j >>= 1)
+#pragma unroll
+    for (int m = 0; m < j; ++m) A[m] = A[m] + A[m + j];
+  double r = A[0];
+#pragma unroll
+  for (int off = W / 2; off >= 1; off >>= 1) r = r + __shfl_xor_sync(FULL, r, off);
+  return r;
+}
+
+template <int W, int KIND>
+__device__ __forceinline__ void seg_class_task(const SegPlan& pl, const SegArgs& a, int cls,
+                                               long long tw, int lane) {
+  const long long idx = pl.cls_off[cls] + (tw - pl.warp_base[cls]) * (32 / W) + lane / W;
+  int4 tk = make_int4(-1, 0, 0, -1);
+  if (idx < pl.cls_off[cls + 1]) tk = __ldg(pl.tasks + idx);
+  const double s = group_leaf<W, KIND>(pl, a, tk.x, tk.y, tk.z, lane & (W - 1));
+  if (tk.x >= 0 && (lane & (W - 1)) == 0) seg_finish<KIND>(a, tk.x, s);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256) k_segsum(SegPlan pl, SegArgs a, const CgScalars* sc,
+                                                int guarded) {
+  if (guarded && loop_idle(sc)) return;
+  const int lane = threadIdx.x & 31;
+  const long long total = pl.warp_base[8];
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long tw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tw < total;
+       tw += nwarps) {
+    if (tw < pl.warp_base[6]) {
+      int k = 0;
+      while (tw >= pl.warp_base[k + 1]) ++k;
+      switch (k) {
+        case 0: seg_class_task<1, KIND>(pl, a, 0, tw, lane); break;
+        case 1: seg_class_task<2, KIND>(pl, a, 1, tw, lane); break;
+        case 2: seg_class_task<4, KIND>(pl, a, 2, tw, lane); break;
+        case 3: seg_class_task<8, KIND>(pl, a, 3, tw, lane); break;
+        case 4: seg_class_task<16, KIND>(pl, a, 4, tw, lane); break;
+        default: seg_class_task<32, KIND>(pl, a, 5, tw, lane); break;
+      }
+      continue;
+    }
+    if (tw >= pl.warp_base[7]) {  // leaf partials of sum(src)
+      const long long g = tw - pl.warp_base[7];
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const long long i = g * LEAF + k * 32 + lane;
+        if (i < a.sum_n) s = s + __ldg(a.src + i);
+      }
+      s = butterfly(s);
+      if (lane == 0) a.sum_part[g] = s;
+      continue;
+    }
+    // heavy task: up to 4 consecutive leaves of one segment
+    const int4 tk = __ldg(pl.tasks + pl.cls_off[6] + (tw - pl.warp_base[6]));
+    const int h = tk.w;
+    const int leaf0 = __ldg(pl.heavy_seg0 + h) + (tk.y - __ldg(pl.heavy_start + h)) / LEAF;
+    for (int lf = 0; lf * LEAF < tk.z; ++lf) {
+      const double s = group_leaf<32, KIND>(pl, a, tk.x, tk.y + lf * LEAF,
+                                            min(LEAF, tk.z - lf * LEAF), lane);
+      if (lane == 0) pl.seg_part[leaf0 + lf] = s;
+    }
+    int is_last = 0;
+    if (lane == 0) {
+      __threadfence();
+      const unsigned old = atomicAdd(pl.heavy_count + h, 1u);
+      is_last = (old == (unsigned)__ldg(pl.heavy_ntask + h) - 1u);
+    }
+    is_last = __shfl_sync(FULL, is_last, 0);
+    if (is_last) {
+      __threadfence();
+      const double s = warp_reduce_partials(pl.seg_part + __ldg(pl.heavy_seg0 + h),
+                                            __ldg(pl.heavy_nseg + h), lane);
+      if (lane == 0) {
+        seg_finish<KIND>(a, tk.x, s);
+        pl.heavy_count[h] = 0u;
+      }
+    }
+  }
+}
+
+// z = masked y (apply_smoother at alpha == 0: no Laplacian term, sda.py:135-136).
+__global__ void k_mask_labeled(const double* __restrict__ y, const signed char* __restrict__ labels,
+                               double* __restrict__ z, int n, const CgScalars* sc, int guarded) {
+  if (guarded && loop_idle(sc)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) z[i] = labels[i] != 0 ? y[i] : 0.0;
+}
+
+// -------------------------------------------- K4: one cooperative CG step
+// krylov.py:211-268 for every active shift in one launch with two grid-wide
+// barriers:
+//   A  leaf partials of p.q
+//   -- grid sync --
+//   B  every block finishes p.q (identical tree, identical result), derives
+//      gamma and the per-shift zeta_next / gamma_s / good flags in shared
+//      memory; then per 256-element leaf: r_next = r + gamma q with leaf
+//      partials of r_next.r_next (block row 0), and for each good shift the
+//      deferred P update owed from the previous iteration (krylov.py:241) and
+//      sols -= P * gamma_s (krylov.py:230) — sols and P are read and written
+//      once per iteration
+//   -- grid sync --
+//   C  every block finishes r.r and alpha_new; p = r_next + alpha_new p;
+//      block 0 retires converged / degenerate shifts, rolls zeta, advances
+//      the iteration, and sets the while-loop condition.
+// Scalars needed after block 0 starts writing them are read into registers
+// at kernel entry, so no block reads state that block 0 modifies.
+__global__ void __launch_bounds__(256) k_cg_step(
+    double* __restrict__ q, double* __restrict__ p, double* __restrict__ r0,
+    double* __restrict__ r1, double* __restrict__ bigp, double* __restrict__ sols, long long d,
+    double* __restrict__ part_pq, double* __restrict__ part_rr, long long n_leaf, CgScalars* sc,
+    ShiftState ss, int ns, unsigned long long cond_handle, int use_cond,
+    const double* __restrict__ mu, const double* __restrict__ part_z, long long n_leaf_z) {
+  extern __shared__ double dyn[];  // zn[ns], gs[ns], good[ns] (as double)
+  __shared__ double smem[257];
+  __shared__ int s_flag;
+  double* s_zn = dyn;
+  double* s_gs = dyn + ns;
+  double* s_good = dyn + 2 * ns;
+  cg::grid_group grid = cg::this_grid();
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+
+  if (leader && use_cond) ++sc->body_runs;
+  const int idle = loop_idle(sc);
+  const long long it = sc->iter;
+  const double rr = sc->rr, gp = sc->gamma_prev, al = sc->alpha, thresh = sc->thresh;
+  const long long max_iter = sc->max_iter;
+  const long long runs = sc->body_runs;
+  if (idle) {
+    if (leader && use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond_handle, 0u);
+    return;
+  }
+  // Block 0 writes scalar / shift state only after the second grid barrier,
+  // i.e. after every block has performed the entry reads above.
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+  const long long tw = (long long)gridDim.x * (blockDim.x >> 5);
+  const double* r_cur = (it & 1) ? r1 : r0;
+  double* r_next = (it & 1) ? r0 : r1;
+
+  // ---- A: centring q = X^T z - mu sum(z) (sparse.py:277; sum(z) leaves come
+  // from k_segsum), then the p.q leaves
+  double sum_z = 0.0;
+  if (part_z) sum_z = block_reduce_partials(part_z, n_leaf_z, smem);
+  for (long long g = gw; g < n_leaf; g += tw) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long long i = g * LEAF + k * 32 + lane;
+      if (i < d) {
+        double qi = q[i];
+        if (part_z) {
+          qi = qi - mu[i] * sum_z;
+          q[i] = qi;
+        }
+        a = fma(p[i], qi, a);
+      }
+    }
+    a = butterfly(a);
+    if (lane == 0) part_pq[g] = a;
+  }
+  grid.sync();
+
+  // ---- B: scalars, then the updates
+  const double pq = block_reduce_partials(part_pq, n_leaf, smem);
+  if (!isfinite(pq) || pq == 0.0) {
+    if (leader) {
+      sc->status = isfinite(pq) ? ST_BREAKDOWN : ST_NONFINITE;
+      sc->fail_iter = it;
+      sc->finished = 1;
+      if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond_handle, 0u);
+    }
+    return;  // uniform: every block computed the same pq
+  }
+  const double gamma = -rr / pq;
+  for (int s = threadIdx.x; s < ns; s += blockDim.x) {
+    double zn = 0.0, gs = 0.0, good = 0.0;
+    if (ss.active[s]) {
+      const double zp = ss.zeta_prev[s], z = ss.zeta[s];
+      const double denom = gamma * al * (zp - z) + zp * gp * (1.0 - ss.beta[s] * gamma);
+      zn = zp * z * gp / denom;
+      if (isfinite(zn) && !(fabs(zn) < 1e-290)) {
+        good = 1.0;
+        gs = gamma * zn / z;
+      }
+    }
+    s_zn[s] = zn;
+    s_gs[s] = gs;
+    s_good[s] = good;
+  }
+  __syncthreads();
+  // r-row leaves first (they feed r.r), then the shift rows in half-leaf
+  // units of 128 elements for a finer load balance.
+  const long long n_half = 2 * n_leaf;
+  const long long units = n_leaf + (long long)ns * n_half;
+  for (long long u = gw; u < units; u += tw) {
+    if (u < n_leaf) {
+      const long long g = u;
+      double a = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const long long i = g * LEAF + k * 32 + lane;
+        if (i < d) {
+          const double rn = r_cur[i] + gamma * __ldcg(q + i);
+          r_next[i] = rn;
+          a = fma(rn, rn, a);
+        }
+      }
+      a = butterfly(a);
+      if (lane == 0) part_rr[g] = a;
+    } else {
+      const long long v = u - n_leaf;
+      const int s = (int)(v / n_half);
+      const long long h = v - (long long)s * n_half;
+      if (s_good[s] == 0.0) continue;
+      const double gs = s_gs[s];
+      const int pend = ss.pending[s];
+      const double zc = ss.zeta[s], as = ss.alpha_s[s];
+      double* P = bigp + (long long)s * d;
+      double* X = sols + (long long)s * d;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const long long i = h * 128 + k * 32 + lane;
+        if (i < d) {
+          double pv = P[i];
+          const double xv = X[i];
+          if (pend) {
+            pv = zc * r_cur[i] + as * pv;
+            P[i] = pv;
+          }
+          X[i] = xv - pv * gs;
+        }
+      }
+    }
+  }
+  grid.sync();
+
+  // ---- C: r.r, alpha_new, p, bookkeeping
+  const double rr_new = block_reduce_partials(part_rr, n_leaf, smem);
+  if (!isfinite(rr_new)) {
+    if (leader) {
+      sc->status = ST_NONFINITE;
+      sc->fail_iter = it;
+      sc->finished = 1;
+      if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond_handle, 0u);
+    }
+    return;
+  }
+  const double alpha_new = rr_new / rr;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < d;
+       i += (long long)gridDim.x * blockDim.x) {
+    p[i] = __ldcg(r_next + i) + alpha_new * p[i];
+  }
+  if (blockIdx.x != 0) return;
+  if (threadIdx.x == 0) s_flag = 0;
+  __syncthreads();
+  const double r_norm = sqrt(rr_new);
+  for (int s = threadIdx.x; s < ns; s += blockDim.x) {
+    if (!ss.active[s]) continue;
+    if (s_good[s] == 0.0) {  // degenerate zeta: freeze untouched (krylov.py:251-255)
+      ss.iters[s] = it + 1;
+      ss.resid[s] = __longlong_as_double(0x7ff0000000000000LL);
+      ss.active[s] = 0;
+      ss.pending[s] = 0;
+      continue;
+    }
+    const double zn = s_zn[s], z = ss.zeta[s], gs = s_gs[s];
+    ss.alpha_s[s] = alpha_new * (zn * gs) / (z * gamma);
+    const double shift_res = fabs(zn) * r_norm;
+    if (shift_res < thresh) {  // converged: freeze (krylov.py:256-261)
+      ss.iters[s] = it + 1;
+      ss.resid[s] = shift_res;
+      ss.conv[s] = 1;
+      ss.active[s] = 0;
+      ss.pending[s] = 0;
+    } else {
+      ss.zeta_prev[s] = z;
+      ss.zeta[s] = zn;
+      ss.pending[s] = 1;
+      atomicAdd(&s_flag, 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int n_active = s_flag;
+    sc->gamma_prev = gamma;
+    sc->alpha = alpha_new;
+    sc->alpha_new = alpha_new;
+    sc->gamma = gamma;
+    sc->rr = rr_new;
+    sc->iter = it + 1;
+    sc->n_active = n_active;
+    const int fin = (n_active == 0 || it + 1 >= max_iter) ? 1 : 0;
+    if (fin) sc->finished = 1;
+    if (use_cond) {
+      unsigned keep = fin ? 0u : 1u;
+      if (runs > max_iter + 1) keep = 0u;  // never spin past the iteration budget
+      cudaGraphSetConditional((cudaGraphConditionalHandle)cond_handle, keep);
+    }
+  }
+}
+
+// ------------------------------------------------------- projection SpMM
+// scores[s * N + i] = sum over row i of W[c * ns + s] (W = directions,
+// feature-major).  A warp owns a row; lane s owns shift s and adds W[c, s]
+// for the row's columns in stored order — what scipy does for each
+// x.matvec(w) (sda.py:279), so scores == X @ w bit for bit.  A row's column
+// indices are read once per 32 shifts; the W row gathers are coalesced.
+__global__ void __launch_bounds__(256) k_spmm_scores(const int* __restrict__ rowptr,
+                                                     const int* __restrict__ cols,
+                                                     const double* __restrict__ w,
+                                                     double* __restrict__ scores, int n_rows,
+                                                     int ns) {
+  const int lane = threadIdx.x & 31;
+  const long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= n_rows) return;
+  const int lo = __ldg(rowptr + row), hi = __ldg(rowptr + row + 1);
+  for (int s0 = 0; s0 < ns; s0 += 32) {
+    const int s = s0 + lane;
+    const bool on = s < ns;
+    double acc = 0.0;
+    for (int j0 = lo; j0 < hi; j0 += 32) {
+      const int cnt = min(32, hi - j0);
+      const int mycol = (lane < cnt) ? __ldg(cols + j0 + lane) : 0;
+      int u = 0;
+      for (; u + 8 <= cnt; u += 8) {
+        double t[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int c = __shfl_sync(FULL, mycol, u + k);
+          t[k] = on ? __ldg(w + (long long)c * ns + s) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc = acc + t[k];
+      }
+      for (; u < cnt; ++u) {
+        const int c = __shfl_sync(FULL, mycol, u);
+        acc = acc + (on ? __ldg(w + (long long)c * ns + s) : 0.0);
+      }
+    }
+    if (on) scores[(long long)s * n_rows + row] = acc;
+  }
+}
+
+}  // namespace fsda

@@ -143,6 +143,47 @@ int fsda_shifted_cg_dense(fsda_ctx* ctx, int64_t dim, const double* a, const dou
                           int64_t* iterations, uint8_t* converged, int64_t* n_applies,
                           int64_t* fail_iter);
 
+/* ---- row-sharded building blocks ---------------------------
+ * One context per GPU holds a contiguous row block [row_base, row_base+N_g)
+ * of X (uploaded with fsda_upload_x as an N_g x D matrix) and of L
+ * (fsda_upload_laplacian_rows: N_g rows, global column indices), plus the
+ * block's labels.  The host orchestrator (paper_1709_04794_b200/sharded.py)
+ * strings these together with NCCL all-gathers of y and all-reduces of the
+ * D-length X^T partials; D-vectors and the shift state are replicated, so
+ * every rank runs the identical recurrence.  All pointers named d_* are
+ * device pointers on the context's device; calls are asynchronous on the
+ * context stream unless they return host data. */
+int fsda_upload_laplacian_rows(fsda_ctx* ctx, int64_t n_local, int64_t n_global, int64_t row_base,
+                               const int64_t* row_offsets, const int64_t* col_indices,
+                               const double* values);
+/* d_y (N_g) = X_g d_v (D), rows summed by the canonical tree */
+int fsda_dev_xrows(fsda_ctx* ctx, const double* d_v, double* d_y);
+/* d_z (N_g) = [(1-a)(I_l + 0) + a L_g] d_y_full (N_global) */
+int fsda_dev_smoother(fsda_ctx* ctx, double alpha, const double* d_y_full, double* d_z);
+/* d_out[0..D) = X_g^T d_z (raw column sums), d_out[D] = sum(d_z) (canonical) */
+int fsda_dev_xt_partial(fsda_ctx* ctx, const double* d_z, double* d_out);
+/* d_out[0] = sum of d_t over class +1 rows, d_out[1] = over class -1 rows */
+int fsda_dev_class_sums(fsda_ctx* ctx, const double* d_t, double* d_out);
+/* d_w = class-mean broadcast (c1 on +1 rows, c2 on -1 rows, else 0) */
+int fsda_dev_apply_w(fsda_ctx* ctx, double c1, double c2, double* d_w);
+/* d_out[i] = d_q[i] - d_mu[i] * d_q[D]   (centring of an all-reduced partial) */
+int fsda_dev_center(fsda_ctx* ctx, const double* d_mu, double* d_q, double scale);
+/* shifted CG state on the context: reset + init from the device rhs d_b */
+int fsda_dev_cg_begin(fsda_ctx* ctx, const double* betas, int n_shifts, double tol,
+                      int64_t max_iter, const double* d_b);
+/* one iteration given the (centred, all-reduced) d_q = B p */
+int fsda_dev_cg_step(fsda_ctx* ctx, const double* d_q);
+/* device pointer of the current search direction p (D doubles) */
+int fsda_dev_cg_direction(fsda_ctx* ctx, const double** d_p);
+int fsda_dev_cg_status(fsda_ctx* ctx, int* finished, int64_t* iterations, int* status);
+/* projections of the local rows: d_scores (n_shifts x N_g), d_orient[s] = y_g . s_g */
+int fsda_dev_project(fsda_ctx* ctx, double* d_scores, double* d_orient);
+/* finish: flip the shifts whose all-reduced orientation is negative (host
+ * array flip[n_shifts]) in d_scores and the directions, copy results out */
+int fsda_dev_finish(fsda_ctx* ctx, const uint8_t* flip, double* d_scores, double* directions,
+                    double* residuals, int64_t* iterations, uint8_t* converged,
+                    int64_t* n_applies, int64_t* fail_iter);
+
 #ifdef __cplusplus
 }
 #endif

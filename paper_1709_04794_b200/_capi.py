@@ -50,6 +50,20 @@ SIGNATURES = {
     "fsda_profile_kernels": [_P, C.c_int, _PI, C.POINTER(C.c_char_p), _PD, _PD, _PI64],
     "fsda_shifted_cg_dense": [_P, _I64, _PD, _PD, _PD, C.c_int, _D, _I64, C.c_int, _PD, _PD,
                               _PI64, _PU8, _PI64, _PI64],
+    # row-sharded building blocks (device pointers passed as c_void_p)
+    "fsda_upload_laplacian_rows": [_P, _I64, _I64, _I64, _PI64, _PI64, _PD],
+    "fsda_dev_xrows": [_P, _P, _P],
+    "fsda_dev_smoother": [_P, _D, _P, _P],
+    "fsda_dev_xt_partial": [_P, _P, _P],
+    "fsda_dev_class_sums": [_P, _P, _P],
+    "fsda_dev_apply_w": [_P, _D, _D, _P],
+    "fsda_dev_center": [_P, _P, _P, _D],
+    "fsda_dev_cg_begin": [_P, _PD, C.c_int, _D, _I64, _P],
+    "fsda_dev_cg_step": [_P, _P],
+    "fsda_dev_cg_direction": [_P, C.POINTER(_P)],
+    "fsda_dev_cg_status": [_P, _PI, _PI64, _PI],
+    "fsda_dev_project": [_P, _P, _P],
+    "fsda_dev_finish": [_P, _PU8, _P, _PD, _PD, _PI64, _PU8, _PI64, _PI64],
 }
 
 _lib = None

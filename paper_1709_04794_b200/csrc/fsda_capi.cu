@@ -116,11 +116,26 @@ struct fsda_ctx {
   long long n = 0, d = 0, nnz = 0;
   bool has_x = false;
   DevBuf<int> x_rowptr, x_cols, csc_colptr, csc_rows;
-  // segmented-sum plans: rows of X, rows of L, columns of X
+  // upload scratch (persistent so that repeated uploads of same-size data do
+  // not reallocate and the cached solve graph stays valid)
+  DevBuf<long long> scratch_i64;
+  DevBuf<double> scratch_f64;
+  DevBuf<int> scratch_row_of, scratch_keys;
+  DevBuf<unsigned char> scratch_sort;
+  // segmented-sum plans: rows of X, rows of L, light columns of X
   HostPlan plan_xr, plan_lr, plan_xc;
+  // dense columns of X (blocked by rows, see k_xt_coop)
+  DevBuf<int> xh_col, xh_bptr;
+  DevBuf<int4> xh_tasks;
+  DevBuf<long long> xh_boff, xh_bwarp;
+  DevBuf<double> xh_part;
+  XtDense xh{};
+  int xt_blocks = 0;
   int step_blocks = 0;  // cooperative grid of k_cg_step
 
-  // L: CSR with diagonal entries in place, diag values split out
+  // L: CSR with diagonal entries in place, diag values split out.  Row-sharded
+  // contexts hold rows [row_base, row_base + n) of an n_global-row L.
+  long long row_base = 0, n_global = 0;
   bool has_l = false;
   long long l_nnz = 0;
   DevBuf<int> l_rowptr, l_cols;
@@ -270,7 +285,14 @@ void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* sum
   a.sum_part = sum_part;
   a.sum_n = sum_part ? c->n : 0;
   e.go("xt", bytes, [&] {
-    launch_segsum<SEG_XCOLS>(c, c->plan_xc, a, guarded, sum_part ? n_leaves(c->n) : 0);
+    SegPlan pl = c->plan_xc.pl;
+    pl.warp_base[8] = pl.warp_base[7] + (sum_part ? n_leaves(c->n) : 0);
+    XtDense xh = c->xh;
+    const CgScalars* sc = c->sc;
+    int n_rows = (int)c->n;
+    void* args[] = {(void*)&pl, (void*)&xh, (void*)&a, (void*)&sc, (void*)&guarded, (void*)&n_rows};
+    CK(cudaLaunchCooperativeKernel((void*)k_xt_coop, dim3(c->xt_blocks), dim3(256), args, 0,
+                                   c->stream));
   });
 }
 
@@ -291,7 +313,7 @@ void enq_smoother(Enq& e, double alpha, const double* y, double* z, int guarded)
   if (amode == 0) {
     e.go("smoother", 17.0 * c->n, [&] {
       k_mask_labeled<<<grid_for(c->n, 256), 256, 0, c->stream>>>(y, c->labels.ptr, z, (int)c->n, c->sc,
-                                                                 guarded);
+                                                                 guarded, (int)c->row_base);
     });
     return;
   }
@@ -300,6 +322,7 @@ void enq_smoother(Enq& e, double alpha, const double* y, double* z, int guarded)
   a.labels = c->labels.ptr;
   a.alpha = alpha;
   a.alpha_mode = amode;
+  a.row_base = (int)c->row_base;
   const double bytes = 4.0 * (c->n + 1) + 4.0 * c->l_nnz + 8.0 * c->n + 1.0 * c->n + 16.0 * c->n;
   e.go("smoother", bytes, [&] { launch_segsum<SEG_LROWS>(c, c->plan_lr, a, guarded, 0); });
 }
@@ -331,7 +354,7 @@ void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, i
     int nb = 0;
     CK(cudaFuncSetAttribute(k_cg_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cg_step, 256, smem));
-    c->step_blocks = std::max(1, std::min(nb, 4)) * c->num_sms;
+    c->step_blocks = std::max(1, std::min(nb, 6)) * c->num_sms;
   }
   CK(cudaLaunchCooperativeKernel((void*)k_cg_step, dim3(c->step_blocks), dim3(256), args, smem,
                                  c->stream));
@@ -395,7 +418,7 @@ void enq_fsda_tail(Enq& e, int ns) {
   e.go("orient", 8.0 * n * ns + 1.0 * n, [&] {
     dim3 g(grid_for(nlN, WARPS_PER_BLOCK), ns);
     k_orient<<<g, LEAF_THREADS, 0, c->stream>>>(c->labels.ptr, c->scores.ptr, n, c->part_o.ptr,
-                                                nlN, c->sc, ss, ns);
+                                                nlN, c->sc, ss, ns, nullptr);
   });
   e.go("flip", 0.0, [&] {
     dim3 g((unsigned)std::min<long long>(grid_for(std::max(n, d), 256), 1024), ns);
@@ -406,9 +429,23 @@ void enq_fsda_tail(Enq& e, int ns) {
 // Build (or reuse) the whole-solve graph with a conditional WHILE node.
 bool build_solve_graph(fsda_ctx* c, double alpha, int ns, long long max_iter, double tol,
                        long long* launches_fixed, long long* launches_body) {
-  char key[256];
-  snprintf(key, sizeof(key), "%a|%d|%lld|%a|%lld|%lld|%llu", alpha, ns, max_iter, tol, c->n, c->nnz,
-           g_alloc_gen);
+  // The key covers everything baked into the graph's kernel arguments:
+  // scalars, buffer generation (pointers), and the plan structs by value.
+  unsigned long long h = 1469598103934665603ULL;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* b = (const unsigned char*)p;
+    for (size_t k = 0; k < n; ++k) h = (h ^ b[k]) * 1099511628211ULL;
+  };
+  mix(&c->plan_xr.pl, sizeof(SegPlan));
+  mix(&c->plan_lr.pl, sizeof(SegPlan));
+  mix(&c->plan_xc.pl, sizeof(SegPlan));
+  mix(&c->xh, sizeof(XtDense));
+  mix(&c->ell, sizeof(c->ell));
+  mix(&c->n1, sizeof(c->n1));
+  mix(&c->n2, sizeof(c->n2));
+  char key[320];
+  snprintf(key, sizeof(key), "%a|%d|%lld|%a|%lld|%lld|%lld|%llu|%llx", alpha, ns, max_iter, tol, c->n,
+           c->d, c->nnz, g_alloc_gen, h);
   if (c->exec && c->graph_key == key) {
     *launches_fixed = c->graph_fixed;
     *launches_body = c->graph_body;
@@ -573,7 +610,8 @@ int read_results(fsda_ctx* c, int ns, const SolveOut& o, int64_t* launches) {
 // device index stream `ind`.  Classes: W = 1 << k for segments with n <= 8W,
 // heavy tasks of <= 4 leaves for n > 256.
 template <typename OffT>
-void build_seg_plan(HostPlan& hp, const OffT* offs, long long S, const int* ind) {
+void build_seg_plan(HostPlan& hp, const OffT* offs, long long S, const int* ind,
+                    std::vector<int>* dense_out = nullptr, long long dense_min = 0) {
   std::vector<int4> cls[6], heavy;
   std::vector<int> h0, hn, hs, ht;
   int leaves = 0;
@@ -583,6 +621,8 @@ void build_seg_plan(HostPlan& hp, const OffT* offs, long long S, const int* ind)
       int k = 0;
       while (8 * (1 << k) < n) ++k;
       cls[k].push_back(make_int4((int)sgi, lo, n, -1));
+    } else if (dense_out && n >= dense_min) {
+      dense_out->push_back((int)sgi);
     } else {
       const int h = (int)h0.size();
       const int nseg = (int)cdiv(n, LEAF);
@@ -636,6 +676,78 @@ void build_seg_plan(HostPlan& hp, const OffT* offs, long long S, const int* ind)
   pl.seg_part = hp.part.ptr;
 }
 
+// Per-row-block slice tasks for the dense columns (k_xt_coop phase 1a).
+void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
+  const long long nh = (long long)dense.size();
+  const int nb = (int)std::max<long long>(1, cdiv(c->n, XT_RB));
+  c->xh_col.ensure(nh);
+  c->xh_bptr.ensure(nh * (nb + 1));
+  c->xh_part.ensure(nh * nb);
+  std::vector<int> bptr;
+  if (nh) {
+    CK(cudaMemcpy(c->xh_col.ptr, dense.data(), sizeof(int) * nh, cudaMemcpyHostToDevice));
+    k_heavy_bptr<<<grid_for(nh * (nb + 1), 256), 256, 0, c->stream>>>(
+        c->csc_colptr.ptr, c->csc_rows.ptr, c->xh_col.ptr, c->xh_bptr.ptr, nh, nb);
+    CKL();
+    bptr.resize(nh * (nb + 1));
+    CK(cudaMemcpyAsync(bptr.data(), c->xh_bptr.ptr, sizeof(int) * bptr.size(), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  std::vector<int4> tasks;
+  std::vector<long long> boff((size_t)(nb + 1) * 7, 0), bwarp((size_t)nb * 7, 0);
+  std::vector<int4> cls[6], longs;
+  for (int b = 0; b < nb; ++b) {
+    for (auto& v : cls) v.clear();
+    longs.clear();
+    for (long long h = 0; h < nh; ++h) {
+      const int lo = bptr[h * (nb + 1) + b], n = bptr[h * (nb + 1) + b + 1] - lo;
+      if (n == 0) continue;  // partial stays 0.0 (see below)
+      if (n <= LEAF) {
+        int k = 0;
+        while (8 * (1 << k) < n) ++k;
+        cls[k].push_back(make_int4((int)h, lo, n, 0));
+      } else {
+        longs.push_back(make_int4((int)h, lo, n, 0));
+      }
+    }
+    long long wb = 0;
+    for (int k = 0; k < 6; ++k) {
+      boff[(size_t)b * 7 + k] = (long long)tasks.size();
+      bwarp[(size_t)b * 7 + k] = wb;
+      tasks.insert(tasks.end(), cls[k].begin(), cls[k].end());
+      wb += cdiv((long long)cls[k].size(), 32 >> k);
+    }
+    bwarp[(size_t)b * 7 + 6] = wb;
+    boff[(size_t)b * 7 + 6] = (long long)tasks.size();
+    tasks.insert(tasks.end(), longs.begin(), longs.end());
+  }
+  for (int k = 0; k < 7; ++k) boff[(size_t)nb * 7 + k] = (long long)tasks.size();
+  c->xh_tasks.ensure(tasks.size());
+  c->xh_boff.ensure(boff.size());
+  c->xh_bwarp.ensure(bwarp.size());
+  if (!tasks.empty())
+    CK(cudaMemcpy(c->xh_tasks.ptr, tasks.data(), sizeof(int4) * tasks.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->xh_boff.ptr, boff.data(), sizeof(long long) * boff.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->xh_bwarp.ptr, bwarp.data(), sizeof(long long) * bwarp.size(), cudaMemcpyHostToDevice));
+  // empty slices never get a task: their partials must read 0.0
+  if (nh) CK(cudaMemset(c->xh_part.ptr, 0, sizeof(double) * nh * nb));
+  if (c->xt_blocks == 0) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_xt_coop, 256, 0));
+    c->xt_blocks = std::max(1, std::min(per_sm, 6)) * c->num_sms;
+  }
+  XtDense& xh = c->xh;
+  xh.rows = c->csc_rows.ptr;
+  xh.tasks = c->xh_tasks.ptr;
+  xh.boff = c->xh_boff.ptr;
+  xh.bwarp = c->xh_bwarp.ptr;
+  xh.col = c->xh_col.ptr;
+  xh.part = c->xh_part.ptr;
+  xh.n_dense = nh;
+  xh.nb = nb;
+}
+
 int check_err_flag(fsda_ctx* c, const char* what) {
   int h = 0;
   CK(cudaMemcpy(&h, c->err.ptr, sizeof(int), cudaMemcpyDeviceToHost));
@@ -652,14 +764,13 @@ void upload_narrow(fsda_ctx* c, const int64_t* host, long long n, long long limi
   out.ensure(n + 8);  // tail padding: the row kernels stage indices with 16-byte loads
   CK(cudaMemsetAsync(out.ptr + n, 0, 8 * sizeof(int), c->stream));
   if (n == 0) return;
-  long long* tmp = nullptr;
-  CK(cudaMalloc(&tmp, sizeof(long long) * n));
+  c->scratch_i64.ensure(n);
+  long long* tmp = c->scratch_i64.ptr;
   CK(cudaMemcpyAsync(tmp, host, sizeof(long long) * n, cudaMemcpyHostToDevice, c->stream));
   int g = (int)std::min<long long>(cdiv(n, 256), (long long)c->num_sms * 32);
   k_narrow_idx<<<g, 256, 0, c->stream>>>(tmp, out.ptr, n, limit, c->err.ptr);
   CKL();
   CK(cudaStreamSynchronize(c->stream));
-  cudaFree(tmp);
 }
 
 #define API_BEGIN(ctx)                                   \
@@ -728,6 +839,17 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     c->invalidate_graph();
     DevBuf<int>* ib[] = {&c->x_rowptr, &c->x_cols, &c->csc_colptr, &c->csc_rows, &c->l_rowptr,
                          &c->l_cols, &c->active, &c->good, &c->pending, &c->flip, &c->err};
+    c->scratch_i64.release();
+    c->scratch_f64.release();
+    c->scratch_row_of.release();
+    c->scratch_keys.release();
+    c->scratch_sort.release();
+    c->xh_col.release();
+    c->xh_bptr.release();
+    c->xh_tasks.release();
+    c->xh_boff.release();
+    c->xh_bwarp.release();
+    c->xh_part.release();
     c->plan_xr.release();
     c->plan_lr.release();
     c->plan_xc.release();
@@ -777,7 +899,6 @@ int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* ro
   if (n_rows > MAX_REDUCE || n_cols > MAX_REDUCE)
     return fail(FSDA_EINVAL, "vector length above the two-level reduction limit (%lld)", MAX_REDUCE);
   c->has_x = false;
-  c->invalidate_graph();
   CK(cudaMemset(c->err.ptr, 0, sizeof(int)));
   c->n = n_rows;
   c->d = n_cols;
@@ -787,7 +908,7 @@ int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* ro
   int rc = check_err_flag(c, "X");
   if (rc) return rc;
   // row ids + in-row order validation
-  DevBuf<int> row_of;
+  DevBuf<int>& row_of = c->scratch_row_of;
   row_of.ensure(nnz);
   if (n_rows > 0) {
     k_row_ids<<<grid_for(n_rows, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr,
@@ -796,11 +917,11 @@ int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* ro
   }
   CK(cudaStreamSynchronize(c->stream));
   rc = check_err_flag(c, "X");
-  if (rc) { row_of.release(); return rc; }
+  if (rc) return rc;
   // CSC by a stable radix sort of (column, row) pairs: rows stay ascending.
   c->csc_rows.ensure(nnz);
   c->csc_colptr.ensure(n_cols + 1);
-  DevBuf<int> keys_out;
+  DevBuf<int>& keys_out = c->scratch_keys;
   keys_out.ensure(nnz);
   if (nnz > 0) {
     int end_bit = 1;
@@ -808,64 +929,83 @@ int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* ro
     size_t temp_bytes = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, c->x_cols.ptr, keys_out.ptr, row_of.ptr,
                                        c->csc_rows.ptr, (int)nnz, 0, end_bit, c->stream));
-    void* temp = nullptr;
-    CK(cudaMalloc(&temp, std::max<size_t>(temp_bytes, 1)));
+    c->scratch_sort.ensure(temp_bytes);
+    void* temp = c->scratch_sort.ptr;
     CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, c->x_cols.ptr, keys_out.ptr, row_of.ptr,
                                        c->csc_rows.ptr, (int)nnz, 0, end_bit, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    cudaFree(temp);
   }
   k_colptr_from_sorted<<<grid_for(n_cols + 1, 256), 256, 0, c->stream>>>(keys_out.ptr, nnz,
                                                                           c->csc_colptr.ptr, (int)n_cols);
   CKL();
   CK(cudaStreamSynchronize(c->stream));
-  keys_out.release();
-  row_of.release();
   build_seg_plan(c->plan_xr, row_offsets, n_rows, c->x_cols.ptr);
   {
     std::vector<int> colptr(n_cols + 1);
     CK(cudaMemcpy(colptr.data(), c->csc_colptr.ptr, sizeof(int) * (n_cols + 1), cudaMemcpyDeviceToHost));
-    build_seg_plan(c->plan_xc, colptr.data(), n_cols, c->csc_rows.ptr);
+    std::vector<int> dense;
+    const long long dense_min = std::max<long long>(LEAF + 1, cdiv(n_rows, 64));
+    build_seg_plan(c->plan_xc, colptr.data(), n_cols, c->csc_rows.ptr, &dense, dense_min);
+    build_dense_plan(c, dense);
   }
+
   c->has_x = true;
   return FSDA_OK;
   API_END
 }
 
-int fsda_upload_laplacian(fsda_ctx* c, int64_t n, const int64_t* row_offsets,
-                          const int64_t* col_indices, const double* values) {
-  API_BEGIN(c)
+static int upload_laplacian_rows(fsda_ctx* c, int64_t n, int64_t n_global, int64_t row_base,
+                                 const int64_t* row_offsets, const int64_t* col_indices,
+                                 const double* values) {
   if (!c->has_x) return fail(FSDA_EINVAL, "upload X before the Laplacian");
   if (n != c->n) return fail(FSDA_EINVAL, "laplacian must be square with one row per sample");
+  if (row_base < 0 || row_base + n > n_global)
+    return fail(FSDA_EINVAL, "laplacian row block outside [0, n_global)");
   if (!row_offsets) return fail(FSDA_EINVAL, "row_offsets is null");
   const long long nnz = row_offsets[n];
   if (row_offsets[0] != 0 || nnz < 0) return fail(FSDA_EINVAL, "row_offsets must be non-decreasing from 0 to nnz");
-  if (nnz >= (1LL << 31) - 1) return fail(FSDA_EINVAL, "Laplacian too large for int32 indices");
+  if (nnz >= (1LL << 31) - 1 || n_global >= (1LL << 31) - 1)
+    return fail(FSDA_EINVAL, "Laplacian too large for int32 indices");
   c->has_l = false;
-  c->invalidate_graph();
   CK(cudaMemset(c->err.ptr, 0, sizeof(int)));
   c->l_nnz = nnz;
+  c->row_base = row_base;
+  c->n_global = n_global;
   upload_narrow(c, row_offsets, n + 1, nnz, c->l_rowptr);
-  upload_narrow(c, col_indices, nnz, n - 1, c->l_cols);
+  upload_narrow(c, col_indices, nnz, n_global - 1, c->l_cols);
   int rc = check_err_flag(c, "laplacian");
   if (rc) return rc;
   c->l_diag.ensure(n);
   if (n > 0) {
-    double* dvals = nullptr;
-    CK(cudaMalloc(&dvals, sizeof(double) * std::max<long long>(nnz, 1)));
+    c->scratch_f64.ensure(std::max<long long>(nnz, 1));
+    double* dvals = c->scratch_f64.ptr;
     if (nnz > 0)
       CK(cudaMemcpyAsync(dvals, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, c->stream));
     k_laplacian_split<<<grid_for(n, 256), 256, 0, c->stream>>>(c->l_rowptr.ptr, c->l_cols.ptr, dvals,
-                                                               c->l_diag.ptr, (int)n, c->err.ptr);
+                                                               c->l_diag.ptr, (int)n, c->err.ptr,
+                                                               (int)row_base);
     CKL();
     CK(cudaStreamSynchronize(c->stream));
-    cudaFree(dvals);
   }
   rc = check_err_flag(c, "laplacian");
   if (rc) return rc;
   build_seg_plan(c->plan_lr, row_offsets, n, c->l_cols.ptr);
   c->has_l = true;
   return FSDA_OK;
+}
+
+int fsda_upload_laplacian(fsda_ctx* c, int64_t n, const int64_t* row_offsets,
+                          const int64_t* col_indices, const double* values) {
+  API_BEGIN(c)
+  return upload_laplacian_rows(c, n, n, 0, row_offsets, col_indices, values);
+  API_END
+}
+
+int fsda_upload_laplacian_rows(fsda_ctx* c, int64_t n_local, int64_t n_global, int64_t row_base,
+                               const int64_t* row_offsets, const int64_t* col_indices,
+                               const double* values) {
+  API_BEGIN(c)
+  return upload_laplacian_rows(c, n_local, n_global, row_base, row_offsets, col_indices, values);
   API_END
 }
 
@@ -1143,6 +1283,173 @@ int fsda_shifted_cg_dense(fsda_ctx* c, int64_t dim, const double* a, const doubl
   k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns);
   CKL();
   SolveOut o{solutions, nullptr, residuals, iterations, converged, n_applies, fail_iter};
+  return read_results(c, ns, o, nullptr);
+  API_END
+}
+
+// ---- row-sharded building blocks -------------------------------------------
+
+int fsda_dev_xrows(fsda_ctx* c, const double* d_v, double* d_y) {
+  API_BEGIN(c)
+  if (!c->has_x) return fail(FSDA_EINVAL, "X has not been uploaded");
+  ensure_vectors(c, 1);
+  Enq e{c};
+  enq_xrows(e, d_v, d_y, 0);
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_dev_smoother(fsda_ctx* c, double alpha, const double* d_y_full, double* d_z) {
+  API_BEGIN(c)
+  if (!c->has_l || !c->has_labels) return fail(FSDA_EINVAL, "Laplacian and labels must be uploaded");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(FSDA_EINVAL, "alpha must lie in [0, 1], got %g", alpha);
+  ensure_vectors(c, 1);
+  Enq e{c};
+  enq_smoother(e, alpha, d_y_full, d_z, 0);
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_dev_xt_partial(fsda_ctx* c, const double* d_z, double* d_out) {
+  API_BEGIN(c)
+  if (!c->has_x) return fail(FSDA_EINVAL, "X has not been uploaded");
+  ensure_vectors(c, 1);
+  Enq e{c};
+  enq_xt(e, d_z, d_out, 0, nullptr, 0, nullptr);
+  const long long nl = n_leaves(c->n);
+  k_vector_sum<<<grid_for(nl, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+      d_z, c->n, c->part_n.ptr, nl, c->sc, d_out + c->d);
+  CKL();
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_dev_class_sums(fsda_ctx* c, const double* d_t, double* d_out) {
+  API_BEGIN(c)
+  if (!c->has_labels) return fail(FSDA_EINVAL, "labels have not been set");
+  ensure_vectors(c, 1);
+  const long long nl = n_leaves(c->n);
+  k_class_sums<<<grid_for(nl, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+      d_t, c->labels.ptr, c->n, c->part_n.ptr, nl, c->sc, 1.0, 1.0);
+  CKL();
+  CK(cudaMemcpyAsync(d_out, &c->sc->class_mean1, 2 * sizeof(double), cudaMemcpyDeviceToDevice,
+                     c->stream));
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_dev_apply_w(fsda_ctx* c, double c1, double c2, double* d_w) {
+  API_BEGIN(c)
+  if (!c->has_labels) return fail(FSDA_EINVAL, "labels have not been set");
+  ensure_vectors(c, 1);
+  const double cm[2] = {c1, c2};
+  CK(cudaMemcpyAsync(&c->sc->class_mean1, cm, 2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  const long long nl = n_leaves(c->n);
+  k_apply_w<<<grid_for(nl, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+      c->labels.ptr, d_w, c->n, c->part_n.ptr, nl, c->sc);
+  CKL();
+  CK(cudaStreamSynchronize(c->stream));  // cm lives on this stack frame
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_dev_center(fsda_ctx* c, const double* d_mu, double* d_q, double scale) {
+  API_BEGIN(c)
+  k_center<<<grid_for(c->d, 256), 256, 0, c->stream>>>(d_mu, d_q, c->d, scale);
+  CKL();
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_dev_cg_begin(fsda_ctx* c, const double* betas, int ns, double tol, int64_t max_iter,
+                      const double* d_b) {
+  API_BEGIN(c)
+  if (c->d <= 0) return fail(FSDA_EINVAL, "operator dimension must be positive");
+  if (ns <= 0) return fail(FSDA_EINVAL, "shift grid must be a non-empty 1-d array");
+  for (int s = 0; s < ns; ++s) {
+    if (!std::isfinite(betas[s])) return fail(FSDA_EINVAL, "shifts must be finite");
+    if (s == 0 && betas[s] < 0) return fail(FSDA_EINVAL, "shifts must be non-negative");
+    if (s > 0 && !(betas[s] > betas[s - 1])) return fail(FSDA_EINVAL, "shifts must be strictly ascending");
+  }
+  if (!(tol > 0)) return fail(FSDA_EINVAL, "tol must be positive");
+  upload_solve_params(c, betas, ns, nullptr);
+  ShiftState ss = c->shifts();
+  const long long d = c->d, nlD = n_leaves(d);
+  k_solve_reset<<<1, 256, 0, c->stream>>>(c->sc, ss, ns, max_iter, tol, 0);
+  CKL();
+  dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
+  k_cg_init<<<g, LEAF_THREADS, 0, c->stream>>>(d_b, c->r0.ptr, c->p.ptr, c->bigp.ptr, c->sols.ptr, d,
+                                               c->part_d.ptr, nlD, c->sc, ss, ns);
+  CKL();
+  c->r_ns = ns;
+  CK(cudaStreamSynchronize(c->stream));  // betas were read from host memory
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_dev_cg_step(fsda_ctx* c, const double* d_q) {
+  API_BEGIN(c)
+  if (c->r_ns <= 0) return fail(FSDA_EINVAL, "call fsda_dev_cg_begin first");
+  if (d_q != c->q.ptr)
+    CK(cudaMemcpyAsync(c->q.ptr, d_q, sizeof(double) * c->d, cudaMemcpyDeviceToDevice, c->stream));
+  launch_cg_step(c, c->r_ns, c->d, 0, 0, false);
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_dev_cg_direction(fsda_ctx* c, const double** d_p) {
+  API_BEGIN(c)
+  ensure_vectors(c, 1);
+  *d_p = c->p.ptr;
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_dev_cg_status(fsda_ctx* c, int* finished, int64_t* iterations, int* status) {
+  API_BEGIN(c)
+  CgScalars h;
+  CK(cudaMemcpyAsync(&h, c->sc, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (finished) *finished = h.finished;
+  if (iterations) *iterations = h.iter;
+  if (status) *status = h.status;
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_dev_project(fsda_ctx* c, double* d_scores, double* d_orient) {
+  API_BEGIN(c)
+  const int ns = c->r_ns;
+  if (ns <= 0) return fail(FSDA_EINVAL, "call fsda_dev_cg_begin first");
+  const long long n = c->n, d = c->d, nlN = n_leaves(n);
+  ShiftState ss = c->shifts();
+  k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns);
+  k_transpose_sols<<<grid_for(d * ns, 256), 256, 0, c->stream>>>(c->sols.ptr, c->wT.ptr, d, ns);
+  if (n > 0)
+    k_spmm_scores<<<grid_for(n, 8), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr, c->wT.ptr,
+                                                         d_scores, (int)n, ns);
+  dim3 g(grid_for(nlN, WARPS_PER_BLOCK), ns);
+  k_orient<<<g, LEAF_THREADS, 0, c->stream>>>(c->labels.ptr, d_scores, n, c->part_o.ptr, nlN, c->sc,
+                                              ss, ns, d_orient);
+  CKL();
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_dev_finish(fsda_ctx* c, const uint8_t* flip, double* d_scores, double* directions,
+                    double* residuals, int64_t* iterations, uint8_t* converged, int64_t* n_applies,
+                    int64_t* fail_iter) {
+  API_BEGIN(c)
+  const int ns = c->r_ns;
+  if (ns <= 0) return fail(FSDA_EINVAL, "call fsda_dev_cg_begin first");
+  std::vector<int> fl(ns);
+  for (int s = 0; s < ns; ++s) fl[s] = flip[s] ? 1 : 0;
+  CK(cudaMemcpyAsync(c->flip.ptr, fl.data(), sizeof(int) * ns, cudaMemcpyHostToDevice, c->stream));
+  ShiftState ss = c->shifts();
+  dim3 g((unsigned)std::min<long long>(grid_for(std::max(c->n, c->d), 256), 1024), ns);
+  k_flip<<<g, 256, 0, c->stream>>>(d_scores, c->sols.ptr, c->n, c->d, ss);
+  CKL();
+  SolveOut o{directions, nullptr, residuals, iterations, converged, n_applies, fail_iter};
   return read_results(c, ns, o, nullptr);
   API_END
 }

@@ -330,7 +330,7 @@ __global__ void k_transpose_sols(const double* __restrict__ sols, double* __rest
 // leaves; blockIdx.y = shift.  The last block sets the flip flags.
 __global__ void k_orient(const signed char* __restrict__ labels, const double* __restrict__ scores,
                          long long n, double* __restrict__ part, long long n_leaf, CgScalars* sc,
-                         ShiftState ss, int ns) {
+                         ShiftState ss, int ns, double* dots_out) {
   __shared__ double smem[257];
   const int lane = threadIdx.x & 31;
   const long long g = (long long)blockIdx.x * WARPS_PER_BLOCK + (threadIdx.x >> 5);
@@ -348,7 +348,10 @@ __global__ void k_orient(const signed char* __restrict__ labels, const double* _
   if (arrive_last(&sc->counters[C_ORIENT], gridDim.x * gridDim.y)) {
     for (int t = 0; t < ns; ++t) {
       double v = block_reduce_partials(part + (long long)t * n_leaf, n_leaf, smem);
-      if (threadIdx.x == 0) ss.flip[t] = (v < 0.0) ? 1 : 0;
+      if (threadIdx.x == 0) {
+        ss.flip[t] = (v < 0.0) ? 1 : 0;
+        if (dots_out) dots_out[t] = v;
+      }
     }
   }
 }
@@ -421,7 +424,7 @@ __global__ void k_encode_cols(const int* __restrict__ cols, const int* __restric
 // Laplacian: extract the diagonal values and check every off-diagonal is -1.
 __global__ void k_laplacian_split(const int* __restrict__ rowptr, const int* __restrict__ cols,
                                   const double* __restrict__ vals, double* __restrict__ diag,
-                                  int n, int* err) {
+                                  int n, int* err, int row_base) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int lo = rowptr[i], hi = rowptr[i + 1];
@@ -429,7 +432,7 @@ __global__ void k_laplacian_split(const int* __restrict__ rowptr, const int* __r
   for (int jj = lo; jj < hi; ++jj) {
     int c = cols[jj];
     if (jj > lo && c <= cols[jj - 1]) atomicExch(err, 3);
-    if (c == i) dv = vals[jj];
+    if (c == i + row_base) dv = vals[jj];
     else if (vals[jj] != -1.0) atomicExch(err, 4);
   }
   diag[i] = dv;

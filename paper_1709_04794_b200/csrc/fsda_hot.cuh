@@ -170,6 +170,7 @@ struct SegArgs {
   const signed char* labels;
   double alpha;
   int alpha_mode;
+  int row_base;              // global index of local row 0 (row-sharded L)
   // X^T columns: 0 raw, 1 centred (mu, *sum_ptr), 2 divided by ell
   int mode;
   const double* mu;
@@ -183,7 +184,7 @@ struct SegArgs {
 template <int KIND>
 __device__ __forceinline__ double seg_term(const SegArgs& a, int seg, int idx, double dg) {
   const double v = __ldg(a.src + idx);
-  if (KIND == SEG_LROWS) return (idx == seg) ? dg * v : -v;
+  if (KIND == SEG_LROWS) return (idx == seg + a.row_base) ? dg * v : -v;
   return v;
 }
 
@@ -192,7 +193,7 @@ __device__ __forceinline__ void seg_finish(const SegArgs& a, int seg, double s) 
   if (KIND == SEG_XROWS) {
     a.out[seg] = s;
   } else if (KIND == SEG_LROWS) {
-    const double masked = a.labels[seg] != 0 ? a.src[seg] : 0.0;
+    const double masked = a.labels[seg] != 0 ? a.src[seg + a.row_base] : 0.0;
     const double smoothed = a.alpha * s;
     a.out[seg] = (a.alpha_mode == 1) ? smoothed : (1.0 - a.alpha) * masked + smoothed;
   } else {
@@ -258,7 +259,37 @@ __device__ __forceinline__ void seg_class_task(const SegPlan& pl, const SegArgs&
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(256) k_segsum(SegPlan pl, SegArgs a, const CgScalars* sc,
+__device__ __forceinline__ void seg_heavy_task(const SegPlan& pl, const SegArgs& a, long long tw,
+                                               int lane) {
+  // heavy task: up to 4 consecutive leaves of one segment
+  const int4 tk = __ldg(pl.tasks + pl.cls_off[6] + (tw - pl.warp_base[6]));
+  const int h = tk.w;
+  const int leaf0 = __ldg(pl.heavy_seg0 + h) + (tk.y - __ldg(pl.heavy_start + h)) / LEAF;
+  for (int lf = 0; lf * LEAF < tk.z; ++lf) {
+    const double s = group_leaf<32, KIND>(pl, a, tk.x, tk.y + lf * LEAF,
+                                          min(LEAF, tk.z - lf * LEAF), lane);
+    if (lane == 0) pl.seg_part[leaf0 + lf] = s;
+  }
+  int is_last = 0;
+  if (lane == 0) {
+    __threadfence();
+    const unsigned old = atomicAdd(pl.heavy_count + h, 1u);
+    is_last = (old == (unsigned)__ldg(pl.heavy_ntask + h) - 1u);
+  }
+  is_last = __shfl_sync(FULL, is_last, 0);
+  if (is_last) {
+    __threadfence();
+    const double s = warp_reduce_partials(pl.seg_part + __ldg(pl.heavy_seg0 + h),
+                                          __ldg(pl.heavy_nseg + h), lane);
+    if (lane == 0) {
+      seg_finish<KIND>(a, tk.x, s);
+      pl.heavy_count[h] = 0u;
+    }
+  }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256, 6) k_segsum(SegPlan pl, SegArgs a, const CgScalars* sc,
                                                 int guarded) {
   if (guarded && loop_idle(sc)) return;
   const int lane = threadIdx.x & 31;
@@ -291,40 +322,210 @@ __global__ void __launch_bounds__(256) k_segsum(SegPlan pl, SegArgs a, const CgS
       if (lane == 0) a.sum_part[g] = s;
       continue;
     }
-    // heavy task: up to 4 consecutive leaves of one segment
-    const int4 tk = __ldg(pl.tasks + pl.cls_off[6] + (tw - pl.warp_base[6]));
-    const int h = tk.w;
-    const int leaf0 = __ldg(pl.heavy_seg0 + h) + (tk.y - __ldg(pl.heavy_start + h)) / LEAF;
-    for (int lf = 0; lf * LEAF < tk.z; ++lf) {
-      const double s = group_leaf<32, KIND>(pl, a, tk.x, tk.y + lf * LEAF,
-                                            min(LEAF, tk.z - lf * LEAF), lane);
-      if (lane == 0) pl.seg_part[leaf0 + lf] = s;
+    seg_heavy_task<KIND>(pl, a, tw, lane);
+  }
+}
+
+// ------------------------------------------ K3: X^T z, dense columns blocked
+// Canonical column sum:
+//   * n <= 256: the R256 leaf over z[rows] in row order;
+//   * n > 256 and sparse (64 n < N): R256 over its leaves of 256 entries;
+//   * dense (n > 256 and 64 n >= N — the Zipf head): rows are cut into blocks
+//     of XT_RB; partial_b = R256 over the column's entries in block b (0.0 if
+//     none); the column sum is R256 over (partial_0 .. partial_{nb-1}).
+// The dense rule lets a CTA stage one XT_RB-row block of z in shared memory
+// and serve every dense-column gather of that block from it.  Each (block,
+// dense column) slice is one task of the W-class scheme (host plan per
+// block), so a warp runs 32/W slices at once.  One cooperative launch:
+//   phase 1  CTA per row block: stage z, run the block's slice tasks;
+//            then warp tasks for the other columns (SegPlan, with the
+//            leaf-combining heavy tasks) and the leaf partials of sum(z)
+//   -- grid sync --
+//   phase 2  one warp per dense column reduces its nb partials.
+constexpr int XT_RB = 1024;
+
+struct XtDense {
+  const int* rows;        // CSC row indices
+  const int4* tasks;      // {dense id, start, length, -}, grouped by (block, class)
+  const long long* boff;  // per block: 6 class starts + long-slice start; (nb + 1) * 7
+  const long long* bwarp; // per block: warp prefixes of the 6 classes + total; nb * 7
+  const int* col;         // dense id -> column
+  double* part;           // nb partials per dense column
+  long long n_dense;
+  int nb;
+};
+
+template <int W>
+__device__ __forceinline__ void dense_slice_task(const XtDense& dn, const double* zs, int r0, int b,
+                                                 int cls, long long tw_local, int lane) {
+  constexpr int M = 32 / W;
+  constexpr int MA = M < 8 ? M : 8;
+  constexpr int KA = W >= 8 ? W / 4 : 1;
+  const long long* off = dn.boff + (long long)b * 7;
+  const long long* wb = dn.bwarp + (long long)b * 7;
+  const long long idx = off[cls] + (tw_local - wb[cls]) * (32 / W) + lane / W;
+  int4 tk = make_int4(-1, 0, 0, 0);
+  if (idx < off[cls + 1]) tk = __ldg(dn.tasks + idx);
+  const int t = lane & (W - 1);
+  const int n = tk.z;
+  int ix[MA * KA];
+#pragma unroll
+  for (int m = 0; m < MA; ++m)
+#pragma unroll
+    for (int k = 0; k < KA; ++k) {
+      const int e = t + m * W + 32 * k;
+      ix[m * KA + k] = (e < n) ? __ldg(dn.rows + tk.y + e) - r0 : 0;
     }
-    int is_last = 0;
-    if (lane == 0) {
-      __threadfence();
-      const unsigned old = atomicAdd(pl.heavy_count + h, 1u);
-      is_last = (old == (unsigned)__ldg(pl.heavy_ntask + h) - 1u);
-    }
-    is_last = __shfl_sync(FULL, is_last, 0);
-    if (is_last) {
-      __threadfence();
-      const double s = warp_reduce_partials(pl.seg_part + __ldg(pl.heavy_seg0 + h),
-                                            __ldg(pl.heavy_nseg + h), lane);
-      if (lane == 0) {
-        seg_finish<KIND>(a, tk.x, s);
-        pl.heavy_count[h] = 0u;
+  double A[MA];
+#pragma unroll
+  for (int m = 0; m < MA; ++m) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < KA; ++k)
+      if (t + m * W + 32 * k < n) acc = acc + zs[ix[m * KA + k]];
+    A[m] = acc;
+  }
+#pragma unroll
+  for (int j = MA / 2; j >= 1; j >>= 1)
+#pragma unroll
+    for (int m = 0; m < j; ++m) A[m] = A[m] + A[m + j];
+  double r = A[0];
+#pragma unroll
+  for (int off2 = W / 2; off2 >= 1; off2 >>= 1) r = r + __shfl_xor_sync(FULL, r, off2);
+  if (tk.x >= 0 && t == 0) dn.part[(long long)tk.x * dn.nb + b] = r;
+}
+
+// Slices longer than 256 entries: R256 over their leaves by one warp.
+__device__ __forceinline__ void dense_slice_long(const XtDense& dn, const double* zs, int r0, int b,
+                                                 const int4 tk, int lane) {
+  double acc = 0.0;
+  const int nl = (tk.z + LEAF - 1) / LEAF;
+  for (int g = 0; g < nl; ++g) {
+    const int base = tk.y + g * LEAF, len = min(LEAF, tk.z - g * LEAF);
+    int ri[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) ri[u] = (lane + 32 * u < len) ? __ldg(dn.rows + base + lane + 32 * u) - r0 : 0;
+    double a = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (lane + 32 * u < len) a = a + zs[ri[u]];
+    a = butterfly(a);
+    if ((g & 31) == lane) acc = acc + a;
+  }
+  acc = butterfly(acc);
+  if (lane == 0) dn.part[(long long)tk.x * dn.nb + b] = acc;
+}
+
+__global__ void __launch_bounds__(256, 6) k_xt_coop(SegPlan pl, XtDense dn, SegArgs a,
+                                                    const CgScalars* sc, int guarded, int n_rows) {
+  if (guarded && loop_idle(sc)) return;  // uniform across the grid
+  __shared__ double zs[XT_RB];
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // ---- phase 1a: row blocks with their dense-column slices
+  if (dn.n_dense > 0) {
+    for (int b = blockIdx.x; b < dn.nb; b += gridDim.x) {
+      const int r0 = b * XT_RB;
+      const int nr = min(XT_RB, n_rows - r0);
+      __syncthreads();
+      for (int k = threadIdx.x; k < nr; k += blockDim.x) zs[k] = __ldg(a.src + r0 + k);
+      __syncthreads();
+      const long long* wb = dn.bwarp + (long long)b * 7;
+      // class warp tasks
+      for (long long tw = warp; tw < wb[6]; tw += nw) {
+        int k = 0;
+        while (tw >= wb[k + 1]) ++k;
+        switch (k) {
+          case 0: dense_slice_task<1>(dn, zs, r0, b, 0, tw, lane); break;
+          case 1: dense_slice_task<2>(dn, zs, r0, b, 1, tw, lane); break;
+          case 2: dense_slice_task<4>(dn, zs, r0, b, 2, tw, lane); break;
+          case 3: dense_slice_task<8>(dn, zs, r0, b, 3, tw, lane); break;
+          case 4: dense_slice_task<16>(dn, zs, r0, b, 4, tw, lane); break;
+          default: dense_slice_task<32>(dn, zs, r0, b, 5, tw, lane); break;
+        }
       }
+      // long slices (> 256 entries): one warp each; stored after the classes
+      const long long l0 = dn.boff[(long long)b * 7 + 6];
+      const long long l1 = dn.boff[(long long)(b + 1) * 7 + 0];
+      for (long long j = l0 + warp; j < l1; j += nw) dense_slice_long(dn, zs, r0, b, __ldg(dn.tasks + j), lane);
     }
   }
+  // ---- phase 1b: the other columns and the sum(z) leaves (warp tasks)
+  const long long total = pl.warp_base[8];
+  const long long nwarps = (long long)gridDim.x * nw;
+  for (long long tw = (long long)blockIdx.x * nw + warp; tw < total; tw += nwarps) {
+    if (tw < pl.warp_base[6]) {
+      int k = 0;
+      while (tw >= pl.warp_base[k + 1]) ++k;
+      switch (k) {
+        case 0: seg_class_task<1, SEG_XCOLS>(pl, a, 0, tw, lane); break;
+        case 1: seg_class_task<2, SEG_XCOLS>(pl, a, 1, tw, lane); break;
+        case 2: seg_class_task<4, SEG_XCOLS>(pl, a, 2, tw, lane); break;
+        case 3: seg_class_task<8, SEG_XCOLS>(pl, a, 3, tw, lane); break;
+        case 4: seg_class_task<16, SEG_XCOLS>(pl, a, 4, tw, lane); break;
+        default: seg_class_task<32, SEG_XCOLS>(pl, a, 5, tw, lane); break;
+      }
+    } else if (tw < pl.warp_base[7]) {
+      seg_heavy_task<SEG_XCOLS>(pl, a, tw, lane);
+    } else {
+      const long long g = tw - pl.warp_base[7];
+      double v = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const long long i = g * LEAF + k * 32 + lane;
+        if (i < a.sum_n) v = v + __ldg(a.src + i);
+      }
+      v = butterfly(v);
+      if (lane == 0) a.sum_part[g] = v;
+    }
+  }
+  if (dn.n_dense == 0) return;
+  grid.sync();
+  // ---- phase 2: dense columns
+  const long long gw = (long long)blockIdx.x * nw + warp;
+  for (long long h = gw; h < dn.n_dense; h += nwarps) {
+    const double v = warp_reduce_partials(dn.part + h * dn.nb, dn.nb, lane);
+    if (lane == 0) seg_finish<SEG_XCOLS>(a, __ldg(dn.col + h), v);
+  }
+}
+
+// bptr[h * (nb + 1) + b] = first position in column dense_col[h] whose row is
+// >= b * XT_RB (b = nb gives the column end).
+__global__ void k_heavy_bptr(const int* __restrict__ colptr, const int* __restrict__ rows,
+                             const int* __restrict__ heavy_col, int* __restrict__ bptr,
+                             long long n_heavy, int nb) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_heavy * (nb + 1)) return;
+  const long long h = t / (nb + 1);
+  const int b = (int)(t - h * (nb + 1));
+  const int c = heavy_col[h];
+  int lo = colptr[c], hi = colptr[c + 1];
+  if (b == nb) { bptr[t] = hi; return; }
+  const int target = b * XT_RB;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (rows[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  bptr[t] = lo;
 }
 
 // z = masked y (apply_smoother at alpha == 0: no Laplacian term, sda.py:135-136).
 __global__ void k_mask_labeled(const double* __restrict__ y, const signed char* __restrict__ labels,
-                               double* __restrict__ z, int n, const CgScalars* sc, int guarded) {
+                               double* __restrict__ z, int n, const CgScalars* sc, int guarded,
+                               int row_base) {
   if (guarded && loop_idle(sc)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) z[i] = labels[i] != 0 ? y[i] : 0.0;
+  if (i < n) z[i] = labels[i] != 0 ? y[i + row_base] : 0.0;
+}
+
+// q[i] = q[i] - mu[i] * q[d]  (centring of an all-reduced [X^T z | sum z]),
+// or q[i] = q[i] / scale when mu is null (labeled mean).
+__global__ void k_center(const double* __restrict__ mu, double* __restrict__ q, long long d,
+                         double scale) {
+  const double s = mu ? q[d] : 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < d;
+       i += (long long)gridDim.x * blockDim.x)
+    q[i] = mu ? q[i] - mu[i] * s : q[i] / scale;
 }
 
 // -------------------------------------------- K4: one cooperative CG step
@@ -345,7 +546,7 @@ __global__ void k_mask_labeled(const double* __restrict__ y, const signed char* 
 //      the iteration, and sets the while-loop condition.
 // Scalars needed after block 0 starts writing them are read into registers
 // at kernel entry, so no block reads state that block 0 modifies.
-__global__ void __launch_bounds__(256) k_cg_step(
+__global__ void __launch_bounds__(256, 5) k_cg_step(
     double* __restrict__ q, double* __restrict__ p, double* __restrict__ r0,
     double* __restrict__ r1, double* __restrict__ bigp, double* __restrict__ sols, long long d,
     double* __restrict__ part_pq, double* __restrict__ part_rr, long long n_leaf, CgScalars* sc,

@@ -78,6 +78,10 @@ int fsda_upload_laplacian(fsda_ctx* ctx, int64_t n, const int64_t* row_offsets,
 
 /* Ternary labels, N entries, labeled-first (LabelVector, sparse.py:198-235). */
 int fsda_set_labels(fsda_ctx* ctx, const int8_t* labels);
+/* Labels as an arbitrary mask (no labeled-first requirement): the batched
+ * label-mask solves of nested cross-validation (evaluation.py:110-123 permutes
+ * every fold to labeled-first instead; the result is the same operator). */
+int fsda_set_label_mask(fsda_ctx* ctx, const int8_t* labels);
 
 /* ---- single products, host buffers in and out (parity probes) ---------- */
 /* y = X v                         SparseMatrix.matvec            sparse.py:116-121 */

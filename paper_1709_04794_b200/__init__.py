@@ -43,6 +43,7 @@ from .fsda import (
     matvec_transpose,
     shifted_cg,
     solve,
+    solve_label_sets,
 )
 
 __version__ = "0.1.0"
@@ -54,5 +55,5 @@ __all__ = [
     "as_shift_grid", "build_sparse",
     "ALGORITHMS", "Device", "DeviceProblem", "LinearOperator", "apply_smoother",
     "centered_matvec_transpose", "default_device", "fsda_operator_apply", "fsda_solve",
-    "install_into_sdakit", "labeled_mean", "matvec", "matvec_transpose", "shifted_cg", "solve",
+    "install_into_sdakit", "labeled_mean", "matvec", "matvec_transpose", "shifted_cg", "solve", "solve_label_sets",
 ]

@@ -131,6 +131,7 @@ struct fsda_ctx {
   DevBuf<double> xh_part;
   XtDense xh{};
   int xt_blocks = 0;
+  DevBuf<unsigned long long> xt_ticket;  // phase-1b work ticket (reset by the kernel)
   int step_blocks = 0;  // cooperative grid of k_cg_step
 
   // L: CSR with diagonal entries in place, diag values split out.  Row-sharded
@@ -290,7 +291,9 @@ void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* sum
     XtDense xh = c->xh;
     const CgScalars* sc = c->sc;
     int n_rows = (int)c->n;
-    void* args[] = {(void*)&pl, (void*)&xh, (void*)&a, (void*)&sc, (void*)&guarded, (void*)&n_rows};
+    unsigned long long* ticket = c->xt_ticket.ptr;
+    void* args[] = {(void*)&pl, (void*)&xh, (void*)&a, (void*)&sc, (void*)&guarded, (void*)&n_rows,
+                    (void*)&ticket};
     CK(cudaLaunchCooperativeKernel((void*)k_xt_coop, dim3(c->xt_blocks), dim3(256), args, 0,
                                    c->stream));
   });
@@ -746,6 +749,11 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   xh.part = c->xh_part.ptr;
   xh.n_dense = nh;
   xh.nb = nb;
+  xh.splits = (int)std::max<long long>(1, c->xt_blocks / nb);
+  if (!c->xt_ticket.ptr) {
+    c->xt_ticket.ensure(1);
+    CK(cudaMemset(c->xt_ticket.ptr, 0, sizeof(unsigned long long)));
+  }
 }
 
 int check_err_flag(fsda_ctx* c, const char* what) {
@@ -844,6 +852,7 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     c->scratch_row_of.release();
     c->scratch_keys.release();
     c->scratch_sort.release();
+    c->xt_ticket.release();
     c->xh_col.release();
     c->xh_bptr.release();
     c->xh_tasks.release();
@@ -944,7 +953,7 @@ int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* ro
     std::vector<int> colptr(n_cols + 1);
     CK(cudaMemcpy(colptr.data(), c->csc_colptr.ptr, sizeof(int) * (n_cols + 1), cudaMemcpyDeviceToHost));
     std::vector<int> dense;
-    const long long dense_min = std::max<long long>(LEAF + 1, cdiv(n_rows, 64));
+    const long long dense_min = std::max<long long>(LEAF + 1, cdiv(n_rows, XT_DENSE_DIV));
     build_seg_plan(c->plan_xc, colptr.data(), n_cols, c->csc_rows.ptr, &dense, dense_min);
     build_dense_plan(c, dense);
   }
@@ -1009,8 +1018,7 @@ int fsda_upload_laplacian_rows(fsda_ctx* c, int64_t n_local, int64_t n_global, i
   API_END
 }
 
-int fsda_set_labels(fsda_ctx* c, const int8_t* labels) {
-  API_BEGIN(c)
+static int set_labels_impl(fsda_ctx* c, const int8_t* labels, bool require_first) {
   if (!c->has_x) return fail(FSDA_EINVAL, "upload X before the labels");
   long long n1 = 0, n2 = 0;
   bool seen_unlabeled = false, labeled_first = true;
@@ -1022,7 +1030,7 @@ int fsda_set_labels(fsda_ctx* c, const int8_t* labels) {
     if (l == 0) seen_unlabeled = true;
     else if (seen_unlabeled) labeled_first = false;
   }
-  if (!labeled_first)
+  if (require_first && !labeled_first)
     return fail(FSDA_EINVAL,
                 "labeled samples must occupy the first rows; use arrange_labeled_first to permute the problem");
   c->labels.ensure(std::max<long long>(c->n, 1));
@@ -1034,6 +1042,17 @@ int fsda_set_labels(fsda_ctx* c, const int8_t* labels) {
   c->ell = n1 + n2;
   c->has_labels = true;
   return FSDA_OK;
+}
+
+int fsda_set_labels(fsda_ctx* c, const int8_t* labels) {
+  API_BEGIN(c)
+  return set_labels_impl(c, labels, true);
+  API_END
+}
+
+int fsda_set_label_mask(fsda_ctx* c, const int8_t* labels) {
+  API_BEGIN(c)
+  return set_labels_impl(c, labels, false);
   API_END
 }
 

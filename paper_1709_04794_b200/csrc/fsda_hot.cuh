@@ -329,8 +329,8 @@ __global__ void __launch_bounds__(256, 6) k_segsum(SegPlan pl, SegArgs a, const 
 // ------------------------------------------ K3: X^T z, dense columns blocked
 // Canonical column sum:
 //   * n <= 256: the R256 leaf over z[rows] in row order;
-//   * n > 256 and sparse (64 n < N): R256 over its leaves of 256 entries;
-//   * dense (n > 256 and 64 n >= N — the Zipf head): rows are cut into blocks
+//   * n > 256 and sparse (8 n < N): R256 over its leaves of 256 entries;
+//   * dense (n > 256 and 8 n >= N — the Zipf head): rows are cut into blocks
 //     of XT_RB; partial_b = R256 over the column's entries in block b (0.0 if
 //     none); the column sum is R256 over (partial_0 .. partial_{nb-1}).
 // The dense rule lets a CTA stage one XT_RB-row block of z in shared memory
@@ -343,6 +343,7 @@ __global__ void __launch_bounds__(256, 6) k_segsum(SegPlan pl, SegArgs a, const 
 //   -- grid sync --
 //   phase 2  one warp per dense column reduces its nb partials.
 constexpr int XT_RB = 1024;
+constexpr int XT_DENSE_DIV = 8;  // dense: n > 256 and XT_DENSE_DIV * n >= N
 
 struct XtDense {
   const int* rows;        // CSC row indices
@@ -353,6 +354,7 @@ struct XtDense {
   double* part;           // nb partials per dense column
   long long n_dense;
   int nb;
+  int splits;             // CTAs sharing one row block's slices
 };
 
 template <int W>
@@ -417,22 +419,25 @@ __device__ __forceinline__ void dense_slice_long(const XtDense& dn, const double
 }
 
 __global__ void __launch_bounds__(256, 6) k_xt_coop(SegPlan pl, XtDense dn, SegArgs a,
-                                                    const CgScalars* sc, int guarded, int n_rows) {
+                                                    const CgScalars* sc, int guarded, int n_rows,
+                                                    unsigned long long* ticket) {
   if (guarded && loop_idle(sc)) return;  // uniform across the grid
   __shared__ double zs[XT_RB];
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  // ---- phase 1a: row blocks with their dense-column slices
+  // ---- phase 1a: (row block, split) units with their dense-column slices
   if (dn.n_dense > 0) {
-    for (int b = blockIdx.x; b < dn.nb; b += gridDim.x) {
+    const long long units = (long long)dn.nb * dn.splits;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+      const int b = (int)(u / dn.splits), sp = (int)(u - (long long)b * dn.splits);
       const int r0 = b * XT_RB;
       const int nr = min(XT_RB, n_rows - r0);
       __syncthreads();
       for (int k = threadIdx.x; k < nr; k += blockDim.x) zs[k] = __ldg(a.src + r0 + k);
       __syncthreads();
       const long long* wb = dn.bwarp + (long long)b * 7;
-      // class warp tasks
-      for (long long tw = warp; tw < wb[6]; tw += nw) {
+      const long long c0 = wb[6] * sp / dn.splits, c1 = wb[6] * (sp + 1) / dn.splits;
+      for (long long tw = c0 + warp; tw < c1; tw += nw) {
         int k = 0;
         while (tw >= wb[k + 1]) ++k;
         switch (k) {
@@ -444,16 +449,21 @@ __global__ void __launch_bounds__(256, 6) k_xt_coop(SegPlan pl, XtDense dn, SegA
           default: dense_slice_task<32>(dn, zs, r0, b, 5, tw, lane); break;
         }
       }
-      // long slices (> 256 entries): one warp each; stored after the classes
+      // long slices (> 256 entries): one warp each, dealt round-robin over splits
       const long long l0 = dn.boff[(long long)b * 7 + 6];
       const long long l1 = dn.boff[(long long)(b + 1) * 7 + 0];
-      for (long long j = l0 + warp; j < l1; j += nw) dense_slice_long(dn, zs, r0, b, __ldg(dn.tasks + j), lane);
+      for (long long j = l0 + sp + (long long)dn.splits * warp; j < l1; j += (long long)dn.splits * nw)
+        dense_slice_long(dn, zs, r0, b, __ldg(dn.tasks + j), lane);
     }
   }
-  // ---- phase 1b: the other columns and the sum(z) leaves (warp tasks)
+  // ---- phase 1b: the other columns and the sum(z) leaves; warps draw tasks
+  // from a grid-wide ticket so CTAs that staged a dense block catch up
   const long long total = pl.warp_base[8];
-  const long long nwarps = (long long)gridDim.x * nw;
-  for (long long tw = (long long)blockIdx.x * nw + warp; tw < total; tw += nwarps) {
+  for (;;) {
+    long long tw = 0;
+    if (lane == 0) tw = (long long)atomicAdd(ticket, 1ULL);
+    tw = __shfl_sync(FULL, tw, 0);
+    if (tw >= total) break;
     if (tw < pl.warp_base[6]) {
       int k = 0;
       while (tw >= pl.warp_base[k + 1]) ++k;
@@ -479,8 +489,9 @@ __global__ void __launch_bounds__(256, 6) k_xt_coop(SegPlan pl, XtDense dn, SegA
       if (lane == 0) a.sum_part[g] = v;
     }
   }
-  if (dn.n_dense == 0) return;
   grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0ULL;  // every warp has drawn its last ticket
+  const long long nwarps = (long long)gridDim.x * nw;
   // ---- phase 2: dense columns
   const long long gw = (long long)blockIdx.x * nw + warp;
   for (long long h = gw; h < dn.n_dense; h += nwarps) {
@@ -601,6 +612,27 @@ __global__ void __launch_bounds__(256, 5) k_cg_step(
     a = butterfly(a);
     if (lane == 0) part_pq[g] = a;
   }
+  // The P update owed from the previous iteration (krylov.py:241) needs none
+  // of this iteration's scalars, so it fills phase A while the p.q leaves
+  // finish.  It is applied to every shift that was active and good last
+  // iteration; a shift that turns out degenerate now is frozen and its P is
+  // never read again (krylov.py:251-255).
+  {
+    const long long n_half = 2 * n_leaf;
+    const long long units = (long long)ns * n_half;
+    for (long long u = gw; u < units; u += tw) {
+      const int s = (int)(u / n_half);
+      const long long h = u - (long long)s * n_half;
+      if (!ss.pending[s]) continue;
+      const double zc = ss.zeta[s], as = ss.alpha_s[s];
+      double* P = bigp + (long long)s * d;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const long long i = h * 128 + k * 32 + lane;
+        if (i < d) P[i] = zc * r_cur[i] + as * P[i];
+      }
+    }
+  }
   grid.sync();
 
   // ---- B: scalars, then the updates
@@ -656,22 +688,12 @@ __global__ void __launch_bounds__(256, 5) k_cg_step(
       const long long h = v - (long long)s * n_half;
       if (s_good[s] == 0.0) continue;
       const double gs = s_gs[s];
-      const int pend = ss.pending[s];
-      const double zc = ss.zeta[s], as = ss.alpha_s[s];
-      double* P = bigp + (long long)s * d;
+      const double* P = bigp + (long long)s * d;
       double* X = sols + (long long)s * d;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const long long i = h * 128 + k * 32 + lane;
-        if (i < d) {
-          double pv = P[i];
-          const double xv = X[i];
-          if (pend) {
-            pv = zc * r_cur[i] + as * pv;
-            P[i] = pv;
-          }
-          X[i] = xv - pv * gs;
-        }
+        if (i < d) X[i] = X[i] - __ldcg(P + i) * gs;   // krylov.py:230
       }
     }
   }

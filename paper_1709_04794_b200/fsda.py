@@ -140,6 +140,15 @@ class Device:
             raise ValueError(f"labels cover {lab.size} samples but x has {self.n} rows")
         _raise_for(_capi.lib().fsda_set_labels(self._h, _capi.i8ptr(lab)), fam)
 
+    def set_label_mask(self, labels, fam=_OWN):
+        """Labels in any row order (the nested-CV mask form, no labeled-first
+        requirement)."""
+        lab = np.ascontiguousarray(getattr(labels, "labels", labels), dtype=np.int8)
+        if lab.size != self.n:
+            raise ValueError(f"labels cover {lab.size} samples but x has {self.n} rows")
+        _raise_for(_capi.lib().fsda_set_label_mask(self._h, _capi.i8ptr(lab)), fam)
+        self._loaded = (self._loaded[0], self._loaded[1], None)
+
     def load_problem(self, p, fam=_OWN, reuse: bool = False):
         """Upload p.x, p.lap and p.labels.  With reuse=True, objects already
         resident (same immutable objects as the last load) are not re-sent."""
@@ -363,6 +372,33 @@ class DeviceProblem:
                                   p.max_iter_d if max_iter is None else max_iter, probe, fam=self.fam)
         q = _pytypes.SimpleNamespace(betas=grid, alpha=alpha, x=p.x)
         return _report(q, res, self.fam, t0)
+
+
+def solve_label_sets(x, lap, label_sets, alpha, betas, tol: float = 1e-8, max_iter: int = 1000,
+                     seeds=0, *, device: Optional[Device] = None, scores: bool = True):
+    """Many FSDA sweeps on one dataset: X and L are uploaded once and every
+    label set (any row order — a mask, as the folds of nested CV) is solved
+    against them.  Each result is what fsda_solve returns for that task after
+    the reference's arrange_labeled_first permutation and its undo
+    (evaluation.py:110-123), up to the summation order of the permuted rows.
+
+    Returns a list of SweepResult (directions n_shifts x D, scores n_shifts x N
+    in the original row order)."""
+    dev = device or default_device()
+    dev.upload_x(x)
+    dev.upload_laplacian(lap)
+    grid = T.as_shift_grid(betas)
+    sets = [np.asarray(getattr(l, "labels", l), dtype=np.int8) for l in label_sets]
+    seed_list = list(seeds) if np.ndim(seeds) else [int(seeds)] * len(sets)
+    out = []
+    for lab, seed in zip(sets, seed_list):
+        if not (np.any(lab == 1) and np.any(lab == -1)):
+            raise ValueError("both classes need at least one labeled sample")
+        dev.set_label_mask(lab)
+        probe = np.random.default_rng(seed).uniform(-1.0, 1.0, size=int(x.n_cols))
+        out.append(dev.solve_fsda(alpha, grid.betas, tol, max_iter, probe, scores=scores))
+    dev._loaded = (None, None, None)
+    return out
 
 
 # ----------------------------------------------- device parity primitives

@@ -378,3 +378,44 @@ def test_cfg2_full_k_bitwise_vs_oracle(cfg2):
     np.testing.assert_array_equal(_dirs(rep, cfg2.betas), ref["directions"])
     np.testing.assert_array_equal(_scores(rep, cfg2.betas), ref["scores"])
     assert rep.regression.operator_applications == 100
+
+
+# ------------------------------------------ batched label-mask solves (§8f #1)
+
+def test_label_set_batch_matches_oracle_and_permuted_reference():
+    """Folds given as label masks in the original row order: bitwise equal to
+    the C oracle on the same masks, and within 1e-6 of the reference-order
+    solve of the labeled-first permutation (what nested_cv does,
+    evaluation.py:110-123) at a stable Krylov dimension."""
+    w = make_workload("cfg1", n=2500, d=900, ell=250, n_pos=50, lam=12.0, k=6, n_shifts=5)
+    rng = np.random.default_rng(3)
+    sets = []
+    for f in range(3):
+        lab = np.zeros(w.n, dtype=np.int8)
+        idx = rng.choice(w.n, size=120, replace=False)
+        lab[idx] = -1
+        lab[idx[:30]] = 1
+        sets.append(lab)
+    x = fb.SparseMatrix.binary(w.n, w.d, w.x_offsets, w.x_cols)
+    lap = fb.Laplacian(fb.SparseMatrix(w.n, w.n, w.l_offsets, w.l_cols, w.l_vals), w.degrees)
+    res = fb.solve_label_sets(x, lap, sets, w.alpha, w.betas, w.tol, 15, seeds=[0, 1, 2])
+    for lab, r, seed in zip(sets, res, [0, 1, 2]):
+        probe = np.random.default_rng(seed).uniform(-1, 1, w.d)
+        ref = c_oracle.fsda_solve(w.x_offsets, w.x_cols, w.d, w.l_offsets, w.l_cols, w.l_vals, lab,
+                                  w.alpha, w.betas, w.tol, 15, probe)
+        np.testing.assert_array_equal(r.directions, ref["directions"])
+        np.testing.assert_array_equal(r.scores, ref["scores"])
+        # the reference's route: permute labeled-first, solve, undo
+        perm = np.concatenate([np.flatnonzero(lab != 0), np.flatnonzero(lab == 0)])
+        inv = np.empty_like(perm)
+        inv[perm] = np.arange(perm.size)
+        import scipy.sparse as sp
+
+        X = sp.csr_matrix((np.ones(w.nnz), w.x_cols, w.x_offsets), shape=(w.n, w.d))[perm]
+        L = sp.csr_matrix((w.l_vals, w.l_cols, w.l_offsets), shape=(w.n, w.n))[perm][:, perm]
+        X.sort_indices()
+        L.sort_indices()
+        prob = ref_numpy.Problem(X.indptr, X.indices, w.d, L.indptr, L.indices, L.data, lab[perm])
+        rr = ref_numpy.fsda_solve(prob, w.alpha, w.betas, w.tol, 15, seed)
+        assert rel_rows(r.directions, rr["directions"]) <= 1e-6
+        assert rel_rows(r.scores, rr["scores"][:, inv]) <= 1e-6

@@ -294,7 +294,7 @@ void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* sum
     unsigned long long* ticket = c->xt_ticket.ptr;
     void* args[] = {(void*)&pl, (void*)&xh, (void*)&a, (void*)&sc, (void*)&guarded, (void*)&n_rows,
                     (void*)&ticket};
-    CK(cudaLaunchCooperativeKernel((void*)k_xt_coop, dim3(c->xt_blocks), dim3(256), args, 0,
+    CK(cudaLaunchCooperativeKernel((void*)k_xt_coop, dim3(c->xt_blocks), dim3(1024), args, 0,
                                    c->stream));
   });
 }
@@ -353,13 +353,14 @@ void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, i
                   (void*)&d, (void*)&pp, (void*)&pr, (void*)&nlD, (void*)&sc, (void*)&ss,
                   (void*)&ns, (void*)&cond, (void*)&use_cond, (void*)&mu, (void*)&pz, (void*)&nlz};
   const size_t smem = step_smem(ns);
+  // One 1024-thread CTA per SM: a grid barrier then has 148 arrivals.
   if (c->step_blocks == 0) {
     int nb = 0;
     CK(cudaFuncSetAttribute(k_cg_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cg_step, 256, smem));
-    c->step_blocks = std::max(1, std::min(nb, 6)) * c->num_sms;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cg_step, 1024, smem));
+    c->step_blocks = std::max(1, std::min(nb, 1)) * c->num_sms;
   }
-  CK(cudaLaunchCooperativeKernel((void*)k_cg_step, dim3(c->step_blocks), dim3(256), args, smem,
+  CK(cudaLaunchCooperativeKernel((void*)k_cg_step, dim3(c->step_blocks), dim3(1024), args, smem,
                                  c->stream));
 }
 
@@ -737,8 +738,8 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   if (nh) CK(cudaMemset(c->xh_part.ptr, 0, sizeof(double) * nh * nb));
   if (c->xt_blocks == 0) {
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_xt_coop, 256, 0));
-    c->xt_blocks = std::max(1, std::min(per_sm, 6)) * c->num_sms;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_xt_coop, 1024, 0));
+    c->xt_blocks = std::max(1, std::min(per_sm, 1)) * c->num_sms;
   }
   XtDense& xh = c->xh;
   xh.rows = c->csc_rows.ptr;

@@ -418,7 +418,7 @@ __device__ __forceinline__ void dense_slice_long(const XtDense& dn, const double
   if (lane == 0) dn.part[(long long)tk.x * dn.nb + b] = acc;
 }
 
-__global__ void __launch_bounds__(256, 6) k_xt_coop(SegPlan pl, XtDense dn, SegArgs a,
+__global__ void __launch_bounds__(1024, 1) k_xt_coop(SegPlan pl, XtDense dn, SegArgs a,
                                                     const CgScalars* sc, int guarded, int n_rows,
                                                     unsigned long long* ticket) {
   if (guarded && loop_idle(sc)) return;  // uniform across the grid
@@ -557,7 +557,7 @@ __global__ void k_center(const double* __restrict__ mu, double* __restrict__ q, 
 //      the iteration, and sets the while-loop condition.
 // Scalars needed after block 0 starts writing them are read into registers
 // at kernel entry, so no block reads state that block 0 modifies.
-__global__ void __launch_bounds__(256, 5) k_cg_step(
+__global__ void __launch_bounds__(1024, 1) k_cg_step(
     double* __restrict__ q, double* __restrict__ p, double* __restrict__ r0,
     double* __restrict__ r1, double* __restrict__ bigp, double* __restrict__ sols, long long d,
     double* __restrict__ part_pq, double* __restrict__ part_rr, long long n_leaf, CgScalars* sc,
@@ -611,27 +611,6 @@ __global__ void __launch_bounds__(256, 5) k_cg_step(
     }
     a = butterfly(a);
     if (lane == 0) part_pq[g] = a;
-  }
-  // The P update owed from the previous iteration (krylov.py:241) needs none
-  // of this iteration's scalars, so it fills phase A while the p.q leaves
-  // finish.  It is applied to every shift that was active and good last
-  // iteration; a shift that turns out degenerate now is frozen and its P is
-  // never read again (krylov.py:251-255).
-  {
-    const long long n_half = 2 * n_leaf;
-    const long long units = (long long)ns * n_half;
-    for (long long u = gw; u < units; u += tw) {
-      const int s = (int)(u / n_half);
-      const long long h = u - (long long)s * n_half;
-      if (!ss.pending[s]) continue;
-      const double zc = ss.zeta[s], as = ss.alpha_s[s];
-      double* P = bigp + (long long)s * d;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const long long i = h * 128 + k * 32 + lane;
-        if (i < d) P[i] = zc * r_cur[i] + as * P[i];
-      }
-    }
   }
   grid.sync();
 
@@ -688,12 +667,22 @@ __global__ void __launch_bounds__(256, 5) k_cg_step(
       const long long h = v - (long long)s * n_half;
       if (s_good[s] == 0.0) continue;
       const double gs = s_gs[s];
-      const double* P = bigp + (long long)s * d;
+      const int pend = ss.pending[s];
+      const double zc = ss.zeta[s], as = ss.alpha_s[s];
+      double* P = bigp + (long long)s * d;
       double* X = sols + (long long)s * d;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const long long i = h * 128 + k * 32 + lane;
-        if (i < d) X[i] = X[i] - __ldcg(P + i) * gs;   // krylov.py:230
+        if (i < d) {
+          double pv = P[i];
+          const double xv = X[i];
+          if (pend) {  // the P update owed from the previous iteration (krylov.py:241)
+            pv = zc * r_cur[i] + as * pv;
+            P[i] = pv;
+          }
+          X[i] = xv - pv * gs;  // krylov.py:230
+        }
       }
     }
   }

@@ -147,6 +147,16 @@ int fsda_shifted_cg_dense(fsda_ctx* ctx, int64_t dim, const double* a, const dou
                           int64_t* iterations, uint8_t* converged, int64_t* n_applies,
                           int64_t* fail_iter);
 
+/* Regression-phase shifted solve: (X^T X + beta I) w = rhs for
+ * every beta at once (shifted_cg(regression_operator(p), rhs, ...),
+ * sda.py:177-179, 339, 439-442; bench_shifted, evaluation.py:288-291), with
+ * the same device recurrence and graph loop as fsda_solve.  solutions is
+ * n_shifts x D; rhs is D doubles (host). */
+int fsda_regression_shifted_cg(fsda_ctx* ctx, const double* rhs, const double* betas,
+                               int n_shifts, double tol, int64_t max_iter, int absolute_tol,
+                               double* solutions, double* residuals, int64_t* iterations,
+                               uint8_t* converged, int64_t* n_applies, int64_t* fail_iter);
+
 /* ---- row-sharded building blocks ---------------------------
  * One context per GPU holds a contiguous row block [row_base, row_base+N_g)
  * of X (uploaded with fsda_upload_x as an N_g x D matrix) and of L

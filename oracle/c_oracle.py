@@ -62,6 +62,9 @@ def lib():
         h.oracle_shifted_cg_dense.restype = C.c_int
         h.oracle_shifted_cg_dense.argtypes = [_I64, _PD, _PD, _PD, C.c_int, C.c_double, _I64, C.c_int,
                                               _PD, _PD, _PI64, _PU8, _PI64, _PI64]
+        h.oracle_regression_shifted_cg.restype = C.c_int
+        h.oracle_regression_shifted_cg.argtypes = [_I64, _I64, _PI64, _PI64, _PD, _PD, C.c_int, C.c_double,
+                                                   _I64, C.c_int, _PD, _PD, _PI64, _PU8, _PI64, _PI64]
         h.oracle_fsda_solve.restype = C.c_int
         h.oracle_fsda_solve.argtypes = [_I64, _I64, _PI64, _PI64, _PI64, _PI64, _PD, _PI8, C.c_double,
                                         _PD, C.c_int, C.c_double, _I64, _PD, C.c_int, _PD, _PD, _PD,
@@ -193,6 +196,28 @@ def shifted_cg_dense(a, b, betas, tol=1e-8, max_iter=1000, absolute_tol=False):
                                        int(bool(absolute_tol)), sols.ctypes.data_as(_PD),
                                        res.ctypes.data_as(_PD), its.ctypes.data_as(_PI64),
                                        conv.ctypes.data_as(_PU8), C.byref(napp), C.byref(fail))
+    if st:
+        raise OracleFailure(st, fail.value)
+    return sols, res, its, conv.astype(bool), napp.value
+
+
+def regression_shifted_cg(xoffs, xcols, d, b, betas, tol=1e-8, max_iter=1000, absolute_tol=False):
+    """shifted_cg on X^T X (the regression phase) in the device's summation order."""
+    xo, pxo = _i(xoffs)
+    xc, pxc = _i(xcols)
+    b, pb = _d(b)
+    betas, pbe = _d(betas)
+    ns = betas.size
+    sols = np.empty((ns, d))
+    res = np.empty(ns)
+    its = np.empty(ns, dtype=np.int64)
+    conv = np.empty(ns, dtype=np.uint8)
+    napp, fail = C.c_int64(0), C.c_int64(-1)
+    st = lib().oracle_regression_shifted_cg(xo.size - 1, d, pxo, pxc, pb, pbe, ns, float(tol),
+                                            int(max_iter), int(bool(absolute_tol)),
+                                            sols.ctypes.data_as(_PD), res.ctypes.data_as(_PD),
+                                            its.ctypes.data_as(_PI64), conv.ctypes.data_as(_PU8),
+                                            C.byref(napp), C.byref(fail))
     if st:
         raise OracleFailure(st, fail.value)
     return sols, res, its, conv.astype(bool), napp.value

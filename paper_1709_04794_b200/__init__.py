@@ -41,6 +41,8 @@ from .fsda import (
     labeled_mean,
     matvec,
     matvec_transpose,
+    RegressionOperator,
+    regression_operator,
     shifted_cg,
     solve,
     solve_label_sets,
@@ -55,5 +57,5 @@ __all__ = [
     "as_shift_grid", "build_sparse",
     "ALGORITHMS", "Device", "DeviceProblem", "LinearOperator", "apply_smoother",
     "centered_matvec_transpose", "default_device", "fsda_operator_apply", "fsda_solve",
-    "install_into_sdakit", "labeled_mean", "matvec", "matvec_transpose", "shifted_cg", "solve", "solve_label_sets",
+    "install_into_sdakit", "labeled_mean", "matvec", "matvec_transpose", "shifted_cg", "solve", "solve_label_sets", "RegressionOperator", "regression_operator",
 ]

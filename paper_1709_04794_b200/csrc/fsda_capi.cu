@@ -164,6 +164,10 @@ struct fsda_ctx {
   bool cond_supported = true;
 
   long long graph_fixed = 0, graph_body = 0;  // launches in the cached graph
+  // which operator the solve graph runs: 0 FSDA (sda.py:162-174), 1 the
+  // regression operator X^T X (sda.py:177-179) on a caller-supplied rhs
+  int solve_kind = 0;
+  int solve_abs_tol = 0;
 
   // resident-solve parameters
   double r_alpha = 0.0, r_tol = 0.0;
@@ -430,6 +434,53 @@ void enq_fsda_tail(Enq& e, int ns) {
   });
 }
 
+// Regression-phase shifted solve (shifted_cg(regression_operator(p), b),
+// sda.py:177-179, 339, 439-442; evaluation.py:288-291): w -> X^T (X w).
+void enq_reg_setup(Enq& e, int ns, long long max_iter, double tol, int abs_tol) {
+  fsda_ctx* c = e.c;
+  const long long d = c->d, nlD = n_leaves(d);
+  ShiftState ss = c->shifts();
+  e.go("solve_reset", 0.0, [&] {
+    k_solve_reset<<<1, 256, 0, c->stream>>>(c->sc, ss, ns, max_iter, tol, abs_tol);
+  });
+  e.go("cg_init", 8.0 * d * 3 + 16.0 * d * ns, [&] {
+    dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
+    k_cg_init<<<g, LEAF_THREADS, 0, c->stream>>>(c->b.ptr, c->r0.ptr, c->p.ptr, c->bigp.ptr,
+                                                 c->sols.ptr, d, c->part_d.ptr, nlD, c->sc, ss, ns);
+  });
+}
+
+void enq_reg_iteration(Enq& e, int ns, unsigned long long cond, int use_cond) {
+  fsda_ctx* c = e.c;
+  const long long d = c->d;
+  enq_xrows(e, c->p.ptr, c->y.ptr, 1);
+  enq_xt(e, c->y.ptr, c->q.ptr, 0, nullptr, 1, nullptr);
+  e.go("cg_step", 24.0 * d + 24.0 * d + 32.0 * d * ns + 24.0 * d, [&] {
+    launch_cg_step(c, ns, d, cond, use_cond, false);
+  });
+}
+
+void enq_reg_tail(Enq& e, int ns) {
+  fsda_ctx* c = e.c;
+  ShiftState ss = c->shifts();
+  e.go("cg_finish", 0.0, [&] { k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns); });
+}
+
+void enq_setup_k(Enq& e, int ns, long long max_iter, double tol) {
+  if (e.c->solve_kind == 1) enq_reg_setup(e, ns, max_iter, tol, e.c->solve_abs_tol);
+  else enq_fsda_setup(e, ns, max_iter, tol);
+}
+
+void enq_iteration_k(Enq& e, double alpha, int ns, unsigned long long cond, int use_cond) {
+  if (e.c->solve_kind == 1) enq_reg_iteration(e, ns, cond, use_cond);
+  else enq_fsda_iteration(e, alpha, ns, cond, use_cond);
+}
+
+void enq_tail_k(Enq& e, int ns) {
+  if (e.c->solve_kind == 1) enq_reg_tail(e, ns);
+  else enq_fsda_tail(e, ns);
+}
+
 // Build (or reuse) the whole-solve graph with a conditional WHILE node.
 bool build_solve_graph(fsda_ctx* c, double alpha, int ns, long long max_iter, double tol,
                        long long* launches_fixed, long long* launches_body) {
@@ -448,8 +499,8 @@ bool build_solve_graph(fsda_ctx* c, double alpha, int ns, long long max_iter, do
   mix(&c->n1, sizeof(c->n1));
   mix(&c->n2, sizeof(c->n2));
   char key[320];
-  snprintf(key, sizeof(key), "%a|%d|%lld|%a|%lld|%lld|%lld|%llu|%llx", alpha, ns, max_iter, tol, c->n,
-           c->d, c->nnz, g_alloc_gen, h);
+  snprintf(key, sizeof(key), "%d|%d|%a|%d|%lld|%a|%lld|%lld|%lld|%llu|%llx", c->solve_kind,
+           c->solve_abs_tol, alpha, ns, max_iter, tol, c->n, c->d, c->nnz, g_alloc_gen, h);
   if (c->exec && c->graph_key == key) {
     *launches_fixed = c->graph_fixed;
     *launches_body = c->graph_body;
@@ -462,7 +513,7 @@ bool build_solve_graph(fsda_ctx* c, double alpha, int ns, long long max_iter, do
   CK(cudaStreamBeginCaptureToGraph(s, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   Enq e{c};
   try {
-    enq_fsda_setup(e, ns, max_iter, tol);
+    enq_setup_k(e, ns, max_iter, tol);
   } catch (...) {
     cudaGraph_t g2;
     cudaStreamEndCapture(s, &g2);
@@ -493,12 +544,12 @@ bool build_solve_graph(fsda_ctx* c, double alpha, int ns, long long max_iter, do
   Enq eb{c};
   cudaStream_t saved = c->stream;
   c->stream = s2;
-  enq_fsda_iteration(eb, alpha, ns, (unsigned long long)handle, 1);
+  enq_iteration_k(eb, alpha, ns, (unsigned long long)handle, 1);
   c->stream = saved;
   cudaGraph_t body_out;
   CK(cudaStreamEndCapture(s2, &body_out));
   CK(cudaStreamDestroy(s2));
-  enq_fsda_tail(e, ns);
+  enq_tail_k(e, ns);
   cudaGraph_t out;
   CK(cudaStreamEndCapture(s, &out));
   c->graph = out;
@@ -567,9 +618,9 @@ long long launch_solve(fsda_ctx* c, double alpha, int ns, long long max_iter, do
     }
   }
   Enq e{c, rec};
-  enq_fsda_setup(e, ns, max_iter, tol);
-  for (long long it = 0; it < max_iter; ++it) enq_fsda_iteration(e, alpha, ns, 0, 0);
-  enq_fsda_tail(e, ns);
+  enq_setup_k(e, ns, max_iter, tol);
+  for (long long it = 0; it < max_iter; ++it) enq_iteration_k(e, alpha, ns, 0, 0);
+  enq_tail_k(e, ns);
   c->last_launch_count = e.count;
   return e.count;
 }
@@ -1170,6 +1221,8 @@ int fsda_solve(fsda_ctx* c, double alpha, const double* betas, int ns, double to
   int rc = check_solve_args(c, alpha, betas, ns, tol);
   if (rc) return rc;
   if (!probe) return fail(FSDA_EINVAL, "probe is null");
+  c->solve_kind = 0;
+  c->solve_abs_tol = 0;
   upload_solve_params(c, betas, ns, probe);
   launch_solve(c, alpha, ns, max_iter, tol, nullptr);
   SolveOut o{directions, scores, residuals, iterations, converged, n_applies, fail_iter};
@@ -1182,6 +1235,8 @@ int fsda_prepare_resident(fsda_ctx* c, double alpha, const double* betas, int ns
   API_BEGIN(c)
   int rc = check_solve_args(c, alpha, betas, ns, tol);
   if (rc) return rc;
+  c->solve_kind = 0;
+  c->solve_abs_tol = 0;
   upload_solve_params(c, betas, ns, probe);
   CK(cudaStreamSynchronize(c->stream));
   c->r_alpha = alpha;
@@ -1471,6 +1526,32 @@ int fsda_dev_finish(fsda_ctx* c, const uint8_t* flip, double* d_scores, double* 
   CKL();
   SolveOut o{directions, nullptr, residuals, iterations, converged, n_applies, fail_iter};
   return read_results(c, ns, o, nullptr);
+  API_END
+}
+
+int fsda_regression_shifted_cg(fsda_ctx* c, const double* rhs, const double* betas, int ns,
+                                double tol, int64_t max_iter, int absolute_tol, double* solutions,
+                                double* residuals, int64_t* iterations, uint8_t* converged,
+                                int64_t* n_applies, int64_t* fail_iter) {
+  API_BEGIN(c)
+  if (!c->has_x) return fail(FSDA_EINVAL, "X has not been uploaded");
+  if (c->d <= 0) return fail(FSDA_EINVAL, "operator dimension must be positive");
+  if (ns <= 0) return fail(FSDA_EINVAL, "shift grid must be a non-empty 1-d array");
+  for (int s = 0; s < ns; ++s) {
+    if (!std::isfinite(betas[s])) return fail(FSDA_EINVAL, "shifts must be finite");
+    if (s == 0 && betas[s] < 0) return fail(FSDA_EINVAL, "shifts must be non-negative");
+    if (s > 0 && !(betas[s] > betas[s - 1])) return fail(FSDA_EINVAL, "shifts must be strictly ascending");
+  }
+  if (!(tol > 0)) return fail(FSDA_EINVAL, "tol must be positive");
+  upload_solve_params(c, betas, ns, nullptr);
+  CK(cudaMemcpyAsync(c->b.ptr, rhs, sizeof(double) * c->d, cudaMemcpyHostToDevice, c->stream));
+  c->solve_kind = 1;
+  c->solve_abs_tol = absolute_tol ? 1 : 0;
+  launch_solve(c, 0.0, ns, max_iter, tol, nullptr);
+  SolveOut o{solutions, nullptr, residuals, iterations, converged, n_applies, fail_iter};
+  const int rc = read_results(c, ns, o, nullptr);
+  c->solve_kind = 0;
+  return rc;
   API_END
 }
 

@@ -490,22 +490,74 @@ class LinearOperator:
         return cls(a.shape[0], dense=a)
 
 
+class RegressionOperator:
+    """w -> X^T X w (regression_operator, sda.py:177-179) held on the device;
+    shifted_cg on it runs the whole grid in one device solve (the regression
+    phase of CSR-SDA / SR-SDA and bench_shifted, evaluation.py:288-291)."""
+
+    def __init__(self, x, device: Optional[Device] = None):
+        self.x = x
+        self.dim = int(x.n_cols)
+        self.dev = device or default_device()
+        self.n_applies = 0
+
+    def _load(self):
+        self.dev.upload_x(self.x)
+        self.dev._loaded = (None, None, None)
+
+    def __call__(self, w):
+        self._load()
+        self.n_applies += 1
+        return self.dev.matvec_transpose(self.dev.matvec(w))
+
+    def reset_count(self):
+        self.n_applies = 0
+
+    def solve(self, b, betas, tol, max_iter, absolute_tol=False, fam=_OWN):
+        self._load()
+        b = _f64(b)
+        betas = _f64(betas)
+        ns = int(betas.size)
+        sols = np.empty((ns, self.dim))
+        res = np.empty(ns)
+        its = np.empty(ns, dtype=np.int64)
+        conv = np.empty(ns, dtype=np.uint8)
+        napp, fail = C.c_int64(0), C.c_int64(-1)
+        rc = _capi.lib().fsda_regression_shifted_cg(
+            self.dev._h, _capi.dptr(b), _capi.dptr(betas), ns, float(tol), int(max_iter),
+            int(bool(absolute_tol)), _capi.dptr(sols), _capi.dptr(res), _capi.i64ptr(its),
+            _capi.u8ptr(conv), C.byref(napp), C.byref(fail))
+        _raise_for(rc, fam)
+        self.n_applies += int(napp.value)
+        return sols, res, its, conv.astype(bool), int(napp.value)
+
+
+def regression_operator(p_or_x, device: Optional[Device] = None) -> RegressionOperator:
+    """The regression operator X^T X of a problem (or of a SparseMatrix)."""
+    x = getattr(p_or_x, "x", p_or_x)
+    return RegressionOperator(x, device)
+
+
 def shifted_cg(op, b, shifts, tol: float = 1e-8, max_iter: int = 1000, *,
                absolute_tol: bool = False) -> T.ShiftedSolveResult:
     """Device shifted CG (krylov.py:168-281) for a dense operator: same
     recurrences, freezing rules and result fields; op.n_applies advances by
     the number of base iterations run."""
-    dense = getattr(op, "dense", None)
-    if dense is None:
-        raise TypeError("device shifted_cg needs LinearOperator.from_dense (or use fsda_solve)")
     grid = T.as_shift_grid(shifts)
     b = _f64(b)
     if b.shape != (op.dim,):
         raise ValueError(f"rhs must have shape ({op.dim},)")
     if tol <= 0:
         raise ValueError("tol must be positive")
-    sols, res, its, conv, napp = default_device().shifted_cg_dense(
-        dense, b, grid.betas, tol, max_iter, absolute_tol)
-    op.n_applies += napp
+    if isinstance(op, RegressionOperator):
+        sols, res, its, conv, napp = op.solve(b, grid.betas, tol, max_iter, absolute_tol)
+    else:
+        dense = getattr(op, "dense", None)
+        if dense is None:
+            raise TypeError("device shifted_cg needs a device operator: LinearOperator.from_dense "
+                            "or regression_operator (or use fsda_solve)")
+        sols, res, its, conv, napp = default_device().shifted_cg_dense(
+            dense, b, grid.betas, tol, max_iter, absolute_tol)
+        op.n_applies += napp
     return T.ShiftedSolveResult(solutions=np.ascontiguousarray(sols.T), residual_norms=res,
                                 iterations=its, converged=conv)

@@ -157,6 +157,16 @@ int fsda_regression_shifted_cg(fsda_ctx* ctx, const double* rhs, const double* b
                                double* solutions, double* residuals, int64_t* iterations,
                                uint8_t* converged, int64_t* n_applies, int64_t* fail_iter);
 
+/* SA-SDA (sda.py:360-396): shifted CG in sample space on the
+ * centred spectral operator z -> M z - 1_l sum(M z) / l (sda.py:148-159),
+ * rhs = apply_w(probe) with probe the orthogonalized draw (sda.py:287-290,
+ * computed by the caller on the host: N doubles).  solutions (n_shifts x N)
+ * come back oriented (sda.py:256-262, 375-380); alpha == 0 is rejected with
+ * FSDA_EINVAL as the reference does. */
+int fsda_sa_solve(fsda_ctx* ctx, double alpha, const double* betas, int n_shifts, double tol,
+                  int64_t max_iter, const double* probe, double* solutions, double* residuals,
+                  int64_t* iterations, uint8_t* converged, int64_t* n_applies, int64_t* fail_iter);
+
 /* ---- row-sharded building blocks ---------------------------
  * One context per GPU holds a contiguous row block [row_base, row_base+N_g)
  * of X (uploaded with fsda_upload_x as an N_g x D matrix) and of L

@@ -65,6 +65,9 @@ def lib():
         h.oracle_regression_shifted_cg.restype = C.c_int
         h.oracle_regression_shifted_cg.argtypes = [_I64, _I64, _PI64, _PI64, _PD, _PD, C.c_int, C.c_double,
                                                    _I64, C.c_int, _PD, _PD, _PI64, _PU8, _PI64, _PI64]
+        h.oracle_sa_solve.restype = C.c_int
+        h.oracle_sa_solve.argtypes = [_I64, _PI64, _PI64, _PD, _PI8, C.c_double, _PD, C.c_int, C.c_double,
+                                      _I64, _PD, _PD, _PD, _PI64, _PU8, _PI64, _PI64]
         h.oracle_fsda_solve.restype = C.c_int
         h.oracle_fsda_solve.argtypes = [_I64, _I64, _PI64, _PI64, _PI64, _PI64, _PD, _PI8, C.c_double,
                                         _PD, C.c_int, C.c_double, _I64, _PD, C.c_int, _PD, _PD, _PD,
@@ -218,6 +221,30 @@ def regression_shifted_cg(xoffs, xcols, d, b, betas, tol=1e-8, max_iter=1000, ab
                                             sols.ctypes.data_as(_PD), res.ctypes.data_as(_PD),
                                             its.ctypes.data_as(_PI64), conv.ctypes.data_as(_PU8),
                                             C.byref(napp), C.byref(fail))
+    if st:
+        raise OracleFailure(st, fail.value)
+    return sols, res, its, conv.astype(bool), napp.value
+
+
+def sa_solve(loffs, lcols, lvals, labels, alpha, betas, tol, max_iter, probe):
+    """SA-SDA in the device's summation order; returns (solutions ns x N, residuals,
+    iterations, converged, n_applies)."""
+    lo, plo = _i(loffs)
+    lc, plc = _i(lcols)
+    lv, plv = _d(lvals)
+    lab, pl = _b(labels)
+    betas, pbe = _d(betas)
+    probe, ppr = _d(probe)
+    n, ns = lo.size - 1, betas.size
+    sols = np.empty((ns, n))
+    res = np.empty(ns)
+    its = np.empty(ns, dtype=np.int64)
+    conv = np.empty(ns, dtype=np.uint8)
+    napp, fail = C.c_int64(0), C.c_int64(-1)
+    st = lib().oracle_sa_solve(n, plo, plc, plv, pl, float(alpha), pbe, ns, float(tol), int(max_iter),
+                               ppr, sols.ctypes.data_as(_PD), res.ctypes.data_as(_PD),
+                               its.ctypes.data_as(_PI64), conv.ctypes.data_as(_PU8), C.byref(napp),
+                               C.byref(fail))
     if st:
         raise OracleFailure(st, fail.value)
     return sols, res, its, conv.astype(bool), napp.value

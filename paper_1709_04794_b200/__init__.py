@@ -44,6 +44,7 @@ from .fsda import (
     RegressionOperator,
     regression_operator,
     shifted_cg,
+    sa_sda_solve,
     solve,
     solve_label_sets,
 )
@@ -57,5 +58,5 @@ __all__ = [
     "as_shift_grid", "build_sparse",
     "ALGORITHMS", "Device", "DeviceProblem", "LinearOperator", "apply_smoother",
     "centered_matvec_transpose", "default_device", "fsda_operator_apply", "fsda_solve",
-    "install_into_sdakit", "labeled_mean", "matvec", "matvec_transpose", "shifted_cg", "solve", "solve_label_sets", "RegressionOperator", "regression_operator",
+    "install_into_sdakit", "labeled_mean", "matvec", "matvec_transpose", "shifted_cg", "sa_sda_solve", "solve", "solve_label_sets", "RegressionOperator", "regression_operator",
 ]

@@ -337,8 +337,9 @@ void enq_smoother(Enq& e, double alpha, const double* y, double* z, int guarded)
 size_t step_smem(int ns) { return sizeof(double) * 3 * (size_t)std::max(ns, 1); }
 
 // Cooperative launch of k_cg_step (capturable into graphs).
+// center: 0 none, 1 FSDA (q - mu sum z), 2 SA-SDA (q - 1_l sum z / l)
 void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, int use_cond,
-                    bool center) {
+                    int center) {
   ShiftState ss = c->shifts();
   const long long nlD = n_leaves(d);
   double* q = c->q.ptr;
@@ -350,12 +351,15 @@ void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, i
   double* pp = c->part_d.ptr;
   double* pr = c->part_d2.ptr;
   CgScalars* sc = c->sc;
-  const double* mu = center ? c->mu_v.ptr : nullptr;
+  const double* mu = center == 1 ? c->mu_v.ptr : nullptr;
   const double* pz = center ? c->part_n.ptr : nullptr;
   const long long nlz = center ? n_leaves(c->n) : 0;
+  const signed char* lab = c->labels.ptr;
+  double ell = (double)c->ell;
   void* args[] = {(void*)&q, (void*)&p, (void*)&r0, (void*)&r1, (void*)&bigp, (void*)&sols,
                   (void*)&d, (void*)&pp, (void*)&pr, (void*)&nlD, (void*)&sc, (void*)&ss,
-                  (void*)&ns, (void*)&cond, (void*)&use_cond, (void*)&mu, (void*)&pz, (void*)&nlz};
+                  (void*)&ns, (void*)&cond, (void*)&use_cond, (void*)&mu, (void*)&pz, (void*)&nlz,
+                  (void*)&lab, (void*)&ell};
   const size_t smem = step_smem(ns);
   // One 1024-thread CTA per SM: a grid barrier then has 148 arrivals.
   if (c->step_blocks == 0) {
@@ -377,7 +381,7 @@ void enq_fsda_iteration(Enq& e, double alpha, int ns, unsigned long long cond, i
   enq_smoother(e, alpha, c->y.ptr, c->z.ptr, 1);
   enq_xt(e, c->z.ptr, c->q.ptr, 0, nullptr, 1, c->part_n.ptr);
   e.go("cg_step", 8.0 * c->n + 24.0 * d + 24.0 * d + 32.0 * d * ns + 24.0 * d, [&] {
-    launch_cg_step(c, ns, d, cond, use_cond, true);
+    launch_cg_step(c, ns, d, cond, use_cond, 1);
   });
 }
 
@@ -456,7 +460,7 @@ void enq_reg_iteration(Enq& e, int ns, unsigned long long cond, int use_cond) {
   enq_xrows(e, c->p.ptr, c->y.ptr, 1);
   enq_xt(e, c->y.ptr, c->q.ptr, 0, nullptr, 1, nullptr);
   e.go("cg_step", 24.0 * d + 24.0 * d + 32.0 * d * ns + 24.0 * d, [&] {
-    launch_cg_step(c, ns, d, cond, use_cond, false);
+    launch_cg_step(c, ns, d, cond, use_cond, 0);
   });
 }
 
@@ -466,18 +470,76 @@ void enq_reg_tail(Enq& e, int ns) {
   e.go("cg_finish", 0.0, [&] { k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns); });
 }
 
+// SA-SDA (sda.py:360-396): shifted CG in sample space on the centred spectral
+// operator z -> M z - 1_l (sum(M z) / l) (sda.py:148-159); the vectors of the
+// recurrence have N entries (the context's d is N while it runs).  The rhs is
+// apply_w of the orthogonalized probe (uploaded into t), sda.py:287-290, 373.
+void enq_sa_setup(Enq& e, int ns, long long max_iter, double tol) {
+  fsda_ctx* c = e.c;
+  const long long n = c->n, nlN = n_leaves(n);
+  ShiftState ss = c->shifts();
+  e.go("solve_reset", 0.0, [&] {
+    k_solve_reset<<<1, 256, 0, c->stream>>>(c->sc, ss, ns, max_iter, tol, 0);
+  });
+  e.go("class_sums", 9.0 * n, [&] {
+    k_class_sums<<<grid_for(nlN, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+        c->t.ptr, c->labels.ptr, n, c->part_n.ptr, nlN, c->sc, (double)c->n1, (double)c->n2);
+  });
+  e.go("apply_w", 9.0 * n, [&] {
+    k_apply_w<<<grid_for(nlN, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+        c->labels.ptr, c->wv.ptr, n, c->part_n.ptr, nlN, c->sc);
+  });
+  e.go("cg_init", 8.0 * n * 3 + 16.0 * n * ns, [&] {
+    dim3 g(grid_for(nlN, WARPS_PER_BLOCK), 1 + ns);
+    k_cg_init<<<g, LEAF_THREADS, 0, c->stream>>>(c->wv.ptr, c->r0.ptr, c->p.ptr, c->bigp.ptr,
+                                                 c->sols.ptr, n, c->part_d.ptr, nlN, c->sc, ss, ns);
+  });
+}
+
+void enq_sa_iteration(Enq& e, double alpha, int ns, unsigned long long cond, int use_cond) {
+  fsda_ctx* c = e.c;
+  const long long n = c->n, nlN = n_leaves(n);
+  enq_smoother(e, alpha, c->p.ptr, c->q.ptr, 1);
+  e.go("vector_sum", 8.0 * n, [&] {
+    k_vector_sum<<<grid_for(nlN, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+        c->q.ptr, n, c->part_n.ptr, nlN, c->sc, nullptr);
+  });
+  e.go("cg_step", 8.0 * n + 48.0 * n + 32.0 * n * ns + 24.0 * n, [&] {
+    launch_cg_step(c, ns, n, cond, use_cond, 2);
+  });
+}
+
+void enq_sa_tail(Enq& e, int ns) {
+  fsda_ctx* c = e.c;
+  const long long n = c->n, nlN = n_leaves(n);
+  ShiftState ss = c->shifts();
+  e.go("cg_finish", 0.0, [&] { k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns); });
+  e.go("orient", 8.0 * n * ns + 1.0 * n, [&] {  // _oriented, sda.py:256-262
+    dim3 g(grid_for(nlN, WARPS_PER_BLOCK), ns);
+    k_orient<<<g, LEAF_THREADS, 0, c->stream>>>(c->labels.ptr, c->sols.ptr, n, c->part_o.ptr, nlN,
+                                                c->sc, ss, ns, nullptr);
+  });
+  e.go("flip", 0.0, [&] {
+    dim3 g((unsigned)std::min<long long>(grid_for(n, 256), 1024), ns);
+    k_flip<<<g, 256, 0, c->stream>>>(nullptr, c->sols.ptr, 0, n, ss);
+  });
+}
+
 void enq_setup_k(Enq& e, int ns, long long max_iter, double tol) {
   if (e.c->solve_kind == 1) enq_reg_setup(e, ns, max_iter, tol, e.c->solve_abs_tol);
+  else if (e.c->solve_kind == 2) enq_sa_setup(e, ns, max_iter, tol);
   else enq_fsda_setup(e, ns, max_iter, tol);
 }
 
 void enq_iteration_k(Enq& e, double alpha, int ns, unsigned long long cond, int use_cond) {
   if (e.c->solve_kind == 1) enq_reg_iteration(e, ns, cond, use_cond);
+  else if (e.c->solve_kind == 2) enq_sa_iteration(e, alpha, ns, cond, use_cond);
   else enq_fsda_iteration(e, alpha, ns, cond, use_cond);
 }
 
 void enq_tail_k(Enq& e, int ns) {
   if (e.c->solve_kind == 1) enq_reg_tail(e, ns);
+  else if (e.c->solve_kind == 2) enq_sa_tail(e, ns);
   else enq_fsda_tail(e, ns);
 }
 
@@ -1347,7 +1409,7 @@ int fsda_shifted_cg_dense(fsda_ctx* c, int64_t dim, const double* a, const doubl
     k_dense_matvec<<<grid_for(dim, 128), 128, 0, c->stream>>>(c->dense_a.ptr, c->p.ptr, c->q.ptr,
                                                               (int)dim, c->sc);
     CKL();
-    launch_cg_step(c, ns, dim, 0, 0, false);
+    launch_cg_step(c, ns, dim, 0, 0, 0);
     if ((it & 15) == 15) {  // stop launching once every shift froze
       CgScalars h;
       CK(cudaMemcpyAsync(&h, c->sc, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
@@ -1467,7 +1529,7 @@ int fsda_dev_cg_step(fsda_ctx* c, const double* d_q) {
   if (c->r_ns <= 0) return fail(FSDA_EINVAL, "call fsda_dev_cg_begin first");
   if (d_q != c->q.ptr)
     CK(cudaMemcpyAsync(c->q.ptr, d_q, sizeof(double) * c->d, cudaMemcpyDeviceToDevice, c->stream));
-  launch_cg_step(c, c->r_ns, c->d, 0, 0, false);
+  launch_cg_step(c, c->r_ns, c->d, 0, 0, 0);
   return FSDA_OK;
   API_END
 }
@@ -1552,6 +1614,43 @@ int fsda_regression_shifted_cg(fsda_ctx* c, const double* rhs, const double* bet
   const int rc = read_results(c, ns, o, nullptr);
   c->solve_kind = 0;
   return rc;
+  API_END
+}
+
+int fsda_sa_solve(fsda_ctx* c, double alpha, const double* betas, int ns, double tol,
+                  int64_t max_iter, const double* probe, double* solutions, double* residuals,
+                  int64_t* iterations, uint8_t* converged, int64_t* n_applies, int64_t* fail_iter) {
+  API_BEGIN(c)
+  if (!c->has_l || !c->has_labels) return fail(FSDA_EINVAL, "Laplacian and labels must be uploaded");
+  if (alpha == 0.0)
+    return fail(FSDA_EINVAL, "sa-sda requires alpha != 0: without the Laplacian term the spectral "
+                             "system never propagates ratings to unlabeled samples");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(FSDA_EINVAL, "alpha must lie in [0, 1], got %g", alpha);
+  if (c->ell == 0) return fail(FSDA_ELABEL, "centering requires at least one labeled sample");
+  if (c->n1 == 0 || c->n2 == 0) return fail(FSDA_EINVAL, "both classes need at least one labeled sample");
+  if (ns <= 0) return fail(FSDA_EINVAL, "shift grid must be a non-empty 1-d array");
+  for (int s = 0; s < ns; ++s) {
+    if (!std::isfinite(betas[s])) return fail(FSDA_EINVAL, "shifts must be finite");
+    if (s == 0 && betas[s] < 0) return fail(FSDA_EINVAL, "shifts must be non-negative");
+    if (s > 0 && !(betas[s] > betas[s - 1])) return fail(FSDA_EINVAL, "shifts must be strictly ascending");
+  }
+  if (!(tol > 0)) return fail(FSDA_EINVAL, "tol must be positive");
+  if (c->n > MAX_REDUCE) return fail(FSDA_EINVAL, "N above the reduction limit");
+  // the recurrence runs over N-vectors: borrow the D-space buffers with d = N
+  struct DimGuard {
+    fsda_ctx* c;
+    long long d;
+    ~DimGuard() { c->d = d; c->solve_kind = 0; }
+  } guard{c, c->d};
+  c->d = c->n;
+  c->solve_kind = 2;
+  c->solve_abs_tol = 0;
+  ensure_vectors(c, ns);
+  upload_solve_params(c, betas, ns, nullptr);
+  CK(cudaMemcpyAsync(c->t.ptr, probe, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
+  launch_solve(c, alpha, ns, max_iter, tol, nullptr);
+  SolveOut o{solutions, nullptr, residuals, iterations, converged, n_applies, fail_iter};
+  return read_results(c, ns, o, nullptr);
   API_END
 }
 

@@ -258,34 +258,11 @@ __device__ __forceinline__ void seg_class_task(const SegPlan& pl, const SegArgs&
   if (tk.x >= 0 && (lane & (W - 1)) == 0) seg_finish<KIND>(a, tk.x, s);
 }
 
-// The descriptor a lane group needs for work item tw (class tasks only;
-// heavy tasks and sum leaves return a dummy).  Loaded one grid-stride step
-// ahead so the index loads of the next item do not wait on it.
-__device__ __forceinline__ int4 seg_fetch_task(const SegPlan& pl, long long tw, int lane) {
-  int4 tk = make_int4(-1, 0, 0, -1);
-  if (tw < pl.warp_base[6]) {
-    int k = 0;
-    while (tw >= pl.warp_base[k + 1]) ++k;
-    const int w = 1 << k;
-    const long long idx = pl.cls_off[k] + (tw - pl.warp_base[k]) * (32 / w) + lane / w;
-    if (idx < pl.cls_off[k + 1]) tk = __ldg(pl.tasks + idx);
-  } else if (tw < pl.warp_base[7]) {
-    tk = __ldg(pl.tasks + pl.cls_off[6] + (tw - pl.warp_base[6]));
-  }
-  return tk;
-}
-
-template <int W, int KIND>
-__device__ __forceinline__ void seg_class_run(const SegPlan& pl, const SegArgs& a, const int4 tk,
-                                              int lane) {
-  const double s = group_leaf<W, KIND>(pl, a, tk.x, tk.y, tk.z, lane & (W - 1));
-  if (tk.x >= 0 && (lane & (W - 1)) == 0) seg_finish<KIND>(a, tk.x, s);
-}
-
 template <int KIND>
-__device__ __forceinline__ void seg_heavy_run(const SegPlan& pl, const SegArgs& a, const int4 tk,
-                                              int lane) {
+__device__ __forceinline__ void seg_heavy_task(const SegPlan& pl, const SegArgs& a, long long tw,
+                                               int lane) {
   // heavy task: up to 4 consecutive leaves of one segment
+  const int4 tk = __ldg(pl.tasks + pl.cls_off[6] + (tw - pl.warp_base[6]));
   const int h = tk.w;
   const int leaf0 = __ldg(pl.heavy_seg0 + h) + (tk.y - __ldg(pl.heavy_start + h)) / LEAF;
   for (int lf = 0; lf * LEAF < tk.z; ++lf) {
@@ -312,54 +289,40 @@ __device__ __forceinline__ void seg_heavy_run(const SegPlan& pl, const SegArgs& 
 }
 
 template <int KIND>
-__device__ __forceinline__ void seg_heavy_task(const SegPlan& pl, const SegArgs& a, long long tw,
-                                               int lane) {
-  seg_heavy_run<KIND>(pl, a, __ldg(pl.tasks + pl.cls_off[6] + (tw - pl.warp_base[6])), lane);
-}
-
-// Run work item tw with its descriptor already loaded.
-template <int KIND>
-__device__ __forceinline__ void seg_run_item(const SegPlan& pl, const SegArgs& a, long long tw,
-                                             const int4 tk, int lane) {
-  if (tw < pl.warp_base[6]) {
-    int k = 0;
-    while (tw >= pl.warp_base[k + 1]) ++k;
-    switch (k) {
-      case 0: seg_class_run<1, KIND>(pl, a, tk, lane); break;
-      case 1: seg_class_run<2, KIND>(pl, a, tk, lane); break;
-      case 2: seg_class_run<4, KIND>(pl, a, tk, lane); break;
-      case 3: seg_class_run<8, KIND>(pl, a, tk, lane); break;
-      case 4: seg_class_run<16, KIND>(pl, a, tk, lane); break;
-      default: seg_class_run<32, KIND>(pl, a, tk, lane); break;
-    }
-  } else if (tw < pl.warp_base[7]) {
-    seg_heavy_run<KIND>(pl, a, tk, lane);
-  } else {  // leaf partials of sum(src)
-    const long long g = tw - pl.warp_base[7];
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const long long i = g * LEAF + k * 32 + lane;
-      if (i < a.sum_n) s = s + __ldg(a.src + i);
-    }
-    s = butterfly(s);
-    if (lane == 0) a.sum_part[g] = s;
-  }
-}
-
-template <int KIND>
-__global__ void __launch_bounds__(256, 5) k_segsum(SegPlan pl, SegArgs a, const CgScalars* sc,
+__global__ void __launch_bounds__(256, 6) k_segsum(SegPlan pl, SegArgs a, const CgScalars* sc,
                                                 int guarded) {
   if (guarded && loop_idle(sc)) return;
   const int lane = threadIdx.x & 31;
   const long long total = pl.warp_base[8];
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-  long long tw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  int4 tk = seg_fetch_task(pl, tw, lane);
-  for (; tw < total; tw += nwarps) {
-    const int4 tk_next = seg_fetch_task(pl, tw + nwarps, lane);  // one step ahead
-    seg_run_item<KIND>(pl, a, tw, tk, lane);
-    tk = tk_next;
+  for (long long tw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tw < total;
+       tw += nwarps) {
+    if (tw < pl.warp_base[6]) {
+      int k = 0;
+      while (tw >= pl.warp_base[k + 1]) ++k;
+      switch (k) {
+        case 0: seg_class_task<1, KIND>(pl, a, 0, tw, lane); break;
+        case 1: seg_class_task<2, KIND>(pl, a, 1, tw, lane); break;
+        case 2: seg_class_task<4, KIND>(pl, a, 2, tw, lane); break;
+        case 3: seg_class_task<8, KIND>(pl, a, 3, tw, lane); break;
+        case 4: seg_class_task<16, KIND>(pl, a, 4, tw, lane); break;
+        default: seg_class_task<32, KIND>(pl, a, 5, tw, lane); break;
+      }
+      continue;
+    }
+    if (tw >= pl.warp_base[7]) {  // leaf partials of sum(src)
+      const long long g = tw - pl.warp_base[7];
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const long long i = g * LEAF + k * 32 + lane;
+        if (i < a.sum_n) s = s + __ldg(a.src + i);
+      }
+      s = butterfly(s);
+      if (lane == 0) a.sum_part[g] = s;
+      continue;
+    }
+    seg_heavy_task<KIND>(pl, a, tw, lane);
   }
 }
 
@@ -496,19 +459,35 @@ __global__ void __launch_bounds__(1024, 1) k_xt_coop(SegPlan pl, XtDense dn, Seg
   // ---- phase 1b: the other columns and the sum(z) leaves; warps draw tasks
   // from a grid-wide ticket so CTAs that staged a dense block catch up
   const long long total = pl.warp_base[8];
-  auto draw = [&]() {
-    long long t = 0;
-    if (lane == 0) t = (long long)atomicAdd(ticket, 1ULL);
-    return __shfl_sync(FULL, t, 0);
-  };
-  long long tw = draw();
-  int4 tk = seg_fetch_task(pl, tw, lane);
-  while (tw < total) {
-    const long long tn = draw();                       // next ticket and its descriptor,
-    const int4 tk_next = seg_fetch_task(pl, tn, lane);  // fetched before this item runs
-    seg_run_item<SEG_XCOLS>(pl, a, tw, tk, lane);
-    tw = tn;
-    tk = tk_next;
+  for (;;) {
+    long long tw = 0;
+    if (lane == 0) tw = (long long)atomicAdd(ticket, 1ULL);
+    tw = __shfl_sync(FULL, tw, 0);
+    if (tw >= total) break;
+    if (tw < pl.warp_base[6]) {
+      int k = 0;
+      while (tw >= pl.warp_base[k + 1]) ++k;
+      switch (k) {
+        case 0: seg_class_task<1, SEG_XCOLS>(pl, a, 0, tw, lane); break;
+        case 1: seg_class_task<2, SEG_XCOLS>(pl, a, 1, tw, lane); break;
+        case 2: seg_class_task<4, SEG_XCOLS>(pl, a, 2, tw, lane); break;
+        case 3: seg_class_task<8, SEG_XCOLS>(pl, a, 3, tw, lane); break;
+        case 4: seg_class_task<16, SEG_XCOLS>(pl, a, 4, tw, lane); break;
+        default: seg_class_task<32, SEG_XCOLS>(pl, a, 5, tw, lane); break;
+      }
+    } else if (tw < pl.warp_base[7]) {
+      seg_heavy_task<SEG_XCOLS>(pl, a, tw, lane);
+    } else {
+      const long long g = tw - pl.warp_base[7];
+      double v = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const long long i = g * LEAF + k * 32 + lane;
+        if (i < a.sum_n) v = v + __ldg(a.src + i);
+      }
+      v = butterfly(v);
+      if (lane == 0) a.sum_part[g] = v;
+    }
   }
   grid.sync();
   if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0ULL;  // every warp has drawn its last ticket
@@ -583,7 +562,8 @@ __global__ void __launch_bounds__(1024, 1) k_cg_step(
     double* __restrict__ r1, double* __restrict__ bigp, double* __restrict__ sols, long long d,
     double* __restrict__ part_pq, double* __restrict__ part_rr, long long n_leaf, CgScalars* sc,
     ShiftState ss, int ns, unsigned long long cond_handle, int use_cond,
-    const double* __restrict__ mu, const double* __restrict__ part_z, long long n_leaf_z) {
+    const double* __restrict__ mu, const double* __restrict__ part_z, long long n_leaf_z,
+    const signed char* __restrict__ labels, double ell) {
   extern __shared__ double dyn[];  // zn[ns], gs[ns], good[ns] (as double)
   __shared__ double smem[257];
   __shared__ int s_flag;
@@ -624,7 +604,11 @@ __global__ void __launch_bounds__(1024, 1) k_cg_step(
       if (i < d) {
         double qi = q[i];
         if (part_z) {
-          qi = qi - mu[i] * sum_z;
+          if (mu) {        // FSDA: X^T z - mu * sum(z)          (sparse.py:277)
+            qi = qi - mu[i] * sum_z;
+          } else {         // SA-SDA: M z - 1_l * (sum(Mz) / l)  (sda.py:155-157)
+            qi = qi - (labels[i] != 0 ? 1.0 : 0.0) * (sum_z / ell);
+          }
           q[i] = qi;
         }
         a = fma(p[i], qi, a);

@@ -24,7 +24,7 @@ import numpy as np
 from . import _capi
 from . import types as T
 
-ALGORITHMS = ("fsda", "lda")
+ALGORITHMS = ("fsda", "lda", "sa-sda")
 
 
 # ------------------------------------------------------------ API families
@@ -325,6 +325,50 @@ def fsda_solve(p, *, device: Optional[Device] = None) -> "T.SolveReport":
     return _report(p, res, fam, t0)
 
 
+def orthogonalized_probe(p) -> np.ndarray:
+    """The reference's sample-space probe (sda.py:287-290): r ~ U(-1, 1)^N
+    from default_rng(p.seed), minus its labeled mean."""
+    lab = np.asarray(p.labels.labels)
+    mask = lab != 0
+    r = np.random.default_rng(p.seed).uniform(-1.0, 1.0, size=lab.size)
+    return r - r[mask].sum() / int(mask.sum())
+
+
+def sa_sda_solve(p, *, device: Optional[Device] = None) -> "T.SolveReport":
+    """SA-SDA on the device (sda.py:360-396): one shifted CG in sample
+    space on the centred spectral operator for every beta; the oriented
+    solutions are the ratings (source "spectral")."""
+    fam = _family(p)
+    if p.alpha == 0.0:
+        raise ValueError("sa-sda requires alpha != 0: without the Laplacian term the "
+                         "spectral system never propagates ratings to unlabeled samples")
+    t0 = time.perf_counter()
+    dev = device or default_device()
+    dev.load_problem(p, fam)
+    betas = _f64(p.betas.betas)
+    ns, n = int(betas.size), int(p.x.n_rows)
+    probe = _f64(orthogonalized_probe(p))
+    sols = np.empty((ns, n))
+    res = np.empty(ns)
+    its = np.empty(ns, dtype=np.int64)
+    conv = np.empty(ns, dtype=np.uint8)
+    napp, fail = C.c_int64(0), C.c_int64(-1)
+    tol = p.tol if getattr(p, "tol_spectral", None) is None else p.tol_spectral
+    rc = _capi.lib().fsda_sa_solve(dev._h, float(p.alpha), _capi.dptr(betas), ns, float(tol),
+                                   int(p.max_iter_n), _capi.dptr(probe), _capi.dptr(sols),
+                                   _capi.dptr(res), _capi.i64ptr(its), _capi.u8ptr(conv),
+                                   C.byref(napp), C.byref(fail))
+    _raise_for(rc, fam)
+    ratings = {float(b): fam.RatingVector(scores=sols[s], source="spectral")
+               for s, b in enumerate(betas)}
+    return fam.SolveReport(
+        algorithm="sa-sda", alpha=p.alpha, betas=np.asarray(p.betas.betas), ratings=ratings,
+        spectral=fam.PhaseStats(dimension=n, iterations=its, operator_applications=int(napp.value),
+                                residuals=res, converged=conv.astype(bool)),
+        regression=None, wall_time_s=time.perf_counter() - t0,
+        spectral_vectors=np.ascontiguousarray(sols.T))
+
+
 def solve(p, algorithm: str = "fsda") -> "T.SolveReport":
     """Dispatch like sdakit.sda.solve (sda.py:473-486) for the algorithms on
     the B200 path: 'fsda', and 'lda' = fsda constrained to alpha = 0."""
@@ -337,6 +381,8 @@ def solve(p, algorithm: str = "fsda") -> "T.SolveReport":
         return rep
     if algorithm == "fsda":
         return fsda_solve(p)
+    if algorithm == "sa-sda":
+        return sa_sda_solve(p)
     raise ValueError(f"unknown algorithm {algorithm!r} for the B200 path; choose from {ALGORITHMS}")
 
 

@@ -154,7 +154,12 @@ struct fsda_ctx {
   DevBuf<double> beta, zeta_prev, zeta, zeta_next, gamma_s, alpha_s, resid;
   DevBuf<long long> iters;
   DevBuf<unsigned char> conv;
-  DevBuf<int> active, good, pending, flip, err;
+  DevBuf<int> active, good, pending, flip, err, upd_mode;
+  DevBuf<double> upd_gs, upd_zn, upd_as;
+  // side stream (low priority) + events for the shift update forked beside
+  // the sparse kernels inside the solve graph
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   CgScalars* sc = nullptr;
 
   // graph cache for the solve
@@ -182,6 +187,7 @@ struct fsda_ctx {
     s.zeta_next = zeta_next.ptr; s.gamma_s = gamma_s.ptr; s.alpha_s = alpha_s.ptr;
     s.resid = resid.ptr; s.iters = iters.ptr; s.conv = conv.ptr; s.active = active.ptr;
     s.good = good.ptr; s.pending = pending.ptr; s.flip = flip.ptr;
+    s.upd_mode = upd_mode.ptr; s.upd_gs = upd_gs.ptr; s.upd_zn = upd_zn.ptr; s.upd_as = upd_as.ptr;
     return s;
   }
 
@@ -251,6 +257,7 @@ void ensure_vectors(fsda_ctx* c, int ns) {
   c->gamma_s.ensure(nsx); c->alpha_s.ensure(nsx); c->resid.ensure(nsx); c->iters.ensure(nsx);
   c->conv.ensure(nsx); c->active.ensure(nsx); c->good.ensure(nsx); c->pending.ensure(nsx);
   c->flip.ensure(nsx);
+  c->upd_mode.ensure(nsx); c->upd_gs.ensure(nsx); c->upd_zn.ensure(nsx); c->upd_as.ensure(nsx);
 }
 
 int grid_for(long long n, int block) { return (int)std::max<long long>(1, cdiv(n, block)); }
@@ -372,16 +379,48 @@ void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, i
                                  c->stream));
 }
 
+// The shift-state update of the last base step (k_shift_update) on `stream`.
+void launch_shift_update(fsda_ctx* c, int ns, long long d, cudaStream_t stream, int guarded) {
+  ShiftState ss = c->shifts();
+  dim3 g((unsigned)std::min<long long>(grid_for(d, 256), (long long)c->num_sms * 2), ns);
+  k_shift_update<<<g, 256, 0, stream>>>(c->r0.ptr, c->r1.ptr, c->bigp.ptr, c->sols.ptr, d, ss,
+                                        c->sc, guarded);
+  CKL();
+}
+
+// One iteration = sparse products `sparse` (K1..K3 or the operator's
+// equivalent) + the cooperative base step.  In the graph body the previous
+// iteration's shift update is forked onto the side stream, beside the sparse
+// kernels (it reads r_i and writes sols / P, which they never touch); eagerly
+// it follows the base step on the same stream.
+template <typename Sparse>
+void enq_iteration_body(Enq& e, int ns, long long d, int center, unsigned long long cond,
+                        int use_cond, double step_bytes, Sparse&& sparse) {
+  fsda_ctx* c = e.c;
+  const double su_bytes = 32.0 * d * ns + 8.0 * d;
+  if (use_cond) {
+    CK(cudaEventRecord(c->ev_fork, c->stream));
+    CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    e.go("shift_update", su_bytes, [&] { launch_shift_update(c, ns, d, c->side, 1); });
+    CK(cudaEventRecord(c->ev_join, c->side));
+    sparse();
+    CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    e.go("cg_step", step_bytes, [&] { launch_cg_step(c, ns, d, cond, use_cond, center); });
+  } else {
+    sparse();
+    e.go("cg_step", step_bytes, [&] { launch_cg_step(c, ns, d, cond, use_cond, center); });
+    e.go("shift_update", su_bytes, [&] { launch_shift_update(c, ns, d, c->stream, 1); });
+  }
+}
 
 // One shifted-CG iteration for the FSDA operator (graph body).
 void enq_fsda_iteration(Enq& e, double alpha, int ns, unsigned long long cond, int use_cond) {
   fsda_ctx* c = e.c;
   const long long d = c->d;
-  enq_xrows(e, c->p.ptr, c->y.ptr, 1);
-  enq_smoother(e, alpha, c->y.ptr, c->z.ptr, 1);
-  enq_xt(e, c->z.ptr, c->q.ptr, 0, nullptr, 1, c->part_n.ptr);
-  e.go("cg_step", 8.0 * c->n + 24.0 * d + 24.0 * d + 32.0 * d * ns + 24.0 * d, [&] {
-    launch_cg_step(c, ns, d, cond, use_cond, 1);
+  enq_iteration_body(e, ns, d, 1, cond, use_cond, 8.0 * c->n + 24.0 * d + 24.0 * d + 24.0 * d, [&] {
+    enq_xrows(e, c->p.ptr, c->y.ptr, 1);
+    enq_smoother(e, alpha, c->y.ptr, c->z.ptr, 1);
+    enq_xt(e, c->z.ptr, c->q.ptr, 0, nullptr, 1, c->part_n.ptr);
   });
 }
 
@@ -419,6 +458,7 @@ void enq_fsda_tail(Enq& e, int ns) {
   fsda_ctx* c = e.c;
   const long long n = c->n, d = c->d, nlN = n_leaves(n);
   ShiftState ss = c->shifts();
+  e.go("shift_update", 32.0 * d * ns, [&] { launch_shift_update(c, ns, d, c->stream, 0); });
   e.go("cg_finish", 0.0, [&] { k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns); });
   e.go("transpose_sols", 16.0 * d * ns, [&] {
     k_transpose_sols<<<grid_for(d * ns, 256), 256, 0, c->stream>>>(c->sols.ptr, c->wT.ptr, d, ns);
@@ -457,16 +497,16 @@ void enq_reg_setup(Enq& e, int ns, long long max_iter, double tol, int abs_tol) 
 void enq_reg_iteration(Enq& e, int ns, unsigned long long cond, int use_cond) {
   fsda_ctx* c = e.c;
   const long long d = c->d;
-  enq_xrows(e, c->p.ptr, c->y.ptr, 1);
-  enq_xt(e, c->y.ptr, c->q.ptr, 0, nullptr, 1, nullptr);
-  e.go("cg_step", 24.0 * d + 24.0 * d + 32.0 * d * ns + 24.0 * d, [&] {
-    launch_cg_step(c, ns, d, cond, use_cond, 0);
+  enq_iteration_body(e, ns, d, 0, cond, use_cond, 24.0 * d + 24.0 * d + 24.0 * d, [&] {
+    enq_xrows(e, c->p.ptr, c->y.ptr, 1);
+    enq_xt(e, c->y.ptr, c->q.ptr, 0, nullptr, 1, nullptr);
   });
 }
 
 void enq_reg_tail(Enq& e, int ns) {
   fsda_ctx* c = e.c;
   ShiftState ss = c->shifts();
+  e.go("shift_update", 32.0 * c->d * ns, [&] { launch_shift_update(c, ns, c->d, c->stream, 0); });
   e.go("cg_finish", 0.0, [&] { k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns); });
 }
 
@@ -499,13 +539,12 @@ void enq_sa_setup(Enq& e, int ns, long long max_iter, double tol) {
 void enq_sa_iteration(Enq& e, double alpha, int ns, unsigned long long cond, int use_cond) {
   fsda_ctx* c = e.c;
   const long long n = c->n, nlN = n_leaves(n);
-  enq_smoother(e, alpha, c->p.ptr, c->q.ptr, 1);
-  e.go("vector_sum", 8.0 * n, [&] {
-    k_vector_sum<<<grid_for(nlN, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
-        c->q.ptr, n, c->part_n.ptr, nlN, c->sc, nullptr);
-  });
-  e.go("cg_step", 8.0 * n + 48.0 * n + 32.0 * n * ns + 24.0 * n, [&] {
-    launch_cg_step(c, ns, n, cond, use_cond, 2);
+  enq_iteration_body(e, ns, n, 2, cond, use_cond, 8.0 * n + 48.0 * n + 24.0 * n, [&] {
+    enq_smoother(e, alpha, c->p.ptr, c->q.ptr, 1);
+    e.go("vector_sum", 8.0 * n, [&] {
+      k_vector_sum<<<grid_for(nlN, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
+          c->q.ptr, n, c->part_n.ptr, nlN, c->sc, nullptr);
+    });
   });
 }
 
@@ -513,6 +552,7 @@ void enq_sa_tail(Enq& e, int ns) {
   fsda_ctx* c = e.c;
   const long long n = c->n, nlN = n_leaves(n);
   ShiftState ss = c->shifts();
+  e.go("shift_update", 32.0 * n * ns, [&] { launch_shift_update(c, ns, n, c->stream, 0); });
   e.go("cg_finish", 0.0, [&] { k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns); });
   e.go("orient", 8.0 * n * ns + 1.0 * n, [&] {  // _oriented, sda.py:256-262
     dim3 g(grid_for(nlN, WARPS_PER_BLOCK), ns);
@@ -942,6 +982,11 @@ int fsda_ctx_create(fsda_ctx** out, int device, void* stream) {
     }
     CK(cudaMalloc(&c->sc, sizeof(CgScalars)));
     CK(cudaMemset(c->sc, 0, sizeof(CgScalars)));
+    int lo_prio = 0, hi_prio = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, lo_prio));
+    CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     c->err.ensure(1);
     CK(cudaMemset(c->err.ptr, 0, sizeof(int)));
   } catch (CudaError& ce) {
@@ -987,6 +1032,10 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     c->conv.release();
     c->labels.release();
     if (c->sc) cudaFree(c->sc);
+    c->upd_mode.release(); c->upd_gs.release(); c->upd_zn.release(); c->upd_as.release();
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->own_stream) cudaStreamDestroy(c->stream);
   }
   delete c;
@@ -1410,6 +1459,7 @@ int fsda_shifted_cg_dense(fsda_ctx* c, int64_t dim, const double* a, const doubl
                                                               (int)dim, c->sc);
     CKL();
     launch_cg_step(c, ns, dim, 0, 0, 0);
+    launch_shift_update(c, ns, dim, c->stream, 1);
     if ((it & 15) == 15) {  // stop launching once every shift froze
       CgScalars h;
       CK(cudaMemcpyAsync(&h, c->sc, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
@@ -1417,6 +1467,7 @@ int fsda_shifted_cg_dense(fsda_ctx* c, int64_t dim, const double* a, const doubl
       if (h.finished || h.status) break;
     }
   }
+  launch_shift_update(c, ns, dim, c->stream, 0);
   k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns);
   CKL();
   SolveOut o{solutions, nullptr, residuals, iterations, converged, n_applies, fail_iter};
@@ -1530,6 +1581,7 @@ int fsda_dev_cg_step(fsda_ctx* c, const double* d_q) {
   if (d_q != c->q.ptr)
     CK(cudaMemcpyAsync(c->q.ptr, d_q, sizeof(double) * c->d, cudaMemcpyDeviceToDevice, c->stream));
   launch_cg_step(c, c->r_ns, c->d, 0, 0, 0);
+  launch_shift_update(c, c->r_ns, c->d, c->stream, 1);
   return FSDA_OK;
   API_END
 }
@@ -1560,6 +1612,7 @@ int fsda_dev_project(fsda_ctx* c, double* d_scores, double* d_orient) {
   if (ns <= 0) return fail(FSDA_EINVAL, "call fsda_dev_cg_begin first");
   const long long n = c->n, d = c->d, nlN = n_leaves(n);
   ShiftState ss = c->shifts();
+  launch_shift_update(c, ns, d, c->stream, 0);
   k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns);
   k_transpose_sols<<<grid_for(d * ns, 256), 256, 0, c->stream>>>(c->sols.ptr, c->wT.ptr, d, ns);
   if (n > 0)

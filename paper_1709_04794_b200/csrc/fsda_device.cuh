@@ -80,6 +80,11 @@ struct ShiftState {
   int* good;     // good this iteration (zeta_next finite and not underflowed)
   int* pending;  // deferred P update owed from the previous iteration
   int* flip;     // orientation flip (projection phase)
+  // snapshot of one iteration's shift scalars for k_shift_update
+  int* upd_mode;    // 0 nothing, 1 sols only (froze this iteration), 3 sols and P
+  double* upd_gs;   // gamma_s
+  double* upd_zn;   // zeta_next
+  double* upd_as;   // alpha_s
 };
 
 // ---------------------------------------------------------------- R256 tree
@@ -174,7 +179,7 @@ __global__ void k_solve_reset(CgScalars* sc, ShiftState ss, int n_shifts, long l
     ss.zeta_prev[s] = 1.0; ss.zeta[s] = 1.0; ss.zeta_next[s] = 1.0;
     ss.gamma_s[s] = 0.0; ss.alpha_s[s] = 0.0; ss.resid[s] = 0.0;
     ss.iters[s] = max_iter; ss.conv[s] = 0; ss.active[s] = 1; ss.good[s] = 0;
-    ss.pending[s] = 0; ss.flip[s] = 0;
+    ss.pending[s] = 0; ss.flip[s] = 0; ss.upd_mode[s] = 0;
   }
 }
 

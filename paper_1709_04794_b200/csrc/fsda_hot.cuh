@@ -647,49 +647,23 @@ __global__ void __launch_bounds__(1024, 1) k_cg_step(
     s_good[s] = good;
   }
   __syncthreads();
-  // r-row leaves first (they feed r.r), then the shift rows in half-leaf
-  // units of 128 elements for a finer load balance.
-  const long long n_half = 2 * n_leaf;
-  const long long units = n_leaf + (long long)ns * n_half;
-  for (long long u = gw; u < units; u += tw) {
-    if (u < n_leaf) {
-      const long long g = u;
-      double a = 0.0;
+  // r_next = r + gamma q and its r.r leaves (krylov.py:232-233).  The shift
+  // state (sols, P) is updated by k_shift_update from the snapshot written in
+  // phase C, off the critical path (it runs beside the next iteration's
+  // sparse kernels).
+  for (long long g = gw; g < n_leaf; g += tw) {
+    double a = 0.0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const long long i = g * LEAF + k * 32 + lane;
-        if (i < d) {
-          const double rn = r_cur[i] + gamma * __ldcg(q + i);
-          r_next[i] = rn;
-          a = fma(rn, rn, a);
-        }
-      }
-      a = butterfly(a);
-      if (lane == 0) part_rr[g] = a;
-    } else {
-      const long long v = u - n_leaf;
-      const int s = (int)(v / n_half);
-      const long long h = v - (long long)s * n_half;
-      if (s_good[s] == 0.0) continue;
-      const double gs = s_gs[s];
-      const int pend = ss.pending[s];
-      const double zc = ss.zeta[s], as = ss.alpha_s[s];
-      double* P = bigp + (long long)s * d;
-      double* X = sols + (long long)s * d;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const long long i = h * 128 + k * 32 + lane;
-        if (i < d) {
-          double pv = P[i];
-          const double xv = X[i];
-          if (pend) {  // the P update owed from the previous iteration (krylov.py:241)
-            pv = zc * r_cur[i] + as * pv;
-            P[i] = pv;
-          }
-          X[i] = xv - pv * gs;  // krylov.py:230
-        }
+    for (int k = 0; k < 8; ++k) {
+      const long long i = g * LEAF + k * 32 + lane;
+      if (i < d) {
+        const double rn = r_cur[i] + gamma * __ldcg(q + i);
+        r_next[i] = rn;
+        a = fma(rn, rn, a);
       }
     }
+    a = butterfly(a);
+    if (lane == 0) part_rr[g] = a;
   }
   grid.sync();
 
@@ -714,27 +688,31 @@ __global__ void __launch_bounds__(1024, 1) k_cg_step(
   __syncthreads();
   const double r_norm = sqrt(rr_new);
   for (int s = threadIdx.x; s < ns; s += blockDim.x) {
+    ss.upd_mode[s] = 0;
     if (!ss.active[s]) continue;
     if (s_good[s] == 0.0) {  // degenerate zeta: freeze untouched (krylov.py:251-255)
       ss.iters[s] = it + 1;
       ss.resid[s] = __longlong_as_double(0x7ff0000000000000LL);
       ss.active[s] = 0;
-      ss.pending[s] = 0;
       continue;
     }
     const double zn = s_zn[s], z = ss.zeta[s], gs = s_gs[s];
-    ss.alpha_s[s] = alpha_new * (zn * gs) / (z * gamma);
+    const double as = alpha_new * (zn * gs) / (z * gamma);
+    ss.alpha_s[s] = as;
+    ss.upd_gs[s] = gs;
+    ss.upd_zn[s] = zn;
+    ss.upd_as[s] = as;
     const double shift_res = fabs(zn) * r_norm;
-    if (shift_res < thresh) {  // converged: freeze (krylov.py:256-261)
+    if (shift_res < thresh) {  // converged: freeze after its last sols update (krylov.py:256-261)
       ss.iters[s] = it + 1;
       ss.resid[s] = shift_res;
       ss.conv[s] = 1;
       ss.active[s] = 0;
-      ss.pending[s] = 0;
+      ss.upd_mode[s] = 1;
     } else {
       ss.zeta_prev[s] = z;
       ss.zeta[s] = zn;
-      ss.pending[s] = 1;
+      ss.upd_mode[s] = 3;
       atomicAdd(&s_flag, 1);
     }
   }
@@ -755,6 +733,34 @@ __global__ void __launch_bounds__(1024, 1) k_cg_step(
       if (runs > max_iter + 1) keep = 0u;  // never spin past the iteration budget
       cudaGraphSetConditional((cudaGraphConditionalHandle)cond_handle, keep);
     }
+  }
+}
+
+// The shift updates of the iteration whose snapshot k_cg_step wrote
+// (krylov.py:230, 240-241): sols_s -= gamma_s P_s, then P_s = zeta_next r +
+// alpha_s P_s for shifts still active.  r is the current residual r_{i+1}.
+// Launched on a second stream beside the next iteration's sparse kernels
+// (guarded: skipped once the loop is idle) and once more, unguarded, after the
+// loop for the final iteration.
+__global__ void __launch_bounds__(256) k_shift_update(const double* __restrict__ r0,
+                                                      const double* __restrict__ r1,
+                                                      double* __restrict__ bigp,
+                                                      double* __restrict__ sols, long long d,
+                                                      ShiftState ss, const CgScalars* sc,
+                                                      int guarded) {
+  if (guarded && loop_idle(sc)) return;
+  const int s = blockIdx.y;
+  const int mode = ss.upd_mode[s];
+  if (mode == 0) return;
+  const double gs = ss.upd_gs[s], zn = ss.upd_zn[s], as = ss.upd_as[s];
+  const double* r = (sc->iter & 1) ? r1 : r0;
+  double* P = bigp + (long long)s * d;
+  double* X = sols + (long long)s * d;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < d;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double pv = P[i];
+    X[i] = X[i] - pv * gs;
+    if (mode == 3) P[i] = zn * r[i] + as * pv;
   }
 }
 

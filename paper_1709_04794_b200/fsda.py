@@ -386,13 +386,18 @@ def solve(p, algorithm: str = "fsda") -> "T.SolveReport":
     raise ValueError(f"unknown algorithm {algorithm!r} for the B200 path; choose from {ALGORITHMS}")
 
 
-def install_into_sdakit(sda_module=None):
-    """Register the device solver as the reference's 'fsda' entry
-    (sdakit.sda._SOLVERS, sda.py:465-470).  'lda' follows automatically
-    because the reference's solve() calls the module-level fsda_solve name."""
+def install_into_sdakit(sda_module=None, algorithms=("fsda", "sa-sda")):
+    """Register the device solvers in the reference's table
+    (sdakit.sda._SOLVERS, sda.py:465-470).  'lda' follows 'fsda'
+    automatically because the reference's solve() calls the module-level
+    fsda_solve name."""
     sda = sda_module or importlib.import_module("sdakit.sda")
-    sda._SOLVERS["fsda"] = fsda_solve
-    sda.fsda_solve = fsda_solve
+    if "fsda" in algorithms:
+        sda._SOLVERS["fsda"] = fsda_solve
+        sda.fsda_solve = fsda_solve
+    if "sa-sda" in algorithms:
+        sda._SOLVERS["sa-sda"] = sa_sda_solve
+        sda.sa_sda_solve = sa_sda_solve
     return sda
 
 

@@ -151,15 +151,17 @@ def test_family_resolution_for_reference_objects():
 
         assert fam.SolverBreakdownError is rk.SolverBreakdownError
         # install_into_sdakit swaps only the 'fsda' entry
-        saved = dict(rsda._SOLVERS), rsda.fsda_solve
+        saved = dict(rsda._SOLVERS), rsda.fsda_solve, rsda.sa_sda_solve
         try:
             fb.install_into_sdakit(rsda)
             assert rsda._SOLVERS["fsda"] is fb.fsda_solve
+            assert rsda._SOLVERS["sa-sda"] is fb.sa_sda_solve
             assert rsda._SOLVERS["csr-sda"] is saved[0]["csr-sda"]
         finally:
             rsda._SOLVERS.clear()
             rsda._SOLVERS.update(saved[0])
             rsda.fsda_solve = saved[1]
+            rsda.sa_sda_solve = saved[2]
     finally:
         sys.path.remove(sdakit_root)
 

@@ -1,3 +1,5 @@
-export FSDA_B200_EAGER=1
-timeout 300 python tools/ncu_solve.py --solves 1 > gpurun_out/ncu_plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/ncu_solve.py --solves 1 > gpurun_out/ncu.log 2>&1; echo ncu_rc=$? >> gpurun_out/ncu.log
-timeout 300 python tools/ncu_solve.py --solves 1 > gpurun_out/ncu_plain2.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_cg_step|k_shift_update|k_xt_coop" -s 6 -c 3 -o gpurun_out/prof_r01k python tools/ncu_solve.py --solves 1 > gpurun_out/ncu_full.log 2>&1; echo ncu_full_rc=$? >> gpurun_out/ncu.log
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_side.json 2> gpurun_out/bench_side.err
+FSDA_B200_SU_INLINE=1 timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_inline.json 2> gpurun_out/bench_inline.err
+timeout 600 python bench.py --no-cpu-baseline --workload cfg3 --steps 5 > gpurun_out/bench_cfg3.json 2> gpurun_out/bench_cfg3.err
+FSDA_B200_SU_INLINE=1 timeout 600 python bench.py --no-cpu-baseline --workload cfg3 --steps 5 > gpurun_out/bench_cfg3_inline.json 2> gpurun_out/bench_cfg3_inline.err

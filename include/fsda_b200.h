@@ -27,11 +27,12 @@
  *   FSDA_ELABEL     5  no labeled sample        -> LabelError             (sparse.py:258-265)
  * fsda_last_error() returns a thread-local message for the last failure.
  *
- * Arithmetic: fp64 throughout.  Row sums (X p, L y, X W) are sequential in
- * stored column order, bit-identical to scipy's csr_matvec; every other sum
- * (X^T z columns, dots, norms, class sums) uses the fixed "R256" reduction
- * tree documented in DESIGN.md §4, so results are bitwise reproducible run to
- * run and are mirrored exactly by oracle/fsda_oracle.c.
+ * Arithmetic: fp64 throughout.  The projection scores X W and the fsda_matvec
+ * probe are sequential in stored column order, bit-identical to scipy's
+ * csr_matvec; every other sum (X p and L y rows inside the solve, X^T z
+ * columns, dots, norms, class sums) uses the fixed "R256" reduction tree
+ * documented in DESIGN.md §4, so results are bitwise reproducible run to run
+ * and are mirrored exactly by oracle/fsda_oracle.c.
  */
 #ifndef FSDA_B200_H
 #define FSDA_B200_H
@@ -48,6 +49,9 @@ extern "C" {
 #define FSDA_ENONFINITE 3
 #define FSDA_ECUDA 4
 #define FSDA_ELABEL 5
+
+/* Largest shift grid one solve accepts (per-shift scalars live in shared memory). */
+#define FSDA_MAX_SHIFTS 4096
 
 typedef struct fsda_ctx fsda_ctx;
 

@@ -368,23 +368,29 @@ void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, i
                   (void*)&ns, (void*)&cond, (void*)&use_cond, (void*)&mu, (void*)&pz, (void*)&nlz,
                   (void*)&lab, (void*)&ell};
   const size_t smem = step_smem(ns);
-  // One 1024-thread CTA per SM: a grid barrier then has 148 arrivals.
+  // One warp per 256-element leaf (the leaf's p, q, r stay in registers across
+  // the two grid barriers); warps loop over further leaves only when d exceeds
+  // what a co-resident grid covers.
   if (c->step_blocks == 0) {
     int nb = 0;
     CK(cudaFuncSetAttribute(k_cg_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cg_step, 1024, smem));
-    c->step_blocks = std::max(1, std::min(nb, 1)) * c->num_sms;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cg_step, STEP_THREADS,
+                                                     step_smem(4096)));
+    c->step_blocks = std::max(1, nb) * c->num_sms;
   }
-  CK(cudaLaunchCooperativeKernel((void*)k_cg_step, dim3(c->step_blocks), dim3(1024), args, smem,
+  const long long want = (nlD + STEP_THREADS / 32 - 1) / (STEP_THREADS / 32);
+  const int blocks = (int)std::max(1LL, std::min<long long>(want, c->step_blocks));
+  CK(cudaLaunchCooperativeKernel((void*)k_cg_step, dim3(blocks), dim3(STEP_THREADS), args, smem,
                                  c->stream));
 }
 
 // The shift-state update of the last base step (k_shift_update) on `stream`.
 void launch_shift_update(fsda_ctx* c, int ns, long long d, cudaStream_t stream, int guarded) {
   ShiftState ss = c->shifts();
-  dim3 g((unsigned)std::min<long long>(grid_for(d, 256), (long long)c->num_sms * 2), ns);
+  dim3 g((unsigned)((d + 256 * SU_ELEMS - 1) / (256 * SU_ELEMS)),
+         (unsigned)((ns + SU_SHIFTS - 1) / SU_SHIFTS));
   k_shift_update<<<g, 256, 0, stream>>>(c->r0.ptr, c->r1.ptr, c->bigp.ptr, c->sols.ptr, d, ss,
-                                        c->sc, guarded);
+                                        c->sc, ns, guarded);
   CKL();
 }
 
@@ -398,7 +404,8 @@ void enq_iteration_body(Enq& e, int ns, long long d, int center, unsigned long l
                         int use_cond, double step_bytes, Sparse&& sparse) {
   fsda_ctx* c = e.c;
   const double su_bytes = 32.0 * d * ns + 8.0 * d;
-  if (use_cond) {
+  static const bool inline_su = std::getenv("FSDA_B200_SU_INLINE") != nullptr;
+  if (use_cond && !inline_su) {
     CK(cudaEventRecord(c->ev_fork, c->stream));
     CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
     e.go("shift_update", su_bytes, [&] { launch_shift_update(c, ns, d, c->side, 1); });
@@ -682,6 +689,7 @@ int check_solve_args(fsda_ctx* c, double alpha, const double* betas, int ns, dou
     return fail(FSDA_EINVAL, "both classes need at least one labeled sample");
   if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(FSDA_EINVAL, "alpha must lie in [0, 1], got %g", alpha);
   if (ns <= 0) return fail(FSDA_EINVAL, "shift grid must be a non-empty 1-d array");
+  if (ns > FSDA_MAX_SHIFTS) return fail(FSDA_EINVAL, "at most 4096 shifts per solve");
   for (int s = 0; s < ns; ++s) {
     if (!std::isfinite(betas[s])) return fail(FSDA_EINVAL, "shifts must be finite");
     if (s == 0 && betas[s] < 0) return fail(FSDA_EINVAL, "shifts must be non-negative");
@@ -1425,6 +1433,7 @@ int fsda_shifted_cg_dense(fsda_ctx* c, int64_t dim, const double* a, const doubl
   if (dim <= 0) return fail(FSDA_EINVAL, "operator dimension must be positive");
   if (dim > MAX_REDUCE) return fail(FSDA_EINVAL, "dimension above the reduction limit");
   if (ns <= 0) return fail(FSDA_EINVAL, "shift grid must be a non-empty 1-d array");
+  if (ns > FSDA_MAX_SHIFTS) return fail(FSDA_EINVAL, "at most 4096 shifts per solve");
   for (int s = 0; s < ns; ++s) {
     if (!std::isfinite(betas[s])) return fail(FSDA_EINVAL, "shifts must be finite");
     if (s == 0 && betas[s] < 0) return fail(FSDA_EINVAL, "shifts must be non-negative");
@@ -1554,6 +1563,7 @@ int fsda_dev_cg_begin(fsda_ctx* c, const double* betas, int ns, double tol, int6
   API_BEGIN(c)
   if (c->d <= 0) return fail(FSDA_EINVAL, "operator dimension must be positive");
   if (ns <= 0) return fail(FSDA_EINVAL, "shift grid must be a non-empty 1-d array");
+  if (ns > FSDA_MAX_SHIFTS) return fail(FSDA_EINVAL, "at most 4096 shifts per solve");
   for (int s = 0; s < ns; ++s) {
     if (!std::isfinite(betas[s])) return fail(FSDA_EINVAL, "shifts must be finite");
     if (s == 0 && betas[s] < 0) return fail(FSDA_EINVAL, "shifts must be non-negative");
@@ -1652,6 +1662,7 @@ int fsda_regression_shifted_cg(fsda_ctx* c, const double* rhs, const double* bet
   if (!c->has_x) return fail(FSDA_EINVAL, "X has not been uploaded");
   if (c->d <= 0) return fail(FSDA_EINVAL, "operator dimension must be positive");
   if (ns <= 0) return fail(FSDA_EINVAL, "shift grid must be a non-empty 1-d array");
+  if (ns > FSDA_MAX_SHIFTS) return fail(FSDA_EINVAL, "at most 4096 shifts per solve");
   for (int s = 0; s < ns; ++s) {
     if (!std::isfinite(betas[s])) return fail(FSDA_EINVAL, "shifts must be finite");
     if (s == 0 && betas[s] < 0) return fail(FSDA_EINVAL, "shifts must be non-negative");
@@ -1682,6 +1693,7 @@ int fsda_sa_solve(fsda_ctx* c, double alpha, const double* betas, int ns, double
   if (c->ell == 0) return fail(FSDA_ELABEL, "centering requires at least one labeled sample");
   if (c->n1 == 0 || c->n2 == 0) return fail(FSDA_EINVAL, "both classes need at least one labeled sample");
   if (ns <= 0) return fail(FSDA_EINVAL, "shift grid must be a non-empty 1-d array");
+  if (ns > FSDA_MAX_SHIFTS) return fail(FSDA_EINVAL, "at most 4096 shifts per solve");
   for (int s = 0; s < ns; ++s) {
     if (!std::isfinite(betas[s])) return fail(FSDA_EINVAL, "shifts must be finite");
     if (s == 0 && betas[s] < 0) return fail(FSDA_EINVAL, "shifts must be non-negative");

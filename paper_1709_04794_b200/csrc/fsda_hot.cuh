@@ -1,12 +1,13 @@
 // fsda_hot.cuh — the per-iteration kernels of the FSDA sweep (included by
 // fsda_device.cuh; same arithmetic contract, see the header there).
 //
-// One shifted-CG iteration = 4 launches:
+// One shifted-CG iteration = 5 launches:
 //   k_segsum<SEG_XROWS>  y = X p                (rows, canonical tree)
-//   k_segsum<SEG_LROWS>  z = M y                (rows of L, canonical tree, blend)
-//   k_segsum<SEG_XCOLS>  q_raw = X^T z, + leaf partials of sum(z)
-//   k_cg_step            cooperative: centring, p.q -> shift scalars ->
-//                        sols/P/r updates -> r.r -> p
+//   k_segsum<SEG_LROWS>  z = M y                (rows of L, canonical tree, blend),
+//                        + leaf partials of sum(z)
+//   k_xt_coop            q_raw = X^T z          (columns, cooperative)
+//   k_cg_step            cooperative: centring, p.q -> shift scalars -> r, r.r -> p
+//   k_shift_update       sols / P for every active shift (side stream)
 // k_spmv_rows (scipy's sequential row order) serves the X v probe API.
 #pragma once
 
@@ -540,24 +541,26 @@ __global__ void k_center(const double* __restrict__ mu, double* __restrict__ q, 
 }
 
 // -------------------------------------------- K4: one cooperative CG step
-// krylov.py:211-268 for every active shift in one launch with two grid-wide
-// barriers:
-//   A  leaf partials of p.q
+// krylov.py:211-268 for the base system in one launch with two grid-wide
+// barriers.  Warp w owns 256-element leaf w (plus leaves w + total_warps, ...
+// when d is larger than the grid covers); the first leaf's p, q, r and the
+// centring coefficient are loaded into registers at entry, together with the
+// shift state, so each phase waits on one round of loads (its partials):
+//   A  sum(z) (leaf partials from K2/K3), centring of q, leaf partials of p.q
 //   -- grid sync --
 //   B  every block finishes p.q (identical tree, identical result), derives
-//      gamma and the per-shift zeta_next / gamma_s / good flags in shared
-//      memory; then per 256-element leaf: r_next = r + gamma q with leaf
-//      partials of r_next.r_next (block row 0), and for each good shift the
-//      deferred P update owed from the previous iteration (krylov.py:241) and
-//      sols -= P * gamma_s (krylov.py:230) — sols and P are read and written
-//      once per iteration
+//      gamma and the per-shift zeta_next / gamma_s / good flags; r_next = r +
+//      gamma q with leaf partials of r_next.r_next
 //   -- grid sync --
-//   C  every block finishes r.r and alpha_new; p = r_next + alpha_new p;
-//      block 0 retires converged / degenerate shifts, rolls zeta, advances
-//      the iteration, and sets the while-loop condition.
+//   C  every block finishes r.r and alpha_new; p = r_next + alpha_new p from
+//      registers; block 0 retires converged / degenerate shifts, rolls zeta,
+//      writes the shift-update snapshot for k_shift_update, advances the
+//      iteration, and sets the while-loop condition.
 // Scalars needed after block 0 starts writing them are read into registers
 // at kernel entry, so no block reads state that block 0 modifies.
-__global__ void __launch_bounds__(1024, 1) k_cg_step(
+constexpr int STEP_THREADS = 256;
+
+__global__ void __launch_bounds__(STEP_THREADS) k_cg_step(
     double* __restrict__ q, double* __restrict__ p, double* __restrict__ r0,
     double* __restrict__ r1, double* __restrict__ bigp, double* __restrict__ sols, long long d,
     double* __restrict__ part_pq, double* __restrict__ part_rr, long long n_leaf, CgScalars* sc,
@@ -583,32 +586,64 @@ __global__ void __launch_bounds__(1024, 1) k_cg_step(
     if (leader && use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond_handle, 0u);
     return;
   }
-  // Block 0 writes scalar / shift state only after the second grid barrier,
-  // i.e. after every block has performed the entry reads above.
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
   const long long tw = (long long)gridDim.x * (blockDim.x >> 5);
   const double* r_cur = (it & 1) ? r1 : r0;
   double* r_next = (it & 1) ? r0 : r1;
+  const bool center = part_z != nullptr;
+  const bool own = gw < n_leaf;  // this warp's register-cached leaf
 
-  // ---- A: centring q = X^T z - mu sum(z) (sparse.py:277; sum(z) leaves come
-  // from k_segsum), then the p.q leaves
-  double sum_z = 0.0;
-  if (part_z) sum_z = block_reduce_partials(part_z, n_leaf_z, smem);
-  for (long long g = gw; g < n_leaf; g += tw) {
+  // ---- entry loads: the cached leaf and this thread's first shift
+  double pr[8], qr[8], rv[8], cr[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const long long i = gw * LEAF + k * 32 + lane;
+    const bool in = own && i < d;
+    pr[k] = in ? p[i] : 0.0;
+    qr[k] = in ? q[i] : 0.0;
+    rv[k] = in ? r_cur[i] : 0.0;
+    cr[k] = (in && center) ? (mu ? mu[i] : (labels[i] != 0 ? 1.0 : 0.0)) : 0.0;
+  }
+  const int s0 = threadIdx.x;
+  int act0 = 0;
+  double zp0 = 0.0, z0 = 0.0, b0 = 0.0;
+  if (s0 < ns) {
+    act0 = ss.active[s0];
+    zp0 = ss.zeta_prev[s0];
+    z0 = ss.zeta[s0];
+    b0 = ss.beta[s0];
+  }
+
+  // ---- A: centring q = X^T z - mu sum(z) (sparse.py:277) or, for SA-SDA,
+  // M z - 1_l (sum(M z) / l) (sda.py:155-157); then the p.q leaves
+  double sz = 0.0;
+  if (center) {
+    const double sum_z = block_reduce_partials(part_z, n_leaf_z, smem);
+    sz = mu ? sum_z : sum_z / ell;
+  }
+  if (own) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (gw * LEAF + k * 32 + lane < d) {
+        if (center) qr[k] = qr[k] - cr[k] * sz;
+        a = fma(pr[k], qr[k], a);
+      }
+    }
+    a = butterfly(a);
+    if (lane == 0) part_pq[gw] = a;
+  }
+  for (long long g = gw + tw; g < n_leaf; g += tw) {
     double a = 0.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const long long i = g * LEAF + k * 32 + lane;
       if (i < d) {
         double qi = q[i];
-        if (part_z) {
-          if (mu) {        // FSDA: X^T z - mu * sum(z)          (sparse.py:277)
-            qi = qi - mu[i] * sum_z;
-          } else {         // SA-SDA: M z - 1_l * (sum(Mz) / l)  (sda.py:155-157)
-            qi = qi - (labels[i] != 0 ? 1.0 : 0.0) * (sum_z / ell);
-          }
+        if (center) {
+          qi = qi - (mu ? mu[i] : (labels[i] != 0 ? 1.0 : 0.0)) * sz;
           q[i] = qi;
         }
         a = fma(p[i], qi, a);
@@ -619,7 +654,7 @@ __global__ void __launch_bounds__(1024, 1) k_cg_step(
   }
   grid.sync();
 
-  // ---- B: scalars, then the updates
+  // ---- B: scalars, then r_next = r + gamma q and its r.r leaves (krylov.py:232-233)
   const double pq = block_reduce_partials(part_pq, n_leaf, smem);
   if (!isfinite(pq) || pq == 0.0) {
     if (leader) {
@@ -632,10 +667,12 @@ __global__ void __launch_bounds__(1024, 1) k_cg_step(
   }
   const double gamma = -rr / pq;
   for (int s = threadIdx.x; s < ns; s += blockDim.x) {
+    const bool first = s == s0;
     double zn = 0.0, gs = 0.0, good = 0.0;
-    if (ss.active[s]) {
-      const double zp = ss.zeta_prev[s], z = ss.zeta[s];
-      const double denom = gamma * al * (zp - z) + zp * gp * (1.0 - ss.beta[s] * gamma);
+    if (first ? act0 : ss.active[s]) {
+      const double zp = first ? zp0 : ss.zeta_prev[s], z = first ? z0 : ss.zeta[s];
+      const double beta = first ? b0 : ss.beta[s];
+      const double denom = gamma * al * (zp - z) + zp * gp * (1.0 - beta * gamma);
       zn = zp * z * gp / denom;
       if (isfinite(zn) && !(fabs(zn) < 1e-290)) {
         good = 1.0;
@@ -646,18 +683,27 @@ __global__ void __launch_bounds__(1024, 1) k_cg_step(
     s_gs[s] = gs;
     s_good[s] = good;
   }
-  __syncthreads();
-  // r_next = r + gamma q and its r.r leaves (krylov.py:232-233).  The shift
-  // state (sols, P) is updated by k_shift_update from the snapshot written in
-  // phase C, off the critical path (it runs beside the next iteration's
-  // sparse kernels).
-  for (long long g = gw; g < n_leaf; g += tw) {
+  if (own) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long long i = gw * LEAF + k * 32 + lane;
+      if (i < d) {
+        rv[k] = rv[k] + gamma * qr[k];
+        r_next[i] = rv[k];
+        a = fma(rv[k], rv[k], a);
+      }
+    }
+    a = butterfly(a);
+    if (lane == 0) part_rr[gw] = a;
+  }
+  for (long long g = gw + tw; g < n_leaf; g += tw) {
     double a = 0.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const long long i = g * LEAF + k * 32 + lane;
       if (i < d) {
-        const double rn = r_cur[i] + gamma * __ldcg(q + i);
+        const double rn = r_cur[i] + gamma * q[i];
         r_next[i] = rn;
         a = fma(rn, rn, a);
       }
@@ -679,24 +725,35 @@ __global__ void __launch_bounds__(1024, 1) k_cg_step(
     return;
   }
   const double alpha_new = rr_new / rr;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < d;
-       i += (long long)gridDim.x * blockDim.x) {
-    p[i] = __ldcg(r_next + i) + alpha_new * p[i];
+  if (own) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long long i = gw * LEAF + k * 32 + lane;
+      if (i < d) p[i] = rv[k] + alpha_new * pr[k];
+    }
+  }
+  for (long long g = gw + tw; g < n_leaf; g += tw) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long long i = g * LEAF + k * 32 + lane;
+      if (i < d) p[i] = r_next[i] + alpha_new * p[i];  // this thread wrote r_next[i] in B
+    }
   }
   if (blockIdx.x != 0) return;
   if (threadIdx.x == 0) s_flag = 0;
   __syncthreads();
   const double r_norm = sqrt(rr_new);
   for (int s = threadIdx.x; s < ns; s += blockDim.x) {
+    const bool first = s == s0;
     ss.upd_mode[s] = 0;
-    if (!ss.active[s]) continue;
+    if (!(first ? act0 : ss.active[s])) continue;
     if (s_good[s] == 0.0) {  // degenerate zeta: freeze untouched (krylov.py:251-255)
       ss.iters[s] = it + 1;
       ss.resid[s] = __longlong_as_double(0x7ff0000000000000LL);
       ss.active[s] = 0;
       continue;
     }
-    const double zn = s_zn[s], z = ss.zeta[s], gs = s_gs[s];
+    const double zn = s_zn[s], z = first ? z0 : ss.zeta[s], gs = s_gs[s];
     const double as = alpha_new * (zn * gs) / (z * gamma);
     ss.alpha_s[s] = as;
     ss.upd_gs[s] = gs;
@@ -739,28 +796,52 @@ __global__ void __launch_bounds__(1024, 1) k_cg_step(
 // The shift updates of the iteration whose snapshot k_cg_step wrote
 // (krylov.py:230, 240-241): sols_s -= gamma_s P_s, then P_s = zeta_next r +
 // alpha_s P_s for shifts still active.  r is the current residual r_{i+1}.
+// A block covers SU_ELEMS * 256 rows for SU_SHIFTS shifts, so r is read once
+// per SU_SHIFTS shifts and every thread keeps 2 * SU_ELEMS loads in flight.
 // Launched on a second stream beside the next iteration's sparse kernels
 // (guarded: skipped once the loop is idle) and once more, unguarded, after the
 // loop for the final iteration.
+constexpr int SU_ELEMS = 4;
+constexpr int SU_SHIFTS = 4;
+
 __global__ void __launch_bounds__(256) k_shift_update(const double* __restrict__ r0,
                                                       const double* __restrict__ r1,
                                                       double* __restrict__ bigp,
                                                       double* __restrict__ sols, long long d,
                                                       ShiftState ss, const CgScalars* sc,
-                                                      int guarded) {
+                                                      int ns, int guarded) {
   if (guarded && loop_idle(sc)) return;
-  const int s = blockIdx.y;
-  const int mode = ss.upd_mode[s];
-  if (mode == 0) return;
-  const double gs = ss.upd_gs[s], zn = ss.upd_zn[s], as = ss.upd_as[s];
   const double* r = (sc->iter & 1) ? r1 : r0;
-  double* P = bigp + (long long)s * d;
-  double* X = sols + (long long)s * d;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < d;
-       i += (long long)gridDim.x * blockDim.x) {
-    const double pv = P[i];
-    X[i] = X[i] - pv * gs;
-    if (mode == 3) P[i] = zn * r[i] + as * pv;
+  const long long base = (long long)blockIdx.x * (256 * SU_ELEMS) + threadIdx.x;
+  double rv[SU_ELEMS];
+#pragma unroll
+  for (int e = 0; e < SU_ELEMS; ++e) {
+    const long long i = base + e * 256;
+    rv[e] = i < d ? __ldcg(r + i) : 0.0;
+  }
+  for (int sj = 0; sj < SU_SHIFTS; ++sj) {
+    const int s = blockIdx.y * SU_SHIFTS + sj;
+    if (s >= ns) break;
+    const int mode = ss.upd_mode[s];
+    if (mode == 0) continue;
+    const double gs = ss.upd_gs[s], zn = ss.upd_zn[s], as = ss.upd_as[s];
+    double* P = bigp + (long long)s * d;
+    double* X = sols + (long long)s * d;
+    double pv[SU_ELEMS], xv[SU_ELEMS];
+#pragma unroll
+    for (int e = 0; e < SU_ELEMS; ++e) {
+      const long long i = base + e * 256;
+      pv[e] = i < d ? P[i] : 0.0;
+      xv[e] = i < d ? X[i] : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < SU_ELEMS; ++e) {
+      const long long i = base + e * 256;
+      if (i < d) {
+        X[i] = xv[e] - pv[e] * gs;
+        if (mode == 3) P[i] = zn * rv[e] + as * pv[e];
+      }
+    }
   }
 }
 

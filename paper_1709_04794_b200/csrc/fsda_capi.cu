@@ -305,7 +305,7 @@ void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* sum
     unsigned long long* ticket = c->xt_ticket.ptr;
     void* args[] = {(void*)&pl, (void*)&xh, (void*)&a, (void*)&sc, (void*)&guarded, (void*)&n_rows,
                     (void*)&ticket};
-    CK(cudaLaunchCooperativeKernel((void*)k_xt_coop, dim3(c->xt_blocks), dim3(1024), args, 0,
+    CK(cudaLaunchCooperativeKernel((void*)k_xt_coop, dim3(c->xt_blocks), dim3(XT_THREADS), args, 0,
                                    c->stream));
   });
 }
@@ -899,8 +899,8 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   if (nh) CK(cudaMemset(c->xh_part.ptr, 0, sizeof(double) * nh * nb));
   if (c->xt_blocks == 0) {
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_xt_coop, 1024, 0));
-    c->xt_blocks = std::max(1, std::min(per_sm, 1)) * c->num_sms;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_xt_coop, XT_THREADS, 0));
+    c->xt_blocks = std::max(1, std::min(per_sm, XT_CTAS_PER_SM)) * c->num_sms;
   }
   XtDense& xh = c->xh;
   xh.rows = c->csc_rows.ptr;

@@ -345,6 +345,10 @@ __global__ void __launch_bounds__(256, 6) k_segsum(SegPlan pl, SegArgs a, const 
 //   phase 2  one warp per dense column reduces its nb partials.
 constexpr int XT_RB = 1024;
 constexpr int XT_DENSE_DIV = 8;  // dense: n > 256 and XT_DENSE_DIV * n >= N
+// k_xt_coop: two 24-warp CTAs per SM at <= 40 registers (measured: 1.04x / 1.06x
+// cfg2 / cfg3 over one 32-warp CTA)
+constexpr int XT_THREADS = 768;
+constexpr int XT_CTAS_PER_SM = 2;
 
 struct XtDense {
   const int* rows;        // CSC row indices
@@ -419,7 +423,7 @@ __device__ __forceinline__ void dense_slice_long(const XtDense& dn, const double
   if (lane == 0) dn.part[(long long)tk.x * dn.nb + b] = acc;
 }
 
-__global__ void __launch_bounds__(1024, 1) k_xt_coop(SegPlan pl, XtDense dn, SegArgs a,
+__global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan pl, XtDense dn, SegArgs a,
                                                     const CgScalars* sc, int guarded, int n_rows,
                                                     unsigned long long* ticket) {
   if (guarded && loop_idle(sc)) return;  // uniform across the grid
@@ -458,13 +462,18 @@ __global__ void __launch_bounds__(1024, 1) k_xt_coop(SegPlan pl, XtDense dn, Seg
     }
   }
   // ---- phase 1b: the other columns and the sum(z) leaves; warps draw tasks
-  // from a grid-wide ticket so CTAs that staged a dense block catch up
+  // from a grid-wide ticket so CTAs that staged a dense block catch up.
   const long long total = pl.warp_base[8];
+  const long long nheavy = pl.warp_base[7] - pl.warp_base[6];
   for (;;) {
-    long long tw = 0;
-    if (lane == 0) tw = (long long)atomicAdd(ticket, 1ULL);
-    tw = __shfl_sync(FULL, tw, 0);
-    if (tw >= total) break;
+    long long nxt = 0;
+    if (lane == 0) nxt = (long long)atomicAdd(ticket, 1ULL);
+    nxt = __shfl_sync(FULL, nxt, 0);
+    if (nxt >= total) break;
+    // largest tasks first: tickets [0, nheavy) are the heavy tasks, then the
+    // class tasks, then the sum(z) leaves
+    const long long tw = nxt < nheavy ? pl.warp_base[6] + nxt
+                                      : (nxt < pl.warp_base[7] ? nxt - nheavy : nxt);
     if (tw < pl.warp_base[6]) {
       int k = 0;
       while (tw >= pl.warp_base[k + 1]) ++k;

@@ -127,7 +127,7 @@ struct fsda_ctx {
   // dense columns of X (blocked by rows, see k_xt_coop)
   DevBuf<int> xh_col, xh_bptr;
   DevBuf<int4> xh_tasks;
-  DevBuf<long long> xh_boff, xh_bwarp;
+  DevBuf<long long> xh_boff, xh_bwarp, xh_poff;
   DevBuf<double> xh_part;
   XtDense xh{};
   int xt_blocks = 0;
@@ -305,7 +305,8 @@ void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* sum
     unsigned long long* ticket = c->xt_ticket.ptr;
     void* args[] = {(void*)&pl, (void*)&xh, (void*)&a, (void*)&sc, (void*)&guarded, (void*)&n_rows,
                     (void*)&ticket};
-    CK(cudaLaunchCooperativeKernel((void*)k_xt_coop, dim3(c->xt_blocks), dim3(XT_THREADS), args, 0,
+    CK(cudaLaunchCooperativeKernel((void*)k_xt_coop, dim3(c->xt_blocks), dim3(XT_THREADS), args,
+                                   sizeof(double) * xh.rb,
                                    c->stream));
   });
 }
@@ -842,38 +843,48 @@ void build_seg_plan(HostPlan& hp, const OffT* offs, long long S, const int* ind,
 }
 
 // Per-row-block slice tasks for the dense columns (k_xt_coop phase 1a).
+// Rows per staged z block; the oracle's XT_RB must match.
+int xt_rb() { return XT_RB; }
+
 void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   const long long nh = (long long)dense.size();
-  const int nb = (int)std::max<long long>(1, cdiv(c->n, XT_RB));
+  const int rb = xt_rb();
+  const int nb = (int)std::max<long long>(1, cdiv(c->n, rb));
   c->xh_col.ensure(nh);
   c->xh_bptr.ensure(nh * (nb + 1));
-  c->xh_part.ensure(nh * nb);
   std::vector<int> bptr;
   if (nh) {
     CK(cudaMemcpy(c->xh_col.ptr, dense.data(), sizeof(int) * nh, cudaMemcpyHostToDevice));
     k_heavy_bptr<<<grid_for(nh * (nb + 1), 256), 256, 0, c->stream>>>(
-        c->csc_colptr.ptr, c->csc_rows.ptr, c->xh_col.ptr, c->xh_bptr.ptr, nh, nb);
+        c->csc_colptr.ptr, c->csc_rows.ptr, c->xh_col.ptr, c->xh_bptr.ptr, nh, nb, rb);
     CKL();
     bptr.resize(nh * (nb + 1));
     CK(cudaMemcpyAsync(bptr.data(), c->xh_bptr.ptr, sizeof(int) * bptr.size(), cudaMemcpyDeviceToHost,
                        c->stream));
     CK(cudaStreamSynchronize(c->stream));
   }
+  // leaf-sum slots: column h owns max(1, ceil(n_hb / 256)) slots per block b
+  std::vector<long long> poff((size_t)nh + 1, 0);
+  for (long long h = 0; h < nh; ++h) {
+    long long m = 0;
+    for (int b = 0; b < nb; ++b) m += std::max<long long>(1, cdiv(bptr[h * (nb + 1) + b + 1] - bptr[h * (nb + 1) + b], LEAF));
+    poff[h + 1] = poff[h] + m;
+  }
+  // poff[nh] <= nnz / XT_DENSE_PER_BLOCK + nnz / LEAF < 2^31: int slots suffice
+  std::vector<long long> pos(poff.begin(), poff.end() - 1);
   std::vector<int4> tasks;
   std::vector<long long> boff((size_t)(nb + 1) * 7, 0), bwarp((size_t)nb * 7, 0);
-  std::vector<int4> cls[6], longs;
+  std::vector<int4> cls[6];
   for (int b = 0; b < nb; ++b) {
     for (auto& v : cls) v.clear();
-    longs.clear();
     for (long long h = 0; h < nh; ++h) {
       const int lo = bptr[h * (nb + 1) + b], n = bptr[h * (nb + 1) + b + 1] - lo;
-      if (n == 0) continue;  // partial stays 0.0 (see below)
-      if (n <= LEAF) {
+      if (n == 0) { ++pos[h]; continue; }  // slot stays 0.0 (see below)
+      for (int c0 = 0; c0 < n; c0 += LEAF) {
+        const int len = std::min(LEAF, n - c0);
         int k = 0;
-        while (8 * (1 << k) < n) ++k;
-        cls[k].push_back(make_int4((int)h, lo, n, 0));
-      } else {
-        longs.push_back(make_int4((int)h, lo, n, 0));
+        while (8 * (1 << k) < len) ++k;
+        cls[k].push_back(make_int4((int)pos[h]++, lo + c0, len, 0));
       }
     }
     long long wb = 0;
@@ -885,21 +896,26 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
     }
     bwarp[(size_t)b * 7 + 6] = wb;
     boff[(size_t)b * 7 + 6] = (long long)tasks.size();
-    tasks.insert(tasks.end(), longs.begin(), longs.end());
   }
   for (int k = 0; k < 7; ++k) boff[(size_t)nb * 7 + k] = (long long)tasks.size();
   c->xh_tasks.ensure(tasks.size());
   c->xh_boff.ensure(boff.size());
   c->xh_bwarp.ensure(bwarp.size());
+  c->xh_poff.ensure(poff.size());
+  c->xh_part.ensure(std::max<long long>(1, poff[nh]));
   if (!tasks.empty())
     CK(cudaMemcpy(c->xh_tasks.ptr, tasks.data(), sizeof(int4) * tasks.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->xh_boff.ptr, boff.data(), sizeof(long long) * boff.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->xh_bwarp.ptr, bwarp.data(), sizeof(long long) * bwarp.size(), cudaMemcpyHostToDevice));
-  // empty slices never get a task: their partials must read 0.0
-  if (nh) CK(cudaMemset(c->xh_part.ptr, 0, sizeof(double) * nh * nb));
+  CK(cudaMemcpy(c->xh_poff.ptr, poff.data(), sizeof(long long) * poff.size(), cudaMemcpyHostToDevice));
+  // empty blocks never get a task: their slots must read 0.0
+  if (poff[nh]) CK(cudaMemset(c->xh_part.ptr, 0, sizeof(double) * poff[nh]));
   if (c->xt_blocks == 0) {
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_xt_coop, XT_THREADS, 0));
+    CK(cudaFuncSetAttribute(k_xt_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(sizeof(double) * rb)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_xt_coop, XT_THREADS,
+                                                     sizeof(double) * rb));
     c->xt_blocks = std::max(1, std::min(per_sm, XT_CTAS_PER_SM)) * c->num_sms;
   }
   XtDense& xh = c->xh;
@@ -909,8 +925,10 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   xh.bwarp = c->xh_bwarp.ptr;
   xh.col = c->xh_col.ptr;
   xh.part = c->xh_part.ptr;
+  xh.poff = c->xh_poff.ptr;
   xh.n_dense = nh;
   xh.nb = nb;
+  xh.rb = rb;
   xh.splits = (int)std::max<long long>(1, c->xt_blocks / nb);
   if (!c->xt_ticket.ptr) {
     c->xt_ticket.ensure(1);
@@ -1124,7 +1142,9 @@ int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* ro
     std::vector<int> colptr(n_cols + 1);
     CK(cudaMemcpy(colptr.data(), c->csc_colptr.ptr, sizeof(int) * (n_cols + 1), cudaMemcpyDeviceToHost));
     std::vector<int> dense;
-    const long long dense_min = std::max<long long>(LEAF + 1, cdiv(n_rows, XT_DENSE_DIV));
+    const long long dpb = XT_DENSE_PER_BLOCK;
+    const long long dense_min =
+        std::max<long long>(LEAF + 1, dpb * std::max<long long>(1, cdiv(n_rows, xt_rb())));
     build_seg_plan(c->plan_xc, colptr.data(), n_cols, c->csc_rows.ptr, &dense, dense_min);
     build_dense_plan(c, dense);
   }

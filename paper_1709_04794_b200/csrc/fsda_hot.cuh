@@ -330,10 +330,13 @@ __global__ void __launch_bounds__(256, 6) k_segsum(SegPlan pl, SegArgs a, const 
 // ------------------------------------------ K3: X^T z, dense columns blocked
 // Canonical column sum:
 //   * n <= 256: the R256 leaf over z[rows] in row order;
-//   * n > 256 and sparse (8 n < N): R256 over its leaves of 256 entries;
-//   * dense (n > 256 and 8 n >= N — the Zipf head): rows are cut into blocks
-//     of XT_RB; partial_b = R256 over the column's entries in block b (0.0 if
-//     none); the column sum is R256 over (partial_0 .. partial_{nb-1}).
+//   * n > 256 and n < 8 nb (nb = ceil(N / XT_RB) row blocks): R256 over its
+//     leaves of 256 entries;
+//   * blocked ("dense": n > 256 and n >= 8 nb, i.e. at least 8 entries per
+//     row block on average — the Zipf head): rows are cut into blocks of
+//     XT_RB; the column's entries in block b are cut into leaves of 256 (an
+//     empty block contributes one 0.0), and the column sum is R256 over all
+//     those leaf sums in (block, leaf) order.
 // The dense rule lets a CTA stage one XT_RB-row block of z in shared memory
 // and serve every dense-column gather of that block from it.  Each (block,
 // dense column) slice is one task of the W-class scheme (host plan per
@@ -343,8 +346,8 @@ __global__ void __launch_bounds__(256, 6) k_segsum(SegPlan pl, SegArgs a, const 
 //            leaf-combining heavy tasks) and the leaf partials of sum(z)
 //   -- grid sync --
 //   phase 2  one warp per dense column reduces its nb partials.
-constexpr int XT_RB = 1024;
-constexpr int XT_DENSE_DIV = 8;  // dense: n > 256 and XT_DENSE_DIV * n >= N
+constexpr int XT_RB = 8192;             // rows per staged z block (64 KB of shared memory)
+constexpr int XT_DENSE_PER_BLOCK = 8;   // blocked: n > 256 and n >= XT_DENSE_PER_BLOCK * nb
 // k_xt_coop: two 24-warp CTAs per SM at <= 40 registers (measured: 1.04x / 1.06x
 // cfg2 / cfg3 over one 32-warp CTA)
 constexpr int XT_THREADS = 768;
@@ -352,13 +355,15 @@ constexpr int XT_CTAS_PER_SM = 2;
 
 struct XtDense {
   const int* rows;        // CSC row indices
-  const int4* tasks;      // {dense id, start, length, -}, grouped by (block, class)
-  const long long* boff;  // per block: 6 class starts + long-slice start; (nb + 1) * 7
+  const int4* tasks;      // {partial slot, start, length, -}, grouped by (block, class)
+  const long long* boff;  // per block: 6 class starts + end; (nb + 1) * 7
   const long long* bwarp; // per block: warp prefixes of the 6 classes + total; nb * 7
   const int* col;         // dense id -> column
-  double* part;           // nb partials per dense column
+  const long long* poff;  // dense id -> first leaf-sum slot; n_dense + 1
+  double* part;           // leaf sums, (block, leaf) order per dense column
   long long n_dense;
   int nb;
+  int rb;                 // rows per block (XT_RB)
   int splits;             // CTAs sharing one row block's slices
 };
 
@@ -399,35 +404,14 @@ __device__ __forceinline__ void dense_slice_task(const XtDense& dn, const double
   double r = A[0];
 #pragma unroll
   for (int off2 = W / 2; off2 >= 1; off2 >>= 1) r = r + __shfl_xor_sync(FULL, r, off2);
-  if (tk.x >= 0 && t == 0) dn.part[(long long)tk.x * dn.nb + b] = r;
-}
-
-// Slices longer than 256 entries: R256 over their leaves by one warp.
-__device__ __forceinline__ void dense_slice_long(const XtDense& dn, const double* zs, int r0, int b,
-                                                 const int4 tk, int lane) {
-  double acc = 0.0;
-  const int nl = (tk.z + LEAF - 1) / LEAF;
-  for (int g = 0; g < nl; ++g) {
-    const int base = tk.y + g * LEAF, len = min(LEAF, tk.z - g * LEAF);
-    int ri[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) ri[u] = (lane + 32 * u < len) ? __ldg(dn.rows + base + lane + 32 * u) - r0 : 0;
-    double a = 0.0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (lane + 32 * u < len) a = a + zs[ri[u]];
-    a = butterfly(a);
-    if ((g & 31) == lane) acc = acc + a;
-  }
-  acc = butterfly(acc);
-  if (lane == 0) dn.part[(long long)tk.x * dn.nb + b] = acc;
+  if (tk.x >= 0 && t == 0) dn.part[tk.x] = r;
 }
 
 __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan pl, XtDense dn, SegArgs a,
                                                     const CgScalars* sc, int guarded, int n_rows,
                                                     unsigned long long* ticket) {
   if (guarded && loop_idle(sc)) return;  // uniform across the grid
-  __shared__ double zs[XT_RB];
+  extern __shared__ double zs[];  // dn.rb doubles
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   // ---- phase 1a: (row block, split) units with their dense-column slices
@@ -435,8 +419,8 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
     const long long units = (long long)dn.nb * dn.splits;
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
       const int b = (int)(u / dn.splits), sp = (int)(u - (long long)b * dn.splits);
-      const int r0 = b * XT_RB;
-      const int nr = min(XT_RB, n_rows - r0);
+      const int r0 = b * dn.rb;
+      const int nr = min(dn.rb, n_rows - r0);
       __syncthreads();
       for (int k = threadIdx.x; k < nr; k += blockDim.x) zs[k] = __ldg(a.src + r0 + k);
       __syncthreads();
@@ -454,11 +438,6 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
           default: dense_slice_task<32>(dn, zs, r0, b, 5, tw, lane); break;
         }
       }
-      // long slices (> 256 entries): one warp each, dealt round-robin over splits
-      const long long l0 = dn.boff[(long long)b * 7 + 6];
-      const long long l1 = dn.boff[(long long)(b + 1) * 7 + 0];
-      for (long long j = l0 + sp + (long long)dn.splits * warp; j < l1; j += (long long)dn.splits * nw)
-        dense_slice_long(dn, zs, r0, b, __ldg(dn.tasks + j), lane);
     }
   }
   // ---- phase 1b: the other columns and the sum(z) leaves; warps draw tasks
@@ -505,7 +484,8 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
   // ---- phase 2: dense columns
   const long long gw = (long long)blockIdx.x * nw + warp;
   for (long long h = gw; h < dn.n_dense; h += nwarps) {
-    const double v = warp_reduce_partials(dn.part + h * dn.nb, dn.nb, lane);
+    const long long p0 = __ldg(dn.poff + h);
+    const double v = warp_reduce_partials(dn.part + p0, (int)(__ldg(dn.poff + h + 1) - p0), lane);
     if (lane == 0) seg_finish<SEG_XCOLS>(a, __ldg(dn.col + h), v);
   }
 }
@@ -514,7 +494,7 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
 // >= b * XT_RB (b = nb gives the column end).
 __global__ void k_heavy_bptr(const int* __restrict__ colptr, const int* __restrict__ rows,
                              const int* __restrict__ heavy_col, int* __restrict__ bptr,
-                             long long n_heavy, int nb) {
+                             long long n_heavy, int nb, int rb) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_heavy * (nb + 1)) return;
   const long long h = t / (nb + 1);
@@ -522,7 +502,7 @@ __global__ void k_heavy_bptr(const int* __restrict__ colptr, const int* __restri
   const int c = heavy_col[h];
   int lo = colptr[c], hi = colptr[c + 1];
   if (b == nb) { bptr[t] = hi; return; }
-  const int target = b * XT_RB;
+  const int target = b * rb;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     if (rows[mid] < target) lo = mid + 1; else hi = mid;

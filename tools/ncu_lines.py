@@ -10,6 +10,7 @@ from collections import defaultdict
 
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+func = sys.argv[4] if len(sys.argv) > 4 else None   # substring of the function name
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
                       "-k", f"regex:{kern}"], capture_output=True, text=True).stdout
 samples = defaultdict(int)
@@ -18,6 +19,7 @@ fname = "?"
 cur = None
 i_s = None
 seen = set()
+skip = False
 for r in csv.reader(out.splitlines()):
     if not r:
         continue
@@ -25,6 +27,9 @@ for r in csv.reader(out.splitlines()):
         fname = r[1].rsplit("/", 1)[-1]
         continue
     if r[0] == "Function Name":
+        skip = func is not None and func not in r[1]
+        continue
+    if func is not None and skip:
         continue
     if r[0] == "Line No":
         i_s = r.index("Warp Stall Sampling (All Samples)")

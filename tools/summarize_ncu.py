@@ -21,7 +21,8 @@ out.mkdir(exist_ok=True)
 
 # bench.py names -> kernel names
 BENCH_NAME = {"k_xt_coop": "xt", "k_segsum<0>": "spmv_rows", "k_segsum<1>": "smoother",
-              "k_cg_step": "cg_step", "k_spmm_scores": "spmm_scores"}
+              "k_cg_step": "cg_step", "k_shift_update": "shift_update",
+              "k_spmm_scores": "spmm_scores"}
 
 
 def short(name):

@@ -287,7 +287,11 @@ def run_b200(args):
                                         pinned_copy(w.l_vals)), w.degrees)
     pp = fb.SdaProblem(x=px, labels=fb.LabelVector(w.labels), lap=plap, alpha=w.alpha,
                        betas=w.betas, tol=w.tol, max_iter_d=w.max_iter, seed=w.seed)
-    fb.fsda_solve(pp, device=dev)          # warm (graph build for this context)
+    # warm: graph build for this context, and two result sets in the pinned
+    # host cache (a caller holding the previous report while the next solve
+    # runs keeps two alive)
+    for _ in range(2):
+        rep = fb.fsda_solve(pp, device=dev)
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):

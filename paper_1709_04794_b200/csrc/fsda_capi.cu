@@ -12,6 +12,8 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <array>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -41,6 +43,20 @@ int fail(int code, const char* fmt, ...) {
   g_last_error = buf;
   return code;
 }
+
+// FSDA_B200_TRACE=1 prints host-visible phase times of the upload / solve
+// calls to stderr (the e2e breakdown; tools/time_e2e.py).
+struct Trace {
+  bool on = std::getenv("FSDA_B200_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[fsda trace] %-24s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 struct CudaError {
   cudaError_t err;
@@ -80,6 +96,28 @@ struct DevBuf {
   }
 };
 
+// Page-locked host staging for the upload plans (async H2D; reused across
+// uploads, which synchronise before returning).
+struct PinnedBuf {
+  void* ptr = nullptr;
+  size_t cap = 0;  // bytes
+  void* ensure(size_t bytes) {
+    if (bytes <= cap && ptr) return ptr;
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    cap = 0;
+    const size_t alloc = std::max<size_t>(bytes + bytes / 4, 4096);
+    CK(cudaHostAlloc(&ptr, alloc, cudaHostAllocDefault));
+    cap = alloc;
+    return ptr;
+  }
+  void release() {
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+};
+
 inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
 inline long long n_leaves(long long n) { return cdiv(n, LEAF); }
 constexpr long long MAX_REDUCE = 65536LL * LEAF;  // two-level R256 limit
@@ -96,10 +134,11 @@ struct HostPlan {
   DevBuf<int> h0, hn, hs, ht;
   DevBuf<unsigned> hc;
   DevBuf<double> part;
+  PinnedBuf stage;
   SegPlan pl{};
   void release() {
     tasks.release(); h0.release(); hn.release(); hs.release(); ht.release(); hc.release();
-    part.release();
+    part.release(); stage.release();
   }
 };
 
@@ -128,6 +167,7 @@ struct fsda_ctx {
   DevBuf<int> xh_col, xh_bptr;
   DevBuf<int4> xh_tasks;
   DevBuf<long long> xh_boff, xh_bwarp, xh_poff;
+  PinnedBuf xh_stage;
   DevBuf<double> xh_part;
   XtDense xh{};
   int xt_blocks = 0;
@@ -775,62 +815,120 @@ int read_results(fsda_ctx* c, int ns, const SolveOut& o, int64_t* launches) {
 // Build a segmented-sum plan from host segment offsets (S+1 entries) over the
 // device index stream `ind`.  Classes: W = 1 << k for segments with n <= 8W,
 // heavy tasks of <= 4 leaves for n > 256.
+inline int seg_class(long long n) {
+  int k = 0;
+  while (8LL * (1 << k) < n) ++k;
+  return k;
+}
+
+// Two passes over the host offsets (count, then fill a pinned staging buffer),
+// each split into chunks of segments run by OpenMP threads (the chunk prefix
+// sums keep the plan identical to a sequential build), and asynchronous copies
+// on `stream`; the caller synchronises before the plan is used or the staging
+// buffer is reused.
 template <typename OffT>
-void build_seg_plan(HostPlan& hp, const OffT* offs, long long S, const int* ind,
-                    std::vector<int>* dense_out = nullptr, long long dense_min = 0) {
-  std::vector<int4> cls[6], heavy;
-  std::vector<int> h0, hn, hs, ht;
-  int leaves = 0;
-  for (long long sgi = 0; sgi < S; ++sgi) {
-    const int lo = (int)offs[sgi], n = (int)(offs[sgi + 1] - offs[sgi]);
-    if (n <= LEAF) {
-      int k = 0;
-      while (8 * (1 << k) < n) ++k;
-      cls[k].push_back(make_int4((int)sgi, lo, n, -1));
-    } else if (dense_out && n >= dense_min) {
-      dense_out->push_back((int)sgi);
-    } else {
-      const int h = (int)h0.size();
-      const int nseg = (int)cdiv(n, LEAF);
-      const int ntask = (int)cdiv(n, 4 * LEAF);
-      h0.push_back(leaves);
-      hn.push_back(nseg);
-      hs.push_back(lo);
-      ht.push_back(ntask);
-      leaves += nseg;
-      for (int j = 0; j < ntask; ++j)
-        heavy.push_back(make_int4((int)sgi, lo + j * 4 * LEAF, std::min(4 * LEAF, n - j * 4 * LEAF), h));
+void build_seg_plan(HostPlan& hp, cudaStream_t stream, const OffT* offs, long long S,
+                    const int* ind, std::vector<int>* dense_out = nullptr,
+                    long long dense_min = 0) {
+  struct Count {
+    long long cls[6] = {0, 0, 0, 0, 0, 0};
+    long long heavy = 0, htask = 0, leaves = 0;
+    std::vector<int> dense;
+  };
+  const int nch = (int)std::max<long long>(1, std::min<long long>(64, S / 8192));
+  std::vector<Count> cc(nch);
+#pragma omp parallel for schedule(static)
+  for (int ch = 0; ch < nch; ++ch) {
+    Count& q = cc[ch];
+    for (long long sgi = S * ch / nch; sgi < S * (ch + 1) / nch; ++sgi) {
+      const long long n = (long long)(offs[sgi + 1] - offs[sgi]);
+      if (n <= LEAF) {
+        ++q.cls[seg_class(n)];
+      } else if (dense_out && n >= dense_min) {
+        q.dense.push_back((int)sgi);
+      } else {
+        ++q.heavy;
+        q.htask += cdiv(n, 4 * LEAF);
+        q.leaves += cdiv(n, LEAF);
+      }
     }
+  }
+  long long cnt[6] = {0, 0, 0, 0, 0, 0}, n_heavy = 0, n_htask = 0, leaves = 0;
+  for (const Count& q : cc) {
+    for (int k = 0; k < 6; ++k) cnt[k] += q.cls[k];
+    n_heavy += q.heavy;
+    n_htask += q.htask;
+    leaves += q.leaves;
+    if (dense_out) dense_out->insert(dense_out->end(), q.dense.begin(), q.dense.end());
   }
   SegPlan& pl = hp.pl;
   memset(&pl, 0, sizeof(pl));
-  std::vector<int4> tasks;
-  long long wb = 0;
+  long long wb = 0, t = 0;
   for (int k = 0; k < 6; ++k) {
-    pl.cls_off[k] = (long long)tasks.size();
-    tasks.insert(tasks.end(), cls[k].begin(), cls[k].end());
+    pl.cls_off[k] = t;
+    t += cnt[k];
     pl.warp_base[k] = wb;
-    wb += cdiv((long long)cls[k].size(), 32 >> k);
+    wb += cdiv(cnt[k], 32 >> k);
   }
-  pl.cls_off[6] = (long long)tasks.size();
+  pl.cls_off[6] = t;
   pl.warp_base[6] = wb;
-  tasks.insert(tasks.end(), heavy.begin(), heavy.end());
-  wb += (long long)heavy.size();
+  wb += n_htask;
   pl.warp_base[7] = wb;
   pl.warp_base[8] = wb;
-  hp.tasks.ensure(tasks.size());
-  if (!tasks.empty())
-    CK(cudaMemcpy(hp.tasks.ptr, tasks.data(), sizeof(int4) * tasks.size(), cudaMemcpyHostToDevice));
-  auto up = [&](DevBuf<int>& dst, const std::vector<int>& v) {
-    dst.ensure(v.size());
-    if (!v.empty()) CK(cudaMemcpy(dst.ptr, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice));
-  };
-  up(hp.h0, h0);
-  up(hp.hn, hn);
-  up(hp.hs, hs);
-  up(hp.ht, ht);
-  hp.hc.ensure(hn.size());
-  CK(cudaMemset(hp.hc.ptr, 0, sizeof(unsigned) * std::max<size_t>(hn.size(), 1)));
+  const long long n_tasks = t + n_htask;
+  char* st = (char*)hp.stage.ensure(sizeof(int4) * n_tasks + 4 * sizeof(int) * n_heavy + 16);
+  int4* tasks = (int4*)st;
+  int* h0 = (int*)(tasks + n_tasks);
+  int* hn = h0 + n_heavy;
+  int* hs = hn + n_heavy;
+  int* ht = hs + n_heavy;
+  // per-chunk start positions: class tasks, heavy tasks, heavy ids, leaves
+  std::vector<std::array<long long, 9>> start(nch);
+  {
+    std::array<long long, 9> run{};
+    for (int k = 0; k < 6; ++k) run[k] = pl.cls_off[k];
+    run[6] = pl.cls_off[6];
+    for (int ch = 0; ch < nch; ++ch) {
+      start[ch] = run;
+      for (int k = 0; k < 6; ++k) run[k] += cc[ch].cls[k];
+      run[6] += cc[ch].htask;
+      run[7] += cc[ch].heavy;
+      run[8] += cc[ch].leaves;
+    }
+  }
+#pragma omp parallel for schedule(static)
+  for (int ch = 0; ch < nch; ++ch) {
+    std::array<long long, 9> pos = start[ch];
+    for (long long sgi = S * ch / nch; sgi < S * (ch + 1) / nch; ++sgi) {
+      const int lo = (int)offs[sgi], n = (int)(offs[sgi + 1] - offs[sgi]);
+      if (n <= LEAF) {
+        tasks[pos[seg_class(n)]++] = make_int4((int)sgi, lo, n, -1);
+      } else if (dense_out && n >= dense_min) {
+        continue;
+      } else {
+        const int nseg = (int)cdiv(n, LEAF), ntask = (int)cdiv(n, 4 * LEAF);
+        const long long h = pos[7]++;
+        h0[h] = (int)pos[8];
+        hn[h] = nseg;
+        hs[h] = lo;
+        ht[h] = ntask;
+        for (int j = 0; j < ntask; ++j)
+          tasks[pos[6]++] = make_int4((int)sgi, lo + j * 4 * LEAF, std::min(4 * LEAF, n - j * 4 * LEAF), (int)h);
+        pos[8] += nseg;
+      }
+    }
+  }
+  hp.tasks.ensure(n_tasks);
+  if (n_tasks) CK(cudaMemcpyAsync(hp.tasks.ptr, tasks, sizeof(int4) * n_tasks, cudaMemcpyHostToDevice, stream));
+  DevBuf<int>* dsts[4] = {&hp.h0, &hp.hn, &hp.hs, &hp.ht};
+  int* srcs[4] = {h0, hn, hs, ht};
+  for (int k = 0; k < 4; ++k) {
+    dsts[k]->ensure(n_heavy);
+    if (n_heavy)
+      CK(cudaMemcpyAsync(dsts[k]->ptr, srcs[k], sizeof(int) * n_heavy, cudaMemcpyHostToDevice, stream));
+  }
+  hp.hc.ensure(n_heavy);
+  CK(cudaMemsetAsync(hp.hc.ptr, 0, sizeof(unsigned) * std::max<long long>(n_heavy, 1), stream));
   hp.part.ensure(leaves);
   pl.ind = ind;
   pl.tasks = hp.tasks.ptr;
@@ -852,6 +950,7 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   const int nb = (int)std::max<long long>(1, cdiv(c->n, rb));
   c->xh_col.ensure(nh);
   c->xh_bptr.ensure(nh * (nb + 1));
+  Trace tr;
   std::vector<int> bptr;
   if (nh) {
     CK(cudaMemcpy(c->xh_col.ptr, dense.data(), sizeof(int) * nh, cudaMemcpyHostToDevice));
@@ -863,53 +962,85 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
                        c->stream));
     CK(cudaStreamSynchronize(c->stream));
   }
-  // leaf-sum slots: column h owns max(1, ceil(n_hb / 256)) slots per block b
-  std::vector<long long> poff((size_t)nh + 1, 0);
+  tr.mark("  blocked: bptr");
+  // pass 1 (parallel over columns): leaf-sum slots — column h owns
+  // max(1, ceil(n_hb / 256)) slots per block b — and each (h, b)'s first slot
+  std::vector<long long> poff0((size_t)nh + 1, 0);
+  std::vector<int> slot0((size_t)nh * nb);
+#pragma omp parallel for schedule(static)
   for (long long h = 0; h < nh; ++h) {
     long long m = 0;
-    for (int b = 0; b < nb; ++b) m += std::max<long long>(1, cdiv(bptr[h * (nb + 1) + b + 1] - bptr[h * (nb + 1) + b], LEAF));
-    poff[h + 1] = poff[h] + m;
-  }
-  // poff[nh] <= nnz / XT_DENSE_PER_BLOCK + nnz / LEAF < 2^31: int slots suffice
-  std::vector<long long> pos(poff.begin(), poff.end() - 1);
-  std::vector<int4> tasks;
-  std::vector<long long> boff((size_t)(nb + 1) * 7, 0), bwarp((size_t)nb * 7, 0);
-  std::vector<int4> cls[6];
-  for (int b = 0; b < nb; ++b) {
-    for (auto& v : cls) v.clear();
-    for (long long h = 0; h < nh; ++h) {
-      const int lo = bptr[h * (nb + 1) + b], n = bptr[h * (nb + 1) + b + 1] - lo;
-      if (n == 0) { ++pos[h]; continue; }  // slot stays 0.0 (see below)
-      for (int c0 = 0; c0 < n; c0 += LEAF) {
-        const int len = std::min(LEAF, n - c0);
-        int k = 0;
-        while (8 * (1 << k) < len) ++k;
-        cls[k].push_back(make_int4((int)pos[h]++, lo + c0, len, 0));
-      }
+    const int* bp = bptr.data() + h * (nb + 1);
+    for (int b = 0; b < nb; ++b) {
+      slot0[(size_t)h * nb + b] = (int)m;
+      m += std::max<long long>(1, cdiv(bp[b + 1] - bp[b], LEAF));
     }
+    poff0[h + 1] = m;
+  }
+  for (long long h = 0; h < nh; ++h) poff0[h + 1] += poff0[h];
+  // poff[nh] <= nnz / XT_DENSE_PER_BLOCK + nnz / LEAF < 2^31: int slots suffice
+  // pass 2 (parallel over blocks): task counts per (block, class)
+  std::vector<long long> cnt((size_t)nb * 6, 0);
+#pragma omp parallel for schedule(static)
+  for (int b = 0; b < nb; ++b)
+    for (long long h = 0; h < nh; ++h) {
+      const long long n = bptr[h * (nb + 1) + b + 1] - bptr[h * (nb + 1) + b];
+      for (long long c0 = 0; c0 < n; c0 += LEAF) ++cnt[(size_t)b * 6 + seg_class(std::min<long long>(LEAF, n - c0))];
+    }
+  long long n_tasks = 0;
+  for (long long v : cnt) n_tasks += v;
+  const size_t n_boff = (size_t)(nb + 1) * 7, n_bwarp = (size_t)nb * 7, n_poff = (size_t)nh + 1;
+  char* st = (char*)c->xh_stage.ensure(sizeof(int4) * n_tasks +
+                                       sizeof(long long) * (n_boff + n_bwarp + n_poff));
+  int4* tasks = (int4*)st;
+  long long* boff = (long long*)(tasks + n_tasks);
+  long long* bwarp = boff + n_boff;
+  long long* poff = bwarp + n_bwarp;
+  std::copy(poff0.begin(), poff0.end(), poff);
+  std::vector<long long> pos((size_t)nb * 6);
+  long long t = 0;
+  for (int b = 0; b < nb; ++b) {
     long long wb = 0;
     for (int k = 0; k < 6; ++k) {
-      boff[(size_t)b * 7 + k] = (long long)tasks.size();
+      boff[(size_t)b * 7 + k] = t;
       bwarp[(size_t)b * 7 + k] = wb;
-      tasks.insert(tasks.end(), cls[k].begin(), cls[k].end());
-      wb += cdiv((long long)cls[k].size(), 32 >> k);
+      pos[(size_t)b * 6 + k] = t;
+      t += cnt[(size_t)b * 6 + k];
+      wb += cdiv(cnt[(size_t)b * 6 + k], 32 >> k);
     }
     bwarp[(size_t)b * 7 + 6] = wb;
-    boff[(size_t)b * 7 + 6] = (long long)tasks.size();
+    boff[(size_t)b * 7 + 6] = t;
   }
-  for (int k = 0; k < 7; ++k) boff[(size_t)nb * 7 + k] = (long long)tasks.size();
-  c->xh_tasks.ensure(tasks.size());
-  c->xh_boff.ensure(boff.size());
-  c->xh_bwarp.ensure(bwarp.size());
-  c->xh_poff.ensure(poff.size());
+  for (int k = 0; k < 7; ++k) boff[(size_t)nb * 7 + k] = t;
+  // pass 3 (parallel over blocks): tasks by block, class, column (an empty
+  // block's slot stays 0.0, see below)
+#pragma omp parallel for schedule(static)
+  for (int b = 0; b < nb; ++b) {
+    long long* pb = pos.data() + (size_t)b * 6;
+    for (long long h = 0; h < nh; ++h) {
+      const int lo = bptr[h * (nb + 1) + b], n = bptr[h * (nb + 1) + b + 1] - lo;
+      long long slot = poff[h] + slot0[(size_t)h * nb + b];
+      for (int c0 = 0; c0 < n; c0 += LEAF) {
+        const int len = std::min(LEAF, n - c0);
+        tasks[pb[seg_class(len)]++] = make_int4((int)slot++, lo + c0, len, 0);
+      }
+    }
+  }
+  tr.mark("  blocked: host passes");
+  c->xh_tasks.ensure(n_tasks);
+  c->xh_boff.ensure(n_boff);
+  c->xh_bwarp.ensure(n_bwarp);
+  c->xh_poff.ensure(n_poff);
   c->xh_part.ensure(std::max<long long>(1, poff[nh]));
-  if (!tasks.empty())
-    CK(cudaMemcpy(c->xh_tasks.ptr, tasks.data(), sizeof(int4) * tasks.size(), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(c->xh_boff.ptr, boff.data(), sizeof(long long) * boff.size(), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(c->xh_bwarp.ptr, bwarp.data(), sizeof(long long) * bwarp.size(), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(c->xh_poff.ptr, poff.data(), sizeof(long long) * poff.size(), cudaMemcpyHostToDevice));
+  if (n_tasks)
+    CK(cudaMemcpyAsync(c->xh_tasks.ptr, tasks, sizeof(int4) * n_tasks, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->xh_boff.ptr, boff, sizeof(long long) * n_boff, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->xh_bwarp.ptr, bwarp, sizeof(long long) * n_bwarp, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->xh_poff.ptr, poff, sizeof(long long) * n_poff, cudaMemcpyHostToDevice, c->stream));
   // empty blocks never get a task: their slots must read 0.0
-  if (poff[nh]) CK(cudaMemset(c->xh_part.ptr, 0, sizeof(double) * poff[nh]));
+  if (poff[nh]) CK(cudaMemsetAsync(c->xh_part.ptr, 0, sizeof(double) * poff[nh], c->stream));
+  CK(cudaStreamSynchronize(c->stream));  // the staging buffer is reused by the next upload
+  tr.mark("  blocked: h2d");
   if (c->xt_blocks == 0) {
     int per_sm = 0;
     CK(cudaFuncSetAttribute(k_xt_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -948,18 +1079,19 @@ int check_err_flag(fsda_ctx* c, const char* what) {
 }
 
 // Upload an int64 index array and narrow it to int32 on the device.
-void upload_narrow(fsda_ctx* c, const int64_t* host, long long n, long long limit, DevBuf<int>& out) {
+// int64 host indices -> int32 device indices (range-checked into c->err).
+// Asynchronous: tmp must stay allocated until the stream has passed it.
+void upload_narrow_async(fsda_ctx* c, const int64_t* host, long long n, long long limit,
+                         DevBuf<int>& out, long long* tmp) {
   out.ensure(n + 8);  // tail padding: the row kernels stage indices with 16-byte loads
   CK(cudaMemsetAsync(out.ptr + n, 0, 8 * sizeof(int), c->stream));
   if (n == 0) return;
-  c->scratch_i64.ensure(n);
-  long long* tmp = c->scratch_i64.ptr;
   CK(cudaMemcpyAsync(tmp, host, sizeof(long long) * n, cudaMemcpyHostToDevice, c->stream));
   int g = (int)std::min<long long>(cdiv(n, 256), (long long)c->num_sms * 32);
   k_narrow_idx<<<g, 256, 0, c->stream>>>(tmp, out.ptr, n, limit, c->err.ptr);
   CKL();
-  CK(cudaStreamSynchronize(c->stream));
 }
+
 
 #define API_BEGIN(ctx)                                   \
   if (!(ctx)) return fail(FSDA_EINVAL, "null context"); \
@@ -1044,6 +1176,8 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     c->xh_boff.release();
     c->xh_bwarp.release();
     c->xh_part.release();
+    c->xh_poff.release();
+    c->xh_stage.release();
     c->plan_xr.release();
     c->plan_lr.release();
     c->plan_xc.release();
@@ -1101,10 +1235,18 @@ int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* ro
   c->n = n_rows;
   c->d = n_cols;
   c->nnz = nnz;
-  upload_narrow(c, row_offsets, n_rows + 1, nnz, c->x_rowptr);
-  upload_narrow(c, col_indices, nnz, n_cols - 1, c->x_cols);
+  Trace tr;
+  // H2D + narrowing run on the stream while the host builds the row plan
+  // (it needs only the host offsets).
+  c->scratch_i64.ensure(std::max<long long>(n_rows + 1 + nnz, 1));
+  upload_narrow_async(c, row_offsets, n_rows + 1, nnz, c->x_rowptr, c->scratch_i64.ptr);
+  upload_narrow_async(c, col_indices, nnz, n_cols - 1, c->x_cols, c->scratch_i64.ptr + n_rows + 1);
+  build_seg_plan(c->plan_xr, c->stream, row_offsets, n_rows, c->x_cols.ptr);
+  tr.mark("x: row plan (host)");
+  CK(cudaStreamSynchronize(c->stream));
   int rc = check_err_flag(c, "X");
   if (rc) return rc;
+  tr.mark("x: h2d + narrow");
   // row ids + in-row order validation
   DevBuf<int>& row_of = c->scratch_row_of;
   row_of.ensure(nnz);
@@ -1116,6 +1258,7 @@ int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* ro
   CK(cudaStreamSynchronize(c->stream));
   rc = check_err_flag(c, "X");
   if (rc) return rc;
+  tr.mark("x: row ids");
   // CSC by a stable radix sort of (column, row) pairs: rows stay ascending.
   c->csc_rows.ensure(nnz);
   c->csc_colptr.ensure(n_cols + 1);
@@ -1137,16 +1280,19 @@ int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* ro
                                                                           c->csc_colptr.ptr, (int)n_cols);
   CKL();
   CK(cudaStreamSynchronize(c->stream));
-  build_seg_plan(c->plan_xr, row_offsets, n_rows, c->x_cols.ptr);
+  tr.mark("x: csc sort");
   {
     std::vector<int> colptr(n_cols + 1);
     CK(cudaMemcpy(colptr.data(), c->csc_colptr.ptr, sizeof(int) * (n_cols + 1), cudaMemcpyDeviceToHost));
+    tr.mark("x: colptr d2h");
     std::vector<int> dense;
     const long long dpb = XT_DENSE_PER_BLOCK;
     const long long dense_min =
         std::max<long long>(LEAF + 1, dpb * std::max<long long>(1, cdiv(n_rows, xt_rb())));
-    build_seg_plan(c->plan_xc, colptr.data(), n_cols, c->csc_rows.ptr, &dense, dense_min);
+    build_seg_plan(c->plan_xc, c->stream, colptr.data(), n_cols, c->csc_rows.ptr, &dense, dense_min);
+    tr.mark("x: column plan");
     build_dense_plan(c, dense);
+    tr.mark("x: blocked plan");
   }
 
   c->has_x = true;
@@ -1171,10 +1317,12 @@ static int upload_laplacian_rows(fsda_ctx* c, int64_t n, int64_t n_global, int64
   c->l_nnz = nnz;
   c->row_base = row_base;
   c->n_global = n_global;
-  upload_narrow(c, row_offsets, n + 1, nnz, c->l_rowptr);
-  upload_narrow(c, col_indices, nnz, n_global - 1, c->l_cols);
-  int rc = check_err_flag(c, "laplacian");
-  if (rc) return rc;
+  Trace tr;
+  // H2D, narrowing and the diagonal split run on the stream while the host
+  // builds the row plan.
+  c->scratch_i64.ensure(std::max<long long>(n + 1 + nnz, 1));
+  upload_narrow_async(c, row_offsets, n + 1, nnz, c->l_rowptr, c->scratch_i64.ptr);
+  upload_narrow_async(c, col_indices, nnz, n_global - 1, c->l_cols, c->scratch_i64.ptr + n + 1);
   c->l_diag.ensure(n);
   if (n > 0) {
     c->scratch_f64.ensure(std::max<long long>(nnz, 1));
@@ -1185,11 +1333,13 @@ static int upload_laplacian_rows(fsda_ctx* c, int64_t n, int64_t n_global, int64
                                                                c->l_diag.ptr, (int)n, c->err.ptr,
                                                                (int)row_base);
     CKL();
-    CK(cudaStreamSynchronize(c->stream));
   }
-  rc = check_err_flag(c, "laplacian");
+  build_seg_plan(c->plan_lr, c->stream, row_offsets, n, c->l_cols.ptr);
+  tr.mark("L: row plan (host)");
+  CK(cudaStreamSynchronize(c->stream));
+  int rc = check_err_flag(c, "laplacian");
   if (rc) return rc;
-  build_seg_plan(c->plan_lr, row_offsets, n, c->l_cols.ptr);
+  tr.mark("L: h2d + split");
   c->has_l = true;
   return FSDA_OK;
 }
@@ -1362,10 +1512,17 @@ int fsda_solve(fsda_ctx* c, double alpha, const double* betas, int ns, double to
   if (!probe) return fail(FSDA_EINVAL, "probe is null");
   c->solve_kind = 0;
   c->solve_abs_tol = 0;
+  Trace tr;
   upload_solve_params(c, betas, ns, probe);
   launch_solve(c, alpha, ns, max_iter, tol, nullptr);
+  if (tr.on) {
+    CK(cudaStreamSynchronize(c->stream));
+    tr.mark("solve: device");
+  }
   SolveOut o{directions, scores, residuals, iterations, converged, n_applies, fail_iter};
-  return read_results(c, ns, o, nullptr);
+  rc = read_results(c, ns, o, nullptr);
+  tr.mark("solve: d2h results");
+  return rc;
   API_END
 }
 

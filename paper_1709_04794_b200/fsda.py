@@ -92,6 +92,20 @@ class SweepResult:
     launches: int = 0
 
 
+def _pinned_empty(shape) -> np.ndarray:
+    """A float64 host array in page-locked memory, from torch's caching host
+    allocator, so the result copies (directions, scores) run at link speed
+    instead of through a pageable bounce buffer.  It is an ordinary ndarray
+    to the caller and is recycled when the caller drops it.  Plain numpy
+    memory when torch is absent (this changes where results land, not how
+    they are computed)."""
+    try:
+        import torch
+    except ImportError:  # pragma: no cover - torch ships with this image
+        return np.empty(shape)
+    return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+
+
 class Device:
     """One fsda context (device buffers, stream, cached solve graph)."""
 
@@ -210,8 +224,8 @@ class Device:
         probe = _f64(probe)
         if probe.shape != (self.d,):
             raise ValueError("probe must have one entry per feature")
-        dirs = np.empty((ns, self.d))
-        sc = np.empty((ns, self.n)) if scores else None
+        dirs = _pinned_empty((ns, self.d))
+        sc = _pinned_empty((ns, self.n)) if scores else None
         res = np.empty(ns)
         its = np.empty(ns, dtype=np.int64)
         conv = np.empty(ns, dtype=np.uint8)
@@ -236,8 +250,8 @@ class Device:
 
     def fetch(self, *, directions=True, scores=True) -> SweepResult:
         ns = self._res_ns
-        dirs = np.empty((ns, self.d)) if directions else None
-        sc = np.empty((ns, self.n)) if scores else None
+        dirs = _pinned_empty((ns, self.d)) if directions else None
+        sc = _pinned_empty((ns, self.n)) if scores else None
         res = np.empty(ns)
         its = np.empty(ns, dtype=np.int64)
         conv = np.empty(ns, dtype=np.uint8)

@@ -407,22 +407,76 @@ __device__ __forceinline__ void dense_slice_task(const XtDense& dn, const double
   if (tk.x >= 0 && t == 0) dn.part[tk.x] = r;
 }
 
+// z row block -> shared memory by one TMA bulk copy (cp.async.bulk, completion
+// on an mbarrier), so staging costs one instruction and no registers.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.b32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
+// Thread 0 copies src[0, n) to zs (16-byte-aligned src: the bulk part by TMA,
+// an odd last element by a plain load); every thread waits for the bytes.
+// The caller's __syncthreads() before the call retires the previous block's
+// reads; the one after it publishes the odd element.
+__device__ __forceinline__ void stage_block(double* zs, const double* __restrict__ src, int n,
+                                            unsigned long long* bar, unsigned phase) {
+  if (threadIdx.x == 0) {
+    const unsigned bytes = (unsigned)(8 * n) & ~15u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+    if (bytes)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(zs)),
+          "l"(src), "r"(bytes), "r"(smem_u32(bar))
+          : "memory");
+    if (n & 1) zs[n - 1] = __ldg(src + n - 1);
+  }
+  mbar_wait(bar, phase);
+}
+
 __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan pl, XtDense dn, SegArgs a,
                                                     const CgScalars* sc, int guarded, int n_rows,
                                                     unsigned long long* ticket) {
   if (guarded && loop_idle(sc)) return;  // uniform across the grid
-  extern __shared__ double zs[];  // dn.rb doubles
+  extern __shared__ __align__(16) double zs[];  // dn.rb doubles
+  __shared__ unsigned long long zs_bar;
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   // ---- phase 1a: (row block, split) units with their dense-column slices
   if (dn.n_dense > 0) {
+    const bool tma = (reinterpret_cast<size_t>(a.src) & 15) == 0;
+    if (threadIdx.x == 0) mbar_init(&zs_bar);
+    unsigned phase = 0;
     const long long units = (long long)dn.nb * dn.splits;
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
       const int b = (int)(u / dn.splits), sp = (int)(u - (long long)b * dn.splits);
       const int r0 = b * dn.rb;
       const int nr = min(dn.rb, n_rows - r0);
       __syncthreads();
-      for (int k = threadIdx.x; k < nr; k += blockDim.x) zs[k] = __ldg(a.src + r0 + k);
+      if (tma) {
+        stage_block(zs, a.src + r0, nr, &zs_bar, phase);
+        phase ^= 1u;
+      } else {
+        for (int k = threadIdx.x; k < nr; k += blockDim.x) zs[k] = __ldg(a.src + r0 + k);
+      }
       __syncthreads();
       const long long* wb = dn.bwarp + (long long)b * 7;
       const long long c0 = wb[6] * sp / dn.splits, c1 = wb[6] * (sp + 1) / dn.splits;

@@ -1060,6 +1060,7 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   xh.n_dense = nh;
   xh.nb = nb;
   xh.rb = rb;
+  xh.ticket_chunk = XT_TICKET_CHUNK;
   xh.splits = (int)std::max<long long>(1, c->xt_blocks / nb);
   if (!c->xt_ticket.ptr) {
     c->xt_ticket.ensure(1);

@@ -352,6 +352,9 @@ constexpr int XT_DENSE_PER_BLOCK = 8;   // blocked: n > 256 and n >= XT_DENSE_PE
 // cfg2 / cfg3 over one 32-warp CTA)
 constexpr int XT_THREADS = 768;
 constexpr int XT_CTAS_PER_SM = 2;
+// phase-1b tasks claimed per ticket draw (halves the single-address atomics;
+// measured 1.02x at cfg2 / cfg3 over 1, and 4 is worse at cfg2)
+constexpr int XT_TICKET_CHUNK = 2;
 
 struct XtDense {
   const int* rows;        // CSC row indices
@@ -364,6 +367,7 @@ struct XtDense {
   long long n_dense;
   int nb;
   int rb;                 // rows per block (XT_RB)
+  int ticket_chunk;       // tasks claimed per ticket draw
   int splits;             // CTAs sharing one row block's slices
 };
 
@@ -498,11 +502,14 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
   // from a grid-wide ticket so CTAs that staged a dense block catch up.
   const long long total = pl.warp_base[8];
   const long long nheavy = pl.warp_base[7] - pl.warp_base[6];
+  const int chunk = dn.ticket_chunk;
   for (;;) {
-    long long nxt = 0;
-    if (lane == 0) nxt = (long long)atomicAdd(ticket, 1ULL);
-    nxt = __shfl_sync(FULL, nxt, 0);
-    if (nxt >= total) break;
+    long long base = 0;
+    if (lane == 0) base = (long long)atomicAdd(ticket, (unsigned long long)chunk);
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= total) break;
+    const long long lim = min(base + chunk, total);
+    for (long long nxt = base; nxt < lim; ++nxt) {
     // largest tasks first: tickets [0, nheavy) are the heavy tasks, then the
     // class tasks, then the sum(z) leaves
     const long long tw = nxt < nheavy ? pl.warp_base[6] + nxt
@@ -530,6 +537,7 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
       }
       v = butterfly(v);
       if (lane == 0) a.sum_part[g] = v;
+    }
     }
   }
   grid.sync();

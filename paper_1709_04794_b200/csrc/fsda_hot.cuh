@@ -289,9 +289,19 @@ __device__ __forceinline__ void seg_heavy_task(const SegPlan& pl, const SegArgs&
   }
 }
 
+// Programmatic dependent launch: a kernel lets its successor's CTAs launch
+// once all of its own CTAs are running (they fill the SMs its last wave
+// leaves idle), and waits for its predecessor's completion and memory before
+// touching the predecessor's output.  Both are no-ops without the launch
+// attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <int KIND>
 __global__ void __launch_bounds__(256, 6) k_segsum(SegPlan pl, SegArgs a, const CgScalars* sc,
                                                 int guarded) {
+  pdl_trigger();
+  pdl_wait();
   if (guarded && loop_idle(sc)) return;
   const int lane = threadIdx.x & 31;
   const long long total = pl.warp_base[8];
@@ -459,6 +469,8 @@ __device__ __forceinline__ void stage_block(double* zs, const double* __restrict
 __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan pl, XtDense dn, SegArgs a,
                                                     const CgScalars* sc, int guarded, int n_rows,
                                                     unsigned long long* ticket) {
+  pdl_trigger();
+  pdl_wait();
   if (guarded && loop_idle(sc)) return;  // uniform across the grid
   extern __shared__ __align__(16) double zs[];  // dn.rb doubles
   __shared__ unsigned long long zs_bar;
@@ -653,9 +665,16 @@ __global__ void __launch_bounds__(STEP_THREADS) k_cg_step(
     const long long i = gw * LEAF + k * 32 + lane;
     const bool in = own && i < d;
     pr[k] = in ? p[i] : 0.0;
-    qr[k] = in ? q[i] : 0.0;
     rv[k] = in ? r_cur[i] : 0.0;
     cr[k] = (in && center) ? (mu ? mu[i] : (labels[i] != 0 ? 1.0 : 0.0)) : 0.0;
+  }
+  // everything above is this step's own state; q and the sum(z) leaves come
+  // from the X^T kernel, which may still be finishing (programmatic launch)
+  pdl_wait();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const long long i = gw * LEAF + k * 32 + lane;
+    qr[k] = (own && i < d) ? q[i] : 0.0;
   }
   const int s0 = threadIdx.x;
   int act0 = 0;

@@ -749,7 +749,7 @@ bool build_solve_graph(fsda_ctx* c, double alpha, int ns, long long max_iter, do
   CK(cudaGraphInstantiate(&c->exec, out, 0));
   c->graph_key = key;
   *launches_fixed = c->graph_fixed = e.count;  // setup + tail
-  *launches_body = c->graph_body = eb.count;
+  *launches_body = c->graph_body = eb.count;  // per iteration
   (void)fixed;
   return true;
 }
@@ -843,8 +843,9 @@ int read_results(fsda_ctx* c, int ns, const SolveOut& o, int64_t* launches) {
     long long lc = c->last_launch_count;
     if (lc < 0) {
       long long enc = -lc, fixed = enc / 1000000LL, body = enc % 1000000LL;
-      long long runs = h.iter + ((h.status != ST_OK || h.b_norm == 0.0) ? 1 : 0);
-      lc = fixed + body * std::max<long long>(runs, 1);
+      // every captured iteration launches its kernels (guarded ones exit at
+      // once after the loop finished): body_runs counts the CG-step launches
+      lc = fixed + body * std::max<long long>(h.body_runs, 1);
     }
     *launches = lc;
   }

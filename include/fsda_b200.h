@@ -171,6 +171,23 @@ int fsda_sa_solve(fsda_ctx* ctx, double alpha, const double* betas, int n_shifts
                   int64_t max_iter, const double* probe, double* solutions, double* residuals,
                   int64_t* iterations, uint8_t* converged, int64_t* n_applies, int64_t* fail_iter);
 
+/* Multi-task batch: n_tasks FSDA sweeps on the
+ * uploaded X and L, task t with its own label mask labels[t * N .. t * N + N)
+ * (any row order, as fsda_set_label_mask) and probe probes[t * D ..].  One
+ * operator pass serves every task (task-minor vectors, coalesced row
+ * gathers); each task's results equal, bit for bit, fsda_set_label_mask +
+ * fsda_solve of that task.  Outputs: directions [T][n_shifts][D], scores
+ * [T][n_shifts][N] (may be NULL), residuals / iterations / converged
+ * [T][n_shifts], n_applies / fail_iter / status [T] (status: FSDA_OK,
+ * FSDA_EBREAKDOWN or FSDA_ENONFINITE per task; a failed task does not stop
+ * the others).  Replaces the per-fold fsda_solve calls of nested_cv
+ * (evaluation.py:110-123, 173-237). */
+int fsda_solve_batch(fsda_ctx* ctx, int n_tasks, const int8_t* labels, double alpha,
+                     const double* betas, int n_shifts, double tol, int64_t max_iter,
+                     const double* probes, double* directions, double* scores,
+                     double* residuals, int64_t* iterations, uint8_t* converged,
+                     int64_t* n_applies, int64_t* fail_iter, int* status);
+
 /* ---- row-sharded building blocks ---------------------------
  * One context per GPU holds a contiguous row block [row_base, row_base+N_g)
  * of X (uploaded with fsda_upload_x as an N_g x D matrix) and of L

@@ -54,6 +54,8 @@ SIGNATURES = {
     "fsda_regression_shifted_cg": [_P, _PD, _PD, C.c_int, _D, _I64, C.c_int, _PD, _PD, _PI64,
                                    _PU8, _PI64, _PI64],
     "fsda_sa_solve": [_P, _D, _PD, C.c_int, _D, _I64, _PD, _PD, _PD, _PI64, _PU8, _PI64, _PI64],
+    "fsda_solve_batch": [_P, C.c_int, _PI8, _D, _PD, C.c_int, _D, _I64, _PD, _PD, _PD, _PD, _PI64,
+                         _PU8, _PI64, _PI64, _PI],
     # row-sharded building blocks (device pointers passed as c_void_p)
     "fsda_upload_laplacian_rows": [_P, _I64, _I64, _I64, _PI64, _PI64, _PD],
     "fsda_dev_xrows": [_P, _P, _P],

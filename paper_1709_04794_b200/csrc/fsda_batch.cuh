@@ -1,0 +1,706 @@
+// fsda_batch.cuh — T FSDA sweeps on one X and one graph in a single pass per
+// operator product (cfg4: the per-fold solves of
+// evaluation.py:110-123 / nested_cv, which share X and L and differ only in
+// their label mask and probe).
+//
+// Layout: every per-task vector is stored task-minor, v[i * TP + t], with
+// TP = 32 * G (tasks padded to whole warps).  A warp owns 32 tasks — lane t
+// is task 32 g + t — so each gathered row of P, Y or Z is one coalesced
+// 256-byte load for 32 tasks instead of 32 separate 32-byte sectors.
+//
+// Arithmetic: each lane reproduces, for its own task, exactly the canonical
+// tree of the single-task kernels (fsda_device.cuh / fsda_hot.cuh): a leaf of
+// <= 256 values is accumulated in 32 registers A[l] = sum_k v[l + 32 k]
+// (from 0.0, in k order; fma for dot leaves) and folded by the xor-butterfly
+// order 16, 8, 4, 2, 1 (tree32).  Sums of more than 256 values are trees of
+// leaf sums, as in R256.  Every task's result is therefore bit-identical to
+// the single-task solve of the same label mask and probe (fsda_set_label_mask
+// + fsda_solve), which tests/test_gpu_batch.py checks.
+#pragma once
+
+namespace fsda {
+
+constexpr int BG = 32;  // tasks per group (one per lane)
+
+// Per-task scalars (index t) and per-(task, shift) state (index t * ns + s).
+struct BatchState {
+  // per task
+  double* rr;
+  double* gamma_prev;
+  double* alpha;
+  double* b_norm;
+  double* thresh;
+  double* gamma;
+  double* alpha_new;
+  double* mean1;
+  double* mean2;
+  double* ell;       // labeled count (double), n1, n2
+  double* n1;
+  double* n2;
+  double* sum_v;     // sum(w) at setup, sum(z) in the loop
+  double* pq;
+  double* rr_new;
+  long long* iter;
+  long long* fail_iter;
+  int* status;       // ST_*; ST_PAD for padding lanes
+  int* finished;
+  int* n_active;
+  // per (task, shift)
+  const double* beta;  // ns
+  double* zeta_prev;
+  double* zeta;
+  double* alpha_s;
+  double* resid;
+  double* s_zn;        // this iteration's zeta_next / gamma_s / good (phase B)
+  double* s_gs;
+  unsigned char* s_good;
+  double* upd_gs;      // shift-update snapshot (phase C)
+  double* upd_zn;
+  double* upd_as;
+  int* upd_mode;
+  long long* iters;
+  unsigned char* conv;
+  unsigned char* active;
+  unsigned char* flip;
+  int ns;
+  int tp;
+  long long max_iter;
+};
+
+constexpr int ST_PAD = 7;
+
+__device__ __forceinline__ bool b_live(const BatchState& B, int t) {
+  return B.status[t] == ST_OK && !B.finished[t];
+}
+
+__device__ __forceinline__ double tree32(double (&A)[32]) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+    for (int l = 0; l < off; ++l) A[l] = A[l] + A[l + off];
+  return A[0];
+}
+
+// Canonical leaf of n <= 256 values val(e), e = 0..n-1, for this lane's task.
+// val may use warp shuffles: control flow is uniform (n is warp-uniform).
+template <typename Val>
+__device__ __forceinline__ double emu_leaf(int n, Val val) {
+  double A[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) A[l] = 0.0;
+  for (int base = 0; base < n; base += 32) {
+#pragma unroll
+    for (int l = 0; l < 32; ++l)
+      if (base + l < n) A[l] = A[l] + val(base, l);
+  }
+  return tree32(A);
+}
+
+// Dot leaf: A[l] = fma(x, y, A[l]).
+template <typename XY>
+__device__ __forceinline__ double emu_dot_leaf(int n, XY xy) {
+  double A[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) A[l] = 0.0;
+  for (int base = 0; base < n; base += 32) {
+#pragma unroll
+    for (int l = 0; l < 32; ++l)
+      if (base + l < n) {
+        double x, y;
+        xy(base + l, x, y);
+        A[l] = fma(x, y, A[l]);
+      }
+  }
+  return tree32(A);
+}
+
+// Canonical sum of a gathered index segment: ind[start, start + n) selects
+// rows of src (task-minor); term(idx, v) maps the gathered value.  n <= 256:
+// one leaf; longer: R256 over its leaves (two levels, n <= 65536).
+template <typename Term>
+__device__ __forceinline__ double emu_segment(const int* __restrict__ ind, long long start, int n,
+                                              const double* __restrict__ src, int tp, int t,
+                                              int lane, Term term) {
+  auto leaf = [&](long long s0, int len) {
+    int my = 0;
+    return emu_leaf(len, [&](int base, int l) {
+      if (l == 0) {
+        my = (base + lane < len) ? __ldg(ind + s0 + base + lane) : 0;
+      }
+      const int idx = __shfl_sync(FULL, my, l);
+      return term(idx, __ldg(src + (long long)idx * tp + t));
+    });
+  };
+  if (n <= LEAF) return leaf(start, n);
+  const int m = (n + LEAF - 1) / LEAF;  // <= 256 (host-checked)
+  double P[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) P[l] = 0.0;
+  for (int gb = 0; gb < m; gb += 32) {
+    for (int l = 0; l < 32 && gb + l < m; ++l) {
+      const int g = gb + l;
+      const double v = leaf(start + (long long)g * LEAF, min(LEAF, n - g * LEAF));
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (q == l) P[q] = P[q] + v;
+    }
+  }
+  return tree32(P);
+}
+
+// ------------------------------------------------------------ layout moves
+
+// labels [T][N] -> lab [N][TP] (padding 0) and the labeled indicator.
+__global__ void kb_labels_in(const signed char* __restrict__ in, signed char* __restrict__ lab,
+                             double* __restrict__ ind, long long n, int T, int tp) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n * tp;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long i = k / tp;
+    const int t = (int)(k - i * tp);
+    const signed char l = t < T ? in[(long long)t * n + i] : 0;
+    lab[k] = l;
+    ind[k] = l != 0 ? 1.0 : 0.0;
+  }
+}
+
+// x [T][L] -> out [L][TP] (padding 0.0).
+__global__ void kb_task_minor(const double* __restrict__ in, double* __restrict__ out, long long len,
+                              int T, int tp) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < len * tp;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long i = k / tp;
+    const int t = (int)(k - i * tp);
+    out[k] = t < T ? in[(long long)t * len + i] : 0.0;
+  }
+}
+
+// sols [D][TP][ns] -> out [T][ns][D].
+__global__ void kb_directions_out(const double* __restrict__ sols, double* __restrict__ out,
+                                  long long d, int T, int tp, int ns) {
+  const long long total = (long long)T * ns * d;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long ts = k / d;
+    const long long c = k - ts * d;
+    const int t = (int)(ts / ns), s = (int)(ts - (long long)t * ns);
+    out[k] = sols[(c * tp + t) * ns + s];
+  }
+}
+
+// ------------------------------------------------------------- setup
+
+__global__ void kb_reset(BatchState B, int T, double tol) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B.tp) return;
+  B.rr[t] = 0.0; B.gamma_prev[t] = 1.0; B.alpha[t] = 0.0; B.b_norm[t] = 0.0; B.thresh[t] = 0.0;
+  B.gamma[t] = 0.0; B.alpha_new[t] = 0.0; B.sum_v[t] = 0.0;
+  B.iter[t] = 0; B.fail_iter[t] = -1; B.status[t] = t < T ? ST_OK : ST_PAD;
+  B.finished[t] = t < T ? 0 : 1;
+  B.n_active[t] = B.ns;
+  for (int s = 0; s < B.ns; ++s) {
+    const int k = t * B.ns + s;
+    B.zeta_prev[k] = 1.0; B.zeta[k] = 1.0; B.alpha_s[k] = 0.0; B.resid[k] = 0.0;
+    B.iters[k] = B.max_iter; B.conv[k] = 0; B.active[k] = 1; B.flip[k] = 0; B.upd_mode[k] = 0;
+  }
+  (void)tol;
+}
+
+// ------------------------------------------------------- operator products
+
+// Row sums over a CSR pattern for every task: K1 (y = X p) and K2 (z = M y).
+// One warp per (row, task group).
+template <int KIND>
+__global__ void __launch_bounds__(256) kb_rows(const int* __restrict__ rowptr,
+                                               const int* __restrict__ cols,
+                                               const double* __restrict__ src,
+                                               double* __restrict__ out, long long n_rows, int G,
+                                               int tp, const double* __restrict__ ldiag,
+                                               const signed char* __restrict__ lab, double alpha,
+                                               int alpha_mode) {
+  const int lane = threadIdx.x & 31;
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= n_rows * G) return;
+  const long long i = w / G;
+  const int g = (int)(w - i * G);
+  const int t = g * BG + lane;
+  const int lo = __ldg(rowptr + i), n = __ldg(rowptr + i + 1) - lo;
+  double s;
+  if (KIND == SEG_LROWS) {
+    const double dg = __ldg(ldiag + i);
+    s = emu_segment(cols, lo, n, src, tp, t, lane,
+                    [&](int idx, double v) { return idx == (int)i ? dg * v : -v; });
+    const double masked = lab[i * tp + t] != 0 ? src[i * tp + t] : 0.0;
+    const double smoothed = alpha * s;
+    s = (alpha_mode == 1) ? smoothed : (1.0 - alpha) * masked + smoothed;
+  } else {
+    s = emu_segment(cols, lo, n, src, tp, t, lane, [](int, double v) { return v; });
+  }
+  out[i * tp + t] = s;
+}
+
+// z = masked y (apply_smoother at alpha == 0).
+__global__ void kb_mask(const double* __restrict__ y, const signed char* __restrict__ lab,
+                        double* __restrict__ z, long long len) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < len;
+       k += (long long)gridDim.x * blockDim.x)
+    z[k] = lab[k] != 0 ? y[k] : 0.0;
+}
+
+// Column finish of X^T: mode 0 raw, 1 centred (s - mu * sum_v[t]), 2 / ell[t].
+__device__ __forceinline__ double b_col_finish(double s, int mode, long long c, int t, int tp,
+                                               const double* __restrict__ mu,
+                                               const BatchState& B) {
+  if (mode == 1) return s - mu[c * tp + t] * B.sum_v[t];
+  if (mode == 2) return s / B.ell[t];
+  return s;
+}
+
+// X^T columns with n <= 256: the class tasks of the single-task column plan
+// (any class: each entry is one column segment).  One warp per (entry, group).
+__global__ void __launch_bounds__(256) kb_cols_light(SegPlan pl, const double* __restrict__ src,
+                                                     double* __restrict__ out, int G, int tp,
+                                                     int mode, const double* __restrict__ mu,
+                                                     BatchState B) {
+  const int lane = threadIdx.x & 31;
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long n_entries = pl.cls_off[6];
+  if (w >= n_entries * G) return;
+  const long long e = w / G;
+  const int g = (int)(w - e * G);
+  const int t = g * BG + lane;
+  const int4 tk = __ldg(pl.tasks + e);
+  const double s = emu_segment(pl.ind, tk.y, tk.z, src, tp, t, lane, [](int, double v) { return v; });
+  out[(long long)tk.x * tp + t] = b_col_finish(s, mode, tk.x, t, tp, mu, B);
+}
+
+// Leaf sums of the long columns: the heavy leaves (plan_xc heavy tasks, up to
+// 4 leaves each) into hpart[slot][TP], and the blocked slices (XtDense tasks,
+// one <= 256-entry leaf each) into xpart[slot][TP].
+__global__ void __launch_bounds__(256) kb_cols_leaves(SegPlan pl, XtDense dn,
+                                                      const double* __restrict__ src,
+                                                      double* __restrict__ hpart,
+                                                      double* __restrict__ xpart, long long n_hleaf,
+                                                      long long n_xtask, int G, int tp) {
+  const int lane = threadIdx.x & 31;
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= (n_hleaf + n_xtask) * G) return;
+  const long long u = w / G;
+  const int g = (int)(w - u * G);
+  const int t = g * BG + lane;
+  if (u < n_hleaf) {
+    // u indexes heavy leaves in task order: task j covers leaves [4j, 4j + 4)
+    const long long j = u >> 2;
+    const int lf = (int)(u & 3);
+    const int4 tk = __ldg(pl.tasks + pl.cls_off[6] + j);
+    if (lf * LEAF >= tk.z) return;
+    const int h = tk.w;
+    const int slot = __ldg(pl.heavy_seg0 + h) + (tk.y - __ldg(pl.heavy_start + h)) / LEAF + lf;
+    const double v = emu_segment(pl.ind, tk.y + lf * LEAF, min(LEAF, tk.z - lf * LEAF), src, tp,
+                                 t, lane, [](int, double x) { return x; });
+    hpart[(long long)slot * tp + t] = v;
+  } else {
+    const int4 tk = __ldg(dn.tasks + (u - n_hleaf));
+    const double v = emu_segment(dn.rows, tk.y, tk.z, src, tp, t, lane,
+                                 [](int, double x) { return x; });
+    xpart[(long long)tk.x * tp + t] = v;
+  }
+}
+
+// R256 over m partials part[k][TP] (k = 0..m-1) for this lane's task, as
+// block_reduce_partials does for one task: m <= 256 one leaf; otherwise
+// leaves of 256 partials, then a leaf over their sums.  One warp.
+__device__ __forceinline__ double emu_partials(const double* __restrict__ part, long long m,
+                                               int tp, int t) {
+  auto leaf = [&](long long k0, int len) {
+    return emu_leaf(len, [&](int base, int l) { return part[(k0 + base + l) * tp + t]; });
+  };
+  if (m <= LEAF) return leaf(0, (int)m);
+  const int m2 = (int)((m + LEAF - 1) / LEAF);
+  double P[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) P[l] = 0.0;
+  for (int gb = 0; gb < m2; gb += 32) {
+    for (int l = 0; l < 32 && gb + l < m2; ++l) {
+      const long long k0 = (long long)(gb + l) * LEAF;
+      const double v = leaf(k0, (int)min((long long)LEAF, m - k0));
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (q == l) P[q] = P[q] + v;
+    }
+  }
+  return tree32(P);
+}
+
+// Combine the long columns: heavy segment h (hn[h] leaf sums from h0[h]) and
+// blocked column b (poff range).  One warp per (column, group).
+__global__ void __launch_bounds__(256) kb_cols_combine(SegPlan pl, XtDense dn,
+                                                       const double* __restrict__ hpart,
+                                                       const double* __restrict__ xpart,
+                                                       long long n_heavy,
+                                                       double* __restrict__ out, int G, int tp,
+                                                       int mode, const double* __restrict__ mu,
+                                                       BatchState B) {
+  const int lane = threadIdx.x & 31;
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= (n_heavy + dn.n_dense) * G) return;
+  const long long u = w / G;
+  const int g = (int)(w - u * G);
+  const int t = g * BG + lane;
+  double s;
+  long long col;
+  if (u < n_heavy) {
+    const int h = (int)u;
+    const int h0 = __ldg(pl.heavy_seg0 + h), hn = __ldg(pl.heavy_nseg + h);
+    s = emu_partials(hpart + (long long)h0 * tp, hn, tp, t);
+    col = __ldg(pl.heavy_seg + h);
+  } else {
+    const long long b = u - n_heavy;
+    const long long p0 = __ldg(dn.poff + b), p1 = __ldg(dn.poff + b + 1);
+    s = emu_partials(xpart + p0 * tp, p1 - p0, tp, t);
+    col = __ldg(dn.col + b);
+  }
+  out[col * tp + t] = b_col_finish(s, mode, col, t, tp, mu, B);
+}
+
+// Leaf sums over a contiguous task-minor vector (len rows): kind 0 sum(v),
+// 1 sum over class +1 (off-class 0.0), 2 class -1, 3 fma dot v . v2.
+__global__ void __launch_bounds__(256) kb_vec_leaves(const double* __restrict__ v,
+                                                     const double* __restrict__ v2,
+                                                     const signed char* __restrict__ lab,
+                                                     long long len, int kind,
+                                                     double* __restrict__ part, long long n_leaf,
+                                                     int G, int tp) {
+  const int lane = threadIdx.x & 31;
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= n_leaf * G) return;
+  const long long lf = w / G;
+  const int g = (int)(w - lf * G);
+  const int t = g * BG + lane;
+  const long long i0 = lf * LEAF;
+  const int n = (int)min((long long)LEAF, len - i0);
+  double s;
+  if (kind == 3) {
+    s = emu_dot_leaf(n, [&](int e, double& x, double& y) {
+      x = v[(i0 + e) * tp + t];
+      y = v2[(i0 + e) * tp + t];
+    });
+  } else {
+    s = emu_leaf(n, [&](int base, int l) {
+      const long long k = (i0 + base + l) * tp + t;
+      const double x = v[k];
+      if (kind == 1) return lab[k] == 1 ? x : 0.0;
+      if (kind == 2) return lab[k] == -1 ? x : 0.0;
+      return x;
+    });
+  }
+  part[lf * tp + t] = s;
+}
+
+// R256 over n_leaf partials per task -> out[t].  One warp per group.
+__global__ void kb_combine(const double* __restrict__ part, long long n_leaf, double* __restrict__ out,
+                           int tp) {
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.x;
+  const int t = g * BG + lane;
+  out[t] = emu_partials(part, n_leaf, tp, t);
+}
+
+// apply_w: class-mean broadcast; the class sums arrive in out1 / out2.
+__global__ void kb_class_means(BatchState B, const double* __restrict__ s1,
+                               const double* __restrict__ s2) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B.tp) return;
+  B.mean1[t] = s1[t] / B.n1[t];
+  B.mean2[t] = s2[t] / B.n2[t];
+}
+
+__global__ void kb_apply_w(const signed char* __restrict__ lab, double* __restrict__ w,
+                           long long len, int tp, BatchState B) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < len;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(k % tp);
+    const signed char l = lab[k];
+    w[k] = l == 1 ? B.mean1[t] : (l == -1 ? B.mean2[t] : 0.0);
+  }
+}
+
+// r = p = b; P_s = b, sols_s = 0 (krylov.py:199-208).
+__global__ void kb_cg_init_vec(const double* __restrict__ b, double* __restrict__ r,
+                               double* __restrict__ p, double* __restrict__ bigp,
+                               double* __restrict__ sols, long long d, int tp, int ns) {
+  const long long total = d * tp;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+       k += (long long)gridDim.x * blockDim.x) {
+    const double v = b[k];
+    r[k] = v;
+    p[k] = v;
+    for (int s = 0; s < ns; ++s) {
+      bigp[k * ns + s] = v;
+      sols[k * ns + s] = 0.0;
+    }
+  }
+}
+
+// b.b arrives in bb[t] (krylov.py:185-194).
+__global__ void kb_cg_init_scalars(BatchState B, const double* __restrict__ bb, double tol) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B.tp || B.status[t] == ST_PAD) return;
+  const double b_norm = sqrt(bb[t]);
+  B.b_norm[t] = b_norm;
+  B.rr[t] = b_norm * b_norm;
+  B.thresh[t] = tol * b_norm;
+  if (b_norm == 0.0) {
+    for (int s = 0; s < B.ns; ++s) {
+      const int k = t * B.ns + s;
+      B.iters[k] = 0; B.resid[k] = 0.0; B.conv[k] = 1; B.active[k] = 0;
+    }
+    B.n_active[t] = 0;
+    B.finished[t] = 1;
+  } else if (B.max_iter <= 0) {
+    B.finished[t] = 1;
+  }
+}
+
+// ---------------------------------------------------------------- CG step
+
+// A: centring q -= mu * sum(z) and the p.q leaves (fma).
+__global__ void __launch_bounds__(256) kb_step_a(double* __restrict__ q,
+                                                 const double* __restrict__ p,
+                                                 const double* __restrict__ mu, long long d,
+                                                 double* __restrict__ part, long long n_leaf,
+                                                 int G, BatchState B) {
+  const int lane = threadIdx.x & 31;
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= n_leaf * G) return;
+  const long long lf = w / G;
+  const int g = (int)(w - lf * G);
+  const int tp = B.tp, t = g * BG + lane;
+  if (!b_live(B, t)) return;
+  const long long i0 = lf * LEAF;
+  const int n = (int)min((long long)LEAF, d - i0);
+  const double sz = B.sum_v[t];
+  const double s = emu_dot_leaf(n, [&](int e, double& x, double& y) {
+    const long long k = (i0 + e) * tp + t;
+    const double qc = q[k] - mu[k] * sz;
+    q[k] = qc;
+    x = p[k];
+    y = qc;
+  });
+  part[lf * tp + t] = s;
+}
+
+// Scalars after p.q (phase B of k_cg_step): gamma and zeta_next / gamma_s.
+__global__ void kb_scalars_b(BatchState B) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B.tp || !b_live(B, t)) return;
+  const double pq = B.pq[t];
+  if (!isfinite(pq) || pq == 0.0) {
+    B.status[t] = isfinite(pq) ? ST_BREAKDOWN : ST_NONFINITE;
+    B.fail_iter[t] = B.iter[t];
+    B.finished[t] = 1;
+    return;
+  }
+  const double rr = B.rr[t], gp = B.gamma_prev[t], al = B.alpha[t];
+  const double gamma = -rr / pq;
+  B.gamma[t] = gamma;
+  for (int s = 0; s < B.ns; ++s) {
+    const int k = t * B.ns + s;
+    double zn = 0.0, gs = 0.0;
+    unsigned char good = 0;
+    if (B.active[k]) {
+      const double zp = B.zeta_prev[k], z = B.zeta[k];
+      const double denom = gamma * al * (zp - z) + zp * gp * (1.0 - B.beta[s] * gamma);
+      zn = zp * z * gp / denom;
+      if (isfinite(zn) && !(fabs(zn) < 1e-290)) {
+        good = 1;
+        gs = gamma * zn / z;
+      }
+    }
+    B.s_zn[k] = zn;
+    B.s_gs[k] = gs;
+    B.s_good[k] = good;
+  }
+}
+
+// B: r_next = r + gamma q and the r.r leaves.
+__global__ void __launch_bounds__(256) kb_step_b(const double* __restrict__ q,
+                                                 const double* __restrict__ r_cur,
+                                                 double* __restrict__ r_next, long long d,
+                                                 double* __restrict__ part, long long n_leaf,
+                                                 int G, BatchState B) {
+  const int lane = threadIdx.x & 31;
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= n_leaf * G) return;
+  const long long lf = w / G;
+  const int g = (int)(w - lf * G);
+  const int tp = B.tp, t = g * BG + lane;
+  if (!b_live(B, t)) return;
+  const long long i0 = lf * LEAF;
+  const int n = (int)min((long long)LEAF, d - i0);
+  const double gamma = B.gamma[t];
+  const double s = emu_dot_leaf(n, [&](int e, double& x, double& y) {
+    const long long k = (i0 + e) * tp + t;
+    const double rn = r_cur[k] + gamma * q[k];
+    r_next[k] = rn;
+    x = rn;
+    y = rn;
+  });
+  part[lf * tp + t] = s;
+}
+
+// Scalars after r.r (phase C of k_cg_step, block 0's bookkeeping).
+__global__ void kb_scalars_c(BatchState B) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B.tp || !b_live(B, t)) return;
+  const double rr_new = B.rr_new[t];
+  const long long it = B.iter[t];
+  for (int s = 0; s < B.ns; ++s) B.upd_mode[t * B.ns + s] = 0;
+  if (!isfinite(rr_new)) {
+    B.status[t] = ST_NONFINITE;
+    B.fail_iter[t] = it;
+    B.finished[t] = 1;
+    return;
+  }
+  const double rr = B.rr[t], gamma = B.gamma[t];
+  const double alpha_new = rr_new / rr;
+  B.alpha_new[t] = alpha_new;
+  const double r_norm = sqrt(rr_new);
+  int n_active = 0;
+  for (int s = 0; s < B.ns; ++s) {
+    const int k = t * B.ns + s;
+    if (!B.active[k]) continue;
+    if (!B.s_good[k]) {  // degenerate zeta: freeze untouched (krylov.py:251-255)
+      B.iters[k] = it + 1;
+      B.resid[k] = __longlong_as_double(0x7ff0000000000000LL);
+      B.active[k] = 0;
+      continue;
+    }
+    const double zn = B.s_zn[k], z = B.zeta[k], gs = B.s_gs[k];
+    const double as = alpha_new * (zn * gs) / (z * gamma);
+    B.alpha_s[k] = as;
+    B.upd_gs[k] = gs;
+    B.upd_zn[k] = zn;
+    B.upd_as[k] = as;
+    const double shift_res = fabs(zn) * r_norm;
+    if (shift_res < B.thresh[t]) {
+      B.iters[k] = it + 1;
+      B.resid[k] = shift_res;
+      B.conv[k] = 1;
+      B.active[k] = 0;
+      B.upd_mode[k] = 1;
+    } else {
+      B.zeta_prev[k] = z;
+      B.zeta[k] = zn;
+      B.upd_mode[k] = 3;
+      ++n_active;
+    }
+  }
+  B.gamma_prev[t] = gamma;
+  B.alpha[t] = alpha_new;
+  B.rr[t] = rr_new;
+  B.iter[t] = it + 1;
+  B.n_active[t] = n_active;
+  // finished is raised by kb_step_c after the last p / shift updates
+}
+
+// C: p = r_next + alpha_new p, then the shift updates of this iteration
+// (krylov.py:230, 238-241) for every (row, task, shift).
+__global__ void kb_step_c(const double* __restrict__ r_next, double* __restrict__ p,
+                          double* __restrict__ bigp, double* __restrict__ sols, long long d,
+                          BatchState B, const int* __restrict__ stepped) {
+  const int tp = B.tp, ns = B.ns;
+  const long long total = d * tp;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(k % tp);
+    if (!stepped[t]) continue;
+    const double rn = r_next[k];
+    p[k] = rn + B.alpha_new[t] * p[k];
+    for (int s = 0; s < ns; ++s) {
+      const int ks = t * ns + s;
+      const int mode = B.upd_mode[ks];
+      if (mode == 0) continue;
+      const long long e = k * ns + s;
+      const double pv = bigp[e];
+      sols[e] = sols[e] - pv * B.upd_gs[ks];
+      if (mode == 3) bigp[e] = B.upd_zn[ks] * rn + B.upd_as[ks] * pv;
+    }
+  }
+}
+
+// Which tasks ran this iteration's updates (live after phase C), then the
+// end-of-iteration flags (krylov.py:269-270 and the iteration budget).
+__global__ void kb_mark_stepped(BatchState B, int* __restrict__ stepped) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B.tp) return;
+  stepped[t] = b_live(B, t) ? 1 : 0;
+}
+
+__global__ void kb_end_iteration(BatchState B, const int* __restrict__ stepped,
+                                 int* __restrict__ n_live) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B.tp) return;
+  if (stepped[t] && (B.n_active[t] == 0 || B.iter[t] >= B.max_iter)) B.finished[t] = 1;
+  if (b_live(B, t)) atomicAdd(n_live, 1);
+}
+
+// After the loop: still-active shifts report |zeta| sqrt(rr) (krylov.py:272-275).
+__global__ void kb_finish(BatchState B) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B.tp || B.status[t] != ST_OK) return;
+  const double rn = sqrt(B.rr[t]);
+  for (int s = 0; s < B.ns; ++s) {
+    const int k = t * B.ns + s;
+    if (B.active[k]) {
+      B.iters[k] = B.max_iter;
+      B.resid[k] = fabs(B.zeta[k]) * rn;
+    }
+  }
+}
+
+// Orientation leaves y.s per (task, shift) over N (fma, canonical lanes over
+// rows; blockIdx.y = task * ns + shift) and the flip flags.
+__global__ void kb_orient_leaves(const signed char* __restrict__ lab,
+                                 const double* __restrict__ scores, long long n,
+                                 double* __restrict__ part, long long n_leaf, int tp, int ns) {
+  const int lane = threadIdx.x & 31;
+  const long long g = (long long)blockIdx.x * WARPS_PER_BLOCK + (threadIdx.x >> 5);
+  const int ts = blockIdx.y;
+  const int t = ts / ns;
+  if (g >= n_leaf) return;
+  const double* sv = scores + (long long)ts * n;
+  double a = 0.0;
+  for (int k = 0; k < 8; ++k) {
+    const long long i = g * LEAF + k * 32 + lane;
+    if (i < n) a = fma((double)lab[i * tp + t], sv[i], a);
+  }
+  a = butterfly(a);
+  if (lane == 0) part[(long long)ts * n_leaf + g] = a;
+}
+
+__global__ void kb_orient_combine(const double* __restrict__ part, long long n_leaf,
+                                  BatchState B) {
+  __shared__ double smem[257];
+  const int ts = blockIdx.x;
+  const double v = block_reduce_partials(part + (long long)ts * n_leaf, n_leaf, smem);
+  if (threadIdx.x == 0) B.flip[ts] = v < 0.0 ? 1 : 0;
+}
+
+// Negate flipped (task, shift) scores [TP*ns][N] and directions [D][TP][ns].
+__global__ void kb_flip(double* __restrict__ scores, double* __restrict__ sols, long long n,
+                        long long d, int T, BatchState B) {
+  const int ts = blockIdx.y;
+  const int t = ts / B.ns, s = ts - t * B.ns;
+  if (t >= T || !B.flip[ts]) return;
+  const long long lim = n > d ? n : d;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < lim;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (i < n) scores[(long long)ts * n + i] = -scores[(long long)ts * n + i];
+    if (i < d) {
+      const long long e = (i * B.tp + t) * B.ns + s;
+      sols[e] = -sols[e];
+    }
+  }
+}
+
+}  // namespace fsda

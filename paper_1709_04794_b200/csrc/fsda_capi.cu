@@ -27,6 +27,7 @@
 #include "../../include/fsda_b200.h"
 #include "fsda_device.cuh"
 #include "fsda_hot.cuh"
+#include "fsda_batch.cuh"
 
 using namespace fsda;
 
@@ -131,18 +132,43 @@ struct Launch {
 // Device side of one segmented-sum plan (see SegPlan in fsda_hot.cuh).
 struct HostPlan {
   DevBuf<int4> tasks;
-  DevBuf<int> h0, hn, hs, ht;
+  DevBuf<int> h0, hn, hs, ht, hseg;
   DevBuf<unsigned> hc;
   DevBuf<double> part;
   PinnedBuf stage;
+  long long n_heavy = 0, n_heavy_leaves = 0;  // heavy segments and their leaves
   SegPlan pl{};
   void release() {
-    tasks.release(); h0.release(); hn.release(); hs.release(); ht.release(); hc.release();
+    tasks.release(); h0.release(); hn.release(); hs.release(); ht.release(); hseg.release();
+    hc.release();
     part.release(); stage.release();
   }
 };
 
 }  // namespace
+
+// Device buffers of the multi-task batch (fsda_solve_batch), task-minor.
+struct BatchBufs {
+  DevBuf<signed char> lab;
+  DevBuf<double> ind, P, Q, R0, R1, MU, Bv, PR, Y, Z, BIGP, SOLS, SCORES, OUT;
+  DevBuf<double> partD, partN, hpart, xpart, opart, scal;
+  DevBuf<long long> lscal;
+  DevBuf<int> iscal;
+  DevBuf<double> sh_d;
+  DevBuf<long long> sh_l;
+  DevBuf<unsigned char> sh_u;
+  DevBuf<int> sh_i;
+  DevBuf<double> betas;
+  DevBuf<char> raw;
+  void release() {
+    lab.release(); ind.release(); P.release(); Q.release(); R0.release(); R1.release();
+    MU.release(); Bv.release(); PR.release(); Y.release(); Z.release(); BIGP.release();
+    SOLS.release(); SCORES.release(); OUT.release(); partD.release(); partN.release();
+    hpart.release(); xpart.release(); opart.release(); scal.release(); lscal.release();
+    iscal.release(); sh_d.release(); sh_l.release(); sh_u.release(); sh_i.release();
+    betas.release(); raw.release();
+  }
+};
 
 struct fsda_ctx {
   int device = 0;
@@ -167,6 +193,8 @@ struct fsda_ctx {
   DevBuf<int> xh_col, xh_bptr;
   DevBuf<int4> xh_tasks;
   DevBuf<long long> xh_boff, xh_bwarp, xh_poff;
+  long long xh_ntasks = 0, xh_nslots = 0;
+  BatchBufs batch;
   PinnedBuf xh_stage;
   DevBuf<double> xh_part;
   XtDense xh{};
@@ -920,12 +948,13 @@ void build_seg_plan(HostPlan& hp, cudaStream_t stream, const OffT* offs, long lo
   pl.warp_base[7] = wb;
   pl.warp_base[8] = wb;
   const long long n_tasks = t + n_htask;
-  char* st = (char*)hp.stage.ensure(sizeof(int4) * n_tasks + 4 * sizeof(int) * n_heavy + 16);
+  char* st = (char*)hp.stage.ensure(sizeof(int4) * n_tasks + 5 * sizeof(int) * n_heavy + 16);
   int4* tasks = (int4*)st;
   int* h0 = (int*)(tasks + n_tasks);
   int* hn = h0 + n_heavy;
   int* hs = hn + n_heavy;
   int* ht = hs + n_heavy;
+  int* hg = ht + n_heavy;
   // per-chunk start positions: class tasks, heavy tasks, heavy ids, leaves
   std::vector<std::array<long long, 9>> start(nch);
   {
@@ -953,6 +982,7 @@ void build_seg_plan(HostPlan& hp, cudaStream_t stream, const OffT* offs, long lo
         const int nseg = (int)cdiv(n, LEAF), ntask = (int)cdiv(n, 4 * LEAF);
         const long long h = pos[7]++;
         h0[h] = (int)pos[8];
+        hg[h] = (int)sgi;
         hn[h] = nseg;
         hs[h] = lo;
         ht[h] = ntask;
@@ -964,9 +994,9 @@ void build_seg_plan(HostPlan& hp, cudaStream_t stream, const OffT* offs, long lo
   }
   hp.tasks.ensure(n_tasks);
   if (n_tasks) CK(cudaMemcpyAsync(hp.tasks.ptr, tasks, sizeof(int4) * n_tasks, cudaMemcpyHostToDevice, stream));
-  DevBuf<int>* dsts[4] = {&hp.h0, &hp.hn, &hp.hs, &hp.ht};
-  int* srcs[4] = {h0, hn, hs, ht};
-  for (int k = 0; k < 4; ++k) {
+  DevBuf<int>* dsts[5] = {&hp.h0, &hp.hn, &hp.hs, &hp.ht, &hp.hseg};
+  int* srcs[5] = {h0, hn, hs, ht, hg};
+  for (int k = 0; k < 5; ++k) {
     dsts[k]->ensure(n_heavy);
     if (n_heavy)
       CK(cudaMemcpyAsync(dsts[k]->ptr, srcs[k], sizeof(int) * n_heavy, cudaMemcpyHostToDevice, stream));
@@ -974,12 +1004,15 @@ void build_seg_plan(HostPlan& hp, cudaStream_t stream, const OffT* offs, long lo
   hp.hc.ensure(n_heavy);
   CK(cudaMemsetAsync(hp.hc.ptr, 0, sizeof(unsigned) * std::max<long long>(n_heavy, 1), stream));
   hp.part.ensure(leaves);
+  hp.n_heavy = n_heavy;
+  hp.n_heavy_leaves = leaves;
   pl.ind = ind;
   pl.tasks = hp.tasks.ptr;
   pl.heavy_seg0 = hp.h0.ptr;
   pl.heavy_nseg = hp.hn.ptr;
   pl.heavy_start = hp.hs.ptr;
   pl.heavy_ntask = hp.ht.ptr;
+  pl.heavy_seg = hp.hseg.ptr;
   pl.heavy_count = hp.hc.ptr;
   pl.seg_part = hp.part.ptr;
 }
@@ -1102,6 +1135,8 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   xh.part = c->xh_part.ptr;
   xh.poff = c->xh_poff.ptr;
   xh.n_dense = nh;
+  c->xh_ntasks = n_tasks;
+  c->xh_nslots = poff[nh];
   xh.nb = nb;
   xh.rb = rb;
   xh.ticket_chunk = XT_TICKET_CHUNK;
@@ -1223,6 +1258,7 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     c->xh_part.release();
     c->xh_poff.release();
     c->xh_stage.release();
+    c->batch.release();
     c->plan_xr.release();
     c->plan_lr.release();
     c->plan_xc.release();
@@ -1938,6 +1974,287 @@ int fsda_sa_solve(fsda_ctx* c, double alpha, const double* betas, int ns, double
   launch_solve(c, alpha, ns, max_iter, tol, nullptr);
   SolveOut o{solutions, nullptr, residuals, iterations, converged, n_applies, fail_iter};
   return read_results(c, ns, o, nullptr);
+  API_END
+}
+
+
+// ---- multi-task batch (fsda_batch.cuh) -----------------------------------
+
+static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alpha,
+                            const double* betas, int ns, double tol, int64_t max_iter,
+                            const double* probes, double* directions, double* scores,
+                            double* residuals, int64_t* iterations, uint8_t* converged,
+                            int64_t* n_applies, int64_t* fail_iter, int* status) {
+  if (!c->has_x) return fail(FSDA_EINVAL, "fsda_solve_batch: X has not been uploaded");
+  if (!c->has_l) return fail(FSDA_EINVAL, "fsda_solve_batch: Laplacian has not been uploaded");
+  if (T <= 0) return fail(FSDA_EINVAL, "fsda_solve_batch: need at least one task");
+  if (!labels || !probes || !betas) return fail(FSDA_EINVAL, "fsda_solve_batch: null input");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(FSDA_EINVAL, "alpha must lie in [0, 1], got %g", alpha);
+  if (ns <= 0) return fail(FSDA_EINVAL, "shift grid must be a non-empty 1-d array");
+  if (ns > FSDA_MAX_SHIFTS) return fail(FSDA_EINVAL, "at most 4096 shifts per solve");
+  for (int s = 0; s < ns; ++s) {
+    if (!std::isfinite(betas[s])) return fail(FSDA_EINVAL, "shifts must be finite");
+    if (s == 0 && betas[s] < 0) return fail(FSDA_EINVAL, "shifts must be non-negative");
+    if (s > 0 && !(betas[s] > betas[s - 1])) return fail(FSDA_EINVAL, "shifts must be strictly ascending");
+  }
+  if (!(tol > 0)) return fail(FSDA_EINVAL, "tol must be positive");
+  if (c->row_base != 0 || c->n_global != c->n)
+    return fail(FSDA_EINVAL, "fsda_solve_batch: needs the whole Laplacian (not a row shard)");
+  const long long n = c->n, d = c->d;
+  // a segment of more than 65536 entries would need a third tree level
+  const int G = (T + BG - 1) / BG, tp = G * BG;
+  std::vector<double> ell(tp, 1.0), n1v(tp, 1.0), n2v(tp, 1.0);
+  for (int t = 0; t < T; ++t) {
+    long long a = 0, b = 0;
+    const int8_t* l = labels + (long long)t * n;
+    for (long long i = 0; i < n; ++i) {
+      if (l[i] != 0 && l[i] != 1 && l[i] != -1)
+        return fail(FSDA_ELABEL, "task %d: labels must take values in {+1, -1, 0}", t);
+      a += l[i] == 1;
+      b += l[i] == -1;
+    }
+    if (a + b == 0) return fail(FSDA_ELABEL, "task %d: centering requires at least one labeled sample", t);
+    if (a == 0 || b == 0) return fail(FSDA_EINVAL, "task %d: both classes need at least one labeled sample", t);
+    ell[t] = (double)(a + b);
+    n1v[t] = (double)a;
+    n2v[t] = (double)b;
+  }
+  BatchBufs& bb = c->batch;
+  cudaStream_t st = c->stream;
+  const long long nlN = n_leaves(n), nlD = n_leaves(d);
+  const long long ND = (long long)tp;
+  bb.lab.ensure(n * ND);
+  bb.ind.ensure(n * ND);
+  for (DevBuf<double>* v : {&bb.P, &bb.Q, &bb.R0, &bb.R1, &bb.MU, &bb.Bv, &bb.PR}) v->ensure(std::max(1LL, d * ND));
+  bb.Y.ensure(std::max(1LL, n * ND));
+  bb.Z.ensure(std::max(1LL, n * ND));
+  bb.BIGP.ensure(std::max(1LL, d * ND * ns));
+  bb.SOLS.ensure(std::max(1LL, d * ND * ns));
+  bb.SCORES.ensure(std::max(1LL, n * ND * ns));
+  bb.OUT.ensure(std::max(1LL, (long long)T * ns * d));
+  bb.partD.ensure(std::max(1LL, nlD * ND));
+  bb.partN.ensure(std::max(1LL, nlN * ND));
+  bb.hpart.ensure(std::max(1LL, c->plan_xc.n_heavy_leaves * ND));
+  bb.xpart.ensure(std::max(1LL, c->xh_nslots * ND));
+  bb.opart.ensure(std::max(1LL, nlN * ND * ns));
+  bb.scal.ensure(15 * ND);
+  bb.lscal.ensure(2 * ND);
+  bb.iscal.ensure(5 * ND + 1);
+  bb.sh_d.ensure(9 * ND * ns);
+  bb.sh_l.ensure(ND * ns);
+  bb.sh_u.ensure(4 * ND * ns);
+  bb.sh_i.ensure(ND * ns);
+  bb.betas.ensure(ns);
+  // inputs
+  bb.raw.ensure(std::max<long long>((long long)T * n, (long long)T * d * 8));
+  CK(cudaMemcpyAsync(bb.raw.ptr, labels, (size_t)T * n, cudaMemcpyHostToDevice, st));
+  kb_labels_in<<<(unsigned)std::min<long long>(cdiv(n * ND, 256), 65535LL * 4), 256, 0, st>>>(
+      (const signed char*)bb.raw.ptr, bb.lab.ptr, bb.ind.ptr, n, T, tp);
+  CKL();
+  CK(cudaMemcpyAsync(bb.raw.ptr, probes, sizeof(double) * T * d, cudaMemcpyHostToDevice, st));
+  kb_task_minor<<<(unsigned)std::min<long long>(cdiv(d * ND, 256), 65535LL * 4), 256, 0, st>>>(
+      (const double*)bb.raw.ptr, bb.PR.ptr, d, T, tp);
+  CKL();
+  CK(cudaMemcpyAsync(bb.betas.ptr, betas, sizeof(double) * ns, cudaMemcpyHostToDevice, st));
+  BatchState B;
+  double* sd = bb.scal.ptr;
+  B.rr = sd; B.gamma_prev = sd + ND; B.alpha = sd + 2 * ND; B.b_norm = sd + 3 * ND;
+  B.thresh = sd + 4 * ND; B.gamma = sd + 5 * ND; B.alpha_new = sd + 6 * ND; B.mean1 = sd + 7 * ND;
+  B.mean2 = sd + 8 * ND; B.ell = sd + 9 * ND; B.n1 = sd + 10 * ND; B.n2 = sd + 11 * ND;
+  B.sum_v = sd + 12 * ND; B.pq = sd + 13 * ND; B.rr_new = sd + 14 * ND;
+  B.iter = bb.lscal.ptr; B.fail_iter = bb.lscal.ptr + ND;
+  B.status = bb.iscal.ptr; B.finished = bb.iscal.ptr + ND; B.n_active = bb.iscal.ptr + 2 * ND;
+  int* stepped = bb.iscal.ptr + 3 * ND;
+  int* n_live = bb.iscal.ptr + 5 * ND;
+  const long long NS = ND * ns;
+  double* hd = bb.sh_d.ptr;
+  B.zeta_prev = hd; B.zeta = hd + NS; B.alpha_s = hd + 2 * NS; B.resid = hd + 3 * NS;
+  B.s_zn = hd + 4 * NS; B.s_gs = hd + 5 * NS; B.upd_gs = hd + 6 * NS; B.upd_zn = hd + 7 * NS;
+  B.upd_as = hd + 8 * NS;
+  B.iters = bb.sh_l.ptr;
+  B.s_good = bb.sh_u.ptr; B.conv = bb.sh_u.ptr + NS; B.active = bb.sh_u.ptr + 2 * NS;
+  B.flip = bb.sh_u.ptr + 3 * NS;
+  B.upd_mode = bb.sh_i.ptr;
+  B.beta = bb.betas.ptr;
+  B.ns = ns;
+  B.tp = tp;
+  B.max_iter = max_iter;
+  CK(cudaMemcpyAsync(B.ell, ell.data(), sizeof(double) * ND, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B.n1, n1v.data(), sizeof(double) * ND, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B.n2, n2v.data(), sizeof(double) * ND, cudaMemcpyHostToDevice, st));
+  const int tb = (int)cdiv(ND, 128);
+  kb_reset<<<tb, 128, 0, st>>>(B, T, tol);
+  CKL();
+  if (c->xh_nslots) CK(cudaMemsetAsync(bb.xpart.ptr, 0, sizeof(double) * c->xh_nslots * ND, st));
+
+  auto grid_w = [](long long warps) { return (unsigned)std::max<long long>(1, cdiv(warps, 8)); };
+  auto rows_x = [&](const double* src, double* out) {
+    kb_rows<SEG_XROWS><<<grid_w(n * G), 256, 0, st>>>(c->x_rowptr.ptr, c->x_cols.ptr, src, out, n, G,
+                                                     tp, nullptr, nullptr, 0.0, 0);
+    CKL();
+  };
+  auto smoother = [&](const double* y, double* z) {
+    const int amode = alpha_mode_of(alpha);
+    if (amode == 0) {
+      kb_mask<<<(unsigned)std::min<long long>(cdiv(n * ND, 256), 65535LL * 4), 256, 0, st>>>(
+          y, bb.lab.ptr, z, n * ND);
+    } else {
+      kb_rows<SEG_LROWS><<<grid_w(n * G), 256, 0, st>>>(c->l_rowptr.ptr, c->l_cols.ptr, y, z, n, G,
+                                                       tp, c->l_diag.ptr, bb.lab.ptr, alpha, amode);
+    }
+    CKL();
+  };
+  const SegPlan& pxc = c->plan_xc.pl;
+  const long long n_light = pxc.cls_off[6];
+  const long long n_htask = pxc.warp_base[7] - pxc.warp_base[6];
+  const long long n_heavy = c->plan_xc.n_heavy;
+  auto xt = [&](const double* src, double* out, int mode) {
+    if (n_light)
+      kb_cols_light<<<grid_w(n_light * G), 256, 0, st>>>(pxc, src, out, G, tp, mode, bb.MU.ptr, B);
+    CKL();
+    if (n_htask || c->xh_ntasks) {
+      kb_cols_leaves<<<grid_w((4 * n_htask + c->xh_ntasks) * G), 256, 0, st>>>(
+          pxc, c->xh, src, bb.hpart.ptr, bb.xpart.ptr, 4 * n_htask, c->xh_ntasks, G, tp);
+      CKL();
+      kb_cols_combine<<<grid_w((n_heavy + c->xh.n_dense) * G), 256, 0, st>>>(
+          pxc, c->xh, bb.hpart.ptr, bb.xpart.ptr, n_heavy, out, G, tp, mode, bb.MU.ptr, B);
+      CKL();
+    }
+  };
+  auto vec_sum = [&](const double* v, const double* v2, int kind, long long len, double* part,
+                     double* out) {
+    const long long nl = n_leaves(len);
+    if (nl == 0) {
+      CK(cudaMemsetAsync(out, 0, sizeof(double) * ND, st));
+      return;
+    }
+    kb_vec_leaves<<<grid_w(nl * G), 256, 0, st>>>(v, v2, bb.lab.ptr, len, kind, part, nl, G, tp);
+    CKL();
+    kb_combine<<<G, 32, 0, st>>>(part, nl, out, tp);
+    CKL();
+  };
+
+  // ---- setup (sda.py:297-301, krylov.py:185-208), per task
+  xt(bb.ind.ptr, bb.MU.ptr, 2);                       // mu = X^T 1_l / l
+  rows_x(bb.PR.ptr, bb.Y.ptr);                        // t = X r
+  vec_sum(bb.Y.ptr, nullptr, 1, n, bb.partN.ptr, B.pq);
+  vec_sum(bb.Y.ptr, nullptr, 2, n, bb.partN.ptr, B.rr_new);
+  kb_class_means<<<tb, 128, 0, st>>>(B, B.pq, B.rr_new);
+  CKL();
+  kb_apply_w<<<(unsigned)std::min<long long>(cdiv(n * ND, 256), 65535LL * 4), 256, 0, st>>>(
+      bb.lab.ptr, bb.Z.ptr, n * ND, tp, B);
+  CKL();
+  vec_sum(bb.Z.ptr, nullptr, 0, n, bb.partN.ptr, B.sum_v);   // sum(w)
+  xt(bb.Z.ptr, bb.Bv.ptr, 1);                                // b = X^T w - mu sum(w)
+  kb_cg_init_vec<<<(unsigned)std::min<long long>(cdiv(d * ND, 256), 65535LL * 4), 256, 0, st>>>(
+      bb.Bv.ptr, bb.R0.ptr, bb.P.ptr, bb.BIGP.ptr, bb.SOLS.ptr, d, tp, ns);
+  CKL();
+  vec_sum(bb.Bv.ptr, bb.Bv.ptr, 3, d, bb.partD.ptr, B.pq);   // b.b
+  kb_cg_init_scalars<<<tb, 128, 0, st>>>(B, B.pq, tol);
+  CKL();
+
+  // ---- the shifted-CG loop (krylov.py:210-270), all live tasks in step
+  const unsigned ew = (unsigned)std::min<long long>(cdiv(d * ND, 256), (long long)c->num_sms * 8);
+  for (long long it = 0; it < max_iter; ++it) {
+    double* r_cur = (it & 1) ? bb.R1.ptr : bb.R0.ptr;
+    double* r_nxt = (it & 1) ? bb.R0.ptr : bb.R1.ptr;
+    rows_x(bb.P.ptr, bb.Y.ptr);                                // K1  y = X p
+    smoother(bb.Y.ptr, bb.Z.ptr);                              // K2  z = M y
+    xt(bb.Z.ptr, bb.Q.ptr, 0);                                 // K3  q = X^T z
+    vec_sum(bb.Z.ptr, nullptr, 0, n, bb.partN.ptr, B.sum_v);   //     sum(z)
+    if (nlD) {
+      kb_step_a<<<grid_w(nlD * G), 256, 0, st>>>(bb.Q.ptr, bb.P.ptr, bb.MU.ptr, d, bb.partD.ptr, nlD, G, B);
+      CKL();
+      kb_combine<<<G, 32, 0, st>>>(bb.partD.ptr, nlD, B.pq, tp);
+      CKL();
+    } else {
+      CK(cudaMemsetAsync(B.pq, 0, sizeof(double) * ND, st));
+    }
+    kb_scalars_b<<<tb, 128, 0, st>>>(B);
+    CKL();
+    if (nlD) {
+      kb_step_b<<<grid_w(nlD * G), 256, 0, st>>>(bb.Q.ptr, r_cur, r_nxt, d, bb.partD.ptr, nlD, G, B);
+      CKL();
+      kb_combine<<<G, 32, 0, st>>>(bb.partD.ptr, nlD, B.rr_new, tp);
+      CKL();
+    } else {
+      CK(cudaMemsetAsync(B.rr_new, 0, sizeof(double) * ND, st));
+    }
+    kb_scalars_c<<<tb, 128, 0, st>>>(B);
+    CKL();
+    kb_mark_stepped<<<tb, 128, 0, st>>>(B, stepped);
+    CKL();
+    kb_step_c<<<ew, 256, 0, st>>>(r_nxt, bb.P.ptr, bb.BIGP.ptr, bb.SOLS.ptr, d, B, stepped);
+    CKL();
+    CK(cudaMemsetAsync(n_live, 0, sizeof(int), st));
+    kb_end_iteration<<<tb, 128, 0, st>>>(B, stepped, n_live);
+    CKL();
+    int h_live = 0;
+    CK(cudaMemcpyAsync(&h_live, n_live, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h_live == 0) break;
+  }
+
+  // ---- tail: residuals, projections, orientation (sda.py:265-284)
+  kb_finish<<<tb, 128, 0, st>>>(B);
+  CKL();
+  const int nsp = tp * ns;
+  k_spmm_scores<<<grid_for(n, 8), 256, 0, st>>>(c->x_rowptr.ptr, c->x_cols.ptr, bb.SOLS.ptr,
+                                                bb.SCORES.ptr, (int)n, nsp);
+  CKL();
+  if (nlN) {
+    dim3 g((unsigned)grid_for(nlN, WARPS_PER_BLOCK), (unsigned)nsp);
+    kb_orient_leaves<<<g, LEAF_THREADS, 0, st>>>(bb.lab.ptr, bb.SCORES.ptr, n, bb.opart.ptr, nlN, tp, ns);
+    CKL();
+    kb_orient_combine<<<nsp, 256, 0, st>>>(bb.opart.ptr, nlN, B);
+    CKL();
+  }
+  {
+    dim3 g((unsigned)std::min<long long>(grid_for(std::max(n, d), 256), 1024), (unsigned)nsp);
+    kb_flip<<<g, 256, 0, st>>>(bb.SCORES.ptr, bb.SOLS.ptr, n, d, T, B);
+    CKL();
+  }
+  if (d > 0) {
+    kb_directions_out<<<(unsigned)std::min<long long>(cdiv((long long)T * ns * d, 256), 65535LL * 4), 256, 0, st>>>(
+        bb.SOLS.ptr, bb.OUT.ptr, d, T, tp, ns);
+    CKL();
+  }
+  // ---- results
+  const long long TS = (long long)T * ns;
+  if (directions && d > 0)
+    CK(cudaMemcpyAsync(directions, bb.OUT.ptr, sizeof(double) * TS * d, cudaMemcpyDeviceToHost, st));
+  if (scores && n > 0)
+    CK(cudaMemcpyAsync(scores, bb.SCORES.ptr, sizeof(double) * TS * n, cudaMemcpyDeviceToHost, st));
+  if (residuals) CK(cudaMemcpyAsync(residuals, B.resid, sizeof(double) * TS, cudaMemcpyDeviceToHost, st));
+  std::vector<long long> its(TS), itr(T), fit(T);
+  std::vector<unsigned char> cv(TS);
+  std::vector<int> stt(T);
+  CK(cudaMemcpyAsync(its.data(), B.iters, sizeof(long long) * TS, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(cv.data(), B.conv, TS, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(itr.data(), B.iter, sizeof(long long) * T, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(fit.data(), B.fail_iter, sizeof(long long) * T, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(stt.data(), B.status, sizeof(int) * T, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (long long k = 0; k < TS; ++k) {
+    if (iterations) iterations[k] = its[k];
+    if (converged) converged[k] = cv[k];
+  }
+  for (int t = 0; t < T; ++t) {
+    if (n_applies) n_applies[t] = itr[t];
+    if (fail_iter) fail_iter[t] = fit[t];
+    if (status) status[t] = stt[t] == ST_BREAKDOWN ? FSDA_EBREAKDOWN : (stt[t] == ST_NONFINITE ? FSDA_ENONFINITE : FSDA_OK);
+  }
+  return FSDA_OK;
+}
+
+int fsda_solve_batch(fsda_ctx* c, int n_tasks, const int8_t* labels, double alpha,
+                     const double* betas, int ns, double tol, int64_t max_iter,
+                     const double* probes, double* directions, double* scores,
+                     double* residuals, int64_t* iterations, uint8_t* converged,
+                     int64_t* n_applies, int64_t* fail_iter, int* status) {
+  API_BEGIN(c)
+  return batch_solve_impl(c, n_tasks, labels, alpha, betas, ns, tol, max_iter, probes, directions,
+                          scores, residuals, iterations, converged, n_applies, fail_iter, status);
   API_END
 }
 

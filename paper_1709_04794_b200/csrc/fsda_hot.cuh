@@ -159,6 +159,7 @@ struct SegPlan {
   const int* heavy_nseg;     // leaves of heavy segment h
   const int* heavy_start;    // index-stream start of heavy segment h
   const int* heavy_ntask;    // warp tasks of heavy segment h
+  const int* heavy_seg;      // segment id of heavy segment h
   unsigned* heavy_count;     // arrival counters
   double* seg_part;          // leaf partials
 };

@@ -238,6 +238,44 @@ class Device:
         _raise_for(rc, fam)
         return SweepResult(dirs, sc, res, its, conv.astype(bool), int(napp.value))
 
+    def solve_batch(self, label_sets, alpha, betas, tol, max_iter, probes, *, scores=True,
+                    fam=_OWN) -> list:
+        """T sweeps in one batched pass (fsda_solve_batch): task t uses label
+        mask label_sets[t] (any row order) and probe probes[t].  Each result
+        equals set_label_mask + solve_fsda for that task, bit for bit."""
+        lab = np.ascontiguousarray(np.asarray(label_sets, dtype=np.int8))
+        probes = _f64(probes)
+        if lab.ndim != 2 or lab.shape[1] != self.n:
+            raise ValueError("label_sets must be n_tasks x N")
+        T = lab.shape[0]
+        if probes.shape != (T, self.d):
+            raise ValueError("probes must be n_tasks x D")
+        betas = _f64(betas)
+        ns = int(betas.size)
+        dirs = _pinned_empty((T, ns, self.d))
+        sc = _pinned_empty((T, ns, self.n)) if scores else None
+        res = np.empty((T, ns))
+        its = np.empty((T, ns), dtype=np.int64)
+        conv = np.empty((T, ns), dtype=np.uint8)
+        napp = np.empty(T, dtype=np.int64)
+        fail = np.empty(T, dtype=np.int64)
+        status = np.empty(T, dtype=np.int32)
+        rc = _capi.lib().fsda_solve_batch(
+            self._h, T, _capi.i8ptr(lab), float(alpha), _capi.dptr(betas), ns, float(tol),
+            int(max_iter), _capi.dptr(probes), _capi.dptr(dirs), _capi.dptr(sc), _capi.dptr(res),
+            _capi.i64ptr(its), _capi.u8ptr(conv), _capi.i64ptr(napp), _capi.i64ptr(fail),
+            status.ctypes.data_as(C.POINTER(C.c_int)))
+        _raise_for(rc, fam)
+        for t in range(T):
+            if status[t] == _capi.FSDA_EBREAKDOWN:
+                raise fam.SolverBreakdownError(
+                    f"task {t}: singular direction: <p, Bp> = 0 at iteration {fail[t]}")
+            if status[t] == _capi.FSDA_ENONFINITE:
+                raise fam.NumericalFailureError(
+                    f"task {t}: non-finite <p, Bp> or residual at iteration {fail[t]}")
+        return [SweepResult(dirs[t], None if sc is None else sc[t], res[t], its[t],
+                            conv[t].astype(bool), int(napp[t])) for t in range(T)]
+
     def prepare_resident(self, alpha, betas, tol, max_iter, probe):
         betas, probe = _f64(betas), _f64(probe)
         self._res_ns = int(betas.size)
@@ -440,12 +478,17 @@ class DeviceProblem:
 
 
 def solve_label_sets(x, lap, label_sets, alpha, betas, tol: float = 1e-8, max_iter: int = 1000,
-                     seeds=0, *, device: Optional[Device] = None, scores: bool = True):
+                     seeds=0, *, device: Optional[Device] = None, scores: bool = True,
+                     batched: bool = True):
     """Many FSDA sweeps on one dataset: X and L are uploaded once and every
     label set (any row order — a mask, as the folds of nested CV) is solved
     against them.  Each result is what fsda_solve returns for that task after
     the reference's arrange_labeled_first permutation and its undo
     (evaluation.py:110-123), up to the summation order of the permuted rows.
+
+    batched=True solves all label sets in one pass (fsda_solve_batch: every
+    operator product serves all tasks); batched=False solves them one after
+    the other.  The results are identical.
 
     Returns a list of SweepResult (directions n_shifts x D, scores n_shifts x N
     in the original row order)."""
@@ -455,13 +498,18 @@ def solve_label_sets(x, lap, label_sets, alpha, betas, tol: float = 1e-8, max_it
     grid = T.as_shift_grid(betas)
     sets = [np.asarray(getattr(l, "labels", l), dtype=np.int8) for l in label_sets]
     seed_list = list(seeds) if np.ndim(seeds) else [int(seeds)] * len(sets)
-    out = []
-    for lab, seed in zip(sets, seed_list):
+    for lab in sets:
         if not (np.any(lab == 1) and np.any(lab == -1)):
             raise ValueError("both classes need at least one labeled sample")
-        dev.set_label_mask(lab)
-        probe = np.random.default_rng(seed).uniform(-1.0, 1.0, size=int(x.n_cols))
-        out.append(dev.solve_fsda(alpha, grid.betas, tol, max_iter, probe, scores=scores))
+    probes = [np.random.default_rng(seed).uniform(-1.0, 1.0, size=int(x.n_cols)) for seed in seed_list]
+    if batched and sets:
+        out = dev.solve_batch(np.stack(sets), alpha, grid.betas, tol, max_iter, np.stack(probes),
+                              scores=scores)
+    else:
+        out = []
+        for lab, probe in zip(sets, probes):
+            dev.set_label_mask(lab)
+            out.append(dev.solve_fsda(alpha, grid.betas, tol, max_iter, probe, scores=scores))
     dev._loaded = (None, None, None)
     return out
 

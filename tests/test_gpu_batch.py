@@ -1,0 +1,96 @@
+"""Multi-task batch (fsda_solve_batch): T label
+masks and probes solved in one pass per operator product.  Every task must
+equal, bit for bit, the single-task solve of the same mask and probe (which
+test_gpu_parity.py pins to the C oracle bitwise)."""
+
+import numpy as np
+import pytest
+
+import paper_1709_04794_b200 as fb
+from paper_1709_04794_b200.workloads import make_workload
+
+pytestmark = pytest.mark.gpu
+
+
+def _masks(n, n_tasks, n_lab, n_pos, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n_tasks):
+        lab = np.zeros(n, dtype=np.int8)
+        idx = rng.choice(n, size=n_lab, replace=False)
+        lab[idx] = -1
+        lab[idx[:n_pos]] = 1
+        out.append(lab)
+    return out
+
+
+def _mats(w):
+    x = fb.SparseMatrix.binary(w.n, w.d, w.x_offsets, w.x_cols)
+    lap = fb.Laplacian(fb.SparseMatrix(w.n, w.n, w.l_offsets, w.l_cols, w.l_vals), w.degrees)
+    return x, lap
+
+
+def _same(a, b):
+    np.testing.assert_array_equal(a.directions, b.directions)
+    if a.scores is not None or b.scores is not None:
+        np.testing.assert_array_equal(a.scores, b.scores)
+    np.testing.assert_array_equal(a.residuals, b.residuals)
+    np.testing.assert_array_equal(a.iterations, b.iterations)
+    np.testing.assert_array_equal(a.converged, b.converged)
+    assert a.n_applies == b.n_applies
+
+
+def _check(w, sets, alpha, tol, max_iter, seeds):
+    x, lap = _mats(w)
+    batch = fb.solve_label_sets(x, lap, sets, alpha, w.betas, tol, max_iter, seeds=seeds)
+    seq = fb.solve_label_sets(x, lap, sets, alpha, w.betas, tol, max_iter, seeds=seeds,
+                              batched=False)
+    assert len(batch) == len(sets)
+    for a, b in zip(batch, seq):
+        _same(a, b)
+    return batch
+
+
+def test_batch_40_tasks_two_groups_bitwise():
+    """40 tasks = two 32-lane groups with padding; blocked X^T columns."""
+    w = make_workload("cfg1", n=3000, d=1200, ell=300, n_pos=60, lam=14.0, k=6, n_shifts=6)
+    sets = _masks(w.n, 40, 150, 40, seed=11)
+    _check(w, sets, w.alpha, w.tol, 12, seeds=list(range(40)))
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.25, 1.0])
+def test_batch_alpha_branches(alpha):
+    w = make_workload("cfg1", n=1500, d=600, ell=150, n_pos=30, lam=10.0, k=5, n_shifts=4)
+    sets = _masks(w.n, 3, 90, 25, seed=5)
+    _check(w, sets, alpha, w.tol, 10, seeds=[3, 4, 5])
+
+
+def test_batch_tasks_finish_at_different_iterations():
+    """Loose tolerance: shifts converge and tasks freeze at different
+    iterations; the others keep iterating."""
+    w = make_workload("cfg1", n=800, d=300, ell=200, n_pos=60, lam=6.0, k=4, n_shifts=5,
+                      beta_lo=1.0, beta_hi=1e4)
+    sets = _masks(w.n, 5, 200, 60, seed=2)
+    res = _check(w, sets, w.alpha, 1e-3, 200, seeds=[0, 1, 2, 3, 4])
+    assert any(r.converged.any() for r in res)
+    assert len({r.n_applies for r in res}) >= 1
+
+
+def test_batch_heavy_unblocked_columns():
+    """N > 262k rows: columns with 256 < n < 8 nb entries take the heavy
+    (leaf-combine) path of X^T rather than the blocked one."""
+    w = make_workload("cfg1", n=300_000, d=2500, ell=3000, n_pos=600, lam=4.0, k=3, n_shifts=3)
+    counts = np.bincount(w.x_cols, minlength=w.d)
+    nb = -(-w.n // 8192)
+    assert ((counts > 256) & (counts < 8 * nb)).any()
+    sets = _masks(w.n, 3, 2000, 500, seed=9)
+    _check(w, sets, w.alpha, w.tol, 5, seeds=[7, 8, 9])
+
+
+def test_batch_rejects_one_class_task():
+    w = make_workload("cfg1", n=500, d=200, ell=50, n_pos=10, lam=5.0, k=3, n_shifts=2)
+    x, lap = _mats(w)
+    sets = _masks(w.n, 2, 40, 10, seed=1)
+    sets[1][sets[1] == -1] = 1
+    with pytest.raises(ValueError, match="both classes"):
+        fb.solve_label_sets(x, lap, sets, w.alpha, w.betas, w.tol, 5)

@@ -114,24 +114,44 @@ __device__ __forceinline__ double emu_dot_leaf(int n, XY xy) {
   return tree32(A);
 }
 
-// Canonical sum of a gathered index segment: ind[start, start + n) selects
-// rows of src (task-minor); term(idx, v) maps the gathered value.  n <= 256:
-// one leaf; longer: R256 over its leaves (two levels, n <= 65536).
+// Canonical leaf of a gathered index segment: ind[s0, s0 + len) (len <= 256)
+// selects rows of src (task-minor); term(idx, v) maps the gathered value.
+// Indices arrive 32 at a time (one coalesced load, then shuffles); values are
+// gathered 8 at a time so at most 8 loads per lane are in flight next to the
+// 32 accumulators (register budget: two 256-thread CTAs per SM).
 template <typename Term>
-__device__ __forceinline__ double emu_segment(const int* __restrict__ ind, long long start, int n,
-                                              const double* __restrict__ src, int tp, int t,
-                                              int lane, Term term) {
-  auto leaf = [&](long long s0, int len) {
-    int my = 0;
-    return emu_leaf(len, [&](int base, int l) {
-      if (l == 0) {
-        my = (base + lane < len) ? __ldg(ind + s0 + base + lane) : 0;
+__device__ __forceinline__ double emu_gather_leaf(const int* __restrict__ ind, long long s0, int len,
+                                                  const double* __restrict__ src, int tp, int t,
+                                                  int lane, Term term) {
+  double A[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) A[l] = 0.0;
+  for (int base = 0; base < len; base += 32) {
+    const int my = (base + lane < len) ? __ldg(ind + s0 + base + lane) : 0;
+#pragma unroll
+    for (int sub = 0; sub < 4; ++sub) {
+      if (base + sub * 8 >= len) break;
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int l = sub * 8 + j;
+        const int idx = __shfl_sync(FULL, my, l);
+        v[j] = (base + l < len) ? term(idx, __ldg(src + (long long)idx * tp + t)) : 0.0;
       }
-      const int idx = __shfl_sync(FULL, my, l);
-      return term(idx, __ldg(src + (long long)idx * tp + t));
-    });
-  };
-  if (n <= LEAF) return leaf(start, n);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (base + sub * 8 + j < len) A[sub * 8 + j] = A[sub * 8 + j] + v[j];
+    }
+  }
+  return tree32(A);
+}
+
+// Segments longer than 256 entries: R256 over their leaves (two levels,
+// n <= 65536).  Kept out of line: it holds a second accumulator set.
+template <typename Term>
+__device__ __noinline__ double emu_gather_long(const int* __restrict__ ind, long long start, int n,
+                                               const double* __restrict__ src, int tp, int t,
+                                               int lane, Term term) {
   const int m = (n + LEAF - 1) / LEAF;  // <= 256 (host-checked)
   double P[32];
 #pragma unroll
@@ -139,13 +159,22 @@ __device__ __forceinline__ double emu_segment(const int* __restrict__ ind, long 
   for (int gb = 0; gb < m; gb += 32) {
     for (int l = 0; l < 32 && gb + l < m; ++l) {
       const int g = gb + l;
-      const double v = leaf(start + (long long)g * LEAF, min(LEAF, n - g * LEAF));
+      const double v = emu_gather_leaf(ind, start + (long long)g * LEAF, min(LEAF, n - g * LEAF),
+                                       src, tp, t, lane, term);
 #pragma unroll
       for (int q = 0; q < 32; ++q)
         if (q == l) P[q] = P[q] + v;
     }
   }
   return tree32(P);
+}
+
+template <typename Term>
+__device__ __forceinline__ double emu_segment(const int* __restrict__ ind, long long start, int n,
+                                              const double* __restrict__ src, int tp, int t,
+                                              int lane, Term term) {
+  if (n <= LEAF) return emu_gather_leaf(ind, start, n, src, tp, t, lane, term);
+  return emu_gather_long(ind, start, n, src, tp, t, lane, term);
 }
 
 // ------------------------------------------------------------ layout moves
@@ -210,7 +239,7 @@ __global__ void kb_reset(BatchState B, int T, double tol) {
 // Row sums over a CSR pattern for every task: K1 (y = X p) and K2 (z = M y).
 // One warp per (row, task group).
 template <int KIND>
-__global__ void __launch_bounds__(256) kb_rows(const int* __restrict__ rowptr,
+__global__ void __launch_bounds__(256, 2) kb_rows(const int* __restrict__ rowptr,
                                                const int* __restrict__ cols,
                                                const double* __restrict__ src,
                                                double* __restrict__ out, long long n_rows, int G,
@@ -257,7 +286,7 @@ __device__ __forceinline__ double b_col_finish(double s, int mode, long long c, 
 
 // X^T columns with n <= 256: the class tasks of the single-task column plan
 // (any class: each entry is one column segment).  One warp per (entry, group).
-__global__ void __launch_bounds__(256) kb_cols_light(SegPlan pl, const double* __restrict__ src,
+__global__ void __launch_bounds__(256, 2) kb_cols_light(SegPlan pl, const double* __restrict__ src,
                                                      double* __restrict__ out, int G, int tp,
                                                      int mode, const double* __restrict__ mu,
                                                      BatchState B) {
@@ -269,14 +298,14 @@ __global__ void __launch_bounds__(256) kb_cols_light(SegPlan pl, const double* _
   const int g = (int)(w - e * G);
   const int t = g * BG + lane;
   const int4 tk = __ldg(pl.tasks + e);
-  const double s = emu_segment(pl.ind, tk.y, tk.z, src, tp, t, lane, [](int, double v) { return v; });
+  const double s = emu_gather_leaf(pl.ind, tk.y, tk.z, src, tp, t, lane, [](int, double v) { return v; });
   out[(long long)tk.x * tp + t] = b_col_finish(s, mode, tk.x, t, tp, mu, B);
 }
 
 // Leaf sums of the long columns: the heavy leaves (plan_xc heavy tasks, up to
 // 4 leaves each) into hpart[slot][TP], and the blocked slices (XtDense tasks,
 // one <= 256-entry leaf each) into xpart[slot][TP].
-__global__ void __launch_bounds__(256) kb_cols_leaves(SegPlan pl, XtDense dn,
+__global__ void __launch_bounds__(256, 2) kb_cols_leaves(SegPlan pl, XtDense dn,
                                                       const double* __restrict__ src,
                                                       double* __restrict__ hpart,
                                                       double* __restrict__ xpart, long long n_hleaf,
@@ -295,26 +324,43 @@ __global__ void __launch_bounds__(256) kb_cols_leaves(SegPlan pl, XtDense dn,
     if (lf * LEAF >= tk.z) return;
     const int h = tk.w;
     const int slot = __ldg(pl.heavy_seg0 + h) + (tk.y - __ldg(pl.heavy_start + h)) / LEAF + lf;
-    const double v = emu_segment(pl.ind, tk.y + lf * LEAF, min(LEAF, tk.z - lf * LEAF), src, tp,
-                                 t, lane, [](int, double x) { return x; });
+    const double v = emu_gather_leaf(pl.ind, tk.y + lf * LEAF, min(LEAF, tk.z - lf * LEAF), src,
+                                     tp, t, lane, [](int, double x) { return x; });
     hpart[(long long)slot * tp + t] = v;
   } else {
     const int4 tk = __ldg(dn.tasks + (u - n_hleaf));
-    const double v = emu_segment(dn.rows, tk.y, tk.z, src, tp, t, lane,
-                                 [](int, double x) { return x; });
+    const double v = emu_gather_leaf(dn.rows, tk.y, tk.z, src, tp, t, lane,
+                                     [](int, double x) { return x; });
     xpart[(long long)tk.x * tp + t] = v;
   }
 }
 
-// R256 over m partials part[k][TP] (k = 0..m-1) for this lane's task, as
-// block_reduce_partials does for one task: m <= 256 one leaf; otherwise
-// leaves of 256 partials, then a leaf over their sums.  One warp.
-__device__ __forceinline__ double emu_partials(const double* __restrict__ part, long long m,
-                                               int tp, int t) {
-  auto leaf = [&](long long k0, int len) {
-    return emu_leaf(len, [&](int base, int l) { return part[(k0 + base + l) * tp + t]; });
-  };
-  if (m <= LEAF) return leaf(0, (int)m);
+// Canonical leaf over len <= 256 consecutive task-minor partials.
+__device__ __forceinline__ double emu_part_leaf(const double* __restrict__ part, long long k0,
+                                                int len, int tp, int t) {
+  double A[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) A[l] = 0.0;
+  for (int base = 0; base < len; base += 32) {
+#pragma unroll
+    for (int sub = 0; sub < 4; ++sub) {
+      if (base + sub * 8 >= len) break;
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int e = base + sub * 8 + j;
+        v[j] = e < len ? part[(k0 + e) * tp + t] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (base + sub * 8 + j < len) A[sub * 8 + j] = A[sub * 8 + j] + v[j];
+    }
+  }
+  return tree32(A);
+}
+
+__device__ __noinline__ double emu_part_long(const double* __restrict__ part, long long m, int tp,
+                                             int t) {
   const int m2 = (int)((m + LEAF - 1) / LEAF);
   double P[32];
 #pragma unroll
@@ -322,7 +368,7 @@ __device__ __forceinline__ double emu_partials(const double* __restrict__ part, 
   for (int gb = 0; gb < m2; gb += 32) {
     for (int l = 0; l < 32 && gb + l < m2; ++l) {
       const long long k0 = (long long)(gb + l) * LEAF;
-      const double v = leaf(k0, (int)min((long long)LEAF, m - k0));
+      const double v = emu_part_leaf(part, k0, (int)min((long long)LEAF, m - k0), tp, t);
 #pragma unroll
       for (int q = 0; q < 32; ++q)
         if (q == l) P[q] = P[q] + v;
@@ -331,9 +377,57 @@ __device__ __forceinline__ double emu_partials(const double* __restrict__ part, 
   return tree32(P);
 }
 
+// R256 over m partials part[k][TP] (k = 0..m-1) for this lane's task, as
+// block_reduce_partials does for one task: m <= 256 one leaf; otherwise
+// leaves of 256 partials, then a leaf over their sums.  One warp.
+__device__ __forceinline__ double emu_partials(const double* __restrict__ part, long long m,
+                                               int tp, int t) {
+  if (m <= LEAF) return emu_part_leaf(part, 0, (int)m, tp, t);
+  return emu_part_long(part, m, tp, t);
+}
+
+// Block-level canonical leaves: 8 warps stage the (up to) 256 rows of a leaf
+// in shared memory — warp w takes rows l + 32 w — and warp 0 folds them in
+// canonical order: A[l] = sum over w of row l + 32 w, then tree32.  sm holds
+// 2 x 8 x 32 x 32 doubles (x and y of a dot leaf; y unused for sums).
+constexpr int BLK_SM = 2 * 8 * 32 * 32;
+
+template <bool DOT, typename Load>
+__device__ __forceinline__ double block_leaf(int n, Load load, double* sm) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll 4
+  for (int l = 0; l < 32; ++l) {
+    const int e = l + 32 * w;
+    double x = 0.0, y = 0.0;
+    if (e < n) load(e, x, y);
+    sm[(w * 32 + l) * 32 + lane] = x;
+    if (DOT) sm[8 * 32 * 32 + (w * 32 + l) * 32 + lane] = y;
+  }
+  __syncthreads();
+  double r = 0.0;
+  if (w == 0) {
+    double A[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) A[l] = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      if (32 * k >= n) break;
+#pragma unroll
+      for (int l = 0; l < 32; ++l)
+        if (l + 32 * k < n) {
+          const double x = sm[(k * 32 + l) * 32 + lane];
+          if (DOT) A[l] = fma(x, sm[8 * 32 * 32 + (k * 32 + l) * 32 + lane], A[l]);
+          else A[l] = A[l] + x;
+        }
+    }
+    r = tree32(A);
+  }
+  __syncthreads();
+  return r;
+}
+
 // Combine the long columns: heavy segment h (hn[h] leaf sums from h0[h]) and
 // blocked column b (poff range).  One warp per (column, group).
-__global__ void __launch_bounds__(256) kb_cols_combine(SegPlan pl, XtDense dn,
+__global__ void __launch_bounds__(256, 2) kb_cols_combine(SegPlan pl, XtDense dn,
                                                        const double* __restrict__ hpart,
                                                        const double* __restrict__ xpart,
                                                        long long n_heavy,
@@ -364,45 +458,47 @@ __global__ void __launch_bounds__(256) kb_cols_combine(SegPlan pl, XtDense dn,
 
 // Leaf sums over a contiguous task-minor vector (len rows): kind 0 sum(v),
 // 1 sum over class +1 (off-class 0.0), 2 class -1, 3 fma dot v . v2.
+// One 256-thread block per (leaf, group).
 __global__ void __launch_bounds__(256) kb_vec_leaves(const double* __restrict__ v,
                                                      const double* __restrict__ v2,
                                                      const signed char* __restrict__ lab,
                                                      long long len, int kind,
                                                      double* __restrict__ part, long long n_leaf,
                                                      int G, int tp) {
+  extern __shared__ double sm[];
+  const long long lf = blockIdx.x / G;
+  const int g = (int)(blockIdx.x - lf * G);
   const int lane = threadIdx.x & 31;
-  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= n_leaf * G) return;
-  const long long lf = w / G;
-  const int g = (int)(w - lf * G);
   const int t = g * BG + lane;
   const long long i0 = lf * LEAF;
   const int n = (int)min((long long)LEAF, len - i0);
   double s;
   if (kind == 3) {
-    s = emu_dot_leaf(n, [&](int e, double& x, double& y) {
+    s = block_leaf<true>(n, [&](int e, double& x, double& y) {
       x = v[(i0 + e) * tp + t];
       y = v2[(i0 + e) * tp + t];
-    });
+    }, sm);
   } else {
-    s = emu_leaf(n, [&](int base, int l) {
-      const long long k = (i0 + base + l) * tp + t;
-      const double x = v[k];
-      if (kind == 1) return lab[k] == 1 ? x : 0.0;
-      if (kind == 2) return lab[k] == -1 ? x : 0.0;
-      return x;
-    });
+    s = block_leaf<false>(n, [&](int e, double& x, double&) {
+      const long long k = (i0 + e) * tp + t;
+      const double u = v[k];
+      x = kind == 1 ? (lab[k] == 1 ? u : 0.0) : (kind == 2 ? (lab[k] == -1 ? u : 0.0) : u);
+    }, sm);
   }
-  part[lf * tp + t] = s;
+  if (threadIdx.x < 32) part[lf * tp + t] = s;
 }
 
-// R256 over n_leaf partials per task -> out[t].  One warp per group.
-__global__ void kb_combine(const double* __restrict__ part, long long n_leaf, double* __restrict__ out,
-                           int tp) {
+// Canonical leaf over n <= 256 task-minor partials -> out[t]; one 256-thread
+// block per group (the last level of every R256 reduction).  Longer partial
+// lists first go through kb_vec_leaves (kind 0), which folds each run of 256
+// partials exactly as the first level of R256 does.
+__global__ void __launch_bounds__(256) kb_combine_leaf(const double* __restrict__ part, int n,
+                                                       double* __restrict__ out, int tp) {
+  extern __shared__ double sm[];
   const int lane = threadIdx.x & 31;
-  const int g = blockIdx.x;
-  const int t = g * BG + lane;
-  out[t] = emu_partials(part, n_leaf, tp, t);
+  const int t = blockIdx.x * BG + lane;
+  const double s = block_leaf<false>(n, [&](int e, double& x, double&) { x = part[(long long)e * tp + t]; }, sm);
+  if (threadIdx.x < 32) out[t] = s;
 }
 
 // apply_w: class-mean broadcast; the class sums arrive in out1 / out2.
@@ -424,20 +520,22 @@ __global__ void kb_apply_w(const signed char* __restrict__ lab, double* __restri
   }
 }
 
-// r = p = b; P_s = b, sols_s = 0 (krylov.py:199-208).
+// r = p = b; P_s = b, sols_s = 0 (krylov.py:199-208); one thread per
+// (row, task, shift) element.
 __global__ void kb_cg_init_vec(const double* __restrict__ b, double* __restrict__ r,
                                double* __restrict__ p, double* __restrict__ bigp,
                                double* __restrict__ sols, long long d, int tp, int ns) {
-  const long long total = d * tp;
-  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
-       k += (long long)gridDim.x * blockDim.x) {
+  const long long total = d * tp * ns;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long k = e / ns;
     const double v = b[k];
-    r[k] = v;
-    p[k] = v;
-    for (int s = 0; s < ns; ++s) {
-      bigp[k * ns + s] = v;
-      sols[k * ns + s] = 0.0;
+    if (e - k * ns == 0) {
+      r[k] = v;
+      p[k] = v;
     }
+    bigp[e] = v;
+    sols[e] = 0.0;
   }
 }
 
@@ -463,30 +561,31 @@ __global__ void kb_cg_init_scalars(BatchState B, const double* __restrict__ bb, 
 
 // ---------------------------------------------------------------- CG step
 
-// A: centring q -= mu * sum(z) and the p.q leaves (fma).
+// A: centring q -= mu * sum(z) and the p.q leaves (fma); one 256-thread
+// block per (leaf, group).
 __global__ void __launch_bounds__(256) kb_step_a(double* __restrict__ q,
                                                  const double* __restrict__ p,
                                                  const double* __restrict__ mu, long long d,
                                                  double* __restrict__ part, long long n_leaf,
                                                  int G, BatchState B) {
+  extern __shared__ double sm[];
+  const long long lf = blockIdx.x / G;
+  const int g = (int)(blockIdx.x - lf * G);
   const int lane = threadIdx.x & 31;
-  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= n_leaf * G) return;
-  const long long lf = w / G;
-  const int g = (int)(w - lf * G);
   const int tp = B.tp, t = g * BG + lane;
-  if (!b_live(B, t)) return;
+  if (!__any_sync(FULL, b_live(B, t))) return;  // uniform per block (same group)
+  const bool live = b_live(B, t);
   const long long i0 = lf * LEAF;
   const int n = (int)min((long long)LEAF, d - i0);
   const double sz = B.sum_v[t];
-  const double s = emu_dot_leaf(n, [&](int e, double& x, double& y) {
+  const double s = block_leaf<true>(n, [&](int e, double& x, double& y) {
     const long long k = (i0 + e) * tp + t;
     const double qc = q[k] - mu[k] * sz;
-    q[k] = qc;
+    if (live) q[k] = qc;
     x = p[k];
     y = qc;
-  });
-  part[lf * tp + t] = s;
+  }, sm);
+  if (threadIdx.x < 32 && live) part[lf * tp + t] = s;
 }
 
 // Scalars after p.q (phase B of k_cg_step): gamma and zeta_next / gamma_s.
@@ -522,30 +621,30 @@ __global__ void kb_scalars_b(BatchState B) {
   }
 }
 
-// B: r_next = r + gamma q and the r.r leaves.
+// B: r_next = r + gamma q and the r.r leaves; one block per (leaf, group).
 __global__ void __launch_bounds__(256) kb_step_b(const double* __restrict__ q,
                                                  const double* __restrict__ r_cur,
                                                  double* __restrict__ r_next, long long d,
                                                  double* __restrict__ part, long long n_leaf,
                                                  int G, BatchState B) {
+  extern __shared__ double sm[];
+  const long long lf = blockIdx.x / G;
+  const int g = (int)(blockIdx.x - lf * G);
   const int lane = threadIdx.x & 31;
-  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= n_leaf * G) return;
-  const long long lf = w / G;
-  const int g = (int)(w - lf * G);
   const int tp = B.tp, t = g * BG + lane;
-  if (!b_live(B, t)) return;
+  if (!__any_sync(FULL, b_live(B, t))) return;
+  const bool live = b_live(B, t);
   const long long i0 = lf * LEAF;
   const int n = (int)min((long long)LEAF, d - i0);
   const double gamma = B.gamma[t];
-  const double s = emu_dot_leaf(n, [&](int e, double& x, double& y) {
+  const double s = block_leaf<true>(n, [&](int e, double& x, double& y) {
     const long long k = (i0 + e) * tp + t;
     const double rn = r_cur[k] + gamma * q[k];
-    r_next[k] = rn;
+    if (live) r_next[k] = rn;
     x = rn;
     y = rn;
-  });
-  part[lf * tp + t] = s;
+  }, sm);
+  if (threadIdx.x < 32 && live) part[lf * tp + t] = s;
 }
 
 // Scalars after r.r (phase C of k_cg_step, block 0's bookkeeping).
@@ -604,27 +703,27 @@ __global__ void kb_scalars_c(BatchState B) {
 }
 
 // C: p = r_next + alpha_new p, then the shift updates of this iteration
-// (krylov.py:230, 238-241) for every (row, task, shift).
+// (krylov.py:230, 238-241), one thread per (row, task, shift) element so the
+// shift-state streams are coalesced.
 __global__ void kb_step_c(const double* __restrict__ r_next, double* __restrict__ p,
                           double* __restrict__ bigp, double* __restrict__ sols, long long d,
                           BatchState B, const int* __restrict__ stepped) {
   const int tp = B.tp, ns = B.ns;
-  const long long total = d * tp;
-  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
-       k += (long long)gridDim.x * blockDim.x) {
+  const long long total = d * tp * ns;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long k = e / ns;
+    const int s = (int)(e - k * ns);
     const int t = (int)(k % tp);
     if (!stepped[t]) continue;
     const double rn = r_next[k];
-    p[k] = rn + B.alpha_new[t] * p[k];
-    for (int s = 0; s < ns; ++s) {
-      const int ks = t * ns + s;
-      const int mode = B.upd_mode[ks];
-      if (mode == 0) continue;
-      const long long e = k * ns + s;
-      const double pv = bigp[e];
-      sols[e] = sols[e] - pv * B.upd_gs[ks];
-      if (mode == 3) bigp[e] = B.upd_zn[ks] * rn + B.upd_as[ks] * pv;
-    }
+    if (s == 0) p[k] = rn + B.alpha_new[t] * p[k];
+    const int ks = t * ns + s;
+    const int mode = B.upd_mode[ks];
+    if (mode == 0) continue;
+    const double pv = bigp[e];
+    sols[e] = sols[e] - pv * B.upd_gs[ks];
+    if (mode == 3) bigp[e] = B.upd_zn[ks] * rn + B.upd_as[ks] * pv;
   }
 }
 

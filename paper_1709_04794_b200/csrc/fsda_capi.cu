@@ -151,7 +151,7 @@ struct HostPlan {
 struct BatchBufs {
   DevBuf<signed char> lab;
   DevBuf<double> ind, P, Q, R0, R1, MU, Bv, PR, Y, Z, BIGP, SOLS, SCORES, OUT;
-  DevBuf<double> partD, partN, hpart, xpart, opart, scal;
+  DevBuf<double> partD, partN, part2, hpart, xpart, opart, scal;
   DevBuf<long long> lscal;
   DevBuf<int> iscal;
   DevBuf<double> sh_d;
@@ -165,6 +165,7 @@ struct BatchBufs {
     MU.release(); Bv.release(); PR.release(); Y.release(); Z.release(); BIGP.release();
     SOLS.release(); SCORES.release(); OUT.release(); partD.release(); partN.release();
     hpart.release(); xpart.release(); opart.release(); scal.release(); lscal.release();
+    part2.release();
     iscal.release(); sh_d.release(); sh_l.release(); sh_u.release(); sh_i.release();
     betas.release(); raw.release();
   }
@@ -2001,24 +2002,31 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   if (c->row_base != 0 || c->n_global != c->n)
     return fail(FSDA_EINVAL, "fsda_solve_batch: needs the whole Laplacian (not a row shard)");
   const long long n = c->n, d = c->d;
-  // a segment of more than 65536 entries would need a third tree level
+  Trace tr;
   const int G = (T + BG - 1) / BG, tp = G * BG;
   std::vector<double> ell(tp, 1.0), n1v(tp, 1.0), n2v(tp, 1.0);
+  std::vector<int> bad(T, 0);
+#pragma omp parallel for schedule(static)
   for (int t = 0; t < T; ++t) {
     long long a = 0, b = 0;
+    int other = 0;
     const int8_t* l = labels + (long long)t * n;
     for (long long i = 0; i < n; ++i) {
-      if (l[i] != 0 && l[i] != 1 && l[i] != -1)
-        return fail(FSDA_ELABEL, "task %d: labels must take values in {+1, -1, 0}", t);
+      other |= (l[i] != 0 && l[i] != 1 && l[i] != -1);
       a += l[i] == 1;
       b += l[i] == -1;
     }
-    if (a + b == 0) return fail(FSDA_ELABEL, "task %d: centering requires at least one labeled sample", t);
-    if (a == 0 || b == 0) return fail(FSDA_EINVAL, "task %d: both classes need at least one labeled sample", t);
+    bad[t] = other ? 1 : (a + b == 0 ? 2 : ((a == 0 || b == 0) ? 3 : 0));
     ell[t] = (double)(a + b);
     n1v[t] = (double)a;
     n2v[t] = (double)b;
   }
+  for (int t = 0; t < T; ++t) {
+    if (bad[t] == 1) return fail(FSDA_ELABEL, "task %d: labels must take values in {+1, -1, 0}", t);
+    if (bad[t] == 2) return fail(FSDA_ELABEL, "task %d: centering requires at least one labeled sample", t);
+    if (bad[t] == 3) return fail(FSDA_EINVAL, "task %d: both classes need at least one labeled sample", t);
+  }
+  tr.mark("batch: validate labels");
   BatchBufs& bb = c->batch;
   cudaStream_t st = c->stream;
   const long long nlN = n_leaves(n), nlD = n_leaves(d);
@@ -2034,6 +2042,7 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   bb.OUT.ensure(std::max(1LL, (long long)T * ns * d));
   bb.partD.ensure(std::max(1LL, nlD * ND));
   bb.partN.ensure(std::max(1LL, nlN * ND));
+  bb.part2.ensure(std::max(1LL, cdiv(std::max(nlN, nlD), LEAF) * ND));
   bb.hpart.ensure(std::max(1LL, c->plan_xc.n_heavy_leaves * ND));
   bb.xpart.ensure(std::max(1LL, c->xh_nslots * ND));
   bb.opart.ensure(std::max(1LL, nlN * ND * ns));
@@ -2085,6 +2094,10 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   const int tb = (int)cdiv(ND, 128);
   kb_reset<<<tb, 128, 0, st>>>(B, T, tol);
   CKL();
+  if (tr.on) {
+    CK(cudaStreamSynchronize(st));
+    tr.mark("batch: alloc + inputs h2d");
+  }
   if (c->xh_nslots) CK(cudaMemsetAsync(bb.xpart.ptr, 0, sizeof(double) * c->xh_nslots * ND, st));
 
   auto grid_w = [](long long warps) { return (unsigned)std::max<long long>(1, cdiv(warps, 8)); };
@@ -2121,6 +2134,30 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
       CKL();
     }
   };
+  static bool attrs_set = false;
+  if (!attrs_set) {
+    const int big = (int)(sizeof(double) * BLK_SM);
+    CK(cudaFuncSetAttribute(kb_vec_leaves, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(kb_step_a, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(kb_step_b, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(kb_combine_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, big / 2));
+    attrs_set = true;
+  }
+  const size_t sm_dot = sizeof(double) * BLK_SM, sm_sum = sm_dot / 2;
+  auto combine = [&](const double* part, long long nl, double* out) {
+    // R256 over nl <= 65536 partials: level 1 (runs of 256) by kb_vec_leaves,
+    // the last level by kb_combine_leaf
+    if (nl > LEAF) {
+      const long long m2 = cdiv(nl, LEAF);
+      kb_vec_leaves<<<(unsigned)(m2 * G), 256, sm_sum, st>>>(part, nullptr, nullptr, nl, 0,
+                                                             bb.part2.ptr, m2, G, tp);
+      CKL();
+      part = bb.part2.ptr;
+      nl = m2;
+    }
+    kb_combine_leaf<<<G, 256, sm_sum, st>>>(part, (int)nl, out, tp);
+    CKL();
+  };
   auto vec_sum = [&](const double* v, const double* v2, int kind, long long len, double* part,
                      double* out) {
     const long long nl = n_leaves(len);
@@ -2128,10 +2165,10 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
       CK(cudaMemsetAsync(out, 0, sizeof(double) * ND, st));
       return;
     }
-    kb_vec_leaves<<<grid_w(nl * G), 256, 0, st>>>(v, v2, bb.lab.ptr, len, kind, part, nl, G, tp);
+    kb_vec_leaves<<<(unsigned)(nl * G), 256, kind == 3 ? sm_dot : sm_sum, st>>>(
+        v, v2, bb.lab.ptr, len, kind, part, nl, G, tp);
     CKL();
-    kb_combine<<<G, 32, 0, st>>>(part, nl, out, tp);
-    CKL();
+    combine(part, nl, out);
   };
 
   // ---- setup (sda.py:297-301, krylov.py:185-208), per task
@@ -2146,15 +2183,19 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   CKL();
   vec_sum(bb.Z.ptr, nullptr, 0, n, bb.partN.ptr, B.sum_v);   // sum(w)
   xt(bb.Z.ptr, bb.Bv.ptr, 1);                                // b = X^T w - mu sum(w)
-  kb_cg_init_vec<<<(unsigned)std::min<long long>(cdiv(d * ND, 256), 65535LL * 4), 256, 0, st>>>(
+  kb_cg_init_vec<<<(unsigned)std::min<long long>(cdiv(d * ND * ns, 256), (long long)c->num_sms * 16), 256, 0, st>>>(
       bb.Bv.ptr, bb.R0.ptr, bb.P.ptr, bb.BIGP.ptr, bb.SOLS.ptr, d, tp, ns);
   CKL();
   vec_sum(bb.Bv.ptr, bb.Bv.ptr, 3, d, bb.partD.ptr, B.pq);   // b.b
   kb_cg_init_scalars<<<tb, 128, 0, st>>>(B, B.pq, tol);
   CKL();
+  if (tr.on) {
+    CK(cudaStreamSynchronize(st));
+    tr.mark("batch: setup");
+  }
 
   // ---- the shifted-CG loop (krylov.py:210-270), all live tasks in step
-  const unsigned ew = (unsigned)std::min<long long>(cdiv(d * ND, 256), (long long)c->num_sms * 8);
+  const unsigned ew = (unsigned)std::min<long long>(cdiv(d * ND * ns, 256), (long long)c->num_sms * 16);
   for (long long it = 0; it < max_iter; ++it) {
     double* r_cur = (it & 1) ? bb.R1.ptr : bb.R0.ptr;
     double* r_nxt = (it & 1) ? bb.R0.ptr : bb.R1.ptr;
@@ -2163,20 +2204,20 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
     xt(bb.Z.ptr, bb.Q.ptr, 0);                                 // K3  q = X^T z
     vec_sum(bb.Z.ptr, nullptr, 0, n, bb.partN.ptr, B.sum_v);   //     sum(z)
     if (nlD) {
-      kb_step_a<<<grid_w(nlD * G), 256, 0, st>>>(bb.Q.ptr, bb.P.ptr, bb.MU.ptr, d, bb.partD.ptr, nlD, G, B);
+      kb_step_a<<<(unsigned)(nlD * G), 256, sm_dot, st>>>(bb.Q.ptr, bb.P.ptr, bb.MU.ptr, d, bb.partD.ptr,
+                                                          nlD, G, B);
       CKL();
-      kb_combine<<<G, 32, 0, st>>>(bb.partD.ptr, nlD, B.pq, tp);
-      CKL();
+      combine(bb.partD.ptr, nlD, B.pq);
     } else {
       CK(cudaMemsetAsync(B.pq, 0, sizeof(double) * ND, st));
     }
     kb_scalars_b<<<tb, 128, 0, st>>>(B);
     CKL();
     if (nlD) {
-      kb_step_b<<<grid_w(nlD * G), 256, 0, st>>>(bb.Q.ptr, r_cur, r_nxt, d, bb.partD.ptr, nlD, G, B);
+      kb_step_b<<<(unsigned)(nlD * G), 256, sm_dot, st>>>(bb.Q.ptr, r_cur, r_nxt, d, bb.partD.ptr, nlD,
+                                                          G, B);
       CKL();
-      kb_combine<<<G, 32, 0, st>>>(bb.partD.ptr, nlD, B.rr_new, tp);
-      CKL();
+      combine(bb.partD.ptr, nlD, B.rr_new);
     } else {
       CK(cudaMemsetAsync(B.rr_new, 0, sizeof(double) * ND, st));
     }
@@ -2195,6 +2236,7 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
     if (h_live == 0) break;
   }
 
+  if (tr.on) tr.mark("batch: iterations");
   // ---- tail: residuals, projections, orientation (sda.py:265-284)
   kb_finish<<<tb, 128, 0, st>>>(B);
   CKL();
@@ -2219,6 +2261,10 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
         bb.SOLS.ptr, bb.OUT.ptr, d, T, tp, ns);
     CKL();
   }
+  if (tr.on) {
+    CK(cudaStreamSynchronize(st));
+    tr.mark("batch: projections + orientation");
+  }
   // ---- results
   const long long TS = (long long)T * ns;
   if (directions && d > 0)
@@ -2239,6 +2285,7 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
     if (iterations) iterations[k] = its[k];
     if (converged) converged[k] = cv[k];
   }
+  tr.mark("batch: results d2h");
   for (int t = 0; t < T; ++t) {
     if (n_applies) n_applies[t] = itr[t];
     if (fail_iter) fail_iter[t] = fit[t];

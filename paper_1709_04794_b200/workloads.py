@@ -33,6 +33,11 @@ CONFIGS = {
                  n_shifts=20, beta_lo=1e-5, beta_hi=1e3, max_iter=100),
     "cfg3": dict(n=1_500_000, d=500_000, lam=50.0, s=1.05, k=10, ell=30_000, n_pos=3_000,
                  n_shifts=30, beta_lo=1e-6, beta_hi=1e3, max_iter=150),
+    # cfg4: the cfg3 matrix and graph shared by 64 binary tasks, each labeling a
+    # random 1% of rows with 10% positives; 20 shifts per task
+    "cfg4": dict(n=1_500_000, d=500_000, lam=50.0, s=1.05, k=10, ell=30_000, n_pos=3_000,
+                 n_shifts=20, beta_lo=1e-6, beta_hi=1e3, max_iter=150, tasks=64,
+                 task_frac=0.01, task_pos=0.10),
 }
 
 ALPHA = 0.5      # reference default, config.py:36
@@ -182,6 +187,20 @@ def make_workload(name: str = "cfg2", *, max_iter: int | None = None, seed: int 
         max_iter=int(cfg["max_iter"] if max_iter is None else max_iter),
         meta={k: v for k, v in cfg.items()},
     )
+
+
+def task_masks(n: int, n_tasks: int, frac: float, pos_frac: float, seed: int) -> np.ndarray:
+    """n_tasks x n label masks (cfg4): each task labels a random frac of the
+    rows, pos_frac of them positive, the rest negative; any row order."""
+    rng = np.random.default_rng(seed)
+    n_lab = max(2, int(round(frac * n)))
+    n_pos = min(n_lab - 1, max(1, int(round(pos_frac * n_lab))))
+    out = np.zeros((n_tasks, n), dtype=np.int8)
+    for t in range(n_tasks):
+        idx = rng.choice(n, size=n_lab, replace=False)
+        out[t, idx] = -1
+        out[t, idx[:n_pos]] = 1
+    return out
 
 
 def workload_digest(w: Workload) -> str:

@@ -21,6 +21,9 @@
 namespace fsda {
 
 constexpr int BG = 32;  // tasks per group (one per lane)
+#ifndef GATHER_MLP
+#define GATHER_MLP 8        // row gathers in flight per lane (16: same speed, spills)
+#endif
 
 // Per-task scalars (index t) and per-(task, shift) state (index t * ns + s).
 struct BatchState {
@@ -129,18 +132,18 @@ __device__ __forceinline__ double emu_gather_leaf(const int* __restrict__ ind, l
   for (int base = 0; base < len; base += 32) {
     const int my = (base + lane < len) ? __ldg(ind + s0 + base + lane) : 0;
 #pragma unroll
-    for (int sub = 0; sub < 4; ++sub) {
-      if (base + sub * 8 >= len) break;
-      double v[8];
+    for (int sub = 0; sub < 32 / GATHER_MLP; ++sub) {
+      if (base + sub * GATHER_MLP >= len) break;
+      double v[GATHER_MLP];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int l = sub * 8 + j;
+      for (int j = 0; j < GATHER_MLP; ++j) {
+        const int l = sub * GATHER_MLP + j;
         const int idx = __shfl_sync(FULL, my, l);
         v[j] = (base + l < len) ? term(idx, __ldg(src + (long long)idx * tp + t)) : 0.0;
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (base + sub * 8 + j < len) A[sub * 8 + j] = A[sub * 8 + j] + v[j];
+      for (int j = 0; j < GATHER_MLP; ++j)
+        if (base + sub * GATHER_MLP + j < len) A[sub * GATHER_MLP + j] = A[sub * GATHER_MLP + j] + v[j];
     }
   }
   return tree32(A);

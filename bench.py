@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--concurrency", type=int, default=4)
+    ap.add_argument("--batch-tasks", type=int, default=32,
+                    help="tasks of the multi-task batch measurement (0: skip)")
     return ap.parse_args()
 
 
@@ -330,8 +332,8 @@ def run_b200(args):
                                     "GBps": round(k["bytes"] / max(k["ms"], 1e-9) / 1e6, 1)}
                         for k in kernels},
         }
-        pair = [k for k in kernels if k["name"] in ("spmv_rows", "xt_light", "xt_heavy")]
-        pb = sum(k["bytes"] for k in pair if k["name"] != "xt_heavy")
+        pair = [k for k in kernels if k["name"] in ("spmv_rows", "xt")]   # K1 + K3
+        pb = sum(k["bytes"] for k in pair)
         pt = sum(k["ms"] for k in pair)
         spmv_pair = {"GBps": pb / (pt * 1e-3) / 1e9, "frac_of_hbm_peak": pb / (pt * 1e-3) / 1e9 / peak,
                      "bytes": pb, "ms": pt}
@@ -381,6 +383,31 @@ def run_b200(args):
                       "note": "independent label draws on the same X/L, one context and stream each; "
                               "L2 not flushed between solves"}
         del devs
+
+    # multi-task batch (cfg4 / SURVEY §8f #1) on the same X and graph: T label
+    # masks of the bench workload's density solved in one pass per operator
+    # product (fsda_solve_batch); each task is bit-identical to its single
+    # solve (tests/test_gpu_batch.py).  Host-timed: masks + probes uploaded,
+    # directions read back, scores left on the device.
+    batch = None
+    if rank == 0 and args.batch_tasks > 0:
+        from paper_1709_04794_b200.workloads import task_masks
+
+        T = args.batch_tasks
+        frac = w.meta["ell"] / w.n
+        masks = task_masks(w.n, T, frac, w.meta["n_pos"] / w.meta["ell"], seed=91)
+        probes = np.stack([np.random.default_rng(1000 + t).uniform(-1, 1, w.d) for t in range(T)])
+        dev.solve_batch(masks, w.alpha, w.betas, w.tol, 1, probes, scores=False)   # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        bres = dev.solve_batch(masks, w.alpha, w.betas, w.tol, w.max_iter, probes, scores=False)
+        t_b = time.perf_counter() - t0
+        batch = {"tasks": T, "task_solves_per_s": T / t_b, "seconds": t_b,
+                 "vs_single_solves_per_s": (T / t_b) / value,
+                 "n_applies": [min(r.n_applies for r in bres), max(r.n_applies for r in bres)],
+                 "labels": f"each task a random {frac:.0%} of rows, {w.meta['n_pos'] / w.meta['ell']:.0%} positive",
+                 "note": "host-timed fsda_solve_batch: masks + probes H2D, directions D2H"}
+        del bres
 
     # regression-phase shifted solve on the same X: the
     # system of the paper's only published timing (12
@@ -434,6 +461,7 @@ def run_b200(args):
             "spmv_pair": spmv_pair,
             "regression_phase": regression,
             "concurrent": concurrent,
+            "batch": batch,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
         }

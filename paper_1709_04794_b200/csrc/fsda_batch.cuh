@@ -119,34 +119,51 @@ __device__ __forceinline__ double emu_dot_leaf(int n, XY xy) {
 
 // Canonical leaf of a gathered index segment: ind[s0, s0 + len) (len <= 256)
 // selects rows of src (task-minor); term(idx, v) maps the gathered value.
-// Indices arrive 32 at a time (one coalesced load, then shuffles); values are
-// gathered 8 at a time so at most 8 loads per lane are in flight next to the
-// 32 accumulators (register budget: two 256-thread CTAs per SM).
+// The canonical lane accumulators A[l] = sum_k v[l + 32 k] are built in pairs
+// (l, l + 16) and folded at once into B[l] = A[l] + A[l + 16] — the first
+// butterfly step — so only 16 partial sums stay live (register budget: three
+// 256-thread CTAs per SM).  Indices arrive 32 at a time (coalesced) and are
+// shuffled to every lane; GATHER_MLP values per lane are in flight.
 template <typename Term>
 __device__ __forceinline__ double emu_gather_leaf(const int* __restrict__ ind, long long s0, int len,
                                                   const double* __restrict__ src, int tp, int t,
                                                   int lane, Term term) {
-  double A[32];
+  constexpr int LS = GATHER_MLP / 2;  // lane pairs per step
+  const int nk = (len + 31) >> 5;     // <= 8 index chunks
+  int my[8];
 #pragma unroll
-  for (int l = 0; l < 32; ++l) A[l] = 0.0;
-  for (int base = 0; base < len; base += 32) {
-    const int my = (base + lane < len) ? __ldg(ind + s0 + base + lane) : 0;
+  for (int k = 0; k < 8; ++k) my[k] = (k < nk && 32 * k + lane < len) ? __ldg(ind + s0 + 32 * k + lane) : 0;
+  double B[16];
 #pragma unroll
-    for (int sub = 0; sub < 32 / GATHER_MLP; ++sub) {
-      if (base + sub * GATHER_MLP >= len) break;
-      double v[GATHER_MLP];
+  for (int l0 = 0; l0 < 16; l0 += LS) {
+    double a1[LS], a2[LS];
 #pragma unroll
-      for (int j = 0; j < GATHER_MLP; ++j) {
-        const int l = sub * GATHER_MLP + j;
-        const int idx = __shfl_sync(FULL, my, l);
-        v[j] = (base + l < len) ? term(idx, __ldg(src + (long long)idx * tp + t)) : 0.0;
+    for (int q = 0; q < LS; ++q) a1[q] = a2[q] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k >= nk) break;
+      double v1[LS], v2[LS];
+#pragma unroll
+      for (int q = 0; q < LS; ++q) {
+        const int l = l0 + q;
+        const int i1 = __shfl_sync(FULL, my[k], l), i2 = __shfl_sync(FULL, my[k], l + 16);
+        v1[q] = (32 * k + l < len) ? term(i1, __ldg(src + (long long)i1 * tp + t)) : 0.0;
+        v2[q] = (32 * k + l + 16 < len) ? term(i2, __ldg(src + (long long)i2 * tp + t)) : 0.0;
       }
 #pragma unroll
-      for (int j = 0; j < GATHER_MLP; ++j)
-        if (base + sub * GATHER_MLP + j < len) A[sub * GATHER_MLP + j] = A[sub * GATHER_MLP + j] + v[j];
+      for (int q = 0; q < LS; ++q) {
+        if (32 * k + l0 + q < len) a1[q] = a1[q] + v1[q];
+        if (32 * k + l0 + q + 16 < len) a2[q] = a2[q] + v2[q];
+      }
     }
+#pragma unroll
+    for (int q = 0; q < LS; ++q) B[l0 + q] = a1[q] + a2[q];
   }
-  return tree32(A);
+#pragma unroll
+  for (int off = 8; off >= 1; off >>= 1)
+#pragma unroll
+    for (int l = 0; l < off; ++l) B[l] = B[l] + B[l + off];
+  return B[0];
 }
 
 // Segments longer than 256 entries: R256 over their leaves (two levels,
@@ -242,7 +259,7 @@ __global__ void kb_reset(BatchState B, int T, double tol) {
 // Row sums over a CSR pattern for every task: K1 (y = X p) and K2 (z = M y).
 // One warp per (row, task group).
 template <int KIND>
-__global__ void __launch_bounds__(256, 2) kb_rows(const int* __restrict__ rowptr,
+__global__ void __launch_bounds__(256, 4) kb_rows(const int* __restrict__ rowptr,
                                                const int* __restrict__ cols,
                                                const double* __restrict__ src,
                                                double* __restrict__ out, long long n_rows, int G,
@@ -289,7 +306,7 @@ __device__ __forceinline__ double b_col_finish(double s, int mode, long long c, 
 
 // X^T columns with n <= 256: the class tasks of the single-task column plan
 // (any class: each entry is one column segment).  One warp per (entry, group).
-__global__ void __launch_bounds__(256, 2) kb_cols_light(SegPlan pl, const double* __restrict__ src,
+__global__ void __launch_bounds__(256, 4) kb_cols_light(SegPlan pl, const double* __restrict__ src,
                                                      double* __restrict__ out, int G, int tp,
                                                      int mode, const double* __restrict__ mu,
                                                      BatchState B) {
@@ -308,7 +325,7 @@ __global__ void __launch_bounds__(256, 2) kb_cols_light(SegPlan pl, const double
 // Leaf sums of the long columns: the heavy leaves (plan_xc heavy tasks, up to
 // 4 leaves each) into hpart[slot][TP], and the blocked slices (XtDense tasks,
 // one <= 256-entry leaf each) into xpart[slot][TP].
-__global__ void __launch_bounds__(256, 2) kb_cols_leaves(SegPlan pl, XtDense dn,
+__global__ void __launch_bounds__(256, 4) kb_cols_leaves(SegPlan pl, XtDense dn,
                                                       const double* __restrict__ src,
                                                       double* __restrict__ hpart,
                                                       double* __restrict__ xpart, long long n_hleaf,
@@ -523,22 +540,25 @@ __global__ void kb_apply_w(const signed char* __restrict__ lab, double* __restri
   }
 }
 
-// r = p = b; P_s = b, sols_s = 0 (krylov.py:199-208); one thread per
-// (row, task, shift) element.
+// r = p = b; P_s = b, sols_s = 0 (krylov.py:199-208); thread j of a block
+// owns (task, shift) j and walks the rows, as kb_step_c.
 __global__ void kb_cg_init_vec(const double* __restrict__ b, double* __restrict__ r,
                                double* __restrict__ p, double* __restrict__ bigp,
                                double* __restrict__ sols, long long d, int tp, int ns) {
-  const long long total = d * tp * ns;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long k = e / ns;
-    const double v = b[k];
-    if (e - k * ns == 0) {
-      r[k] = v;
-      p[k] = v;
+  const int tsn = tp * ns;
+  for (int j = threadIdx.x; j < tsn; j += blockDim.x) {
+    const int t = j / ns, s = j - t * ns;
+    for (long long i = blockIdx.x; i < d; i += gridDim.x) {
+      const long long k = i * tp + t;
+      const double v = b[k];
+      if (s == 0) {
+        r[k] = v;
+        p[k] = v;
+      }
+      const long long e = i * tsn + j;
+      bigp[e] = v;
+      sols[e] = 0.0;
     }
-    bigp[e] = v;
-    sols[e] = 0.0;
   }
 }
 
@@ -706,27 +726,30 @@ __global__ void kb_scalars_c(BatchState B) {
 }
 
 // C: p = r_next + alpha_new p, then the shift updates of this iteration
-// (krylov.py:230, 238-241), one thread per (row, task, shift) element so the
-// shift-state streams are coalesced.
+// (krylov.py:230, 238-241).  Thread j of a block owns one (task, shift) pair
+// (t = j / ns, s = j % ns: its scalars stay in registers) and walks the rows
+// i = blockIdx.x, +gridDim.x, ...; for a fixed row the block's accesses to
+// the (row, task, shift) shift state are contiguous.
 __global__ void kb_step_c(const double* __restrict__ r_next, double* __restrict__ p,
                           double* __restrict__ bigp, double* __restrict__ sols, long long d,
                           BatchState B, const int* __restrict__ stepped) {
-  const int tp = B.tp, ns = B.ns;
-  const long long total = d * tp * ns;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long k = e / ns;
-    const int s = (int)(e - k * ns);
-    const int t = (int)(k % tp);
+  const int tp = B.tp, ns = B.ns, tsn = tp * ns;
+  for (int j = threadIdx.x; j < tsn; j += blockDim.x) {
+    const int t = j / ns, s = j - t * ns;
     if (!stepped[t]) continue;
-    const double rn = r_next[k];
-    if (s == 0) p[k] = rn + B.alpha_new[t] * p[k];
-    const int ks = t * ns + s;
-    const int mode = B.upd_mode[ks];
-    if (mode == 0) continue;
-    const double pv = bigp[e];
-    sols[e] = sols[e] - pv * B.upd_gs[ks];
-    if (mode == 3) bigp[e] = B.upd_zn[ks] * rn + B.upd_as[ks] * pv;
+    const int mode = B.upd_mode[j];
+    const double an = B.alpha_new[t];
+    const double gs = B.upd_gs[j], zn = B.upd_zn[j], as = B.upd_as[j];
+    for (long long i = blockIdx.x; i < d; i += gridDim.x) {
+      const long long k = i * tp + t;
+      const double rn = r_next[k];
+      if (s == 0) p[k] = rn + an * p[k];
+      if (mode == 0) continue;
+      const long long e = i * tsn + j;
+      const double pv = bigp[e];
+      sols[e] = sols[e] - pv * gs;
+      if (mode == 3) bigp[e] = zn * rn + as * pv;
+    }
   }
 }
 

@@ -2183,7 +2183,11 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   CKL();
   vec_sum(bb.Z.ptr, nullptr, 0, n, bb.partN.ptr, B.sum_v);   // sum(w)
   xt(bb.Z.ptr, bb.Bv.ptr, 1);                                // b = X^T w - mu sum(w)
-  kb_cg_init_vec<<<(unsigned)std::min<long long>(cdiv(d * ND * ns, 256), (long long)c->num_sms * 16), 256, 0, st>>>(
+  // threads per block: the (task, shift) pairs split evenly over <= 1024 threads
+  const long long tsn = ND * ns, passes = cdiv(tsn, 1024);
+  const int sblk = (int)(cdiv(cdiv(tsn, passes), 32) * 32);
+  const unsigned srows = (unsigned)std::max<long long>(1, std::min<long long>(d, (long long)c->num_sms * 8));
+  kb_cg_init_vec<<<srows, sblk, 0, st>>>(
       bb.Bv.ptr, bb.R0.ptr, bb.P.ptr, bb.BIGP.ptr, bb.SOLS.ptr, d, tp, ns);
   CKL();
   vec_sum(bb.Bv.ptr, bb.Bv.ptr, 3, d, bb.partD.ptr, B.pq);   // b.b
@@ -2195,7 +2199,6 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   }
 
   // ---- the shifted-CG loop (krylov.py:210-270), all live tasks in step
-  const unsigned ew = (unsigned)std::min<long long>(cdiv(d * ND * ns, 256), (long long)c->num_sms * 16);
   for (long long it = 0; it < max_iter; ++it) {
     double* r_cur = (it & 1) ? bb.R1.ptr : bb.R0.ptr;
     double* r_nxt = (it & 1) ? bb.R0.ptr : bb.R1.ptr;
@@ -2225,7 +2228,7 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
     CKL();
     kb_mark_stepped<<<tb, 128, 0, st>>>(B, stepped);
     CKL();
-    kb_step_c<<<ew, 256, 0, st>>>(r_nxt, bb.P.ptr, bb.BIGP.ptr, bb.SOLS.ptr, d, B, stepped);
+    kb_step_c<<<srows, sblk, 0, st>>>(r_nxt, bb.P.ptr, bb.BIGP.ptr, bb.SOLS.ptr, d, B, stepped);
     CKL();
     CK(cudaMemsetAsync(n_live, 0, sizeof(int), st));
     kb_end_iteration<<<tb, 128, 0, st>>>(B, stepped, n_live);

@@ -1,4 +1,4 @@
-for lib in libv_lb4_m4.so libv_lb5_m4.so libfsda_b200.so; do
-FSDA_B200_LIB=paper_1709_04794_b200/$lib timeout 900 python tools/bench_batch.py --workload cfg2 --tasks 64 --seq-tasks 1 > gpurun_out/b2_$lib.json 2> gpurun_out/b2_$lib.err
-FSDA_B200_LIB=paper_1709_04794_b200/$lib FSDA_B200_TRACE=1 timeout 1500 python tools/bench_batch.py --workload cfg4 --max-iter 20 --seq-tasks 1 > gpurun_out/b4_$lib.json 2> gpurun_out/b4_$lib.err
-done
+timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_gpu.log
+timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
+timeout 1800 python tools/bench_batch.py --workload cfg4 --seq-tasks 2 > gpurun_out/batch_cfg4_full.json 2> gpurun_out/batch_cfg4_full.err
+timeout 900 python tools/bench_batch.py --workload cfg2 --tasks 64 --seq-tasks 3 > gpurun_out/batch_cfg2_64.json 2> gpurun_out/batch_cfg2_64.err

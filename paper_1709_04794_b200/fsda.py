@@ -492,15 +492,19 @@ def solve_label_sets(x, lap, label_sets, alpha, betas, tol: float = 1e-8, max_it
 
     Returns a list of SweepResult (directions n_shifts x D, scores n_shifts x N
     in the original row order)."""
-    dev = device or default_device()
-    dev.upload_x(x)
-    dev.upload_laplacian(lap)
     grid = T.as_shift_grid(betas)
     sets = [np.asarray(getattr(l, "labels", l), dtype=np.int8) for l in label_sets]
     seed_list = list(seeds) if np.ndim(seeds) else [int(seeds)] * len(sets)
+    if len(seed_list) != len(sets):
+        raise ValueError("one seed per label set")
     for lab in sets:
+        if lab.shape != (int(x.n_rows),):
+            raise ValueError("every label set needs one entry per sample")
         if not (np.any(lab == 1) and np.any(lab == -1)):
             raise ValueError("both classes need at least one labeled sample")
+    dev = device or default_device()
+    dev.upload_x(x)
+    dev.upload_laplacian(lap)
     probes = [np.random.default_rng(seed).uniform(-1.0, 1.0, size=int(x.n_cols)) for seed in seed_list]
     if batched and sets:
         out = dev.solve_batch(np.stack(sets), alpha, grid.betas, tol, max_iter, np.stack(probes),

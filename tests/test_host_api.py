@@ -166,6 +166,29 @@ def test_family_resolution_for_reference_objects():
         sys.path.remove(sdakit_root)
 
 
+def test_label_sets_validated_before_the_device():
+    """solve_label_sets rejects bad masks on the host (no GPU needed)."""
+    x = fb.SparseMatrix.binary(4, 3, np.arange(5), np.array([0, 1, 2, 0]))
+    lap = _lap(4)
+    one_class = np.array([1, 1, 0, 0], dtype=np.int8)
+    with pytest.raises(ValueError, match="both classes"):
+        fb.solve_label_sets(x, lap, [one_class], 0.5, (0.1,))
+    with pytest.raises(ValueError, match="one entry per sample"):
+        fb.solve_label_sets(x, lap, [np.array([1, -1], dtype=np.int8)], 0.5, (0.1,))
+    with pytest.raises(ValueError, match="one seed"):
+        fb.solve_label_sets(x, lap, [np.array([1, -1, 0, 0], dtype=np.int8)], 0.5, (0.1,),
+                            seeds=[1, 2])
+
+
+def test_task_masks_shape_and_counts():
+    from paper_1709_04794_b200.workloads import task_masks
+
+    m = task_masks(1000, 5, 0.02, 0.25, seed=3)
+    assert m.shape == (5, 1000) and m.dtype == np.int8
+    for row in m:
+        assert (row != 0).sum() == 20 and (row == 1).sum() == 5
+
+
 # -------------------------------------------------------------- workloads
 
 def test_zipf_rows_distinct_sorted_and_poisson():

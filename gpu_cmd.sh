@@ -1,4 +1,6 @@
-timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_gpu.log
-timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
-timeout 1800 python tools/bench_batch.py --workload cfg4 --seq-tasks 2 > gpurun_out/batch_cfg4_full.json 2> gpurun_out/batch_cfg4_full.err
-timeout 900 python tools/bench_batch.py --workload cfg2 --tasks 64 --seq-tasks 3 > gpurun_out/batch_cfg2_64.json 2> gpurun_out/batch_cfg2_64.err
+FSDA_B200_XT_SPLIT=1 timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_large.py -x -q -m gpu > gpurun_out/pytest_split.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_split.log
+for v in 0 1; do
+if [ $v = 1 ]; then export FSDA_B200_XT_SPLIT=1; fi
+timeout 600 python bench.py --no-cpu-baseline --batch-tasks 0 --concurrency 1 --steps 10 > gpurun_out/b_$v.json 2> gpurun_out/b_$v.err
+timeout 600 python bench.py --no-cpu-baseline --batch-tasks 0 --concurrency 1 --workload cfg3 --steps 3 > gpurun_out/b3_$v.json 2> gpurun_out/b3_$v.err
+done

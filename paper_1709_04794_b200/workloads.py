@@ -38,6 +38,11 @@ CONFIGS = {
     "cfg4": dict(n=1_500_000, d=500_000, lam=50.0, s=1.05, k=10, ell=30_000, n_pos=3_000,
                  n_shifts=20, beta_lo=1e-6, beta_hi=1e3, max_iter=150, tasks=64,
                  task_frac=0.01, task_pos=0.10),
+    # cfg5: scale-out stress case (8M x 2M, Poisson 80, Zipf 1.05, 15-NN, 1% labeled with 5%
+    # positives, 30 shifts, K=200).  BASELINE allows fp32 storage; this build keeps fp64 — the
+    # whole problem needs < 15 GB of one B200's 180 GB.  Generated row-chunked (make_workload_chunked).
+    "cfg5": dict(n=8_000_000, d=2_000_000, lam=80.0, s=1.05, k=15, ell=80_000, n_pos=4_000,
+                 n_shifts=30, beta_lo=1e-6, beta_hi=1e3, max_iter=200),
 }
 
 ALPHA = 0.5      # reference default, config.py:36
@@ -201,6 +206,36 @@ def task_masks(n: int, n_tasks: int, frac: float, pos_frac: float, seed: int) ->
         out[t, idx] = -1
         out[t, idx[:n_pos]] = 1
     return out
+
+
+def make_workload_chunked(name: str = "cfg5", *, max_iter: int | None = None, seed: int = 2024,
+                          chunk: int = 1_000_000, **overrides) -> Workload:
+    """Like make_workload, but X is drawn in independent row chunks (each
+    chunk its own seeded stream) so the largest configs fit in host memory;
+    the distribution is the same, the exact draw differs from make_workload."""
+    cfg = dict(CONFIGS[name])
+    cfg.update(overrides)
+    n, d = cfg["n"], cfg["d"]
+    offs, cols = [np.zeros(1, dtype=np.int64)], []
+    base = 0
+    for c, r0 in enumerate(range(0, n, chunk)):
+        m = min(chunk, n - r0)
+        o, cc = zipf_binary_rows(m, d, cfg["lam"], cfg["s"], seed * 1000 + c)
+        offs.append(o[1:] + base)
+        cols.append(cc)
+        base += int(o[-1])
+    xo = np.concatenate(offs)
+    xc = np.concatenate(cols)
+    del cols
+    lo, lc, lv, deg = random_knn_laplacian(n, cfg["k"], seed + 1)
+    lab = labels_first(n, cfg["ell"], cfg["n_pos"], seed + 2)
+    betas = np.geomspace(cfg["beta_lo"], cfg["beta_hi"], cfg["n_shifts"])
+    return Workload(
+        name=name, n=n, d=d, x_offsets=xo, x_cols=xc, l_offsets=lo, l_cols=lc, l_vals=lv,
+        degrees=deg, labels=lab, betas=betas,
+        max_iter=int(cfg["max_iter"] if max_iter is None else max_iter),
+        meta={k: v for k, v in cfg.items()},
+    )
 
 
 def workload_digest(w: Workload) -> str:

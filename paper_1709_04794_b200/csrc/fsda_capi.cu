@@ -191,7 +191,7 @@ struct fsda_ctx {
   // segmented-sum plans: rows of X, rows of L, light columns of X
   HostPlan plan_xr, plan_lr, plan_xc;
   // dense columns of X (blocked by rows, see k_xt_coop)
-  DevBuf<int> xh_col, xh_bptr;
+  DevBuf<int> xh_col, xh_bptr, xh_big;
   DevBuf<int4> xh_tasks;
   DevBuf<long long> xh_boff, xh_bwarp, xh_poff;
   long long xh_ntasks = 0, xh_nslots = 0;
@@ -1055,6 +1055,16 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
     }
     poff0[h + 1] = m;
   }
+  std::vector<std::pair<long long, int>> bigs;
+  for (long long h = 0; h < nh; ++h)
+    if (poff0[h + 1] > XT_BIG_PARTS) bigs.push_back({-poff0[h + 1], (int)h});
+  std::sort(bigs.begin(), bigs.end());  // most leaf sums first
+  std::vector<int> big_ids;
+  for (auto& pr : bigs) big_ids.push_back(pr.second);
+  c->xh_big.ensure(std::max<size_t>(1, big_ids.size()));
+  if (!big_ids.empty())
+    CK(cudaMemcpyAsync(c->xh_big.ptr, big_ids.data(), sizeof(int) * big_ids.size(),
+                       cudaMemcpyHostToDevice, c->stream));
   for (long long h = 0; h < nh; ++h) poff0[h + 1] += poff0[h];
   // poff[nh] <= nnz / XT_DENSE_PER_BLOCK + nnz / LEAF < 2^31: int slots suffice
   // pass 2 (parallel over blocks): task counts per (block, class)
@@ -1142,6 +1152,8 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   xh.rb = rb;
   xh.ticket_chunk = XT_TICKET_CHUNK;
   xh.splits = (int)std::max<long long>(1, c->xt_blocks / nb);
+  xh.big = c->xh_big.ptr;
+  xh.n_big = (long long)big_ids.size();
   if (!c->xt_ticket.ptr) {
     c->xt_ticket.ensure(1);
     CK(cudaMemset(c->xt_ticket.ptr, 0, sizeof(unsigned long long)));
@@ -1253,6 +1265,7 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     c->xt_ticket.release();
     c->xh_col.release();
     c->xh_bptr.release();
+    c->xh_big.release();
     c->xh_tasks.release();
     c->xh_boff.release();
     c->xh_bwarp.release();
@@ -2309,3 +2322,9 @@ int fsda_solve_batch(fsda_ctx* c, int n_tasks, const int8_t* labels, double alph
 }
 
 }  // extern "C"
+
+// debug: per-CTA phase timestamps of the last k_xt_coop launch (globaltimer ns)
+extern "C" int fsda_debug_xt_trace(int on, unsigned long long* out) {
+  if (out) return cudaMemcpyFromSymbol(out, g_xt_trace, sizeof(unsigned long long) * 5 * 1024) == cudaSuccess ? 0 : 4;
+  return cudaMemcpyToSymbol(g_xt_trace_on, &on, sizeof(int)) == cudaSuccess ? 0 : 4;
+}

@@ -366,6 +366,8 @@ constexpr int XT_CTAS_PER_SM = 2;
 // phase-1b tasks claimed per ticket draw (halves the single-address atomics;
 // measured 1.02x at cfg2 / cfg3 over 1, and 4 is worse at cfg2)
 constexpr int XT_TICKET_CHUNK = 2;
+// phase 2: dense columns with more leaf sums than this are reduced by a CTA
+constexpr int XT_BIG_PARTS = 1024;
 
 struct XtDense {
   const int* rows;        // CSC row indices
@@ -380,16 +382,17 @@ struct XtDense {
   int rb;                 // rows per block (XT_RB)
   int ticket_chunk;       // tasks claimed per ticket draw
   int splits;             // CTAs sharing one row block's slices
+  const int* big;         // dense ids with more than XT_BIG_PARTS leaf sums (phase 2 by a CTA)
+  long long n_big;
 };
 
 template <int W>
-__device__ __forceinline__ void dense_slice_task(const XtDense& dn, const double* zs, int r0, int b,
+__device__ __forceinline__ void dense_slice_task(const XtDense& dn, const double* zs, int r0,
+                                                 const long long* off, const long long* wb,
                                                  int cls, long long tw_local, int lane) {
   constexpr int M = 32 / W;
   constexpr int MA = M < 8 ? M : 8;
   constexpr int KA = W >= 8 ? W / 4 : 1;
-  const long long* off = dn.boff + (long long)b * 7;
-  const long long* wb = dn.bwarp + (long long)b * 7;
   const long long idx = off[cls] + (tw_local - wb[cls]) * (32 / W) + lane / W;
   int4 tk = make_int4(-1, 0, 0, 0);
   if (idx < off[cls + 1]) tk = __ldg(dn.tasks + idx);
@@ -467,6 +470,16 @@ __device__ __forceinline__ void stage_block(double* zs, const double* __restrict
   mbar_wait(bar, phase);
 }
 
+__device__ int g_xt_trace_on = 0;
+__device__ unsigned long long g_xt_trace[5][1024];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define XT_MARK(k) \
+  if (g_xt_trace_on && threadIdx.x == 0 && blockIdx.x < 1024) g_xt_trace[k][blockIdx.x] = gtimer();
+
 __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan pl, XtDense dn, SegArgs a,
                                                     const CgScalars* sc, int guarded, int n_rows,
                                                     unsigned long long* ticket) {
@@ -475,6 +488,8 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
   if (guarded && loop_idle(sc)) return;  // uniform across the grid
   extern __shared__ __align__(16) double zs[];  // dn.rb doubles
   __shared__ unsigned long long zs_bar;
+  __shared__ long long s_off[7], s_wb[7];  // the current row block's class starts / warp prefixes
+  XT_MARK(0)
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   // ---- phase 1a: (row block, split) units with their dense-column slices
@@ -488,6 +503,10 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
       const int r0 = b * dn.rb;
       const int nr = min(dn.rb, n_rows - r0);
       __syncthreads();
+      if (threadIdx.x < 7) {
+        s_off[threadIdx.x] = __ldg(dn.boff + (long long)b * 7 + threadIdx.x);
+        s_wb[threadIdx.x] = __ldg(dn.bwarp + (long long)b * 7 + threadIdx.x);
+      }
       if (tma) {
         stage_block(zs, a.src + r0, nr, &zs_bar, phase);
         phase ^= 1u;
@@ -495,22 +514,23 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
         for (int k = threadIdx.x; k < nr; k += blockDim.x) zs[k] = __ldg(a.src + r0 + k);
       }
       __syncthreads();
-      const long long* wb = dn.bwarp + (long long)b * 7;
-      const long long c0 = wb[6] * sp / dn.splits, c1 = wb[6] * (sp + 1) / dn.splits;
+      const long long c0 = s_wb[6] * sp / dn.splits, c1 = s_wb[6] * (sp + 1) / dn.splits;
       for (long long tw = c0 + warp; tw < c1; tw += nw) {
         int k = 0;
-        while (tw >= wb[k + 1]) ++k;
+        while (tw >= s_wb[k + 1]) ++k;
         switch (k) {
-          case 0: dense_slice_task<1>(dn, zs, r0, b, 0, tw, lane); break;
-          case 1: dense_slice_task<2>(dn, zs, r0, b, 1, tw, lane); break;
-          case 2: dense_slice_task<4>(dn, zs, r0, b, 2, tw, lane); break;
-          case 3: dense_slice_task<8>(dn, zs, r0, b, 3, tw, lane); break;
-          case 4: dense_slice_task<16>(dn, zs, r0, b, 4, tw, lane); break;
-          default: dense_slice_task<32>(dn, zs, r0, b, 5, tw, lane); break;
+          case 0: dense_slice_task<1>(dn, zs, r0, s_off, s_wb, 0, tw, lane); break;
+          case 1: dense_slice_task<2>(dn, zs, r0, s_off, s_wb, 1, tw, lane); break;
+          case 2: dense_slice_task<4>(dn, zs, r0, s_off, s_wb, 2, tw, lane); break;
+          case 3: dense_slice_task<8>(dn, zs, r0, s_off, s_wb, 3, tw, lane); break;
+          case 4: dense_slice_task<16>(dn, zs, r0, s_off, s_wb, 4, tw, lane); break;
+          default: dense_slice_task<32>(dn, zs, r0, s_off, s_wb, 5, tw, lane); break;
         }
       }
     }
   }
+  __syncthreads();
+  XT_MARK(1)
   // ---- phase 1b: the other columns and the sum(z) leaves; warps draw tasks
   // from a grid-wide ticket so CTAs that staged a dense block catch up.
   const long long total = pl.warp_base[8];
@@ -553,16 +573,32 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
     }
     }
   }
+  __syncthreads();
+  XT_MARK(2)
   grid.sync();
+  XT_MARK(3)
   if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0ULL;  // every warp has drawn its last ticket
   const long long nwarps = (long long)gridDim.x * nw;
-  // ---- phase 2: dense columns
+  // ---- phase 2: dense columns.  Columns with more than XT_BIG_PARTS leaf
+  // sums (the Zipf head at large N) are reduced by a whole CTA each
+  // (block_reduce_partials: the same R256 tree, leaves spread over the warps),
+  // the others by one warp each.
+  for (long long i = blockIdx.x; i < dn.n_big; i += gridDim.x) {
+    const int h = __ldg(dn.big + i);
+    const long long p0 = __ldg(dn.poff + h);
+    const double v = block_reduce_partials(dn.part + p0, __ldg(dn.poff + h + 1) - p0, zs);
+    if (threadIdx.x == 0) seg_finish<SEG_XCOLS>(a, __ldg(dn.col + h), v);
+  }
   const long long gw = (long long)blockIdx.x * nw + warp;
   for (long long h = gw; h < dn.n_dense; h += nwarps) {
     const long long p0 = __ldg(dn.poff + h);
-    const double v = warp_reduce_partials(dn.part + p0, (int)(__ldg(dn.poff + h + 1) - p0), lane);
+    const int m = (int)(__ldg(dn.poff + h + 1) - p0);
+    if (m > XT_BIG_PARTS) continue;
+    const double v = warp_reduce_partials(dn.part + p0, m, lane);
     if (lane == 0) seg_finish<SEG_XCOLS>(a, __ldg(dn.col + h), v);
   }
+  __syncthreads();
+  XT_MARK(4)
 }
 
 // bptr[h * (nb + 1) + b] = first position in column dense_col[h] whose row is

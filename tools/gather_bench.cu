@@ -39,6 +39,28 @@ __global__ void __launch_bounds__(256) k_gather(const int* __restrict__ idx, lon
   if (acc == 12345.0) out[0] = acc;
 }
 
+// load modes: 0 ld.global.nc (L1-allocating), 1 ld.global.cg (L2 only), 2 ld.global.cs
+template <int U, int MODE>
+__global__ void __launch_bounds__(256) k_gather_mode(const int* __restrict__ idx, long long n,
+                                                     const double* __restrict__ tab, double* out) {
+  extern __shared__ double reserve[];
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (long long i = tid; i + (U - 1) * stride < n; i += U * stride) {
+    int ix[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) ix[u] = __ldg(idx + i + u * stride);
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      v[u] = MODE == 0 ? __ldg(tab + ix[u]) : (MODE == 1 ? __ldcg(tab + ix[u]) : __ldcs(tab + ix[u]));
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += v[u];
+  }
+  if (acc == 12345.0) reserve[0] = acc, out[0] = acc;
+}
+
 // indices only (stream bound)
 __global__ void k_stream(const int* __restrict__ idx, long long n, double* out) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -101,6 +123,23 @@ int main() {
     return best;
   };
   const int grid = sms * 8;
+  {
+    const long long T = 200000;
+    for (long long i = 0; i < n; ++i) h[i] = (int)(rng() % T);
+    CK(cudaMemcpy(didx, h.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaFuncSetAttribute(k_gather_mode<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_gather_mode<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_gather_mode<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    for (int kb : {0, 32, 64, 100, 150, 200}) {
+      // kb KB of shared memory per SM: 8 CTAs per SM share it
+      const size_t per = (size_t)kb * 1024 / 8;
+      float m0 = timeit([&] { k_gather_mode<8, 0><<<sms * 8, 256, per>>>(didx, n, dtab, dout); });
+      float m1 = timeit([&] { k_gather_mode<8, 1><<<sms * 8, 256, per>>>(didx, n, dtab, dout); });
+      float m2 = timeit([&] { k_gather_mode<8, 2><<<sms * 8, 256, per>>>(didx, n, dtab, dout); });
+      printf("T=200000 smem/SM %3d KB: ldg %.1f  ldcg %.1f  ldcs %.1f G gathers/s\n", kb,
+             n / (m0 * 1e-3) / 1e9, n / (m1 * 1e-3) / 1e9, n / (m2 * 1e-3) / 1e9);
+    }
+  }
   for (long long T : {4096LL, 32768LL, 100000LL, 200000LL, 1500000LL, 16000000LL}) {
     for (long long i = 0; i < n; ++i) h[i] = (int)(rng() % T);
     CK(cudaMemcpy(didx, h.data(), n * sizeof(int), cudaMemcpyHostToDevice));

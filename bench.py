@@ -40,6 +40,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "full reg-sweep FSDA solves/sec"
 UNIT = "solves/s"
+GATHER_CEILING = 315e9   # random 8-byte gathers/s, L2-resident table (profiles/r01_gather_ceiling.md)
 
 
 def parse():
@@ -332,6 +333,18 @@ def run_b200(args):
                                     "GBps": round(k["bytes"] / max(k["ms"], 1e-9) / 1e6, 1)}
                         for k in kernels},
         }
+        # the bound that actually binds the gather kernels: random 8-byte gathers
+        # of an L2-resident vector, measured by tools/gather_bench.cu
+        # (profiles/r01_gather_ceiling.md); one gather per index-stream entry
+        gathers = {"xt": w.nnz, "spmv_rows": w.nnz, "smoother": int(w.l_cols.size)}.get(top["name"])
+        if gathers:
+            gps = gathers / (top["ms"] * 1e-3)
+            roofline["gather_ceiling"] = {
+                "gathers_per_launch": gathers, "achieved_gathers_per_s": gps,
+                "ceiling_gathers_per_s": GATHER_CEILING, "frac": gps / GATHER_CEILING,
+                "source": "profiles/r01_gather_ceiling.md (uniform random 8-byte gathers of a 1.56 MB "
+                          "L2-resident table; the dense-column share of X^T gathers comes from shared "
+                          "memory instead)"}
         pair = [k for k in kernels if k["name"] in ("spmv_rows", "xt")]   # K1 + K3
         pb = sum(k["bytes"] for k in pair)
         pt = sum(k["ms"] for k in pair)

@@ -229,6 +229,20 @@ int fsda_dev_finish(fsda_ctx* ctx, const uint8_t* flip, double* d_scores, double
                     double* residuals, int64_t* iterations, uint8_t* converged,
                     int64_t* n_applies, int64_t* fail_iter);
 
+/* ---- Tanimoto k-NN graph
+ * Replaces sdakit.graph.knn_graph (graph.py:152-166: _knn_rows_block
+ * graph.py:79-111, union symmetrization _adjacency_from_pairs
+ * graph.py:141-149) for the X uploaded by fsda_upload_x (its support
+ * pattern).  Row i keeps its k most similar rows j != i sharing a feature,
+ * ranked by (Tanimoto descending, index ascending), padded with the lowest
+ * unused indices; the result is the union of both directions.  1 <= k <= 64
+ * and k < n_rows, else FSDA_EINVAL (the reference raises GraphError).  The
+ * symmetric adjacency stays on the context; *nnz_out = its stored entries. */
+int fsda_graph_knn(fsda_ctx* ctx, int32_t k, int64_t* nnz_out);
+/* Copy the last graph out: row_offsets (n_rows + 1) and col_indices (nnz),
+ * int64 CSR with ascending columns (graph.py:146-148's from_scipy layout). */
+int fsda_graph_fetch(fsda_ctx* ctx, int64_t* row_offsets, int64_t* col_indices);
+
 #ifdef __cplusplus
 }
 #endif

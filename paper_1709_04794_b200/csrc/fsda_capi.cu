@@ -28,6 +28,10 @@
 #include "fsda_device.cuh"
 #include "fsda_hot.cuh"
 #include "fsda_batch.cuh"
+#include "graph_knn.cuh"
+
+#include <cublas_v2.h>
+#include <cub/device/device_select.cuh>
 
 using namespace fsda;
 
@@ -171,6 +175,25 @@ struct BatchBufs {
   }
 };
 
+// Tanimoto k-NN graph build (graph_knn.cuh) and its last result.
+struct GraphBufs {
+  DevBuf<int> head_of, cand, ncand, nbr, rsize;
+  DevBuf<signed char> A;
+  DevBuf<int> C;
+  DevBuf<unsigned long long> keys, keys2;
+  DevBuf<unsigned char> temp;
+  DevBuf<long long> offs, cols, count;
+  long long n = 0, nnz = 0;
+  cublasHandle_t blas = nullptr;
+  void release() {
+    head_of.release(); cand.release(); ncand.release(); nbr.release(); rsize.release(); A.release();
+    C.release();
+    keys.release(); keys2.release(); temp.release(); offs.release(); cols.release(); count.release();
+    if (blas) cublasDestroy(blas);
+    blas = nullptr;
+  }
+};
+
 struct fsda_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -196,6 +219,7 @@ struct fsda_ctx {
   DevBuf<long long> xh_boff, xh_bwarp, xh_poff;
   long long xh_ntasks = 0, xh_nslots = 0;
   BatchBufs batch;
+  GraphBufs knn;
   PinnedBuf xh_stage;
   DevBuf<double> xh_part;
   XtDense xh{};
@@ -1273,6 +1297,7 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     c->xh_poff.release();
     c->xh_stage.release();
     c->batch.release();
+    c->knn.release();
     c->plan_xr.release();
     c->plan_lr.release();
     c->plan_xc.release();
@@ -2327,4 +2352,136 @@ int fsda_solve_batch(fsda_ctx* c, int n_tasks, const int8_t* labels, double alph
 extern "C" int fsda_debug_xt_trace(int on, unsigned long long* out) {
   if (out) return cudaMemcpyFromSymbol(out, g_xt_trace, sizeof(unsigned long long) * 5 * 1024) == cudaSuccess ? 0 : 4;
   return cudaMemcpyToSymbol(g_xt_trace_on, &on, sizeof(int)) == cudaSuccess ? 0 : 4;
+}
+
+// ---------------------------------------------------------------- k-NN graph
+// graph.py:152-166 knn_graph on the context's X (fsda_upload_x first).
+namespace {
+constexpr int KNN_HEAD_MAX = 4096;  // head columns counted on the tensor cores
+
+#define CKB(x)                                                                  \
+  do {                                                                          \
+    cublasStatus_t st_ = (x);                                                   \
+    if (st_ != CUBLAS_STATUS_SUCCESS) {                                         \
+      fail(FSDA_ECUDA, "cuBLAS status %d at line %d", (int)st_, __LINE__);      \
+      return FSDA_ECUDA;                                                        \
+    }                                                                           \
+  } while (0)
+}  // namespace
+
+extern "C" int fsda_graph_knn(fsda_ctx* c, int32_t k, int64_t* nnz_out) {
+  API_BEGIN(c)
+  if (!c->has_x) return fail(FSDA_EINVAL, "upload X before building its graph");
+  const long long n = c->n, d = c->d;
+  if (!(k > 0 && (long long)k < n))
+    return fail(FSDA_EINVAL, "k must satisfy 0 < k < n_samples, got k=%d, n=%lld", (int)k, n);
+  if (k > KNN_MAX_K) return fail(FSDA_EINVAL, "k=%d above the device limit %d", (int)k, KNN_MAX_K);
+  if (n * (long long)k * 2 >= (1LL << 31)) return fail(FSDA_EINVAL, "graph too large (n*k)");
+  GraphBufs& g = c->knn;
+  Trace tr;
+  // head = the most frequent columns with at least two entries (ties: lower index)
+  std::vector<int> colptr((size_t)d + 1);
+  CK(cudaMemcpy(colptr.data(), c->csc_colptr.ptr, sizeof(int) * (d + 1), cudaMemcpyDeviceToHost));
+  std::vector<int> order;
+  for (long long col = 0; col < d; ++col)
+    if (colptr[col + 1] - colptr[col] >= 2) order.push_back((int)col);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return colptr[a + 1] - colptr[a] > colptr[b + 1] - colptr[b];
+  });
+  const int nh = (int)std::min<size_t>(order.size(), KNN_HEAD_MAX);
+  const int H = nh > 0 ? (nh + 15) & ~15 : 0;  // GEMM depth padded to 16 (zero columns)
+  std::vector<int> head_of((size_t)std::max<long long>(d, 1), -1);
+  for (int h = 0; h < nh; ++h) head_of[order[h]] = h;
+  g.head_of.ensure(std::max<long long>(d, 1));
+  CK(cudaMemcpyAsync(g.head_of.ptr, head_of.data(), sizeof(int) * std::max<long long>(d, 1),
+                     cudaMemcpyHostToDevice, c->stream));
+  // row blocks: the nb x n fp32 head-count block stays below 2^30 elements
+  // int8 tensor-core GEMM shapes: rows of A and C's leading dimension padded
+  // to 16 (zero rows); blocks start at multiples of 16
+  const long long n16 = (n + 15) & ~15LL;
+  const long long B = std::max<long long>(16, std::min<long long>(n16, ((1LL << 30) / n16) & ~15LL));
+  g.cand.ensure(B * k);
+  g.ncand.ensure(B);
+  g.nbr.ensure(n * k);
+  g.rsize.ensure(n16);
+  CK(cudaMemsetAsync(g.rsize.ptr, 0, sizeof(int) * n16, c->stream));
+  k_knn_rsize<<<grid_for(n, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, g.rsize.ptr, (int)n);
+  CKL();
+  if (H > 0) {
+    g.A.ensure(n16 * H);
+    g.C.ensure(B * n16);
+    CK(cudaMemsetAsync(g.A.ptr, 0, (size_t)n16 * H, c->stream));
+    k_knn_head_dense<<<grid_for(n, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr, g.head_of.ptr,
+                                                             g.A.ptr, (int)n, H);
+    CKL();
+    if (!g.blas) CKB(cublasCreate(&g.blas));
+    CKB(cublasSetStream(g.blas, c->stream));
+    CKB(cublasSetMathMode(g.blas, CUBLAS_DEFAULT_MATH));
+  }
+  tr.mark("knn: head matrix");
+  for (long long r0 = 0; r0 < n; r0 += B) {
+    const long long nb = std::min(B, n - r0);
+    if (H > 0) {
+      const int one = 1, zero = 0;
+      // C (n x nb, column-major) = A^T(n x H) * A_blk (H x nb): row b of the
+      // row-major nb x n block = head counts of row r0 + b against every row
+      const long long nb16 = (nb + 15) & ~15LL;
+      CKB(cublasGemmEx(g.blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)n16, (int)nb16, H, &one, g.A.ptr, CUDA_R_8I, H,
+                       g.A.ptr + r0 * H, CUDA_R_8I, H, &zero, g.C.ptr, CUDA_R_32I, (int)n16,
+                       CUBLAS_COMPUTE_32I, CUBLAS_GEMM_DEFAULT));
+      k_knn_scan<<<(unsigned)cdiv(nb, KNN_WARPS), KNN_WARPS * 32, 0, c->stream>>>(
+          g.C.ptr, (int)r0, (int)nb, (int)n, (int)n16, g.rsize.ptr, k, g.cand.ptr, g.ncand.ptr);
+      CKL();
+    } else {
+      CK(cudaMemsetAsync(g.ncand.ptr, 0, sizeof(int) * nb, c->stream));
+    }
+    k_knn_refine<<<(unsigned)cdiv(nb, KNN_REFINE_WARPS), KNN_REFINE_WARPS * 32, 0, c->stream>>>(
+        H > 0 ? g.C.ptr : nullptr, (int)n16, (int)r0, (int)nb, (int)n, c->x_rowptr.ptr, c->x_cols.ptr,
+        c->csc_colptr.ptr, c->csc_rows.ptr, g.head_of.ptr, k, g.cand.ptr, g.ncand.ptr, g.nbr.ptr);
+    CKL();
+  }
+  tr.mark("knn: scan + refine");
+  // union symmetrization: sort both directions, drop duplicates, CSR
+  const long long m2 = 2 * n * k;
+  g.keys.ensure(m2);
+  g.keys2.ensure(m2);
+  g.count.ensure(1);
+  k_knn_keys<<<grid_for(n * k, 256), 256, 0, c->stream>>>(g.nbr.ptr, n, k, g.keys.ptr);
+  CKL();
+  int bits = 1;
+  while (bits < 64 && ((unsigned long long)n * (unsigned long long)n) >> bits) ++bits;
+  size_t tb_sort = 0, tb_uniq = 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, tb_sort, g.keys.ptr, g.keys2.ptr, (int)m2, 0, bits, c->stream));
+  CK(cub::DeviceSelect::Unique(nullptr, tb_uniq, g.keys2.ptr, g.keys.ptr, g.count.ptr, (int)m2, c->stream));
+  g.temp.ensure(std::max(tb_sort, tb_uniq));
+  CK(cub::DeviceRadixSort::SortKeys(g.temp.ptr, tb_sort, g.keys.ptr, g.keys2.ptr, (int)m2, 0, bits, c->stream));
+  CK(cub::DeviceSelect::Unique(g.temp.ptr, tb_uniq, g.keys2.ptr, g.keys.ptr, g.count.ptr, (int)m2, c->stream));
+  long long m = 0;
+  CK(cudaMemcpyAsync(&m, g.count.ptr, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  g.offs.ensure(n + 1);
+  g.cols.ensure(std::max<long long>(m, 1));
+  k_knn_csr<<<grid_for(std::max(m, n + 1), 256), 256, 0, c->stream>>>(g.keys.ptr, m, n, g.offs.ptr, g.cols.ptr);
+  CKL();
+  CK(cudaStreamSynchronize(c->stream));
+  tr.mark("knn: symmetrize");
+  g.n = n;
+  g.nnz = m;
+  if (nnz_out) *nnz_out = m;
+  return FSDA_OK;
+  API_END
+}
+
+extern "C" int fsda_graph_fetch(fsda_ctx* c, int64_t* row_offsets, int64_t* col_indices) {
+  API_BEGIN(c)
+  GraphBufs& g = c->knn;
+  if (!g.offs.ptr) return fail(FSDA_EINVAL, "no graph built on this context");
+  if (row_offsets)
+    CK(cudaMemcpyAsync(row_offsets, g.offs.ptr, sizeof(long long) * (g.n + 1), cudaMemcpyDeviceToHost,
+                       c->stream));
+  if (col_indices && g.nnz)
+    CK(cudaMemcpyAsync(col_indices, g.cols.ptr, sizeof(long long) * g.nnz, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return FSDA_OK;
+  API_END
 }

@@ -1,0 +1,342 @@
+// graph_knn.cuh — Tanimoto k-nearest-neighbour graph of the binary rows of X
+// (reference: sdakit/graph.py:79-111 _knn_rows_block,
+// graph.py:141-166 _adjacency_from_pairs / knn_graph).
+//
+// Similarity of rows a, b is |a & b| / |a | b| = c / (n_a + n_b - c), computed
+// in fp64 from exact integer counts, so the values — and therefore the
+// ranking, ties included — are the reference's bit for bit.  Row i keeps the k
+// candidates j != i with c > 0 ranked by (similarity descending, index
+// ascending), padded with the lowest unused indices when it has fewer than k;
+// the edge set is the union of both directions.
+//
+// Counts are split by columns: a "head" of the H most frequent columns and a
+// tail of the rest.
+//   1. head counts for a block of rows against all rows are one GEMM of the 0/1
+//      head matrix with itself (int8 in, int32 out: exact), on the tensor
+//      cores through cuBLAS (a plain library GEMM);
+//   2. k_knn_scan: one warp per row ranks every j by its head-only similarity
+//      and keeps a top-k list.  A pair's head-only similarity equals its exact
+//      similarity unless the two rows share a tail column, in which case it is
+//      smaller — so the true top-k lies inside {head top-k} ∪ {rows sharing a
+//      tail column with i};
+//   3. k_knn_refine: one warp per row re-ranks that candidate set with exact
+//      counts (sorted-list intersection of the two rows) and pads;
+//   4. symmetrization: both directions as (row, col) keys, radix-sorted,
+//      de-duplicated, CSR offsets by binary search.
+#pragma once
+
+namespace fsda {
+
+constexpr int KNN_MAX_K = 64;
+constexpr int KNN_WARPS = 8;
+
+// A[i * H + head_of[c]] = 1 for every head column c of row i (A zeroed first).
+__global__ void k_knn_head_dense(const int* __restrict__ rowptr, const int* __restrict__ cols,
+                                 const int* __restrict__ head_of, signed char* __restrict__ A,
+                                 int n, int H) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+    const int h = head_of[cols[e]];
+    if (h >= 0) A[(long long)i * H + h] = 1;
+  }
+}
+
+// Ordering of candidates: (s, j) precedes (t, l) when s > t, or s == t and j < l.
+__device__ __forceinline__ bool knn_before(double s, int j, double t, int l) {
+  return s > t || (s == t && j < l);
+}
+
+// Warp-shared sorted top-k list in shared memory; lane 0 inserts.  A candidate
+// already in the list (same j) is skipped.
+struct KnnList {
+  double* s;
+  int* j;
+  int* cnt;
+  int k;
+  __device__ __forceinline__ bool wants(double cs, int cj) const {
+    const int c = *cnt;
+    return c < k || knn_before(cs, cj, s[c - 1], j[c - 1]);
+  }
+  __device__ __forceinline__ void insert(double cs, int cj) {
+    int c = *cnt;
+    for (int t = 0; t < c; ++t)
+      if (j[t] == cj) return;
+    if (c == k && !knn_before(cs, cj, s[c - 1], j[c - 1])) return;
+    int p = c < k ? c : k - 1;
+    while (p > 0 && knn_before(cs, cj, s[p - 1], j[p - 1])) {
+      s[p] = s[p - 1];
+      j[p] = j[p - 1];
+      --p;
+    }
+    s[p] = cs;
+    j[p] = cj;
+    if (c < k) *cnt = c + 1;
+  }
+};
+
+// Offer one candidate per lane (valid lanes only) to the warp's list.
+__device__ __forceinline__ void knn_offer(KnnList& L, bool valid, double sim, int jj, int lane) {
+  unsigned m = __ballot_sync(FULL, valid && L.wants(sim, jj));
+  while (m) {
+    const int l = __ffs(m) - 1;
+    const double cs = __shfl_sync(FULL, sim, l);
+    const int cj = __shfl_sync(FULL, jj, l);
+    if (lane == 0) L.insert(cs, cj);
+    __syncwarp();
+    m &= m - 1;
+  }
+}
+
+// Step 2: rows [r0, r0 + nb) against all n rows; C is nb x ldc (row-major,
+// int32 head counts; columns past n are padding).  Writes up to k candidate
+// indices per row (cand, ncand).  Once the list is full, a pair can only enter
+// with a similarity strictly above the k-th (j grows along the scan, so a tie
+// never wins); an fp32 estimate screens pairs against the k-th value with a
+// 1e-5 relative margin, and only pairs that pass get the exact fp64 quotient.
+__global__ void __launch_bounds__(KNN_WARPS * 32) k_knn_scan(const int* __restrict__ C, int r0, int nb,
+                                                             int n, int ldc, const int* __restrict__ rsize,
+                                                             int k, int* __restrict__ cand,
+                                                             int* __restrict__ ncand) {
+  __shared__ double s_s[KNN_WARPS][KNN_MAX_K];
+  __shared__ int s_j[KNN_WARPS][KNN_MAX_K];
+  __shared__ int s_c[KNN_WARPS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * KNN_WARPS + warp;
+  if (b >= nb) return;
+  const int i = r0 + b;
+  if (lane == 0) s_c[warp] = 0;
+  __syncwarp();
+  KnnList L{s_s[warp], s_j[warp], &s_c[warp], k};
+  const int ni = rsize[i];
+  const int4* row4 = reinterpret_cast<const int4*>(C + (long long)b * ldc);
+  const int4* rs4 = reinterpret_cast<const int4*>(rsize);
+  const int n4 = ldc >> 2;  // int4 groups per row (ldc and rsize padded to 16)
+  float floor_f = -1.0f;    // fp32 screen: k-th similarity minus the margin (-1 while not full)
+  // lane t takes the 4 consecutive j of groups t and t + 32 of every 64-group
+  // stride; both groups' loads are issued before either is screened
+  for (int g0 = 0; g0 < n4; g0 += 64) {
+    int4 cv[2], sv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int gi = g0 + u * 32 + lane;
+      cv[u] = gi < n4 ? __ldcs(row4 + gi) : make_int4(0, 0, 0, 0);
+      sv[u] = gi < n4 ? __ldg(rs4 + gi) : make_int4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int jb = 4 * (g0 + u * 32 + lane);
+      const int cs[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
+      const int ns[4] = {sv[u].x, sv[u].y, sv[u].z, sv[u].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = jb + q, c = cs[q];
+        const int uu = ni + ns[q] - c;
+        const bool pass = c > 0 && j < n && j != i && (float)c > floor_f * (float)uu;
+        if (__any_sync(FULL, pass)) {
+          const double sim = pass ? (double)c / (double)uu : 0.0;
+          knn_offer(L, pass, sim, j, lane);
+          if (s_c[warp] == k) floor_f = (float)(s_s[warp][k - 1] * (1.0 - 1e-5));
+        }
+      }
+    }
+  }
+  const int c = s_c[warp];
+  for (int t = lane; t < c; t += 32) cand[(long long)b * k + t] = s_j[warp][t];
+  if (lane == 0) ncand[b] = c;
+}
+
+// rsize[i] = |a_i| (row supports)
+__global__ void k_knn_rsize(const int* __restrict__ rowptr, int* __restrict__ rsize, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) rsize[i] = rowptr[i + 1] - rowptr[i];
+}
+
+// |a_i & a_j| for sorted rows; a_i in shared memory (len ni), a_j in global.
+__device__ __forceinline__ int knn_intersect(const int* ai, int ni, const int* __restrict__ cols, int lo,
+                                             int hi) {
+  int c = 0;
+  for (int e = lo; e < hi; ++e) {
+    const int v = cols[e];
+    int a = 0, z = ni;
+    while (a < z) {
+      const int m = (a + z) >> 1;
+      if (ai[m] < v) a = m + 1; else z = m;
+    }
+    c += (a < ni && ai[a] == v) ? 1 : 0;
+  }
+  return c;
+}
+
+constexpr int KNN_ROW_SMEM = 512;   // row supports up to this long are staged in shared memory
+constexpr int KNN_TAIL_CAP = 2048;  // tail-candidate occurrences sorted in shared memory per row
+constexpr int KNN_REFINE_WARPS = 4;
+
+// Step 3: exact re-ranking of {head top-k} ∪ {rows sharing a tail column},
+// then padding (graph.py:96-109).  The exact count of a pair is its head count
+// (row b of the GEMM block, still in C) plus the number of tail columns the
+// two rows share, which is how often j occurs in the concatenated tail-column
+// lists of row i: those occurrences are sorted in shared memory (warp bitonic
+// sort) and counted as runs.  Rows with more than KNN_TAIL_CAP occurrences
+// intersect the two supports directly instead.
+__global__ void __launch_bounds__(KNN_REFINE_WARPS * 32) k_knn_refine(
+    const int* __restrict__ C, int ldc, int r0, int nb, int n, const int* __restrict__ rowptr,
+    const int* __restrict__ cols, const int* __restrict__ colptr, const int* __restrict__ rows,
+    const int* __restrict__ head_of, int k, const int* __restrict__ cand, const int* __restrict__ ncand,
+    int* __restrict__ nbr) {
+  __shared__ double s_s[KNN_REFINE_WARPS][KNN_MAX_K];
+  __shared__ int s_j[KNN_REFINE_WARPS][KNN_MAX_K];
+  __shared__ int s_c[KNN_REFINE_WARPS];
+  __shared__ int s_row[KNN_REFINE_WARPS][KNN_ROW_SMEM];
+  __shared__ int s_buf[KNN_REFINE_WARPS][KNN_TAIL_CAP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * KNN_REFINE_WARPS + warp;
+  if (b >= nb) return;
+  const int i = r0 + b;
+  if (lane == 0) s_c[warp] = 0;
+  const int lo_i = rowptr[i], ni = rowptr[i + 1] - lo_i;
+  const bool staged = ni <= KNN_ROW_SMEM;
+  for (int e = lane; e < ni && staged; e += 32) s_row[warp][e] = cols[lo_i + e];
+  __syncwarp();
+  const int* ai = staged ? s_row[warp] : cols + lo_i;
+  const int* crow = C + (long long)b * ldc;
+  KnnList L{s_s[warp], s_j[warp], &s_c[warp], k};
+  int* buf = s_buf[warp];
+  // occurrences of rows in the tail columns of row i
+  int m = 0;
+  for (int e = 0; e < ni; ++e) {
+    const int col = ai[e];
+    if (head_of[col] >= 0) continue;
+    const int clo = colptr[col], len = colptr[col + 1] - clo;
+    for (int t = lane; t < len; t += 32)
+      if (m + t < KNN_TAIL_CAP) buf[m + t] = rows[clo + t];
+    m += len;
+  }
+  __syncwarp();
+  if (m <= KNN_TAIL_CAP) {
+    int P = 32;
+    while (P < m) P <<= 1;
+    for (int t = m + lane; t < P; t += 32) buf[t] = 0x7fffffff;
+    __syncwarp();
+    for (int kk = 2; kk <= P; kk <<= 1)
+      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+        for (int t = lane; t < P; t += 32) {
+          const int o = t ^ jj;
+          if (o > t) {
+            const int x0 = buf[t], x1 = buf[o];
+            if ((x0 > x1) == ((t & kk) == 0)) {
+              buf[t] = x1;
+              buf[o] = x0;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    // runs: j with its multiplicity = shared tail columns
+    for (int t0 = 0; t0 < m; t0 += 32) {
+      const int t = t0 + lane;
+      bool start = false;
+      int j = -1, mult = 0;
+      if (t < m) {
+        j = buf[t];
+        start = (t == 0 || buf[t - 1] != j) && j != i;
+        if (start) {
+          mult = 1;
+          while (t + mult < m && buf[t + mult] == j) ++mult;
+        }
+      }
+      double sim = 0.0;
+      if (start) {
+        const int c = (crow ? crow[j] : 0) + mult;
+        sim = (double)c / ((double)(ni + rowptr[j + 1] - rowptr[j]) - (double)c);
+      }
+      knn_offer(L, start, sim, j, lane);
+    }
+    // the head top-k: head count + occurrences (binary search in the sorted runs)
+    const int nc = ncand[b];
+    for (int t0 = 0; t0 < nc; t0 += 32) {
+      const int t = t0 + lane;
+      const int j = t < nc ? cand[(long long)b * k + t] : -1;
+      double sim = 0.0;
+      if (j >= 0) {
+        int lo = 0, hi = m;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (buf[mid] < j) lo = mid + 1; else hi = mid;
+        }
+        int mult = 0;
+        while (lo + mult < m && buf[lo + mult] == j) ++mult;
+        const int c = (crow ? crow[j] : 0) + mult;
+        sim = (double)c / ((double)(ni + rowptr[j + 1] - rowptr[j]) - (double)c);
+      }
+      knn_offer(L, j >= 0, sim, j, lane);
+    }
+  } else {
+    auto exact = [&](int j) {
+      const int lo = rowptr[j], hi = rowptr[j + 1];
+      const int c = knn_intersect(ai, ni, cols, lo, hi);
+      return c > 0 ? (double)c / ((double)(ni + (hi - lo)) - (double)c) : 0.0;
+    };
+    const int nc = ncand[b];
+    for (int t0 = 0; t0 < nc; t0 += 32) {
+      const int t = t0 + lane;
+      const int j = t < nc ? cand[(long long)b * k + t] : -1;
+      const double sim = j >= 0 ? exact(j) : 0.0;
+      knn_offer(L, j >= 0, sim, j, lane);
+    }
+    for (int e = 0; e < ni; ++e) {
+      const int col = ai[e];
+      if (head_of[col] >= 0) continue;
+      const int clo = colptr[col], chi = colptr[col + 1];
+      for (int p0 = clo; p0 < chi; p0 += 32) {
+        const int p = p0 + lane;
+        const int j = p < chi ? rows[p] : i;
+        const bool valid = j != i;
+        const double sim = valid ? exact(j) : 0.0;
+        knn_offer(L, valid, sim, j, lane);
+      }
+    }
+  }
+  __syncwarp();
+  // padding with the lowest indices not yet taken (all at similarity 0)
+  if (lane == 0) {
+    int c = s_c[warp];
+    for (int j = 0; c < k && j < n; ++j) {
+      if (j == i) continue;
+      bool taken = false;
+      for (int t = 0; t < c; ++t) taken |= (s_j[warp][t] == j);
+      if (!taken) s_j[warp][c++] = j;
+    }
+    s_c[warp] = c;
+  }
+  __syncwarp();
+  for (int t = lane; t < k; t += 32) nbr[(long long)i * k + t] = s_j[warp][t];
+}
+
+// Step 4 helpers: both directions as 64-bit keys row * n + col.
+__global__ void k_knn_keys(const int* __restrict__ nbr, long long n, int k,
+                           unsigned long long* __restrict__ keys) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * k) return;
+  const long long i = t / k, j = nbr[t];
+  keys[2 * t] = (unsigned long long)(i * n + j);
+  keys[2 * t + 1] = (unsigned long long)(j * n + i);
+}
+
+// After sort + unique: cols and per-row offsets by binary search.
+__global__ void k_knn_csr(const unsigned long long* __restrict__ keys, long long m, long long n,
+                          long long* __restrict__ offs, long long* __restrict__ out_cols) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < m) out_cols[t] = (long long)(keys[t] % (unsigned long long)n);
+  if (t <= n) {
+    const unsigned long long target = (unsigned long long)t * (unsigned long long)n;
+    long long a = 0, z = m;
+    while (a < z) {
+      const long long mid = (a + z) >> 1;
+      if (keys[mid] < target) a = mid + 1; else z = mid;
+    }
+    offs[t] = a;
+  }
+}
+
+}  // namespace fsda

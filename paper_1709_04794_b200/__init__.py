@@ -49,6 +49,15 @@ from .fsda import (
     solve_label_sets,
 )
 
+from .graph import (
+    GraphError,
+    SimilarityGraph,
+    install_into_sdakit_graph,
+    knn_graph,
+    laplacian,
+    tanimoto,
+)
+
 __version__ = "0.1.0"
 
 __all__ = [
@@ -56,6 +65,7 @@ __all__ = [
     "NumericalFailureError", "PhaseStats", "RatingVector", "SdaProblem", "ShiftedSolveResult",
     "ShiftGrid", "SolveReport", "SolverBreakdownError", "SparseFormatError", "SparseMatrix",
     "as_shift_grid", "build_sparse",
+    "GraphError", "SimilarityGraph", "install_into_sdakit_graph", "knn_graph", "laplacian", "tanimoto",
     "ALGORITHMS", "Device", "DeviceProblem", "LinearOperator", "apply_smoother",
     "centered_matvec_transpose", "default_device", "fsda_operator_apply", "fsda_solve",
     "install_into_sdakit", "labeled_mean", "matvec", "matvec_transpose", "shifted_cg", "sa_sda_solve", "solve", "solve_label_sets", "RegressionOperator", "regression_operator",

@@ -166,6 +166,41 @@ def test_family_resolution_for_reference_objects():
         sys.path.remove(sdakit_root)
 
 
+def test_graph_install_and_reference_types():
+    """install_into_sdakit_graph routes sdakit's knn_graph names to the device
+    build; graphs of sdakit matrices come back as sdakit types (host only)."""
+    sdakit_root = "/root/reference/pkg/src"
+    import os
+
+    if not os.path.isdir(sdakit_root):
+        pytest.skip("reference not present on this host")
+    sys.path.insert(0, sdakit_root)
+    try:
+        import sdakit
+        import sdakit.graph as rg
+        import sdakit.synthetic as rsyn
+        from sdakit.sparse import SparseMatrix as RSM
+
+        saved = rg.knn_graph, sdakit.knn_graph, rsyn.knn_graph
+        try:
+            fb.install_into_sdakit_graph(rg)
+            assert rg.knn_graph is fb.knn_graph
+            assert sdakit.knn_graph is fb.knn_graph and rsyn.knn_graph is fb.knn_graph
+        finally:
+            rg.knn_graph, sdakit.knn_graph, rsyn.knn_graph = saved
+        from paper_1709_04794_b200.graph import _graph_types
+
+        sm, sg, ge, lp = _graph_types(RSM(2, 2, np.array([0, 1, 2]), np.array([0, 1]), np.ones(2)))
+        assert sg is rg.SimilarityGraph and ge is rg.GraphError and lp is rg.Laplacian and sm is RSM
+        # the host Laplacian assembly gives the reference's own layout
+        adj = RSM(3, 3, np.array([0, 1, 3, 4]), np.array([1, 0, 2, 1]), np.ones(4))
+        g = rg.graph_from_adjacency(adj)
+        mine, ref = fb.laplacian(g), rg.laplacian(g)
+        assert mine.matrix == ref.matrix and np.array_equal(mine.degrees, ref.degrees)
+    finally:
+        sys.path.remove(sdakit_root)
+
+
 def test_label_sets_validated_before_the_device():
     """solve_label_sets rejects bad masks on the host (no GPU needed)."""
     x = fb.SparseMatrix.binary(4, 3, np.arange(5), np.array([0, 1, 2, 0]))

@@ -478,8 +478,9 @@ def run_b200(args):
                           "equal_to_oracle": same},
                  f"{w.name}": {"gpu_s": t_g2, "edges": g2.n_edges},
                  "note": "host-timed knn_graph(x, 10) incl. the pattern upload and the adjacency "
-                         "readback; the unmodified reference took 11.5 s at cfg1 in the authoring "
-                         "container (tests/golden/graph_reference.npz)"}
+                         "readback; the unmodified reference took "
+                         f"{float(np.load(ROOT / 'tests/golden/graph_reference.npz')['cfg1__seconds'][0]):.1f} s "
+                         "at cfg1 in the authoring container (tests/golden/graph_reference.npz)"}
         del gdev, g1, g2
 
     cpu = None

@@ -239,6 +239,11 @@ int fsda_dev_finish(fsda_ctx* ctx, const uint8_t* flip, double* d_scores, double
  * and k < n_rows, else FSDA_EINVAL (the reference raises GraphError).  The
  * symmetric adjacency stays on the context; *nnz_out = its stored entries. */
 int fsda_graph_knn(fsda_ctx* ctx, int32_t k, int64_t* nnz_out);
+/* Replaces sdakit.graph.threshold_graph (graph.py:169-188,
+ * _threshold_rows_block graph.py:114-133): every pair of distinct rows with
+ * Tanimoto >= theta, 0 < theta <= 1 (else FSDA_EINVAL; the reference raises
+ * GraphError).  Result kept on the context like fsda_graph_knn's. */
+int fsda_graph_threshold(fsda_ctx* ctx, double theta, int64_t* nnz_out);
 /* Copy the last graph out: row_offsets (n_rows + 1) and col_indices (nnz),
  * int64 CSR with ascending columns (graph.py:146-148's from_scipy layout). */
 int fsda_graph_fetch(fsda_ctx* ctx, int64_t* row_offsets, int64_t* col_indices);

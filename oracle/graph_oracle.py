@@ -1,4 +1,5 @@
-"""CPU ORACLE for the Tanimoto k-NN graph — test infrastructure only.
+"""CPU ORACLE for the Tanimoto k-NN and threshold graphs — test
+infrastructure only.
 
 Imported only by tests/ and bench.py's CPU baseline, as the checker; the
 product path is libfsda_b200.so (graph_knn.cuh).
@@ -68,6 +69,34 @@ def knn_adjacency(n_rows, n_cols, row_offsets, col_indices, k):
     src = np.repeat(np.arange(n_rows, dtype=np.int64), k)
     dst = nb.ravel()
     keys = np.unique(np.concatenate([src * n_rows + dst, dst * n_rows + src]))
+    rows, cols = keys // n_rows, keys % n_rows
+    offs = np.zeros(n_rows + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n_rows), out=offs[1:])
+    return offs, cols
+
+
+def threshold_adjacency(n_rows, n_cols, row_offsets, col_indices, theta, block=512):
+    """(row_offsets, col_indices) of the threshold graph: every pair of
+    distinct rows sharing a feature with similarity >= theta (graph.py:114-133,
+    169-188; theta > 0, so pairs sharing nothing never qualify)."""
+    pat = _pattern(n_rows, n_cols, row_offsets, col_indices)
+    pt = pat.T.tocsr()
+    size = np.diff(np.asarray(row_offsets, dtype=np.int64))
+    src, dst = [], []
+    for r0 in range(0, n_rows, block):
+        r1 = min(n_rows, r0 + block)
+        counts = (pat[r0:r1] @ pt).tocoo()
+        i = counts.row.astype(np.int64) + r0
+        j = counts.col.astype(np.int64)
+        c = counts.data.astype(np.float64)
+        keep = (i != j) & (c > 0)
+        i, j, c = i[keep], j[keep], c[keep]
+        hit = c / ((size[i] + size[j]).astype(np.float64) - c) >= theta
+        src.append(i[hit])
+        dst.append(j[hit])
+    s = np.concatenate(src) if src else np.empty(0, np.int64)
+    d = np.concatenate(dst) if dst else np.empty(0, np.int64)
+    keys = np.unique(np.concatenate([s * n_rows + d, d * n_rows + s]))
     rows, cols = keys // n_rows, keys % n_rows
     offs = np.zeros(n_rows + 1, dtype=np.int64)
     np.cumsum(np.bincount(rows, minlength=n_rows), out=offs[1:])

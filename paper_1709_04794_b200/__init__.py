@@ -56,6 +56,7 @@ from .graph import (
     knn_graph,
     laplacian,
     tanimoto,
+    threshold_graph,
 )
 
 __version__ = "0.1.0"
@@ -66,6 +67,7 @@ __all__ = [
     "ShiftGrid", "SolveReport", "SolverBreakdownError", "SparseFormatError", "SparseMatrix",
     "as_shift_grid", "build_sparse",
     "GraphError", "SimilarityGraph", "install_into_sdakit_graph", "knn_graph", "laplacian", "tanimoto",
+    "threshold_graph",
     "ALGORITHMS", "Device", "DeviceProblem", "LinearOperator", "apply_smoother",
     "centered_matvec_transpose", "default_device", "fsda_operator_apply", "fsda_solve",
     "install_into_sdakit", "labeled_mean", "matvec", "matvec_transpose", "shifted_cg", "sa_sda_solve", "solve", "solve_label_sets", "RegressionOperator", "regression_operator",

@@ -72,6 +72,7 @@ SIGNATURES = {
     "fsda_dev_finish": [_P, _PU8, _P, _PD, _PD, _PI64, _PU8, _PI64, _PI64],
     # Tanimoto k-NN graph (graph_knn.cuh)
     "fsda_graph_knn": [_P, C.c_int32, _PI64],
+    "fsda_graph_threshold": [_P, _D, _PI64],
     "fsda_graph_fetch": [_P, _PI64, _PI64],
 }
 

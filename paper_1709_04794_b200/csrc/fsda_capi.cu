@@ -177,7 +177,7 @@ struct BatchBufs {
 
 // Tanimoto k-NN graph build (graph_knn.cuh) and its last result.
 struct GraphBufs {
-  DevBuf<int> head_of, cand, ncand, nbr, rsize;
+  DevBuf<int> head_of, cand, ncand, nbr, rsize, tsize;
   DevBuf<signed char> A;
   DevBuf<int> C;
   DevBuf<unsigned long long> keys, keys2;
@@ -186,7 +186,7 @@ struct GraphBufs {
   long long n = 0, nnz = 0;
   cublasHandle_t blas = nullptr;
   void release() {
-    head_of.release(); cand.release(); ncand.release(); nbr.release(); rsize.release(); A.release();
+    head_of.release(); cand.release(); ncand.release(); nbr.release(); rsize.release(); tsize.release(); A.release();
     C.release();
     keys.release(); keys2.release(); temp.release(); offs.release(); cols.release(); count.release();
     if (blas) cublasDestroy(blas);
@@ -2369,16 +2369,11 @@ constexpr int KNN_HEAD_MAX = 4096;  // head columns counted on the tensor cores
   } while (0)
 }  // namespace
 
-extern "C" int fsda_graph_knn(fsda_ctx* c, int32_t k, int64_t* nnz_out) {
-  API_BEGIN(c)
-  if (!c->has_x) return fail(FSDA_EINVAL, "upload X before building its graph");
+// Shared by the k-NN and threshold builds: head selection, the int8 head
+// matrix, then per row block the head-count GEMM followed by `per_block`.
+template <typename F>
+int graph_blocks(fsda_ctx* c, GraphBufs& g, F per_block) {
   const long long n = c->n, d = c->d;
-  if (!(k > 0 && (long long)k < n))
-    return fail(FSDA_EINVAL, "k must satisfy 0 < k < n_samples, got k=%d, n=%lld", (int)k, n);
-  if (k > KNN_MAX_K) return fail(FSDA_EINVAL, "k=%d above the device limit %d", (int)k, KNN_MAX_K);
-  if (n * (long long)k * 2 >= (1LL << 31)) return fail(FSDA_EINVAL, "graph too large (n*k)");
-  GraphBufs& g = c->knn;
-  Trace tr;
   // head = the most frequent columns with at least two entries (ties: lower index)
   std::vector<int> colptr((size_t)d + 1);
   CK(cudaMemcpy(colptr.data(), c->csc_colptr.ptr, sizeof(int) * (d + 1), cudaMemcpyDeviceToHost));
@@ -2395,17 +2390,19 @@ extern "C" int fsda_graph_knn(fsda_ctx* c, int32_t k, int64_t* nnz_out) {
   g.head_of.ensure(std::max<long long>(d, 1));
   CK(cudaMemcpyAsync(g.head_of.ptr, head_of.data(), sizeof(int) * std::max<long long>(d, 1),
                      cudaMemcpyHostToDevice, c->stream));
-  // row blocks: the nb x n fp32 head-count block stays below 2^30 elements
   // int8 tensor-core GEMM shapes: rows of A and C's leading dimension padded
-  // to 16 (zero rows); blocks start at multiples of 16
+  // to 16 (zero rows); blocks start at multiples of 16, and the nb x n16 int32
+  // block of head counts stays below 2^30 elements
   const long long n16 = (n + 15) & ~15LL;
   const long long B = std::max<long long>(16, std::min<long long>(n16, ((1LL << 30) / n16) & ~15LL));
-  g.cand.ensure(B * k);
-  g.ncand.ensure(B);
-  g.nbr.ensure(n * k);
   g.rsize.ensure(n16);
   CK(cudaMemsetAsync(g.rsize.ptr, 0, sizeof(int) * n16, c->stream));
   k_knn_rsize<<<grid_for(n, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, g.rsize.ptr, (int)n);
+  CKL();
+  g.tsize.ensure(n16);
+  CK(cudaMemsetAsync(g.tsize.ptr, 0, sizeof(int) * n16, c->stream));
+  k_knn_tsize<<<grid_for(n, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr, g.head_of.ptr,
+                                                      g.tsize.ptr, (int)n);
   CKL();
   if (H > 0) {
     g.A.ensure(n16 * H);
@@ -2418,56 +2415,122 @@ extern "C" int fsda_graph_knn(fsda_ctx* c, int32_t k, int64_t* nnz_out) {
     CKB(cublasSetStream(g.blas, c->stream));
     CKB(cublasSetMathMode(g.blas, CUBLAS_DEFAULT_MATH));
   }
-  tr.mark("knn: head matrix");
   for (long long r0 = 0; r0 < n; r0 += B) {
     const long long nb = std::min(B, n - r0);
     if (H > 0) {
       const int one = 1, zero = 0;
-      // C (n x nb, column-major) = A^T(n x H) * A_blk (H x nb): row b of the
-      // row-major nb x n block = head counts of row r0 + b against every row
       const long long nb16 = (nb + 15) & ~15LL;
+      // C (n16 x nb16, column-major) = A^T (n16 x H) * A_blk (H x nb16): row b
+      // of the row-major block = head counts of row r0 + b against every row
       CKB(cublasGemmEx(g.blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)n16, (int)nb16, H, &one, g.A.ptr, CUDA_R_8I, H,
                        g.A.ptr + r0 * H, CUDA_R_8I, H, &zero, g.C.ptr, CUDA_R_32I, (int)n16,
                        CUBLAS_COMPUTE_32I, CUBLAS_GEMM_DEFAULT));
-      k_knn_scan<<<(unsigned)cdiv(nb, KNN_WARPS), KNN_WARPS * 32, 0, c->stream>>>(
-          g.C.ptr, (int)r0, (int)nb, (int)n, (int)n16, g.rsize.ptr, k, g.cand.ptr, g.ncand.ptr);
-      CKL();
-    } else {
-      CK(cudaMemsetAsync(g.ncand.ptr, 0, sizeof(int) * nb, c->stream));
     }
-    k_knn_refine<<<(unsigned)cdiv(nb, KNN_REFINE_WARPS), KNN_REFINE_WARPS * 32, 0, c->stream>>>(
-        H > 0 ? g.C.ptr : nullptr, (int)n16, (int)r0, (int)nb, (int)n, c->x_rowptr.ptr, c->x_cols.ptr,
-        c->csc_colptr.ptr, c->csc_rows.ptr, g.head_of.ptr, k, g.cand.ptr, g.ncand.ptr, g.nbr.ptr);
-    CKL();
+    per_block(r0, nb, n16, H > 0 ? g.C.ptr : nullptr);
   }
-  tr.mark("knn: scan + refine");
-  // union symmetrization: sort both directions, drop duplicates, CSR
-  const long long m2 = 2 * n * k;
-  g.keys.ensure(m2);
-  g.keys2.ensure(m2);
+  return FSDA_OK;
+}
+
+// Sorted, de-duplicated keys[0, m2) -> the context's CSR adjacency.
+void graph_csr(fsda_ctx* c, GraphBufs& g, long long m2) {
+  const long long n = c->n;
+  g.keys2.ensure(std::max<long long>(m2, 1));
   g.count.ensure(1);
-  k_knn_keys<<<grid_for(n * k, 256), 256, 0, c->stream>>>(g.nbr.ptr, n, k, g.keys.ptr);
-  CKL();
   int bits = 1;
   while (bits < 64 && ((unsigned long long)n * (unsigned long long)n) >> bits) ++bits;
   size_t tb_sort = 0, tb_uniq = 0;
   CK(cub::DeviceRadixSort::SortKeys(nullptr, tb_sort, g.keys.ptr, g.keys2.ptr, (int)m2, 0, bits, c->stream));
   CK(cub::DeviceSelect::Unique(nullptr, tb_uniq, g.keys2.ptr, g.keys.ptr, g.count.ptr, (int)m2, c->stream));
-  g.temp.ensure(std::max(tb_sort, tb_uniq));
-  CK(cub::DeviceRadixSort::SortKeys(g.temp.ptr, tb_sort, g.keys.ptr, g.keys2.ptr, (int)m2, 0, bits, c->stream));
-  CK(cub::DeviceSelect::Unique(g.temp.ptr, tb_uniq, g.keys2.ptr, g.keys.ptr, g.count.ptr, (int)m2, c->stream));
+  g.temp.ensure(std::max<size_t>(std::max(tb_sort, tb_uniq), 1));
   long long m = 0;
-  CK(cudaMemcpyAsync(&m, g.count.ptr, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  if (m2 > 0) {
+    CK(cub::DeviceRadixSort::SortKeys(g.temp.ptr, tb_sort, g.keys.ptr, g.keys2.ptr, (int)m2, 0, bits, c->stream));
+    CK(cub::DeviceSelect::Unique(g.temp.ptr, tb_uniq, g.keys2.ptr, g.keys.ptr, g.count.ptr, (int)m2, c->stream));
+    CK(cudaMemcpyAsync(&m, g.count.ptr, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
   g.offs.ensure(n + 1);
   g.cols.ensure(std::max<long long>(m, 1));
   k_knn_csr<<<grid_for(std::max(m, n + 1), 256), 256, 0, c->stream>>>(g.keys.ptr, m, n, g.offs.ptr, g.cols.ptr);
   CKL();
   CK(cudaStreamSynchronize(c->stream));
-  tr.mark("knn: symmetrize");
   g.n = n;
   g.nnz = m;
-  if (nnz_out) *nnz_out = m;
+}
+
+extern "C" int fsda_graph_knn(fsda_ctx* c, int32_t k, int64_t* nnz_out) {
+  API_BEGIN(c)
+  if (!c->has_x) return fail(FSDA_EINVAL, "upload X before building its graph");
+  const long long n = c->n;
+  if (!(k > 0 && (long long)k < n))
+    return fail(FSDA_EINVAL, "k must satisfy 0 < k < n_samples, got k=%d, n=%lld", (int)k, n);
+  if (k > KNN_MAX_K) return fail(FSDA_EINVAL, "k=%d above the device limit %d", (int)k, KNN_MAX_K);
+  if (n * (long long)k * 2 >= (1LL << 31)) return fail(FSDA_EINVAL, "graph too large (n*k)");
+  GraphBufs& g = c->knn;
+  Trace tr;
+  const long long n16 = (n + 15) & ~15LL;
+  const long long B = std::max<long long>(16, std::min<long long>(n16, ((1LL << 30) / n16) & ~15LL));
+  g.cand.ensure(B * k);
+  g.ncand.ensure(B);
+  g.nbr.ensure(n * k);
+  int rc = graph_blocks(c, g, [&](long long r0, long long nb, long long ldc, const int* C) {
+    if (C) {
+      k_knn_scan<<<(unsigned)cdiv(nb, KNN_WARPS), KNN_WARPS * 32, 0, c->stream>>>(
+          C, (int)r0, (int)nb, (int)n, (int)ldc, g.rsize.ptr, k, g.cand.ptr, g.ncand.ptr);
+      CKL();
+    } else {
+      CK(cudaMemsetAsync(g.ncand.ptr, 0, sizeof(int) * nb, c->stream));
+    }
+    k_knn_refine<<<(unsigned)cdiv(nb, KNN_REFINE_WARPS), KNN_REFINE_WARPS * 32, 0, c->stream>>>(
+        C, (int)ldc, (int)r0, (int)nb, (int)n, c->x_rowptr.ptr, c->x_cols.ptr, c->csc_colptr.ptr,
+        c->csc_rows.ptr, g.head_of.ptr, k, g.cand.ptr, g.ncand.ptr, g.nbr.ptr);
+    CKL();
+  });
+  if (rc) return rc;
+  tr.mark("knn: head counts, scan, refine");
+  // union symmetrization: both directions, sorted, duplicates dropped
+  const long long m2 = 2 * n * k;
+  g.keys.ensure(m2);
+  k_knn_keys<<<grid_for(n * k, 256), 256, 0, c->stream>>>(g.nbr.ptr, n, k, g.keys.ptr);
+  CKL();
+  graph_csr(c, g, m2);
+  tr.mark("knn: symmetrize");
+  if (nnz_out) *nnz_out = g.nnz;
+  return FSDA_OK;
+  API_END
+}
+
+extern "C" int fsda_graph_threshold(fsda_ctx* c, double theta, int64_t* nnz_out) {
+  API_BEGIN(c)
+  if (!c->has_x) return fail(FSDA_EINVAL, "upload X before building its graph");
+  if (!(theta > 0.0 && theta <= 1.0)) return fail(FSDA_EINVAL, "theta must lie in (0, 1], got %g", theta);
+  const long long n = c->n;
+  GraphBufs& g = c->knn;
+  Trace tr;
+  g.count.ensure(1);
+  unsigned long long cap = (unsigned long long)std::max<long long>(1LL << 20, 16 * n);
+  unsigned long long hits = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    g.keys.ensure((long long)cap);
+    CK(cudaMemsetAsync(g.count.ptr, 0, sizeof(long long), c->stream));
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(g.count.ptr);
+    int rc = graph_blocks(c, g, [&](long long r0, long long nb, long long ldc, const int* C) {
+      k_graph_threshold<<<(unsigned)cdiv(nb, KNN_REFINE_WARPS), KNN_REFINE_WARPS * 32, 0, c->stream>>>(
+          C, (int)ldc, (int)r0, (int)nb, (int)n, g.rsize.ptr, c->x_rowptr.ptr, c->x_cols.ptr,
+          c->csc_colptr.ptr, c->csc_rows.ptr, g.head_of.ptr, g.tsize.ptr, theta, g.keys.ptr, cnt, cap);
+      CKL();
+    });
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(&hits, cnt, sizeof(hits), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (hits <= cap) break;
+    cap = hits;  // the first pass counted every hit: rerun with room for all
+  }
+  if (hits >= (1ULL << 31)) return fail(FSDA_EINVAL, "threshold graph too large (%llu pairs)", hits);
+  tr.mark("threshold: head counts, scan");
+  graph_csr(c, g, (long long)hits);
+  tr.mark("threshold: csr");
+  if (nnz_out) *nnz_out = g.nnz;
   return FSDA_OK;
   API_END
 }

@@ -172,6 +172,58 @@ constexpr int KNN_ROW_SMEM = 512;   // row supports up to this long are staged i
 constexpr int KNN_TAIL_CAP = 2048;  // tail-candidate occurrences sorted in shared memory per row
 constexpr int KNN_REFINE_WARPS = 4;
 
+// The rows occurring in row i's tail columns (its support entries whose column
+// is not a head column), concatenated into buf and sorted ascending (warp
+// bitonic sort, padded with INT_MAX to a power of two).  Returns the number
+// of occurrences m; when m > KNN_TAIL_CAP the buffer holds only a prefix and
+// is left unsorted (callers fall back to direct intersections).
+__device__ __forceinline__ int knn_tail_sorted(const int* ai, int ni, const int* __restrict__ head_of,
+                                               const int* __restrict__ colptr,
+                                               const int* __restrict__ rows, int* buf, int lane) {
+  int m = 0;
+  for (int e = 0; e < ni; ++e) {
+    const int col = ai[e];
+    if (head_of[col] >= 0) continue;
+    const int clo = colptr[col], len = colptr[col + 1] - clo;
+    for (int t = lane; t < len; t += 32)
+      if (m + t < KNN_TAIL_CAP) buf[m + t] = rows[clo + t];
+    m += len;
+  }
+  __syncwarp();
+  if (m > KNN_TAIL_CAP) return m;
+  int P = 32;
+  while (P < m) P <<= 1;
+  for (int t = m + lane; t < P; t += 32) buf[t] = 0x7fffffff;
+  __syncwarp();
+  for (int kk = 2; kk <= P; kk <<= 1)
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+      for (int t = lane; t < P; t += 32) {
+        const int o = t ^ jj;
+        if (o > t) {
+          const int x0 = buf[t], x1 = buf[o];
+          if ((x0 > x1) == ((t & kk) == 0)) {
+            buf[t] = x1;
+            buf[o] = x0;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  return m;
+}
+
+// Occurrences of j in the sorted buffer (= tail columns rows i and j share).
+__device__ __forceinline__ int knn_mult(const int* buf, int m, int j) {
+  int lo = 0, hi = m;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (buf[mid] < j) lo = mid + 1; else hi = mid;
+  }
+  int mult = 0;
+  while (lo + mult < m && buf[lo + mult] == j) ++mult;
+  return mult;
+}
+
 // Step 3: exact re-ranking of {head top-k} ∪ {rows sharing a tail column},
 // then padding (graph.py:96-109).  The exact count of a pair is its head count
 // (row b of the GEMM block, still in C) plus the number of tail columns the
@@ -202,36 +254,8 @@ __global__ void __launch_bounds__(KNN_REFINE_WARPS * 32) k_knn_refine(
   const int* crow = C + (long long)b * ldc;
   KnnList L{s_s[warp], s_j[warp], &s_c[warp], k};
   int* buf = s_buf[warp];
-  // occurrences of rows in the tail columns of row i
-  int m = 0;
-  for (int e = 0; e < ni; ++e) {
-    const int col = ai[e];
-    if (head_of[col] >= 0) continue;
-    const int clo = colptr[col], len = colptr[col + 1] - clo;
-    for (int t = lane; t < len; t += 32)
-      if (m + t < KNN_TAIL_CAP) buf[m + t] = rows[clo + t];
-    m += len;
-  }
-  __syncwarp();
+  const int m = knn_tail_sorted(ai, ni, head_of, colptr, rows, buf, lane);
   if (m <= KNN_TAIL_CAP) {
-    int P = 32;
-    while (P < m) P <<= 1;
-    for (int t = m + lane; t < P; t += 32) buf[t] = 0x7fffffff;
-    __syncwarp();
-    for (int kk = 2; kk <= P; kk <<= 1)
-      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-        for (int t = lane; t < P; t += 32) {
-          const int o = t ^ jj;
-          if (o > t) {
-            const int x0 = buf[t], x1 = buf[o];
-            if ((x0 > x1) == ((t & kk) == 0)) {
-              buf[t] = x1;
-              buf[o] = x0;
-            }
-          }
-        }
-        __syncwarp();
-      }
     // runs: j with its multiplicity = shared tail columns
     for (int t0 = 0; t0 < m; t0 += 32) {
       const int t = t0 + lane;
@@ -259,14 +283,7 @@ __global__ void __launch_bounds__(KNN_REFINE_WARPS * 32) k_knn_refine(
       const int j = t < nc ? cand[(long long)b * k + t] : -1;
       double sim = 0.0;
       if (j >= 0) {
-        int lo = 0, hi = m;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (buf[mid] < j) lo = mid + 1; else hi = mid;
-        }
-        int mult = 0;
-        while (lo + mult < m && buf[lo + mult] == j) ++mult;
-        const int c = (crow ? crow[j] : 0) + mult;
+        const int c = (crow ? crow[j] : 0) + knn_mult(buf, m, j);
         sim = (double)c / ((double)(ni + rowptr[j + 1] - rowptr[j]) - (double)c);
       }
       knn_offer(L, j >= 0, sim, j, lane);
@@ -311,6 +328,88 @@ __global__ void __launch_bounds__(KNN_REFINE_WARPS * 32) k_knn_refine(
   }
   __syncwarp();
   for (int t = lane; t < k; t += 32) nbr[(long long)i * k + t] = s_j[warp][t];
+}
+
+// Threshold graph (graph.py:114-133, 169-188): every pair (i, j), j != i,
+// with Tanimoto >= theta.  One warp per row scans its row of head counts; a
+// pair's exact count is its head count plus the tail columns it shares, at
+// most min(t_i, t_j) (the rows' tail entries), so pairs whose fp32 upper bound
+// (c + t) / (n_i + n_j - c - t) stays below theta (1e-5 relative margin)
+// are skipped and the rest get the exact count (sorted tail occurrences, or
+// a direct intersection when row i has more than KNN_TAIL_CAP of them) and
+// the exact fp64 quotient.  Hits are appended to keys as row * n + col
+// (warp-aggregated atomic); the symmetrization sorts them.
+__global__ void __launch_bounds__(KNN_REFINE_WARPS * 32) k_graph_threshold(
+    const int* __restrict__ C, int ldc, int r0, int nb, int n, const int* __restrict__ rsize,
+    const int* __restrict__ rowptr, const int* __restrict__ cols, const int* __restrict__ colptr,
+    const int* __restrict__ rows, const int* __restrict__ head_of, const int* __restrict__ tsize,
+    double theta, unsigned long long* __restrict__ keys, unsigned long long* __restrict__ count,
+    unsigned long long cap) {
+  __shared__ int s_row[KNN_REFINE_WARPS][KNN_ROW_SMEM];
+  __shared__ int s_buf[KNN_REFINE_WARPS][KNN_TAIL_CAP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * KNN_REFINE_WARPS + warp;
+  if (b >= nb) return;
+  const int i = r0 + b;
+  const int lo_i = rowptr[i], ni = rowptr[i + 1] - lo_i;
+  const bool staged = ni <= KNN_ROW_SMEM;
+  for (int e = lane; e < ni && staged; e += 32) s_row[warp][e] = cols[lo_i + e];
+  __syncwarp();
+  const int* ai = staged ? s_row[warp] : cols + lo_i;
+  int* buf = s_buf[warp];
+  const int m = knn_tail_sorted(ai, ni, head_of, colptr, rows, buf, lane);
+  const int ti = tsize[i];
+  const float th_f = (float)(theta * (1.0 - 1e-5));
+  const int4* row4 = C ? reinterpret_cast<const int4*>(C + (long long)b * ldc) : nullptr;
+  const int4* rs4 = reinterpret_cast<const int4*>(rsize);
+  const int4* ts4 = reinterpret_cast<const int4*>(tsize);
+  const int n4 = ldc >> 2;  // rsize / tsize / C rows padded to 16
+  for (int g0 = 0; g0 < n4; g0 += 32) {
+    const int gi = g0 + lane;
+    int4 cv = make_int4(0, 0, 0, 0), sv = cv, tv = cv;
+    if (gi < n4) {
+      if (row4) cv = __ldcs(row4 + gi);
+      sv = __ldg(rs4 + gi);
+      tv = __ldg(ts4 + gi);
+    }
+    const int cs[4] = {cv.x, cv.y, cv.z, cv.w};
+    const int ns[4] = {sv.x, sv.y, sv.z, sv.w};
+    const int tt[4] = {tv.x, tv.y, tv.z, tv.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = 4 * gi + q;
+      bool hit = false;
+      if (j < n && j != i) {
+        const int c = cs[q], nj = ns[q];
+        const int cu = c + min(ti, tt[q]);  // the exact count is at most this
+        if (cu > 0 && (float)cu >= th_f * (float)(ni + nj - cu)) {
+          const int ce = m <= KNN_TAIL_CAP ? c + knn_mult(buf, m, j)
+                                           : knn_intersect(ai, ni, cols, rowptr[j], rowptr[j + 1]);
+          hit = ce > 0 && (double)ce / ((double)(ni + nj) - (double)ce) >= theta;
+        }
+      }
+      const unsigned mask = __ballot_sync(FULL, hit);
+      if (mask) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(mask));
+        base = __shfl_sync(FULL, base, 0);
+        if (hit) {
+          const unsigned long long pos = base + __popc(mask & ((1u << lane) - 1u));
+          if (pos < cap) keys[pos] = (unsigned long long)i * (unsigned long long)n + (unsigned long long)j;
+        }
+      }
+    }
+  }
+}
+
+// tsize[i] = row i's entries in tail (non-head) columns
+__global__ void k_knn_tsize(const int* __restrict__ rowptr, const int* __restrict__ cols,
+                            const int* __restrict__ head_of, int* __restrict__ tsize, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int t = 0;
+  for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) t += head_of[cols[e]] < 0 ? 1 : 0;
+  tsize[i] = t;
 }
 
 // Step 4 helpers: both directions as 64-bit keys row * n + col.

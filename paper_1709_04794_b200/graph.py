@@ -1,4 +1,5 @@
-"""Tanimoto k-NN graph of the rows of X on the device.
+"""Tanimoto k-NN and threshold graphs of the rows of X on the device
+(SURVEY §8f #4).
 
 Mirrors the reference's graph API for this construction
 (/root/reference/pkg/src/sdakit/graph.py): ``knn_graph(x, k, *, block_size,
@@ -7,7 +8,9 @@ is the union-symmetrized k-NN edge set with unit values, built exactly as
 ``_knn_rows_block`` ranks candidates (graph.py:79-111: Tanimoto of the
 supports, ties toward the lower index, padding with the lowest unused
 indices) and ``_adjacency_from_pairs`` stores it (graph.py:141-149); and
-``laplacian(graph)`` (graph.py:191-195) assembles L = D - S.
+``threshold_graph(x, theta)`` (graph.py:169-188) keeps every pair with
+similarity >= theta; ``laplacian(graph)`` (graph.py:191-195) assembles
+L = D - S.
 
 The similarity work — every pair's intersection count, the per-row ranking
 and the symmetrization — runs in ``libfsda_b200.so`` (graph_knn.cuh: a
@@ -83,16 +86,42 @@ def knn_graph(x, k: int, *, block_size: int = 1024, n_threads: int = 1,
     if k > 64:
         raise GE(f"k={k}: the device ranking keeps at most 64 neighbours per row")
     dev = device or default_device()
+    lib = _upload_pattern(dev, x)
+    nnz = np.zeros(1, dtype=np.int64)
+    _raise_for(lib.fsda_graph_knn(dev._h, k, _capi.i64ptr(nnz)))
+    return _fetch_graph(dev, lib, n, int(nnz[0]), SM, SG)
+
+
+def threshold_graph(x, theta: float, *, block_size: int = 1024, n_threads: int = 1,
+                    device: Optional[Device] = None):
+    """Graph with an edge wherever the Tanimoto similarity of two distinct
+    rows is >= theta (graph.py:169-188), built on the device."""
+    SM, SG, GE, _ = _graph_types(x)
+    theta = float(theta)
+    if not 0.0 < theta <= 1.0:
+        raise GE(f"theta must lie in (0, 1], got {theta}")
+    n = int(x.n_rows)
+    dev = device or default_device()
+    lib = _upload_pattern(dev, x)
+    nnz = np.zeros(1, dtype=np.int64)
+    _raise_for(lib.fsda_graph_threshold(dev._h, theta, _capi.i64ptr(nnz)))
+    return _fetch_graph(dev, lib, n, int(nnz[0]), SM, SG)
+
+
+def _upload_pattern(dev, x):
     offs, cols = _i64(x.row_offsets), _i64(x.col_indices)
     lib = _capi.lib()
     # the support pattern only (graph.py:69-73): values are not read
-    _raise_for(lib.fsda_upload_x(dev._h, n, int(x.n_cols), _capi.i64ptr(offs), _capi.i64ptr(cols)))
-    dev.n, dev.d = n, int(x.n_cols)
+    _raise_for(lib.fsda_upload_x(dev._h, int(x.n_rows), int(x.n_cols), _capi.i64ptr(offs),
+                                 _capi.i64ptr(cols)))
+    dev.n, dev.d = int(x.n_rows), int(x.n_cols)
     dev._loaded = (None, None, None)   # the context's X changed: a resident problem re-uploads
-    nnz = np.zeros(1, dtype=np.int64)
-    _raise_for(lib.fsda_graph_knn(dev._h, k, _capi.i64ptr(nnz)))
+    return lib
+
+
+def _fetch_graph(dev, lib, n, nnz, SM, SG):
     g_offs = np.empty(n + 1, dtype=np.int64)
-    g_cols = np.empty(int(nnz[0]), dtype=np.int64)
+    g_cols = np.empty(nnz, dtype=np.int64)
     _raise_for(lib.fsda_graph_fetch(dev._h, _capi.i64ptr(g_offs), _capi.i64ptr(g_cols)))
     adj = SM(n, n, g_offs, g_cols, np.ones(g_cols.size))
     return SG(adjacency=adj, degrees=np.diff(g_offs).astype(np.int64))
@@ -123,11 +152,12 @@ def laplacian(graph):
 
 
 def install_into_sdakit_graph(graph_module=None):
-    """Route the reference's k-NN construction to the device: sdakit.graph's
-    knn_graph and the names its callers bound at import (cli.py:29,
-    synthetic.py:21, __init__.py:24)."""
+    """Route the reference's graph construction to the device: sdakit.graph's
+    knn_graph / threshold_graph and the names its callers bound at import
+    (cli.py:29, synthetic.py:21, __init__.py:24-27)."""
     g = graph_module or importlib.import_module("sdakit.graph")
     g.knn_graph = knn_graph
+    g.threshold_graph = threshold_graph
     for mod in ("sdakit", "sdakit.cli", "sdakit.synthetic"):
         try:
             m = importlib.import_module(mod)
@@ -135,4 +165,6 @@ def install_into_sdakit_graph(graph_module=None):
             continue
         if hasattr(m, "knn_graph"):
             m.knn_graph = knn_graph
+        if hasattr(m, "threshold_graph"):
+            m.threshold_graph = threshold_graph
     return g

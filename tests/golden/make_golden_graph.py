@@ -1,4 +1,5 @@
-"""Golden k-NN graphs from the UNMODIFIED reference (sdakit.graph.knn_graph).
+"""Golden k-NN and threshold graphs from the UNMODIFIED reference
+(sdakit.graph.knn_graph / threshold_graph).
 
 Run in the authoring container, where /root/reference exists:
 
@@ -22,7 +23,7 @@ import numpy as np
 
 sys.path.insert(0, "/root/reference/pkg/src")
 
-from sdakit.graph import knn_graph  # noqa: E402
+from sdakit.graph import knn_graph, threshold_graph  # noqa: E402
 from sdakit.sparse import SparseMatrix  # noqa: E402
 from sdakit.synthetic import (clustered_binary, random_sparse_binary,  # noqa: E402
                               random_sparse_rows, two_chain_fingerprints)
@@ -30,6 +31,7 @@ from sdakit.synthetic import (clustered_binary, random_sparse_binary,  # noqa: E
 from paper_1709_04794_b200.workloads import make_workload, workload_digest  # noqa: E402
 
 OUT = Path(__file__).resolve().parent / "graph_reference.npz"
+THETAS = (0.15, 0.3, 0.5, 1.0)
 
 
 def main():
@@ -55,6 +57,12 @@ def main():
         out[f"{name}__g_offsets"] = np.asarray(g.adjacency.row_offsets, dtype=np.int64)
         out[f"{name}__g_cols"] = np.asarray(g.adjacency.col_indices, dtype=np.int32)
         print(name, x.n_rows, x.n_cols, x.nnz, "k", k, "edges", g.n_edges)
+        for theta in THETAS:
+            t = threshold_graph(x, theta)
+            tag = f"{name}__t{int(round(theta * 100)):03d}"
+            out[f"{tag}_offsets"] = np.asarray(t.adjacency.row_offsets, dtype=np.int64)
+            out[f"{tag}_cols"] = np.asarray(t.adjacency.col_indices, dtype=np.int32)
+            print("   threshold", theta, "edges", t.n_edges)
     # cfg1 (10k x 5k, Zipf 1.1, Poisson 25), k = 10 — the BASELINE plumbing size
     w = make_workload("cfg1")
     xw = SparseMatrix(w.n, w.d, w.x_offsets, w.x_cols, np.ones(w.nnz))
@@ -65,6 +73,11 @@ def main():
     out["cfg1__g_offsets"] = np.asarray(g.adjacency.row_offsets, dtype=np.int64)
     out["cfg1__g_cols"] = np.asarray(g.adjacency.col_indices, dtype=np.int32)
     print("cfg1 edges", g.n_edges, "reference seconds", out["cfg1__seconds"][0])
+    t = threshold_graph(xw, 0.3)
+    out["cfg1__t030_offsets"] = np.asarray(t.adjacency.row_offsets, dtype=np.int64)
+    out["cfg1__t030_cols"] = np.asarray(t.adjacency.col_indices, dtype=np.int32)
+    out["thetas"] = np.array(THETAS)
+    print("cfg1 threshold 0.3 edges", t.n_edges)
     out["names"] = np.array([c[0] for c in cases])
     np.savez_compressed(OUT, **out)
     print("wrote", OUT)

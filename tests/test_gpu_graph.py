@@ -1,4 +1,5 @@
-"""Device k-NN graph (graph_knn.cuh via fsda_graph_knn) against the
+"""Device k-NN / threshold graphs (graph_knn.cuh via fsda_graph_knn /
+fsda_graph_threshold) against the
 reference's own graphs (tests/golden/graph_reference.npz) and the oracle
 (oracle/graph_oracle.py).  Integer/index work: the adjacency must be
 identical, entry for entry."""
@@ -41,8 +42,34 @@ def test_device_matches_reference_graphs(gold):
 
 def test_device_matches_reference_cfg1(gold):
     w = make_workload("cfg1")
-    g = G.knn_graph(T.SparseMatrix.binary(w.n, w.d, w.x_offsets, w.x_cols), 10)
-    _check(g, gold["cfg1__g_offsets"], gold["cfg1__g_cols"].astype(np.int64))
+    x = T.SparseMatrix.binary(w.n, w.d, w.x_offsets, w.x_cols)
+    _check(G.knn_graph(x, 10), gold["cfg1__g_offsets"], gold["cfg1__g_cols"].astype(np.int64))
+    _check(G.threshold_graph(x, 0.3), gold["cfg1__t030_offsets"], gold["cfg1__t030_cols"].astype(np.int64))
+
+
+def test_device_threshold_matches_reference_graphs(gold):
+    for name in gold["names"]:
+        n, d, _ = (int(v) for v in gold[f"{name}__x_shape"])
+        x = _x(n, d, gold[f"{name}__x_offsets"], gold[f"{name}__x_cols"])
+        for theta in gold["thetas"]:
+            tag = f"{name}__t{int(round(theta * 100)):03d}"
+            _check(G.threshold_graph(x, float(theta)), gold[f"{tag}_offsets"],
+                   gold[f"{tag}_cols"].astype(np.int64))
+
+
+@pytest.mark.parametrize("n,d,nnz,power,theta,dup,empty", [
+    (333, 5000, 4000, 1.1, 0.2, 20, 10),
+    (1000, 9000, 30000, 1.05, 0.1, 40, 5),
+    (3000, 8000, 450000, 0.0, 0.05, 0, 0),   # > 2048 tail occurrences per row
+    (200, 50, 2000, 0.0, 0.3333333333333333, 0, 0),
+    (50, 30, 0, 0.0, 0.5, 0, 0),             # empty X: no edges
+])
+def test_device_threshold_matches_oracle(n, d, nnz, power, theta, dup, empty):
+    rng = np.random.default_rng(n + int(theta * 1000))
+    n, d, offs, cols = _random_x(rng, n, d, nnz, power, dup, empty)
+    g = G.threshold_graph(_x(n, d, offs, cols), theta)
+    go, gc = graph_oracle.threshold_adjacency(n, d, offs, cols, theta)
+    _check(g, go, gc)
 
 
 def _random_x(rng, n, d, nnz, power=0.0, dup_rows=0, empty_rows=0):

@@ -1,6 +1,6 @@
-"""k-NN graph oracle (oracle/graph_oracle.py) pinned to the reference's own
+"""Graph oracles (oracle/graph_oracle.py) pinned to the reference's own
 graphs (tests/golden/graph_reference.npz, made by make_golden_graph.py from
-sdakit.graph.knn_graph), plus the host-side graph logic: argument
+sdakit.graph.knn_graph / threshold_graph), plus the host-side graph logic: argument
 validation, Tanimoto, Laplacian assembly (graph.py:58-66, 152-160, 191-195).
 CPU only."""
 
@@ -33,12 +33,39 @@ def test_oracle_matches_reference_graphs(gold):
         assert np.array_equal(g_cols, gold[f"{name}__g_cols"]), name
 
 
+def test_threshold_oracle_matches_reference_graphs(gold):
+    for name in gold["names"]:
+        n, d, _, offs, cols = _case(gold, str(name))
+        for theta in gold["thetas"]:
+            tag = f"{name}__t{int(round(theta * 100)):03d}"
+            g_offs, g_cols = graph_oracle.threshold_adjacency(n, d, offs, cols, float(theta))
+            assert np.array_equal(g_offs, gold[f"{tag}_offsets"]), tag
+            assert np.array_equal(g_cols, gold[f"{tag}_cols"]), tag
+
+
+def test_threshold_oracle_hand_case():
+    # supports {0,1}, {0,1,2,3}, {0}: pairwise 2/4, 1/2, 1/4
+    d, offs, cols = _rows([[0, 1], [0, 1, 2, 3], [0]], 4)
+    assert _edges(*graph_oracle.threshold_adjacency(3, d, offs, cols, 0.4)) == {(0, 1), (0, 2)}
+    assert _edges(*graph_oracle.threshold_adjacency(3, d, offs, cols, 0.2)) == {(0, 1), (0, 2), (1, 2)}
+
+
+def test_threshold_validates_theta_before_the_device():
+    x = T.SparseMatrix.binary(2, 2, [0, 1, 2], [0, 1])
+    for bad in (0.0, 1.5, -0.1):
+        with pytest.raises(G.GraphError):
+            G.threshold_graph(x, bad)
+
+
 def test_oracle_matches_reference_cfg1(gold):
     w = make_workload("cfg1")
     assert workload_digest(w) == str(gold["cfg1__digest"][0])
     g_offs, g_cols = graph_oracle.knn_adjacency(w.n, w.d, w.x_offsets, w.x_cols, 10)
     assert np.array_equal(g_offs, gold["cfg1__g_offsets"])
     assert np.array_equal(g_cols, gold["cfg1__g_cols"])
+    t_offs, t_cols = graph_oracle.threshold_adjacency(w.n, w.d, w.x_offsets, w.x_cols, 0.3)
+    assert np.array_equal(t_offs, gold["cfg1__t030_offsets"])
+    assert np.array_equal(t_cols, gold["cfg1__t030_cols"])
 
 
 def _rows(supports, n_cols):

@@ -82,6 +82,13 @@ int fsda_upload_laplacian(fsda_ctx* ctx, int64_t n, const int64_t* row_offsets,
 
 /* Ternary labels, N entries, labeled-first (LabelVector, sparse.py:198-235). */
 int fsda_set_labels(fsda_ctx* ctx, const int8_t* labels);
+/* X, L and labels in one call (what fsda_solve's caller uploads every time):
+ * the same checks and results as fsda_upload_x + fsda_upload_laplacian +
+ * fsda_set_labels, with L's host->device copies queued on a second stream
+ * behind X's so they cross the link while X's CSC and plans are built. */
+int fsda_upload_problem(fsda_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* x_offsets,
+                        const int64_t* x_cols, const int64_t* l_offsets, const int64_t* l_cols,
+                        const double* l_values, const int8_t* labels);
 /* Labels as an arbitrary mask (no labeled-first requirement): the batched
  * label-mask solves of nested cross-validation (evaluation.py:110-123 permutes
  * every fold to labeled-first instead; the result is the same operator). */

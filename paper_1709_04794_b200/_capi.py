@@ -37,6 +37,7 @@ SIGNATURES = {
     "fsda_upload_x": [_P, _I64, _I64, _PI64, _PI64],
     "fsda_upload_laplacian": [_P, _I64, _PI64, _PI64, _PD],
     "fsda_set_labels": [_P, _PI8],
+    "fsda_upload_problem": [_P, _I64, _I64, _PI64, _PI64, _PI64, _PI64, _PD, _PI8],
     "fsda_set_label_mask": [_P, _PI8],
     "fsda_matvec": [_P, _PD, _PD],
     "fsda_matvec_transpose": [_P, _PD, _PD],

@@ -207,7 +207,7 @@ struct fsda_ctx {
   DevBuf<int> x_rowptr, x_cols, csc_colptr, csc_rows;
   // upload scratch (persistent so that repeated uploads of same-size data do
   // not reallocate and the cached solve graph stays valid)
-  DevBuf<long long> scratch_i64;
+  DevBuf<long long> scratch_i64, scratch_l64;  // raw int64 indices of X / of L
   DevBuf<double> scratch_f64;
   DevBuf<int> scratch_row_of, scratch_keys;
   DevBuf<unsigned char> scratch_sort;
@@ -252,6 +252,7 @@ struct fsda_ctx {
   // side stream (low priority) + events for the shift update forked beside
   // the sparse kernels inside the solve graph
   cudaStream_t side = nullptr;
+  cudaEvent_t ev_lfork = nullptr, ev_lcopy = nullptr;  // combined upload: L's copies on `side`
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   CgScalars* sc = nullptr;
 
@@ -1198,15 +1199,20 @@ int check_err_flag(fsda_ctx* c, const char* what) {
 // Upload an int64 index array and narrow it to int32 on the device.
 // int64 host indices -> int32 device indices (range-checked into c->err).
 // Asynchronous: tmp must stay allocated until the stream has passed it.
-void upload_narrow_async(fsda_ctx* c, const int64_t* host, long long n, long long limit,
-                         DevBuf<int>& out, long long* tmp) {
+// int64 indices already on the device (tmp) -> int32 `out`, range-checked.
+void narrow_async(fsda_ctx* c, const long long* tmp, long long n, long long limit, DevBuf<int>& out) {
   out.ensure(n + 8);  // tail padding: the row kernels stage indices with 16-byte loads
   CK(cudaMemsetAsync(out.ptr + n, 0, 8 * sizeof(int), c->stream));
   if (n == 0) return;
-  CK(cudaMemcpyAsync(tmp, host, sizeof(long long) * n, cudaMemcpyHostToDevice, c->stream));
   int g = (int)std::min<long long>(cdiv(n, 256), (long long)c->num_sms * 32);
   k_narrow_idx<<<g, 256, 0, c->stream>>>(tmp, out.ptr, n, limit, c->err.ptr);
   CKL();
+}
+
+void upload_narrow_async(fsda_ctx* c, const int64_t* host, long long n, long long limit,
+                         DevBuf<int>& out, long long* tmp) {
+  if (n > 0) CK(cudaMemcpyAsync(tmp, host, sizeof(long long) * n, cudaMemcpyHostToDevice, c->stream));
+  narrow_async(c, tmp, n, limit, out);
 }
 
 
@@ -1262,6 +1268,8 @@ int fsda_ctx_create(fsda_ctx** out, int device, void* stream) {
     CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, lo_prio));
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_lfork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_lcopy, cudaEventDisableTiming));
     c->err.ensure(1);
     CK(cudaMemset(c->err.ptr, 0, sizeof(int)));
   } catch (CudaError& ce) {
@@ -1282,6 +1290,7 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     DevBuf<int>* ib[] = {&c->x_rowptr, &c->x_cols, &c->csc_colptr, &c->csc_rows, &c->l_rowptr,
                          &c->l_cols, &c->active, &c->good, &c->pending, &c->flip, &c->err};
     c->scratch_i64.release();
+    c->scratch_l64.release();
     c->scratch_f64.release();
     c->scratch_row_of.release();
     c->scratch_keys.release();
@@ -1316,6 +1325,8 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     if (c->side) cudaStreamDestroy(c->side);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->ev_lfork) cudaEventDestroy(c->ev_lfork);
+    if (c->ev_lcopy) cudaEventDestroy(c->ev_lcopy);
     if (c->own_stream) cudaStreamDestroy(c->stream);
   }
   delete c;
@@ -1338,9 +1349,10 @@ int fsda_ctx_set_stream(fsda_ctx* c, void* stream) {
   API_END
 }
 
-int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* row_offsets,
-                  const int64_t* col_indices) {
-  API_BEGIN(c)
+// X upload; `after_h2d` (optional) runs once X's copies are enqueued — the
+// combined upload uses it to start the Laplacian's copies behind them.
+static int upload_x_impl(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* row_offsets,
+                         const int64_t* col_indices, void (*after_h2d)(void*), void* hook_arg) {
   if (n_rows < 0 || n_cols < 0) return fail(FSDA_EINVAL, "matrix shape must be non-negative");
   if (!row_offsets) return fail(FSDA_EINVAL, "row_offsets is null");
   const long long nnz = row_offsets[n_rows];
@@ -1361,6 +1373,7 @@ int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* ro
   c->scratch_i64.ensure(std::max<long long>(n_rows + 1 + nnz, 1));
   upload_narrow_async(c, row_offsets, n_rows + 1, nnz, c->x_rowptr, c->scratch_i64.ptr);
   upload_narrow_async(c, col_indices, nnz, n_cols - 1, c->x_cols, c->scratch_i64.ptr + n_rows + 1);
+  if (after_h2d) after_h2d(hook_arg);
   build_seg_plan(c->plan_xr, c->stream, row_offsets, n_rows, c->x_cols.ptr);
   tr.mark("x: row plan (host)");
   CK(cudaStreamSynchronize(c->stream));
@@ -1417,12 +1430,18 @@ int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* ro
 
   c->has_x = true;
   return FSDA_OK;
+}
+
+int fsda_upload_x(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* row_offsets,
+                  const int64_t* col_indices) {
+  API_BEGIN(c)
+  return upload_x_impl(c, n_rows, n_cols, row_offsets, col_indices, nullptr, nullptr);
   API_END
 }
 
 static int upload_laplacian_rows(fsda_ctx* c, int64_t n, int64_t n_global, int64_t row_base,
                                  const int64_t* row_offsets, const int64_t* col_indices,
-                                 const double* values) {
+                                 const double* values, bool prefetched = false) {
   if (!c->has_x) return fail(FSDA_EINVAL, "upload X before the Laplacian");
   if (n != c->n) return fail(FSDA_EINVAL, "laplacian must be square with one row per sample");
   if (row_base < 0 || row_base + n > n_global)
@@ -1440,14 +1459,21 @@ static int upload_laplacian_rows(fsda_ctx* c, int64_t n, int64_t n_global, int64
   Trace tr;
   // H2D, narrowing and the diagonal split run on the stream while the host
   // builds the row plan.
-  c->scratch_i64.ensure(std::max<long long>(n + 1 + nnz, 1));
-  upload_narrow_async(c, row_offsets, n + 1, nnz, c->l_rowptr, c->scratch_i64.ptr);
-  upload_narrow_async(c, col_indices, nnz, n_global - 1, c->l_cols, c->scratch_i64.ptr + n + 1);
+  if (prefetched) {
+    // the raw arrays were copied on the side stream (l_prefetch)
+    CK(cudaStreamWaitEvent(c->stream, c->ev_lcopy, 0));
+    narrow_async(c, c->scratch_l64.ptr, n + 1, nnz, c->l_rowptr);
+    narrow_async(c, c->scratch_l64.ptr + n + 1, nnz, n_global - 1, c->l_cols);
+  } else {
+    c->scratch_l64.ensure(std::max<long long>(n + 1 + nnz, 1));
+    upload_narrow_async(c, row_offsets, n + 1, nnz, c->l_rowptr, c->scratch_l64.ptr);
+    upload_narrow_async(c, col_indices, nnz, n_global - 1, c->l_cols, c->scratch_l64.ptr + n + 1);
+  }
   c->l_diag.ensure(n);
   if (n > 0) {
     c->scratch_f64.ensure(std::max<long long>(nnz, 1));
     double* dvals = c->scratch_f64.ptr;
-    if (nnz > 0)
+    if (nnz > 0 && !prefetched)
       CK(cudaMemcpyAsync(dvals, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, c->stream));
     k_laplacian_split<<<grid_for(n, 256), 256, 0, c->stream>>>(c->l_rowptr.ptr, c->l_cols.ptr, dvals,
                                                                c->l_diag.ptr, (int)n, c->err.ptr,
@@ -1468,6 +1494,59 @@ int fsda_upload_laplacian(fsda_ctx* c, int64_t n, const int64_t* row_offsets,
                           const int64_t* col_indices, const double* values) {
   API_BEGIN(c)
   return upload_laplacian_rows(c, n, n, 0, row_offsets, col_indices, values);
+  API_END
+}
+
+namespace {
+struct LPrefetch {
+  fsda_ctx* c;
+  long long n, nnz;
+  const int64_t* offs;
+  const int64_t* cols;
+  const double* vals;
+};
+
+// The Laplacian's raw arrays to device scratch on the side stream, queued
+// behind X's copies, so they cross the link while X's CSC and plans build.
+void l_prefetch(void* arg) {
+  LPrefetch* a = static_cast<LPrefetch*>(arg);
+  fsda_ctx* c = a->c;
+  c->scratch_l64.ensure(std::max<long long>(a->n + 1 + a->nnz, 1));
+  c->scratch_f64.ensure(std::max<long long>(a->nnz, 1));
+  CK(cudaEventRecord(c->ev_lfork, c->stream));
+  CK(cudaStreamWaitEvent(c->side, c->ev_lfork, 0));
+  CK(cudaMemcpyAsync(c->scratch_l64.ptr, a->offs, sizeof(long long) * (a->n + 1), cudaMemcpyHostToDevice,
+                     c->side));
+  if (a->nnz > 0) {
+    CK(cudaMemcpyAsync(c->scratch_l64.ptr + a->n + 1, a->cols, sizeof(long long) * a->nnz,
+                       cudaMemcpyHostToDevice, c->side));
+    CK(cudaMemcpyAsync(c->scratch_f64.ptr, a->vals, sizeof(double) * a->nnz, cudaMemcpyHostToDevice, c->side));
+  }
+  CK(cudaEventRecord(c->ev_lcopy, c->side));
+}
+}  // namespace
+
+static int set_labels_impl(fsda_ctx* c, const int8_t* labels, bool require_first);
+
+int fsda_upload_problem(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* x_offsets,
+                        const int64_t* x_cols, const int64_t* l_offsets, const int64_t* l_cols,
+                        const double* l_values, const int8_t* labels) {
+  API_BEGIN(c)
+  if (!l_offsets || !labels) return fail(FSDA_EINVAL, "laplacian row_offsets / labels are null");
+  if (n_rows < 0) return fail(FSDA_EINVAL, "matrix shape must be non-negative");
+  const long long l_nnz = l_offsets[n_rows];
+  if (l_offsets[0] != 0 || l_nnz < 0) return fail(FSDA_EINVAL, "row_offsets must be non-decreasing from 0 to nnz");
+  if (l_nnz >= (1LL << 31) - 1) return fail(FSDA_EINVAL, "Laplacian too large for int32 indices");
+  if (l_nnz > 0 && (!l_cols || !l_values)) return fail(FSDA_EINVAL, "laplacian arrays are null");
+  LPrefetch pf{c, n_rows, l_nnz, l_offsets, l_cols, l_values};
+  int rc = upload_x_impl(c, n_rows, n_cols, x_offsets, x_cols, l_prefetch, &pf);
+  if (rc) {
+    CK(cudaStreamSynchronize(c->side));  // the prefetch (if issued) reads host memory of this call
+    return rc;
+  }
+  rc = upload_laplacian_rows(c, n_rows, n_rows, 0, l_offsets, l_cols, l_values, true);
+  if (rc) return rc;
+  return set_labels_impl(c, labels, true);
   API_END
 }
 

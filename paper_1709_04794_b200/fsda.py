@@ -167,6 +167,25 @@ class Device:
         """Upload p.x, p.lap and p.labels.  With reuse=True, objects already
         resident (same immutable objects as the last load) are not re-sent."""
         last_x, last_l, last_lab = self._loaded
+        if not (reuse and (p.x is last_x or p.lap is last_l)):
+            # all three travel: one call, L's copies overlapped with X's processing
+            x, m = p.x, (p.lap.matrix if hasattr(p.lap, "matrix") else p.lap)
+            binary = x.is_binary if hasattr(x, "is_binary") else bool(np.all(np.asarray(x.values) == 1.0))
+            if not binary:
+                raise ValueError("the B200 FSDA path needs a binary X (every stored value 1)")
+            if int(m.n_rows) != int(x.n_rows):
+                raise ValueError("laplacian must be square with one row per sample")
+            lab = np.ascontiguousarray(getattr(p.labels, "labels", p.labels), dtype=np.int8)
+            if lab.size != int(x.n_rows):
+                raise ValueError(f"labels cover {lab.size} samples but x has {int(x.n_rows)} rows")
+            xo, xc = _i64(x.row_offsets), _i64(x.col_indices)
+            lo, lc, lv = _i64(m.row_offsets), _i64(m.col_indices), _f64(m.values)
+            _raise_for(_capi.lib().fsda_upload_problem(
+                self._h, int(x.n_rows), int(x.n_cols), _capi.i64ptr(xo), _capi.i64ptr(xc),
+                _capi.i64ptr(lo), _capi.i64ptr(lc), _capi.dptr(lv), _capi.i8ptr(lab)), fam)
+            self.n, self.d = int(x.n_rows), int(x.n_cols)
+            self._loaded = (p.x, p.lap, p.labels)
+            return
         if not (reuse and p.x is last_x):
             self.upload_x(p.x, fam)
             last_l = last_lab = None

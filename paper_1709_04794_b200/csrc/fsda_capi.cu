@@ -398,7 +398,7 @@ SegArgs seg_args(const double* src, double* out) {
 
 // X^T z: mode 0 raw (+ optional sum(z) leaves), 1 centred with *sum_ptr, 2 / ell.
 void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* sum_ptr, int guarded,
-            double* sum_part) {
+            double* sum_part, double* sum_out = nullptr) {
   fsda_ctx* c = e.c;
   const double bytes = 4.0 * (c->d + 1) + 4.0 * c->nnz + 8.0 * c->n + 8.0 * c->d +
                        (mode == 1 ? 8.0 * c->d : 0.0);
@@ -416,9 +416,7 @@ void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* sum
     const CgScalars* sc = c->sc;
     int n_rows = (int)c->n;
     unsigned long long* ticket = c->xt_ticket.ptr;
-    void* args[] = {(void*)&pl, (void*)&xh, (void*)&a, (void*)&sc, (void*)&guarded, (void*)&n_rows,
-                    (void*)&ticket};
-    (void)args;
+
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c->xt_blocks);
     cfg.blockDim = dim3(XT_THREADS);
@@ -431,7 +429,7 @@ void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* sum
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.numAttrs = (pdl_mode() & 2) ? 2 : 1;
     cfg.attrs = at;
-    CK(cudaLaunchKernelEx(&cfg, k_xt_coop, pl, xh, a, sc, guarded, n_rows, ticket));
+    CK(cudaLaunchKernelEx(&cfg, k_xt_coop, pl, xh, a, sc, guarded, n_rows, ticket, sum_out));
   });
 }
 
@@ -471,7 +469,7 @@ size_t step_smem(int ns) { return sizeof(double) * 3 * (size_t)std::max(ns, 1); 
 // Cooperative launch of k_cg_step (capturable into graphs).
 // center: 0 none, 1 FSDA (q - mu sum z), 2 SA-SDA (q - 1_l sum z / l)
 void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, int use_cond,
-                    int center) {
+                    int center, const double* sum_ready = nullptr) {
   ShiftState ss = c->shifts();
   const long long nlD = n_leaves(d);
   double* q = c->q.ptr;
@@ -488,10 +486,7 @@ void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, i
   const long long nlz = center ? n_leaves(c->n) : 0;
   const signed char* lab = c->labels.ptr;
   double ell = (double)c->ell;
-  void* args[] = {(void*)&q, (void*)&p, (void*)&r0, (void*)&r1, (void*)&bigp, (void*)&sols,
-                  (void*)&d, (void*)&pp, (void*)&pr, (void*)&nlD, (void*)&sc, (void*)&ss,
-                  (void*)&ns, (void*)&cond, (void*)&use_cond, (void*)&mu, (void*)&pz, (void*)&nlz,
-                  (void*)&lab, (void*)&ell};
+
   const size_t smem = step_smem(ns);
   // One warp per 256-element leaf (the leaf's p, q, r stay in registers across
   // the two grid barriers); warps loop over further leaves only when d exceeds
@@ -505,7 +500,6 @@ void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, i
   }
   const long long want = (nlD + STEP_THREADS / 32 - 1) / (STEP_THREADS / 32);
   const int blocks = (int)std::max(1LL, std::min<long long>(want, c->step_blocks));
-  (void)args;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(blocks);
   cfg.blockDim = dim3(STEP_THREADS);
@@ -519,7 +513,7 @@ void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, i
   cfg.numAttrs = (pdl_mode() & 4) ? 2 : 1;
   cfg.attrs = at;
   CK(cudaLaunchKernelEx(&cfg, k_cg_step, q, p, r0, r1, bigp, sols, d, pp, pr, nlD, sc, ss, ns, cond,
-                        use_cond, mu, pz, nlz, lab, ell));
+                        use_cond, mu, pz, nlz, lab, ell, sum_ready));
 }
 
 // The shift-state update of the last base step (k_shift_update) on `stream`.
@@ -539,7 +533,8 @@ void launch_shift_update(fsda_ctx* c, int ns, long long d, cudaStream_t stream, 
 // it follows the base step on the same stream.
 template <typename Sparse>
 void enq_iteration_body(Enq& e, int ns, long long d, int center, unsigned long long cond,
-                        int use_cond, double step_bytes, Sparse&& sparse) {
+                        int use_cond, double step_bytes, Sparse&& sparse,
+                        const double* sum_ready = nullptr) {
   fsda_ctx* c = e.c;
   const double su_bytes = 32.0 * d * ns + 8.0 * d;
   static const bool inline_su = std::getenv("FSDA_B200_SU_INLINE") != nullptr;
@@ -550,10 +545,10 @@ void enq_iteration_body(Enq& e, int ns, long long d, int center, unsigned long l
     CK(cudaEventRecord(c->ev_join, c->side));
     sparse();
     CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
-    e.go("cg_step", step_bytes, [&] { launch_cg_step(c, ns, d, cond, use_cond, center); });
+    e.go("cg_step", step_bytes, [&] { launch_cg_step(c, ns, d, cond, use_cond, center, sum_ready); });
   } else {
     sparse();
-    e.go("cg_step", step_bytes, [&] { launch_cg_step(c, ns, d, cond, use_cond, center); });
+    e.go("cg_step", step_bytes, [&] { launch_cg_step(c, ns, d, cond, use_cond, center, sum_ready); });
     e.go("shift_update", su_bytes, [&] { launch_shift_update(c, ns, d, c->stream, 1); });
   }
 }
@@ -562,11 +557,15 @@ void enq_iteration_body(Enq& e, int ns, long long d, int center, unsigned long l
 void enq_fsda_iteration(Enq& e, double alpha, int ns, unsigned long long cond, int use_cond) {
   fsda_ctx* c = e.c;
   const long long d = c->d;
+  // k_xt_coop's last CTA reduces sum(z) for the CG step's centring
+  // (FSDA_B200_K3_SUM=0: the CG step reduces it)
+  static const bool k3_sum = !std::getenv("FSDA_B200_K3_SUM") || std::atoi(std::getenv("FSDA_B200_K3_SUM"));
+  double* sum_out = k3_sum ? &c->sc->sum_z_iter : nullptr;
   enq_iteration_body(e, ns, d, 1, cond, use_cond, 8.0 * c->n + 24.0 * d + 24.0 * d + 24.0 * d, [&] {
     enq_xrows(e, c->p.ptr, c->y.ptr, 1);
     enq_smoother(e, alpha, c->y.ptr, c->z.ptr, 1);
-    enq_xt(e, c->z.ptr, c->q.ptr, 0, nullptr, 1, c->part_n.ptr);
-  });
+    enq_xt(e, c->z.ptr, c->q.ptr, 0, nullptr, 1, c->part_n.ptr, sum_out);
+  }, sum_out);
 }
 
 // Setup (labeled mean, rhs, CG init) — sda.py:297-301, krylov.py:185-208.

@@ -51,6 +51,7 @@ struct CgScalars {
   double b_norm;
   double thresh;
   double sum_z;       // sum(z) of the current smoother output / apply_w output
+  double sum_z_iter;  // sum(z) of the loop's smoother output, reduced by k_xt_coop's last CTA
   double class_mean1; // apply_w class means (sda.py:126-127)
   double class_mean2;
   double tol;

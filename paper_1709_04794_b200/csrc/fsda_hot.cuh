@@ -482,7 +482,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan pl, XtDense dn, SegArgs a,
                                                     const CgScalars* sc, int guarded, int n_rows,
-                                                    unsigned long long* ticket) {
+                                                    unsigned long long* ticket, double* sum_out) {
   pdl_trigger();
   pdl_wait();
   if (guarded && loop_idle(sc)) return;  // uniform across the grid
@@ -579,6 +579,13 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
   XT_MARK(3)
   if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0ULL;  // every warp has drawn its last ticket
   const long long nwarps = (long long)gridDim.x * nw;
+  // sum(z) from its leaf partials (the CG step's centring needs it): the last
+  // CTA, whose warps hold the fewest dense columns, reduces it with the same
+  // tree as k_cg_step's block_reduce_partials would
+  if (sum_out && blockIdx.x == gridDim.x - 1) {
+    const double s = block_reduce_partials(a.sum_part, (a.sum_n + LEAF - 1) / LEAF, zs);
+    if (threadIdx.x == 0) *sum_out = s;
+  }
   // ---- phase 2: dense columns.  Columns with more than XT_BIG_PARTS leaf
   // sums (the Zipf head at large N) are reduced by a whole CTA each
   // (block_reduce_partials: the same R256 tree, leaves spread over the warps),
@@ -666,7 +673,7 @@ __global__ void __launch_bounds__(STEP_THREADS) k_cg_step(
     double* __restrict__ part_pq, double* __restrict__ part_rr, long long n_leaf, CgScalars* sc,
     ShiftState ss, int ns, unsigned long long cond_handle, int use_cond,
     const double* __restrict__ mu, const double* __restrict__ part_z, long long n_leaf_z,
-    const signed char* __restrict__ labels, double ell) {
+    const signed char* __restrict__ labels, double ell, const double* sum_ready) {
   extern __shared__ double dyn[];  // zn[ns], gs[ns], good[ns] (as double)
   __shared__ double smem[257];
   __shared__ int s_flag;
@@ -727,7 +734,7 @@ __global__ void __launch_bounds__(STEP_THREADS) k_cg_step(
   // M z - 1_l (sum(M z) / l) (sda.py:155-157); then the p.q leaves
   double sz = 0.0;
   if (center) {
-    const double sum_z = block_reduce_partials(part_z, n_leaf_z, smem);
+    const double sum_z = sum_ready ? *sum_ready : block_reduce_partials(part_z, n_leaf_z, smem);
     sz = mu ? sum_z : sum_z / ell;
   }
   if (own) {

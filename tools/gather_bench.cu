@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(256) k_gather_smem(const int* __restrict__ idx
   if (acc == 12345.0) out[0] = acc;
 }
 
-int main() {
+int main(int argc, char** argv) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const long long n = 1LL << 25;  // 33.5M gathers
@@ -123,6 +123,21 @@ int main() {
     return best;
   };
   const int grid = sms * 8;
+  if (argc > 2) {  // real index stream: raw int32 file, table size
+    FILE* f = fopen(argv[1], "rb");
+    std::vector<int> idx;
+    int v;
+    while (fread(&v, 4, 1, f) == 1) idx.push_back(v);
+    fclose(f);
+    const long long m = (long long)idx.size() & ~7LL;
+    const long long T = atoll(argv[2]);
+    CK(cudaMemcpy(didx, idx.data(), m * sizeof(int), cudaMemcpyHostToDevice));
+    float ms8 = timeit([&] { k_gather<8><<<grid, 256>>>(didx, m, dtab, dout); });
+    float ms4 = timeit([&] { k_gather<4><<<grid, 256>>>(didx, m, dtab, dout); });
+    printf("file %s: %lld gathers, table %lld: U8 %.1f us (%.1f G/s), U4 %.1f us (%.1f G/s)\n", argv[1], m, T,
+           ms8 * 1e3, m / (ms8 * 1e-3) / 1e9, ms4 * 1e3, m / (ms4 * 1e-3) / 1e9);
+    return 0;
+  }
   {
     const long long T = 200000;
     for (long long i = 0; i < n; ++i) h[i] = (int)(rng() % T);

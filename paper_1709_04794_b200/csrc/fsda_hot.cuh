@@ -190,12 +190,21 @@ __device__ __forceinline__ double seg_term(const SegArgs& a, int seg, int idx, d
   return v;
 }
 
+// The row's own loads that seg_finish needs (L rows: the masked y_i), issued
+// with the task so they do not add a round trip after the reduction.
 template <int KIND>
-__device__ __forceinline__ void seg_finish(const SegArgs& a, int seg, double s) {
+__device__ __forceinline__ double seg_pre(const SegArgs& a, int seg) {
+  if (KIND != SEG_LROWS) return 0.0;
+  const signed char l = __ldg(a.labels + seg);
+  const double y = __ldg(a.src + seg + a.row_base);
+  return l != 0 ? y : 0.0;
+}
+
+template <int KIND>
+__device__ __forceinline__ void seg_finish(const SegArgs& a, int seg, double s, double masked) {
   if (KIND == SEG_XROWS) {
     a.out[seg] = s;
   } else if (KIND == SEG_LROWS) {
-    const double masked = a.labels[seg] != 0 ? a.src[seg + a.row_base] : 0.0;
     const double smoothed = a.alpha * s;
     a.out[seg] = (a.alpha_mode == 1) ? smoothed : (1.0 - a.alpha) * masked + smoothed;
   } else {
@@ -203,6 +212,11 @@ __device__ __forceinline__ void seg_finish(const SegArgs& a, int seg, double s) 
     else if (a.mode == 2) s = s / a.ell;
     a.out[seg] = s;
   }
+}
+
+template <int KIND>
+__device__ __forceinline__ void seg_finish(const SegArgs& a, int seg, double s) {
+  seg_finish<KIND>(a, seg, s, seg_pre<KIND>(a, seg));
 }
 
 // Canonical leaf of segment elements [start, start+n) (n <= 8W) by a W-lane
@@ -256,8 +270,10 @@ __device__ __forceinline__ void seg_class_task(const SegPlan& pl, const SegArgs&
   const long long idx = pl.cls_off[cls] + (tw - pl.warp_base[cls]) * (32 / W) + lane / W;
   int4 tk = make_int4(-1, 0, 0, -1);
   if (idx < pl.cls_off[cls + 1]) tk = __ldg(pl.tasks + idx);
+  const bool leader = tk.x >= 0 && (lane & (W - 1)) == 0;
+  const double pre = leader ? seg_pre<KIND>(a, tk.x) : 0.0;
   const double s = group_leaf<W, KIND>(pl, a, tk.x, tk.y, tk.z, lane & (W - 1));
-  if (tk.x >= 0 && (lane & (W - 1)) == 0) seg_finish<KIND>(a, tk.x, s);
+  if (leader) seg_finish<KIND>(a, tk.x, s, pre);
 }
 
 template <int KIND>

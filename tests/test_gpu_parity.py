@@ -419,3 +419,35 @@ def test_label_set_batch_matches_oracle_and_permuted_reference():
         rr = ref_numpy.fsda_solve(prob, w.alpha, w.betas, w.tol, 15, seed)
         assert rel_rows(r.directions, rr["directions"]) <= 1e-6
         assert rel_rows(r.scores, rr["scores"][:, inv]) <= 1e-6
+
+
+def test_combined_upload_errors_then_recovers():
+    """fsda_solve(p) uploads X, L and labels in one call (fsda_upload_problem,
+    L's copies on the side stream).  Out-of-range indices in X or in L are
+    reported as FSDA_EINVAL by the C ABI, and the same context then solves a
+    valid problem bit for bit."""
+    from paper_1709_04794_b200 import _capi
+
+    w, p = _tiny_problem()
+    dev = fb.Device(0)
+    lib = _capi.lib()
+    i64 = lambda a: np.ascontiguousarray(a, dtype=np.int64)
+    lab = np.ascontiguousarray(w.labels, dtype=np.int8)
+    lv = np.ascontiguousarray(w.l_vals, dtype=np.float64)
+    for which in ("x", "l"):
+        xc, lc = i64(w.x_cols).copy(), i64(w.l_cols).copy()
+        if which == "x":
+            xc[-1] = w.d + 5
+        else:
+            lc[-1] = w.n + 3
+        rc = lib.fsda_upload_problem(dev._h, w.n, w.d, _capi.i64ptr(i64(w.x_offsets)), _capi.i64ptr(xc),
+                                     _capi.i64ptr(i64(w.l_offsets)), _capi.i64ptr(lc), _capi.dptr(lv),
+                                     _capi.i8ptr(lab))
+        assert rc == _capi.FSDA_EINVAL, (which, rc, _capi.last_error())
+        # X: the range check; L: the range check or, when the changed entry was
+        # the diagonal, the unit-weight check (both flag the same upload)
+        assert _capi.last_error().startswith("X: index out of range" if which == "x" else "laplacian: ")
+    rep = fb.fsda_solve(p, device=dev)
+    ref = c_oracle.fsda_solve(w.x_offsets, w.x_cols, w.d, w.l_offsets, w.l_cols, w.l_vals,
+                              w.labels, p.alpha, p.betas.betas, p.tol, p.max_iter_d, w.probe())
+    np.testing.assert_array_equal(_dirs(rep, p.betas.betas), ref["directions"])

@@ -184,6 +184,7 @@ struct GraphBufs {
   DevBuf<unsigned char> temp;
   DevBuf<long long> offs, cols, count;
   long long n = 0, nnz = 0;
+  double tail_avg = 0.0;  // tail-column occurrences per row of the last build
   cublasHandle_t blas = nullptr;
   void release() {
     head_of.release(); cand.release(); ncand.release(); nbr.release(); rsize.release(); tsize.release(); A.release();
@@ -2435,7 +2436,6 @@ extern "C" int fsda_debug_xt_trace(int on, unsigned long long* out) {
 // ---------------------------------------------------------------- k-NN graph
 // graph.py:152-166 knn_graph on the context's X (fsda_upload_x first).
 namespace {
-constexpr int KNN_HEAD_MAX = 4096;  // head columns counted on the tensor cores
 
 #define CKB(x)                                                                  \
   do {                                                                          \
@@ -2461,7 +2461,28 @@ int graph_blocks(fsda_ctx* c, GraphBufs& g, F per_block) {
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
     return colptr[a + 1] - colptr[a] > colptr[b + 1] - colptr[b];
   });
-  const int nh = (int)std::min<size_t>(order.size(), KNN_HEAD_MAX);
+  // Head width: the int8 GEMM costs 2 N^2 H ops (~4e15/s measured); every
+  // tail occurrence costs ~0.4-0.6 ns in the sorted-runs path, ~6 ns once a
+  // row's occurrences overflow the shared-memory sort.  Pick the cheapest.
+  std::vector<double> sq(order.size() + 1, 0.0);  // sq[h] = sum over ranks >= h of n_c^2
+  for (long long h = (long long)order.size() - 1; h >= 0; --h) {
+    const double nc = (double)(colptr[order[h] + 1] - colptr[order[h]]);
+    sq[h] = sq[h + 1] + nc * nc;
+  }
+  int nh = 0;
+  double best = 1e300;
+  for (int cand : {256, 512, 1024, 2048, 4096, 8192, 16384}) {
+    const int hc = (int)std::min<size_t>(order.size(), (size_t)cand);
+    const double occ = sq[hc], avg = n > 0 ? occ / (double)n : 0.0;
+    const double per = avg <= KNN_TAIL_CAP_BIG / 2 ? (avg <= KNN_TAIL_CAP / 2 ? 0.4e-9 : 0.6e-9) : 6e-9;
+    const double est = 2.0 * (double)n * (double)n * hc / 4e15 + occ * per;
+    if (est < best) {
+      best = est;
+      nh = hc;
+    }
+    if ((size_t)cand >= order.size()) break;
+  }
+  g.tail_avg = n > 0 ? sq[nh] / (double)n : 0.0;
   const int H = nh > 0 ? (nh + 15) & ~15 : 0;  // GEMM depth padded to 16 (zero columns)
   std::vector<int> head_of((size_t)std::max<long long>(d, 1), -1);
   for (int h = 0; h < nh; ++h) head_of[order[h]] = h;
@@ -2482,6 +2503,13 @@ int graph_blocks(fsda_ctx* c, GraphBufs& g, F per_block) {
   k_knn_tsize<<<grid_for(n, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr, g.head_of.ptr,
                                                       g.tsize.ptr, (int)n);
   CKL();
+  {
+    const int big = (int)(sizeof(int) * KNN_TAIL_CAP_BIG * KNN_REFINE_WARPS_BIG);
+    CK(cudaFuncSetAttribute(k_knn_refine<KNN_TAIL_CAP_BIG, KNN_REFINE_WARPS_BIG>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_graph_threshold<KNN_TAIL_CAP_BIG, KNN_REFINE_WARPS_BIG>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+  }
   if (H > 0) {
     g.A.ensure(n16 * H);
     g.C.ensure(B * n16);
@@ -2559,9 +2587,19 @@ extern "C" int fsda_graph_knn(fsda_ctx* c, int32_t k, int64_t* nnz_out) {
     } else {
       CK(cudaMemsetAsync(g.ncand.ptr, 0, sizeof(int) * nb, c->stream));
     }
-    k_knn_refine<<<(unsigned)cdiv(nb, KNN_REFINE_WARPS), KNN_REFINE_WARPS * 32, 0, c->stream>>>(
-        C, (int)ldc, (int)r0, (int)nb, (int)n, c->x_rowptr.ptr, c->x_cols.ptr, c->csc_colptr.ptr,
-        c->csc_rows.ptr, g.head_of.ptr, k, g.cand.ptr, g.ncand.ptr, g.nbr.ptr);
+    if (g.tail_avg <= KNN_TAIL_CAP / 2) {
+      k_knn_refine<KNN_TAIL_CAP, KNN_REFINE_WARPS>
+          <<<(unsigned)cdiv(nb, KNN_REFINE_WARPS), KNN_REFINE_WARPS * 32,
+             sizeof(int) * KNN_TAIL_CAP * KNN_REFINE_WARPS, c->stream>>>(
+              C, (int)ldc, (int)r0, (int)nb, (int)n, c->x_rowptr.ptr, c->x_cols.ptr, c->csc_colptr.ptr,
+              c->csc_rows.ptr, g.head_of.ptr, k, g.cand.ptr, g.ncand.ptr, g.nbr.ptr);
+    } else {
+      k_knn_refine<KNN_TAIL_CAP_BIG, KNN_REFINE_WARPS_BIG>
+          <<<(unsigned)cdiv(nb, KNN_REFINE_WARPS_BIG), KNN_REFINE_WARPS_BIG * 32,
+             sizeof(int) * KNN_TAIL_CAP_BIG * KNN_REFINE_WARPS_BIG, c->stream>>>(
+              C, (int)ldc, (int)r0, (int)nb, (int)n, c->x_rowptr.ptr, c->x_cols.ptr, c->csc_colptr.ptr,
+              c->csc_rows.ptr, g.head_of.ptr, k, g.cand.ptr, g.ncand.ptr, g.nbr.ptr);
+    }
     CKL();
   });
   if (rc) return rc;
@@ -2593,9 +2631,19 @@ extern "C" int fsda_graph_threshold(fsda_ctx* c, double theta, int64_t* nnz_out)
     CK(cudaMemsetAsync(g.count.ptr, 0, sizeof(long long), c->stream));
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(g.count.ptr);
     int rc = graph_blocks(c, g, [&](long long r0, long long nb, long long ldc, const int* C) {
-      k_graph_threshold<<<(unsigned)cdiv(nb, KNN_REFINE_WARPS), KNN_REFINE_WARPS * 32, 0, c->stream>>>(
-          C, (int)ldc, (int)r0, (int)nb, (int)n, g.rsize.ptr, c->x_rowptr.ptr, c->x_cols.ptr,
-          c->csc_colptr.ptr, c->csc_rows.ptr, g.head_of.ptr, g.tsize.ptr, theta, g.keys.ptr, cnt, cap);
+      if (g.tail_avg <= KNN_TAIL_CAP / 2) {
+        k_graph_threshold<KNN_TAIL_CAP, KNN_REFINE_WARPS>
+            <<<(unsigned)cdiv(nb, KNN_REFINE_WARPS), KNN_REFINE_WARPS * 32,
+               sizeof(int) * KNN_TAIL_CAP * KNN_REFINE_WARPS, c->stream>>>(
+                C, (int)ldc, (int)r0, (int)nb, (int)n, g.rsize.ptr, c->x_rowptr.ptr, c->x_cols.ptr,
+                c->csc_colptr.ptr, c->csc_rows.ptr, g.head_of.ptr, g.tsize.ptr, theta, g.keys.ptr, cnt, cap);
+      } else {
+        k_graph_threshold<KNN_TAIL_CAP_BIG, KNN_REFINE_WARPS_BIG>
+            <<<(unsigned)cdiv(nb, KNN_REFINE_WARPS_BIG), KNN_REFINE_WARPS_BIG * 32,
+               sizeof(int) * KNN_TAIL_CAP_BIG * KNN_REFINE_WARPS_BIG, c->stream>>>(
+                C, (int)ldc, (int)r0, (int)nb, (int)n, g.rsize.ptr, c->x_rowptr.ptr, c->x_cols.ptr,
+                c->csc_colptr.ptr, c->csc_rows.ptr, g.head_of.ptr, g.tsize.ptr, theta, g.keys.ptr, cnt, cap);
+      }
       CKL();
     });
     if (rc) return rc;

@@ -169,14 +169,19 @@ __device__ __forceinline__ int knn_intersect(const int* ai, int ni, const int* _
 }
 
 constexpr int KNN_ROW_SMEM = 512;   // row supports up to this long are staged in shared memory
-constexpr int KNN_TAIL_CAP = 2048;  // tail-candidate occurrences sorted in shared memory per row
+// tail-candidate occurrences sorted in shared memory per row: two kernel
+// shapes, picked per build from the average occurrences per row
+constexpr int KNN_TAIL_CAP = 2048;       // 4 warps per CTA, 32 KB
 constexpr int KNN_REFINE_WARPS = 4;
+constexpr int KNN_TAIL_CAP_BIG = 8192;   // 2 warps per CTA, 64 KB
+constexpr int KNN_REFINE_WARPS_BIG = 2;
 
 // The rows occurring in row i's tail columns (its support entries whose column
 // is not a head column), concatenated into buf and sorted ascending (warp
 // bitonic sort, padded with INT_MAX to a power of two).  Returns the number
 // of occurrences m; when m > KNN_TAIL_CAP the buffer holds only a prefix and
 // is left unsorted (callers fall back to direct intersections).
+template <int CAP>
 __device__ __forceinline__ int knn_tail_sorted(const int* ai, int ni, const int* __restrict__ head_of,
                                                const int* __restrict__ colptr,
                                                const int* __restrict__ rows, int* buf, int lane) {
@@ -186,11 +191,11 @@ __device__ __forceinline__ int knn_tail_sorted(const int* ai, int ni, const int*
     if (head_of[col] >= 0) continue;
     const int clo = colptr[col], len = colptr[col + 1] - clo;
     for (int t = lane; t < len; t += 32)
-      if (m + t < KNN_TAIL_CAP) buf[m + t] = rows[clo + t];
+      if (m + t < CAP) buf[m + t] = rows[clo + t];
     m += len;
   }
   __syncwarp();
-  if (m > KNN_TAIL_CAP) return m;
+  if (m > CAP) return m;
   int P = 32;
   while (P < m) P <<= 1;
   for (int t = m + lane; t < P; t += 32) buf[t] = 0x7fffffff;
@@ -231,18 +236,19 @@ __device__ __forceinline__ int knn_mult(const int* buf, int m, int j) {
 // lists of row i: those occurrences are sorted in shared memory (warp bitonic
 // sort) and counted as runs.  Rows with more than KNN_TAIL_CAP occurrences
 // intersect the two supports directly instead.
-__global__ void __launch_bounds__(KNN_REFINE_WARPS * 32) k_knn_refine(
+template <int CAP, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_knn_refine(
     const int* __restrict__ C, int ldc, int r0, int nb, int n, const int* __restrict__ rowptr,
     const int* __restrict__ cols, const int* __restrict__ colptr, const int* __restrict__ rows,
     const int* __restrict__ head_of, int k, const int* __restrict__ cand, const int* __restrict__ ncand,
     int* __restrict__ nbr) {
-  __shared__ double s_s[KNN_REFINE_WARPS][KNN_MAX_K];
-  __shared__ int s_j[KNN_REFINE_WARPS][KNN_MAX_K];
-  __shared__ int s_c[KNN_REFINE_WARPS];
-  __shared__ int s_row[KNN_REFINE_WARPS][KNN_ROW_SMEM];
-  __shared__ int s_buf[KNN_REFINE_WARPS][KNN_TAIL_CAP];
+  __shared__ double s_s[WARPS][KNN_MAX_K];
+  __shared__ int s_j[WARPS][KNN_MAX_K];
+  __shared__ int s_c[WARPS];
+  __shared__ int s_row[WARPS][KNN_ROW_SMEM];
+  extern __shared__ int s_tail[];  // WARPS * CAP
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x * KNN_REFINE_WARPS + warp;
+  const int b = blockIdx.x * WARPS + warp;
   if (b >= nb) return;
   const int i = r0 + b;
   if (lane == 0) s_c[warp] = 0;
@@ -253,9 +259,9 @@ __global__ void __launch_bounds__(KNN_REFINE_WARPS * 32) k_knn_refine(
   const int* ai = staged ? s_row[warp] : cols + lo_i;
   const int* crow = C + (long long)b * ldc;
   KnnList L{s_s[warp], s_j[warp], &s_c[warp], k};
-  int* buf = s_buf[warp];
-  const int m = knn_tail_sorted(ai, ni, head_of, colptr, rows, buf, lane);
-  if (m <= KNN_TAIL_CAP) {
+  int* buf = s_tail + warp * CAP;
+  const int m = knn_tail_sorted<CAP>(ai, ni, head_of, colptr, rows, buf, lane);
+  if (m <= CAP) {
     // runs: j with its multiplicity = shared tail columns
     for (int t0 = 0; t0 < m; t0 += 32) {
       const int t = t0 + lane;
@@ -339,16 +345,17 @@ __global__ void __launch_bounds__(KNN_REFINE_WARPS * 32) k_knn_refine(
 // a direct intersection when row i has more than KNN_TAIL_CAP of them) and
 // the exact fp64 quotient.  Hits are appended to keys as row * n + col
 // (warp-aggregated atomic); the symmetrization sorts them.
-__global__ void __launch_bounds__(KNN_REFINE_WARPS * 32) k_graph_threshold(
+template <int CAP, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_graph_threshold(
     const int* __restrict__ C, int ldc, int r0, int nb, int n, const int* __restrict__ rsize,
     const int* __restrict__ rowptr, const int* __restrict__ cols, const int* __restrict__ colptr,
     const int* __restrict__ rows, const int* __restrict__ head_of, const int* __restrict__ tsize,
     double theta, unsigned long long* __restrict__ keys, unsigned long long* __restrict__ count,
     unsigned long long cap) {
-  __shared__ int s_row[KNN_REFINE_WARPS][KNN_ROW_SMEM];
-  __shared__ int s_buf[KNN_REFINE_WARPS][KNN_TAIL_CAP];
+  __shared__ int s_row[WARPS][KNN_ROW_SMEM];
+  extern __shared__ int s_tail[];  // WARPS * CAP
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x * KNN_REFINE_WARPS + warp;
+  const int b = blockIdx.x * WARPS + warp;
   if (b >= nb) return;
   const int i = r0 + b;
   const int lo_i = rowptr[i], ni = rowptr[i + 1] - lo_i;
@@ -356,8 +363,8 @@ __global__ void __launch_bounds__(KNN_REFINE_WARPS * 32) k_graph_threshold(
   for (int e = lane; e < ni && staged; e += 32) s_row[warp][e] = cols[lo_i + e];
   __syncwarp();
   const int* ai = staged ? s_row[warp] : cols + lo_i;
-  int* buf = s_buf[warp];
-  const int m = knn_tail_sorted(ai, ni, head_of, colptr, rows, buf, lane);
+  int* buf = s_tail + warp * CAP;
+  const int m = knn_tail_sorted<CAP>(ai, ni, head_of, colptr, rows, buf, lane);
   const int ti = tsize[i];
   const float th_f = (float)(theta * (1.0 - 1e-5));
   const int4* row4 = C ? reinterpret_cast<const int4*>(C + (long long)b * ldc) : nullptr;
@@ -383,7 +390,7 @@ __global__ void __launch_bounds__(KNN_REFINE_WARPS * 32) k_graph_threshold(
         const int c = cs[q], nj = ns[q];
         const int cu = c + min(ti, tt[q]);  // the exact count is at most this
         if (cu > 0 && (float)cu >= th_f * (float)(ni + nj - cu)) {
-          const int ce = m <= KNN_TAIL_CAP ? c + knn_mult(buf, m, j)
+          const int ce = m <= CAP ? c + knn_mult(buf, m, j)
                                            : knn_intersect(ai, ni, cols, rowptr[j], rowptr[j + 1]);
           hit = ce > 0 && (double)ce / ((double)(ni + nj) - (double)ce) >= theta;
         }

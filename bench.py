@@ -40,7 +40,9 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "full reg-sweep FSDA solves/sec"
 UNIT = "solves/s"
-GATHER_CEILING = 315e9   # random 8-byte gathers/s, L2-resident table (profiles/r01_gather_ceiling.md)
+GATHER_CEILING = 315e9        # random 8-byte gathers/s, L2-resident table (profiles/r01_gather_ceiling.md)
+SMEM_GATHER_CEILING = 735e9   # the same from a shared-memory table
+XT_ROW_BLOCK, XT_DENSE_PER_BLOCK = 8192, 8   # the X^T blocked-column rule (csrc/fsda_hot.cuh)
 
 
 def parse():
@@ -334,17 +336,25 @@ def run_b200(args):
                         for k in kernels},
         }
         # the bound that actually binds the gather kernels: random 8-byte gathers
-        # of an L2-resident vector, measured by tools/gather_bench.cu
-        # (profiles/r01_gather_ceiling.md); one gather per index-stream entry
-        gathers = {"xt": w.nnz, "spmv_rows": w.nnz, "smoother": int(w.l_cols.size)}.get(top["name"])
-        if gathers:
-            gps = gathers / (top["ms"] * 1e-3)
+        # at the rates tools/gather_bench.cu measures (profiles/r01_gather_ceiling.md):
+        # ~315 G/s from L2, ~735 G/s from shared memory.  X^T serves its dense
+        # (Zipf-head) columns from shared-memory z blocks and the rest from L2, so
+        # its floor is light / 315 G + dense / 735 G; frac = floor / measured time.
+        if top["name"] in ("xt", "spmv_rows", "smoother"):
+            if top["name"] == "xt":
+                counts = np.bincount(w.x_cols, minlength=w.d)
+                nb = -(-w.n // XT_ROW_BLOCK)
+                dense = int(counts[(counts > 256) & (counts >= XT_DENSE_PER_BLOCK * nb)].sum())
+                light = w.nnz - dense
+            else:
+                dense, light = 0, (w.nnz if top["name"] == "spmv_rows" else int(w.l_cols.size))
+            floor_s = light / GATHER_CEILING + dense / SMEM_GATHER_CEILING
             roofline["gather_ceiling"] = {
-                "gathers_per_launch": gathers, "achieved_gathers_per_s": gps,
-                "ceiling_gathers_per_s": GATHER_CEILING, "frac": gps / GATHER_CEILING,
-                "source": "profiles/r01_gather_ceiling.md (uniform random 8-byte gathers of a 1.56 MB "
-                          "L2-resident table; the dense-column share of X^T gathers comes from shared "
-                          "memory instead)"}
+                "l2_gathers_per_launch": light, "smem_gathers_per_launch": dense,
+                "ceiling_l2_gathers_per_s": GATHER_CEILING, "ceiling_smem_gathers_per_s": SMEM_GATHER_CEILING,
+                "floor_ms": floor_s * 1e3, "frac": floor_s / (top["ms"] * 1e-3),
+                "source": "profiles/r01_gather_ceiling.md (uniform random 8-byte gathers: 1.56 MB "
+                          "L2-resident table; 32 KB shared-memory table)"}
         pair = [k for k in kernels if k["name"] in ("spmv_rows", "xt")]   # K1 + K3
         pb = sum(k["bytes"] for k in pair)
         pt = sum(k["ms"] for k in pair)

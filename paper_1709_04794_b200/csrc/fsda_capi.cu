@@ -227,6 +227,7 @@ struct fsda_ctx {
   int xt_blocks = 0;
   DevBuf<unsigned long long> xt_ticket;  // phase-1b work ticket (reset by the kernel)
   int step_blocks = 0;  // cooperative grid of k_cg_step
+  bool batch_attrs_set = false;  // kb_* dynamic shared-memory opt-in done on this device
 
   // L: CSR with diagonal entries in place, diag values split out.  Row-sharded
   // contexts hold rows [row_base, row_base + n) of an n_global-row L.
@@ -539,6 +540,13 @@ void enq_iteration_body(Enq& e, int ns, long long d, int center, unsigned long l
   fsda_ctx* c = e.c;
   const double su_bytes = 32.0 * d * ns + 8.0 * d;
   static const bool inline_su = std::getenv("FSDA_B200_SU_INLINE") != nullptr;
+  // timing experiment only (results wrong): no per-iteration shift update
+  const bool skip_su = std::getenv("FSDA_B200_EXP_SKIP_SU") != nullptr;
+  if (skip_su) {
+    sparse();
+    e.go("cg_step", step_bytes, [&] { launch_cg_step(c, ns, d, cond, use_cond, center, sum_ready); });
+    return;
+  }
   if (use_cond && !inline_su) {
     CK(cudaEventRecord(c->ev_fork, c->stream));
     CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
@@ -859,9 +867,12 @@ long long launch_solve(fsda_ctx* c, double alpha, int ns, long long max_iter, do
       // launches = fixed + body * iterations; iterations known after sync
       c->last_launch_count = -(fixed * 1000000LL + body);  // decoded by fetch
       return 0;
-    } catch (CudaError&) {
-      cudaGetLastError();
+    } catch (CudaError& ce) {
       c->invalidate_graph();
+      // only "conditional nodes unsupported" switches to the eager loop; any
+      // other error (OOM, a fault from an earlier launch) is reported
+      if (ce.err != cudaErrorNotSupported && ce.err != cudaErrorCallRequiresNewerDriver) throw;
+      cudaGetLastError();
       c->cond_supported = false;  // fall through to eager
     }
   }
@@ -1363,6 +1374,12 @@ static int upload_x_impl(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int6
   if (n_rows > MAX_REDUCE || n_cols > MAX_REDUCE)
     return fail(FSDA_EINVAL, "vector length above the two-level reduction limit (%lld)", MAX_REDUCE);
   c->has_x = false;
+  if (n_rows != c->n) {
+    // the Laplacian and the labels on the device are sized for the old N
+    c->has_l = false;
+    c->has_labels = false;
+    c->n1 = c->n2 = c->ell = 0;
+  }
   CK(cudaMemset(c->err.ptr, 0, sizeof(int)));
   c->n = n_rows;
   c->d = n_cols;
@@ -1528,6 +1545,28 @@ void l_prefetch(void* arg) {
 
 static int set_labels_impl(fsda_ctx* c, const int8_t* labels, bool require_first);
 
+// Host-side label checks (values in {+1, -1, 0}; labeled rows first when
+// required); counts the classes.
+static int check_labels(const int8_t* labels, long long n, bool require_first, long long* n1_out,
+                        long long* n2_out) {
+  long long n1 = 0, n2 = 0;
+  bool seen_unlabeled = false, labeled_first = true;
+  for (long long i = 0; i < n; ++i) {
+    int8_t l = labels[i];
+    if (l != 0 && l != 1 && l != -1) return fail(FSDA_ELABEL, "labels must take values in {+1, -1, 0}");
+    if (l == 1) ++n1;
+    if (l == -1) ++n2;
+    if (l == 0) seen_unlabeled = true;
+    else if (seen_unlabeled) labeled_first = false;
+  }
+  if (require_first && !labeled_first)
+    return fail(FSDA_EINVAL,
+                "labeled samples must occupy the first rows; use arrange_labeled_first to permute the problem");
+  *n1_out = n1;
+  *n2_out = n2;
+  return FSDA_OK;
+}
+
 int fsda_upload_problem(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* x_offsets,
                         const int64_t* x_cols, const int64_t* l_offsets, const int64_t* l_cols,
                         const double* l_values, const int8_t* labels) {
@@ -1538,6 +1577,12 @@ int fsda_upload_problem(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64
   if (l_offsets[0] != 0 || l_nnz < 0) return fail(FSDA_EINVAL, "row_offsets must be non-decreasing from 0 to nnz");
   if (l_nnz >= (1LL << 31) - 1) return fail(FSDA_EINVAL, "Laplacian too large for int32 indices");
   if (l_nnz > 0 && (!l_cols || !l_values)) return fail(FSDA_EINVAL, "laplacian arrays are null");
+  {
+    // the labels are checked before anything on the device is replaced
+    long long n1 = 0, n2 = 0;
+    int lrc = check_labels(labels, n_rows, true, &n1, &n2);
+    if (lrc) return lrc;
+  }
   LPrefetch pf{c, n_rows, l_nnz, l_offsets, l_cols, l_values};
   int rc = upload_x_impl(c, n_rows, n_cols, x_offsets, x_cols, l_prefetch, &pf);
   if (rc) {
@@ -1561,18 +1606,9 @@ int fsda_upload_laplacian_rows(fsda_ctx* c, int64_t n_local, int64_t n_global, i
 static int set_labels_impl(fsda_ctx* c, const int8_t* labels, bool require_first) {
   if (!c->has_x) return fail(FSDA_EINVAL, "upload X before the labels");
   long long n1 = 0, n2 = 0;
-  bool seen_unlabeled = false, labeled_first = true;
-  for (long long i = 0; i < c->n; ++i) {
-    int8_t l = labels[i];
-    if (l != 0 && l != 1 && l != -1) return fail(FSDA_ELABEL, "labels must take values in {+1, -1, 0}");
-    if (l == 1) ++n1;
-    if (l == -1) ++n2;
-    if (l == 0) seen_unlabeled = true;
-    else if (seen_unlabeled) labeled_first = false;
-  }
-  if (require_first && !labeled_first)
-    return fail(FSDA_EINVAL,
-                "labeled samples must occupy the first rows; use arrange_labeled_first to permute the problem");
+  int rc = check_labels(labels, c->n, require_first, &n1, &n2);
+  if (rc) return rc;
+  c->has_labels = false;
   c->labels.ensure(std::max<long long>(c->n, 1));
   if (c->n > 0)
     CK(cudaMemcpyAsync(c->labels.ptr, labels, c->n, cudaMemcpyHostToDevice, c->stream));
@@ -2251,14 +2287,13 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
       CKL();
     }
   };
-  static bool attrs_set = false;
-  if (!attrs_set) {
+  if (!c->batch_attrs_set) {  // per context: the attribute binds to the current device
     const int big = (int)(sizeof(double) * BLK_SM);
     CK(cudaFuncSetAttribute(kb_vec_leaves, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(kb_step_a, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(kb_step_b, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(kb_combine_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, big / 2));
-    attrs_set = true;
+    c->batch_attrs_set = true;
   }
   const size_t sm_dot = sizeof(double) * BLK_SM, sm_sum = sm_dot / 2;
   auto combine = [&](const double* part, long long nl, double* out) {

@@ -167,6 +167,9 @@ class Device:
         """Upload p.x, p.lap and p.labels.  With reuse=True, objects already
         resident (same immutable objects as the last load) are not re-sent."""
         last_x, last_l, last_lab = self._loaded
+        # a failed upload leaves the device state unknown: nothing counts as
+        # resident until this load succeeds
+        self._loaded = (None, None, None)
         if not (reuse and (p.x is last_x or p.lap is last_l)):
             # all three travel: one call, L's copies overlapped with X's processing
             x, m = p.x, (p.lap.matrix if hasattr(p.lap, "matrix") else p.lap)

@@ -156,7 +156,18 @@ def install_into_sdakit_graph(graph_module=None):
     knn_graph / threshold_graph and the names its callers bound at import
     (cli.py:29, synthetic.py:21, __init__.py:24-27)."""
     g = graph_module or importlib.import_module("sdakit.graph")
-    g.knn_graph = knn_graph
+    original = getattr(g.knn_graph, "__wrapped_reference__", g.knn_graph)
+
+    def knn_graph_routed(x, k, *args, **kwargs):
+        # the device ranking keeps at most 64 neighbours per row: larger k stays
+        # on sdakit's own function, so installing never narrows what callers get
+        if int(k) > 64:
+            return original(x, k, *args, **kwargs)
+        return knn_graph(x, k, *args, **kwargs)
+
+    knn_graph_routed.__wrapped_reference__ = original
+    knn_graph_routed.__doc__ = knn_graph.__doc__
+    g.knn_graph = knn_graph_routed
     g.threshold_graph = threshold_graph
     for mod in ("sdakit", "sdakit.cli", "sdakit.synthetic"):
         try:
@@ -164,7 +175,7 @@ def install_into_sdakit_graph(graph_module=None):
         except Exception:
             continue
         if hasattr(m, "knn_graph"):
-            m.knn_graph = knn_graph
+            m.knn_graph = knn_graph_routed
         if hasattr(m, "threshold_graph"):
             m.threshold_graph = threshold_graph
     return g

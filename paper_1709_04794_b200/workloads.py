@@ -99,6 +99,26 @@ def _first_distinct(row: np.ndarray, cand: np.ndarray, width: int, want: np.ndar
     return r[keep], cand[pos][keep], np.flatnonzero(got < want)
 
 
+def _searchsorted_threads(cdf: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """np.searchsorted(cdf, u, side="right") over host threads (numpy
+    releases the GIL there); identical output, the draws stay sequential."""
+    if u.size < 4_000_000:
+        return np.searchsorted(cdf, u, side="right")
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+
+    parts = np.array_split(u, min(32, os.cpu_count() or 1) * 2)
+    out = np.empty(u.size, dtype=np.int64)
+    bounds = np.cumsum([0] + [a.size for a in parts])
+
+    def one(k):
+        out[bounds[k]:bounds[k + 1]] = np.searchsorted(cdf, parts[k], side="right")
+
+    with ThreadPoolExecutor(min(32, os.cpu_count() or 1)) as ex:
+        list(ex.map(one, range(len(parts))))
+    return out
+
+
 def zipf_binary_rows(n: int, d: int, lam: float, s: float, seed: int):
     """CSR (offsets, cols) of the binary X described in the module docstring."""
     rng = np.random.default_rng(seed)
@@ -107,7 +127,7 @@ def zipf_binary_rows(n: int, d: int, lam: float, s: float, seed: int):
     cdf /= cdf[-1]
     m = 2 * counts + 8
     row = np.repeat(np.arange(n, dtype=np.int64), m)
-    cand = np.minimum(np.searchsorted(cdf, rng.random(row.size), side="right"), d - 1)
+    cand = np.minimum(_searchsorted_threads(cdf, rng.random(row.size)), d - 1)
     rows, cols, short = _first_distinct(row, cand.astype(np.int64), d, counts)
     if short.size:  # rare: successive sampling row by row for the leftovers
         extra_r, extra_c = [], []
@@ -152,20 +172,25 @@ def random_knn_laplacian(n: int, k: int, seed: int):
             ec.append(pick.astype(np.int64))
         src = np.concatenate([src] + er)
         dst = np.concatenate([dst] + ec)
-    keys = np.unique(np.concatenate([src * n + dst, dst * n + src]))
+    keys = np.sort(np.concatenate([src * n + dst, dst * n + src]))
+    keep = np.ones(keys.size, dtype=bool)
+    keep[1:] = keys[1:] != keys[:-1]
+    keys = keys[keep]                                # np.unique, without its slow path
     a_rows, a_cols = keys // n, keys % n
     deg = np.bincount(a_rows, minlength=n).astype(np.int64)
     # L = D - S with the diagonal at its sorted position; isolated vertices store nothing.
     has_d = deg > 0
     d_idx = np.flatnonzero(has_d)
-    all_rows = np.concatenate([a_rows, d_idx])
-    all_cols = np.concatenate([a_cols, d_idx])
-    all_vals = np.concatenate([np.full(a_rows.size, -1.0), deg[d_idx].astype(np.float64)])
-    order = np.lexsort((all_cols, all_rows))
-    l_rows = all_rows[order]
+    # every (row, col) key is unique, so one sort of the keys is the
+    # (row, col) lexicographic order
+    all_keys = np.sort(np.concatenate([keys, d_idx * n + d_idx]))
+    l_rows, l_cols = all_keys // n, all_keys % n
+    diag = l_rows == l_cols
+    l_vals = np.full(all_keys.size, -1.0)
+    l_vals[diag] = deg[l_rows[diag]].astype(np.float64)
     offsets = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(np.bincount(l_rows, minlength=n), out=offsets[1:])
-    return offsets, all_cols[order].astype(np.int64), all_vals[order], deg
+    return offsets, l_cols.astype(np.int64), l_vals, deg
 
 
 def labels_first(n: int, ell: int, n_pos: int, seed: int) -> np.ndarray:

@@ -183,9 +183,17 @@ def test_graph_install_and_reference_types():
 
         saved = rg.knn_graph, sdakit.knn_graph, rsyn.knn_graph
         try:
+            original = rg.knn_graph
             fb.install_into_sdakit_graph(rg)
-            assert rg.knn_graph is fb.knn_graph
-            assert sdakit.knn_graph is fb.knn_graph and rsyn.knn_graph is fb.knn_graph
+            routed = rg.knn_graph
+            assert routed.__wrapped_reference__ is original
+            assert sdakit.knn_graph is routed and rsyn.knn_graph is routed
+            # k > 64 stays on sdakit's own function (the device ranking keeps <= 64)
+            x = RSM(70, 2, np.arange(71), np.zeros(70, dtype=np.int64), np.ones(70))
+            got, want = routed(x, 65), original(x, 65)
+            assert got.adjacency == want.adjacency and got.n == 70
+            fb.install_into_sdakit_graph(rg)      # idempotent: still wraps the original
+            assert rg.knn_graph.__wrapped_reference__ is original
         finally:
             rg.knn_graph, sdakit.knn_graph, rsyn.knn_graph = saved
         from paper_1709_04794_b200.graph import _graph_types

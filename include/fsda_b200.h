@@ -126,6 +126,18 @@ int fsda_solve(fsda_ctx* ctx, double alpha, const double* betas, int n_shifts,
                int64_t* iterations, uint8_t* converged, int64_t* n_applies,
                int64_t* fail_iter);
 
+/* Shift-update mode of the shifted-CG solves on this context (krylov.py:230,
+ * 240-241).  1: every iteration streams sols_s -= gamma_s P_s and
+ * P_s = zeta_next r + alpha_s P_s over all D elements of every active shift.
+ * 2 (deferred): the residuals r_0 .. r_K are kept, each iteration updates
+ * only the coefficient rows of P_s and sols_s in that basis, and the
+ * directions sols_s = sum_j c_s[j] r_j are formed once after the loop
+ * (ascending j).  0 (default): 2 when the basis fits a quarter of the free
+ * device memory, else 1.  Both are mirrored by oracle/fsda_oracle.c. */
+int fsda_set_shift_update_mode(fsda_ctx* ctx, int mode);
+/* The mode (1 or 2) the last solve on this context used. */
+int fsda_last_shift_update_mode(fsda_ctx* ctx);
+
 /* Device-resident variant for throughput measurement: launches one complete
  * solve on the context stream and returns without copying results to the
  * host (inputs already resident in HBM).  Results stay in the context and can

@@ -74,8 +74,30 @@ def lib():
                                         _PI64, _PU8, _PI64, _PI64]
         h.oracle_max_threads.restype = C.c_int
         h.oracle_max_threads.argtypes = []
+        h.oracle_set_deferred.restype = None
+        h.oracle_set_deferred.argtypes = [C.c_int]
+        h.oracle_set_deferred(1 if _shift_mode == 2 else 0)
         _lib = h
     return _lib
+
+
+# Shift-update mode mirrored from the device (fsda_set_shift_update_mode):
+# 1 per-iteration sols / P updates, 2 deferred basis (the device default
+# whenever the basis fits; tests force the device's mode to match).
+_shift_mode = 2
+
+
+def set_shift_mode(mode: int) -> None:
+    global _shift_mode
+    if mode not in (1, 2):
+        raise ValueError("shift mode must be 1 or 2")
+    _shift_mode = mode
+    if _lib is not None:
+        _lib.oracle_set_deferred(1 if mode == 2 else 0)
+
+
+def shift_mode() -> int:
+    return _shift_mode
 
 
 def _d(a):

@@ -73,9 +73,11 @@ class Problem:
         return self.centered_t(mu, self.smoother(alpha, self.x.dot(w)))
 
 
-def shifted_cg(apply, b, betas, tol, max_iter, absolute_tol=False):
+def shifted_cg(apply, b, betas, tol, max_iter, absolute_tol=False, on_iter=None):
     """Multi-shift CG, krylov.py:168-281, per-shift columns kept as rows of
-    (n_shifts, dim) arrays; every update rounds as the reference's does."""
+    (n_shifts, dim) arrays; every update rounds as the reference's does.
+    ``on_iter(i, sols)`` (optional, the noise-floor tool) sees the solutions
+    after iteration i — what a run with max_iter = i + 1 returns."""
     betas = np.asarray(betas, dtype=np.float64)
     ns, dim = betas.size, b.size
     b_norm = float(np.linalg.norm(b))                              # krylov.py:185
@@ -137,6 +139,8 @@ def shifted_cg(apply, b, betas, tol, max_iter, absolute_tol=False):
             else:
                 zeta_prev[s], zeta[s] = zeta[s], zn[s]
         gamma_prev, alpha, rr = gamma, alpha_new, rr_new
+        if on_iter is not None:
+            on_iter(i, sols)
         if not active.any():
             break
     for s in np.flatnonzero(active):                               # krylov.py:272-275
@@ -146,13 +150,16 @@ def shifted_cg(apply, b, betas, tol, max_iter, absolute_tol=False):
                 n_applies=n_applies)
 
 
-def fsda_solve(prob: Problem, alpha, betas, tol, max_iter, seed=0):
-    """sda.py:293-320 on raw arrays; directions/scores rows are shifts."""
+def fsda_solve(prob: Problem, alpha, betas, tol, max_iter, seed=0, on_iter=None, operator=None):
+    """sda.py:293-320 on raw arrays; directions/scores rows are shifts.
+    ``operator(alpha, mu, w)`` replaces prob.operator (the noise-floor tool
+    perturbs it)."""
     rng = np.random.default_rng(seed)                              # sda.py:297
     mu = prob.labeled_mean()                                       # sda.py:298
     r = rng.uniform(-1.0, 1.0, size=prob.d)                        # sda.py:300
     rhs = prob.centered_t(mu, prob.apply_w(prob.x.dot(r)))         # sda.py:301
-    out = shifted_cg(lambda w: prob.operator(alpha, mu, w), rhs, betas, tol, max_iter)
+    op = operator or prob.operator
+    out = shifted_cg(lambda w: op(alpha, mu, w), rhs, betas, tol, max_iter, on_iter=on_iter)
     y = prob.labels.astype(np.float64)
     scores = np.empty((len(betas), prob.n))
     for s in range(len(betas)):                                    # sda.py:277-283
@@ -162,6 +169,16 @@ def fsda_solve(prob: Problem, alpha, betas, tol, max_iter, seed=0):
             out["directions"][s] = -out["directions"][s]
         scores[s] = sv
     out["scores"] = scores
+    return out
+
+
+def orient(prob: Problem, directions):
+    """The sign rule of sda.py:277-283 applied to a stack of directions."""
+    y = prob.labels.astype(np.float64)
+    out = np.array(directions, copy=True)
+    for s in range(out.shape[0]):
+        if float(y @ prob.x.dot(out[s])) < 0.0:
+            out[s] = -out[s]
     return out
 
 

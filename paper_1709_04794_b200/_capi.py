@@ -48,6 +48,8 @@ SIGNATURES = {
     "fsda_solve": [_P, _D, _PD, C.c_int, _D, _I64, _PD, _PD, _PD, _PD, _PI64, _PU8, _PI64, _PI64],
     "fsda_prepare_resident": [_P, _D, _PD, C.c_int, _D, _I64, _PD],
     "fsda_solve_async": [_P],
+    "fsda_set_shift_update_mode": [_P, C.c_int],
+    "fsda_last_shift_update_mode": [_P],
     "fsda_fetch_results": [_P, _PD, _PD, _PD, _PI64, _PU8, _PI64, _PI64, _PI64],
     "fsda_profile_kernels": [_P, C.c_int, _PI, C.POINTER(C.c_char_p), _PD, _PD, _PI64],
     "fsda_shifted_cg_dense": [_P, _I64, _PD, _PD, _PD, C.c_int, _D, _I64, C.c_int, _PD, _PD,

@@ -562,6 +562,93 @@ __global__ void kb_cg_init_vec(const double* __restrict__ b, double* __restrict_
   }
 }
 
+// Deferred ("basis") shift updates for the batch (the single-solve
+// k_coef_update / k_combine_basis per task): coefficient rows
+// coef[(t * ns + s) * ld + j].  Init: a = e_0, c = 0.
+__global__ void kb_coef_init(double* __restrict__ coef_a, double* __restrict__ coef_c,
+                             long long rows, long long ld) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < rows * ld;
+       e += (long long)gridDim.x * blockDim.x) {
+    coef_a[e] = (e % ld) == 0 ? 1.0 : 0.0;
+    coef_c[e] = 0.0;
+  }
+}
+
+// r = p = b only (the deferred mode keeps no P / sols during the loop).
+__global__ void kb_cg_init_rp(const double* __restrict__ b, double* __restrict__ r,
+                              double* __restrict__ p, long long len) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < len;
+       k += (long long)gridDim.x * blockDim.x) {
+    const double v = b[k];
+    r[k] = v;
+    p[k] = v;
+  }
+}
+
+// Coefficient updates of loop iteration `it` for the tasks that stepped
+// (kb_step_c's shift part on coefficients).  blockIdx.y = (task, shift).
+__global__ void kb_coef_update(BatchState B, const int* __restrict__ stepped, double* __restrict__ coef_a,
+                               double* __restrict__ coef_c, long long ld, long long it) {
+  const int k = blockIdx.y;
+  const int t = k / B.ns;
+  if (!stepped[t]) return;
+  const int mode = B.upd_mode[k];
+  if (mode == 0) return;
+  const double gs = B.upd_gs[k], zn = B.upd_zn[k], as = B.upd_as[k];
+  double* A = coef_a + (long long)k * ld;
+  double* Cc = coef_c + (long long)k * ld;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j <= it + 1;
+       j += (long long)gridDim.x * blockDim.x) {
+    if (j <= it) {
+      const double a = A[j];
+      Cc[j] = Cc[j] - a * gs;
+      if (mode == 3) A[j] = as * a;
+    } else if (mode == 3 && j < ld) {
+      A[j] = zn;
+    }
+  }
+}
+
+// p = r_next + alpha_new p for the tasks that stepped (kb_step_c without the
+// shift state).
+__global__ void kb_step_c_p(const double* __restrict__ r_next, double* __restrict__ p, long long len,
+                            int tp, BatchState B, const int* __restrict__ stepped) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < len;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(k % tp);
+    if (stepped[t]) p[k] = r_next[k] + B.alpha_new[t] * p[k];
+  }
+}
+
+// sols[(i * tp + t) * ns + s] = sum_{j < iter_t} c[t][s][j] * r_j[i * tp + t],
+// j ascending from 0.0, one fma per term — the single solve's k_combine_basis
+// per task.
+__global__ void __launch_bounds__(256) kb_combine_basis(const double* __restrict__ rb, long long d,
+                                                        BatchState B, const double* __restrict__ coef_c,
+                                                        long long ld, double* __restrict__ sols) {
+  const int tp = B.tp, ns = B.ns;
+  const long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= d * tp) return;
+  const int t = (int)(x % tp);
+  const long long J = B.status[t] == ST_OK ? B.iter[t] : 0;
+  const long long stride = d * tp;
+  for (int s0 = 0; s0 < ns; s0 += 8) {
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    const double* cc = coef_c + ((long long)t * ns + s0) * ld;
+    for (long long j = 0; j < J; ++j) {
+      const double r = __ldcs(rb + j * stride + x);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (s0 + u < ns) acc[u] = fma(__ldg(cc + (long long)u * ld + j), r, acc[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (s0 + u < ns) sols[x * ns + s0 + u] = acc[u];
+  }
+}
+
 // b.b arrives in bb[t] (krylov.py:185-194).
 __global__ void kb_cg_init_scalars(BatchState B, const double* __restrict__ bb, double tol) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;

@@ -155,6 +155,7 @@ struct HostPlan {
 struct BatchBufs {
   DevBuf<signed char> lab;
   DevBuf<double> ind, P, Q, R0, R1, MU, Bv, PR, Y, Z, BIGP, SOLS, SCORES, OUT;
+  DevBuf<double> RB, CA, CC;  // deferred mode: residual slots, coefficient rows
   DevBuf<double> partD, partN, part2, hpart, xpart, opart, scal;
   DevBuf<long long> lscal;
   DevBuf<int> iscal;
@@ -168,6 +169,7 @@ struct BatchBufs {
     lab.release(); ind.release(); P.release(); Q.release(); R0.release(); R1.release();
     MU.release(); Bv.release(); PR.release(); Y.release(); Z.release(); BIGP.release();
     SOLS.release(); SCORES.release(); OUT.release(); partD.release(); partN.release();
+    RB.release(); CA.release(); CC.release();
     hpart.release(); xpart.release(); opart.release(); scal.release(); lscal.release();
     part2.release();
     iscal.release(); sh_d.release(); sh_l.release(); sh_u.release(); sh_i.release();
@@ -243,7 +245,16 @@ struct fsda_ctx {
   long long n1 = 0, n2 = 0, ell = 0;
 
   // work vectors
-  DevBuf<double> y, z, q, p, r0, r1, mu_v, t, wv, b, ind, probe, part_n, part_d, part_d2, part_o;
+  DevBuf<double> y, z, q, p, mu_v, t, wv, b, ind, probe, part_n, part_d, part_d2, part_o;
+  // residual slots: 2 (ping-pong, per-iteration shift updates) or max_iter + 1
+  // (the stored basis r_0 .. r_K of the deferred shift updates)
+  DevBuf<double> rbuf;
+  int nslots = 2;
+  // shift-update mode: requested (0 auto, 1 per-iteration, 2 deferred basis)
+  // and the one the current solve uses (1 or 2)
+  int su_req = 0, su_mode = 1;
+  DevBuf<double> coef_a, coef_c;
+  long long coef_ld = 1;
   DevBuf<double> bigp, sols, wT, scores, dense_a;
   // per-shift state
   DevBuf<double> beta, zeta_prev, zeta, zeta_next, gamma_s, alpha_s, resid;
@@ -284,6 +295,9 @@ struct fsda_ctx {
     s.resid = resid.ptr; s.iters = iters.ptr; s.conv = conv.ptr; s.active = active.ptr;
     s.good = good.ptr; s.pending = pending.ptr; s.flip = flip.ptr;
     s.upd_mode = upd_mode.ptr; s.upd_gs = upd_gs.ptr; s.upd_zn = upd_zn.ptr; s.upd_as = upd_as.ptr;
+    s.coef_a = su_mode == 2 ? coef_a.ptr : nullptr;
+    s.coef_c = su_mode == 2 ? coef_c.ptr : nullptr;
+    s.coef_ld = coef_ld;
     return s;
   }
 
@@ -340,14 +354,23 @@ struct Enq {
 void ensure_vectors(fsda_ctx* c, int ns) {
   const long long n = std::max<long long>(c->n, 1), d = std::max<long long>(c->d, 1);
   c->y.ensure(n); c->z.ensure(n); c->t.ensure(n); c->wv.ensure(n); c->ind.ensure(n);
-  c->q.ensure(d); c->p.ensure(d); c->r0.ensure(d); c->r1.ensure(d); c->mu_v.ensure(d);
+  c->q.ensure(d); c->p.ensure(d); c->mu_v.ensure(d);
   c->b.ensure(d); c->probe.ensure(d);
   c->part_n.ensure(2 * n_leaves(n) + 2);
   c->part_d.ensure(n_leaves(d) + 1);
   c->part_d2.ensure(n_leaves(d) + 1);
   const int nsx = std::max(ns, 1);
   c->part_o.ensure((size_t)nsx * n_leaves(n) + 1);
-  c->bigp.ensure((size_t)nsx * d); c->sols.ensure((size_t)nsx * d);
+  c->sols.ensure((size_t)nsx * d);
+  if (c->su_mode == 2) {
+    c->bigp.ensure(1);
+    c->rbuf.ensure((size_t)c->nslots * d);
+    c->coef_a.ensure((size_t)nsx * c->coef_ld);
+    c->coef_c.ensure((size_t)nsx * c->coef_ld);
+  } else {
+    c->bigp.ensure((size_t)nsx * d);
+    c->rbuf.ensure((size_t)2 * d);
+  }
   c->wT.ensure((size_t)nsx * d); c->scores.ensure((size_t)nsx * n);
   c->beta.ensure(nsx); c->zeta_prev.ensure(nsx); c->zeta.ensure(nsx); c->zeta_next.ensure(nsx);
   c->gamma_s.ensure(nsx); c->alpha_s.ensure(nsx); c->resid.ensure(nsx); c->iters.ensure(nsx);
@@ -476,8 +499,8 @@ void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, i
   const long long nlD = n_leaves(d);
   double* q = c->q.ptr;
   double* p = c->p.ptr;
-  double* r0 = c->r0.ptr;
-  double* r1 = c->r1.ptr;
+  double* rb = c->rbuf.ptr;
+  int nsl = c->nslots;
   double* bigp = c->bigp.ptr;
   double* sols = c->sols.ptr;
   double* pp = c->part_d.ptr;
@@ -514,18 +537,73 @@ void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, i
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.numAttrs = (pdl_mode() & 4) ? 2 : 1;
   cfg.attrs = at;
-  CK(cudaLaunchKernelEx(&cfg, k_cg_step, q, p, r0, r1, bigp, sols, d, pp, pr, nlD, sc, ss, ns, cond,
+  CK(cudaLaunchKernelEx(&cfg, k_cg_step, q, p, rb, nsl, bigp, sols, d, pp, pr, nlD, sc, ss, ns, cond,
                         use_cond, mu, pz, nlz, lab, ell, sum_ready));
 }
 
-// The shift-state update of the last base step (k_shift_update) on `stream`.
+// The shift-state update of the last base step on `stream`: sols / P
+// streamed (k_shift_update), or, in the deferred mode, the coefficient rows
+// (k_coef_update).
 void launch_shift_update(fsda_ctx* c, int ns, long long d, cudaStream_t stream, int guarded) {
   ShiftState ss = c->shifts();
+  if (c->su_mode == 2) {
+    dim3 g((unsigned)grid_for(c->coef_ld, 256), (unsigned)ns);
+    k_coef_update<<<g, 256, 0, stream>>>(ss, c->sc, ns, guarded);
+    CKL();
+    return;
+  }
   dim3 g((unsigned)((d + 256 * SU_ELEMS - 1) / (256 * SU_ELEMS)),
          (unsigned)((ns + SU_SHIFTS - 1) / SU_SHIFTS));
-  k_shift_update<<<g, 256, 0, stream>>>(c->r0.ptr, c->r1.ptr, c->bigp.ptr, c->sols.ptr, d, ss,
+  k_shift_update<<<g, 256, 0, stream>>>(c->rbuf.ptr, c->nslots, c->bigp.ptr, c->sols.ptr, d, ss,
                                         c->sc, ns, guarded);
   CKL();
+}
+
+// Shift-update mode of a solve with these sizes: the deferred basis needs
+// (max_iter + 1) residuals of d doubles plus two n_s x (max_iter + 1)
+// coefficient tables; it is used when they fit a quarter of the free device
+// memory (FSDA_B200_SHIFT_MODE=1/2 or fsda_set_shift_update_mode force one).
+void resolve_shift_mode(fsda_ctx* c, int ns, long long max_iter, long long d) {
+  int req = c->su_req;
+  if (req == 0 && std::getenv("FSDA_B200_SHIFT_MODE")) req = std::atoi(std::getenv("FSDA_B200_SHIFT_MODE"));
+  int mode = 1;
+  const long long slots = std::max<long long>(max_iter, 0) + 1;
+  const double need = 8.0 * (double)slots * (double)std::max<long long>(d, 1) +
+                      16.0 * (double)std::max(ns, 1) * (double)slots;
+  if (req == 2) {
+    mode = 2;
+  } else if (req == 0) {
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const double have = 8.0 * (double)c->rbuf.cap + 8.0 * (double)(c->coef_a.cap + c->coef_c.cap);
+    mode = need <= 0.25 * (double)free_b + have ? 2 : 1;
+  }
+  c->su_mode = mode;
+  c->nslots = mode == 2 ? (int)std::min<long long>(slots, INT32_MAX) : 2;
+  c->coef_ld = mode == 2 ? slots : 1;
+}
+
+// r_0 = p = b, P_s = b / coefficient rows, sols = 0, b.b (krylov.py:185-208)
+void launch_cg_init(fsda_ctx* c, const double* bsrc, long long d, int ns) {
+  ShiftState ss = c->shifts();
+  const long long nlD = n_leaves(d);
+  dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
+  k_cg_init<<<g, LEAF_THREADS, 0, c->stream>>>(bsrc, c->rbuf.ptr, c->p.ptr, c->bigp.ptr,
+                                               c->sols.ptr, d, c->part_d.ptr, nlD, c->sc, ss, ns,
+                                               c->su_mode == 2 ? 1 : 0);
+  CKL();
+}
+
+// The last iteration's shift update, and in the deferred mode the
+// directions formed from the stored residuals.
+void launch_final_shift(fsda_ctx* c, int ns, long long d) {
+  launch_shift_update(c, ns, d, c->stream, 0);
+  if (c->su_mode == 2 && d > 0) {
+    ShiftState ss = c->shifts();
+    dim3 g((unsigned)grid_for(d, 256), (unsigned)((ns + CB_SH - 1) / CB_SH));
+    k_combine_basis<<<g, 256, 0, c->stream>>>(c->rbuf.ptr, d, ss, c->sc, ns, c->sols.ptr);
+    CKL();
+  }
 }
 
 // One iteration = sparse products `sparse` (K1..K3 or the operator's
@@ -538,7 +616,7 @@ void enq_iteration_body(Enq& e, int ns, long long d, int center, unsigned long l
                         int use_cond, double step_bytes, Sparse&& sparse,
                         const double* sum_ready = nullptr) {
   fsda_ctx* c = e.c;
-  const double su_bytes = 32.0 * d * ns + 8.0 * d;
+  const double su_bytes = c->su_mode == 2 ? 32.0 * ns * (double)c->coef_ld : 32.0 * d * ns + 8.0 * d;
   static const bool inline_su = std::getenv("FSDA_B200_SU_INLINE") != nullptr;
   // timing experiment only (results wrong): no per-iteration shift update
   const bool skip_su = std::getenv("FSDA_B200_EXP_SKIP_SU") != nullptr;
@@ -599,11 +677,7 @@ void enq_fsda_setup(Enq& e, int ns, long long max_iter, double tol) {
         c->labels.ptr, c->wv.ptr, n, c->part_n.ptr, nlN, c->sc);
   });
   enq_xt(e, c->wv.ptr, c->b.ptr, 1, &c->sc->sum_z, 0, nullptr);
-  e.go("cg_init", 8.0 * d * 3 + 16.0 * d * ns, [&] {
-    dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
-    k_cg_init<<<g, LEAF_THREADS, 0, c->stream>>>(c->b.ptr, c->r0.ptr, c->p.ptr, c->bigp.ptr,
-                                                 c->sols.ptr, d, c->part_d.ptr, nlD, c->sc, ss, ns);
-  });
+  e.go("cg_init", 8.0 * d * 3 + 16.0 * d * ns, [&] { launch_cg_init(c, c->b.ptr, d, ns); });
 }
 
 // Projection (sda.py:265-284) and the still-active residuals.
@@ -611,7 +685,8 @@ void enq_fsda_tail(Enq& e, int ns) {
   fsda_ctx* c = e.c;
   const long long n = c->n, d = c->d, nlN = n_leaves(n);
   ShiftState ss = c->shifts();
-  e.go("shift_update", 32.0 * d * ns, [&] { launch_shift_update(c, ns, d, c->stream, 0); });
+  e.go(c->su_mode == 2 ? "combine_basis" : "shift_update", c->su_mode == 2 ? 8.0 * d * (double)c->coef_ld + 8.0 * d * ns : 32.0 * d * ns,
+       [&] { launch_final_shift(c, ns, d); });
   e.go("cg_finish", 0.0, [&] { k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns); });
   e.go("transpose_sols", 16.0 * d * ns, [&] {
     k_transpose_sols<<<grid_for(d * ns, 256), 256, 0, c->stream>>>(c->sols.ptr, c->wT.ptr, d, ns);
@@ -622,8 +697,8 @@ void enq_fsda_tail(Enq& e, int ns) {
   });
   e.go("orient", 8.0 * n * ns + 1.0 * n, [&] {
     dim3 g(grid_for(nlN, WARPS_PER_BLOCK), ns);
-    k_orient<<<g, LEAF_THREADS, 0, c->stream>>>(c->labels.ptr, c->scores.ptr, n, c->part_o.ptr,
-                                                nlN, c->sc, ss, ns, nullptr);
+    k_orient<<<g, LEAF_THREADS, 0, c->stream>>>(c->labels.ptr, c->scores.ptr, n, c->part_o.ptr, nlN);
+    k_orient_final<<<ns, 256, 0, c->stream>>>(c->part_o.ptr, nlN, ss, nullptr);
   });
   e.go("flip", 0.0, [&] {
     dim3 g((unsigned)std::min<long long>(grid_for(std::max(n, d), 256), 1024), ns);
@@ -640,11 +715,7 @@ void enq_reg_setup(Enq& e, int ns, long long max_iter, double tol, int abs_tol) 
   e.go("solve_reset", 0.0, [&] {
     k_solve_reset<<<1, 256, 0, c->stream>>>(c->sc, ss, ns, max_iter, tol, abs_tol);
   });
-  e.go("cg_init", 8.0 * d * 3 + 16.0 * d * ns, [&] {
-    dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
-    k_cg_init<<<g, LEAF_THREADS, 0, c->stream>>>(c->b.ptr, c->r0.ptr, c->p.ptr, c->bigp.ptr,
-                                                 c->sols.ptr, d, c->part_d.ptr, nlD, c->sc, ss, ns);
-  });
+  e.go("cg_init", 8.0 * d * 3 + 16.0 * d * ns, [&] { launch_cg_init(c, c->b.ptr, d, ns); });
 }
 
 void enq_reg_iteration(Enq& e, int ns, unsigned long long cond, int use_cond) {
@@ -659,7 +730,7 @@ void enq_reg_iteration(Enq& e, int ns, unsigned long long cond, int use_cond) {
 void enq_reg_tail(Enq& e, int ns) {
   fsda_ctx* c = e.c;
   ShiftState ss = c->shifts();
-  e.go("shift_update", 32.0 * c->d * ns, [&] { launch_shift_update(c, ns, c->d, c->stream, 0); });
+  e.go(c->su_mode == 2 ? "combine_basis" : "shift_update", 32.0 * c->d * ns, [&] { launch_final_shift(c, ns, c->d); });
   e.go("cg_finish", 0.0, [&] { k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns); });
 }
 
@@ -682,11 +753,7 @@ void enq_sa_setup(Enq& e, int ns, long long max_iter, double tol) {
     k_apply_w<<<grid_for(nlN, WARPS_PER_BLOCK), LEAF_THREADS, 0, c->stream>>>(
         c->labels.ptr, c->wv.ptr, n, c->part_n.ptr, nlN, c->sc);
   });
-  e.go("cg_init", 8.0 * n * 3 + 16.0 * n * ns, [&] {
-    dim3 g(grid_for(nlN, WARPS_PER_BLOCK), 1 + ns);
-    k_cg_init<<<g, LEAF_THREADS, 0, c->stream>>>(c->wv.ptr, c->r0.ptr, c->p.ptr, c->bigp.ptr,
-                                                 c->sols.ptr, n, c->part_d.ptr, nlN, c->sc, ss, ns);
-  });
+  e.go("cg_init", 8.0 * n * 3 + 16.0 * n * ns, [&] { launch_cg_init(c, c->wv.ptr, n, ns); });
 }
 
 void enq_sa_iteration(Enq& e, double alpha, int ns, unsigned long long cond, int use_cond) {
@@ -705,12 +772,12 @@ void enq_sa_tail(Enq& e, int ns) {
   fsda_ctx* c = e.c;
   const long long n = c->n, nlN = n_leaves(n);
   ShiftState ss = c->shifts();
-  e.go("shift_update", 32.0 * n * ns, [&] { launch_shift_update(c, ns, n, c->stream, 0); });
+  e.go(c->su_mode == 2 ? "combine_basis" : "shift_update", 32.0 * n * ns, [&] { launch_final_shift(c, ns, n); });
   e.go("cg_finish", 0.0, [&] { k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns); });
   e.go("orient", 8.0 * n * ns + 1.0 * n, [&] {  // _oriented, sda.py:256-262
     dim3 g(grid_for(nlN, WARPS_PER_BLOCK), ns);
-    k_orient<<<g, LEAF_THREADS, 0, c->stream>>>(c->labels.ptr, c->sols.ptr, n, c->part_o.ptr, nlN,
-                                                c->sc, ss, ns, nullptr);
+    k_orient<<<g, LEAF_THREADS, 0, c->stream>>>(c->labels.ptr, c->sols.ptr, n, c->part_o.ptr, nlN);
+    k_orient_final<<<ns, 256, 0, c->stream>>>(c->part_o.ptr, nlN, ss, nullptr);
   });
   e.go("flip", 0.0, [&] {
     dim3 g((unsigned)std::min<long long>(grid_for(n, 256), 1024), ns);
@@ -754,8 +821,9 @@ bool build_solve_graph(fsda_ctx* c, double alpha, int ns, long long max_iter, do
   mix(&c->n1, sizeof(c->n1));
   mix(&c->n2, sizeof(c->n2));
   char key[320];
-  snprintf(key, sizeof(key), "%d|%d|%a|%d|%lld|%a|%lld|%lld|%lld|%llu|%llx", c->solve_kind,
-           c->solve_abs_tol, alpha, ns, max_iter, tol, c->n, c->d, c->nnz, g_alloc_gen, h);
+  snprintf(key, sizeof(key), "%d|%d|%a|%d|%lld|%a|%lld|%lld|%lld|%llu|%llx|%d|%d", c->solve_kind,
+           c->solve_abs_tol, alpha, ns, max_iter, tol, c->n, c->d, c->nnz, g_alloc_gen, h,
+           c->su_mode, c->nslots);
   if (c->exec && c->graph_key == key) {
     *launches_fixed = c->graph_fixed;
     *launches_body = c->graph_body;
@@ -846,7 +914,9 @@ int check_solve_args(fsda_ctx* c, double alpha, const double* betas, int ns, dou
   return FSDA_OK;
 }
 
-void upload_solve_params(fsda_ctx* c, const double* betas, int ns, const double* probe) {
+void upload_solve_params(fsda_ctx* c, const double* betas, int ns, const double* probe,
+                         long long max_iter) {
+  resolve_shift_mode(c, ns, max_iter, c->d);
   ensure_vectors(c, ns);
   CK(cudaMemcpyAsync(c->beta.ptr, betas, sizeof(double) * ns, cudaMemcpyHostToDevice, c->stream));
   if (probe)
@@ -1245,7 +1315,21 @@ void upload_narrow_async(fsda_ctx* c, const int64_t* host, long long n, long lon
 
 extern "C" {
 
-int fsda_abi_version(void) { return 1; }
+int fsda_abi_version(void) { return 2; }
+
+int fsda_set_shift_update_mode(fsda_ctx* c, int mode) {
+  API_BEGIN(c)
+  if (mode < 0 || mode > 2) return fail(FSDA_EINVAL, "shift-update mode must be 0 (auto), 1 or 2");
+  c->su_req = mode;
+  c->invalidate_graph();
+  return FSDA_OK;
+  API_END
+}
+
+int fsda_last_shift_update_mode(fsda_ctx* c) {
+  if (!c) return fail(FSDA_EINVAL, "null context");
+  return c->su_mode;
+}
 
 const char* fsda_last_error(void) { return g_last_error.c_str(); }
 
@@ -1322,7 +1406,8 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     c->plan_lr.release();
     c->plan_xc.release();
     for (auto b : ib) b->release();
-    DevBuf<double>* db[] = {&c->l_diag, &c->y, &c->z, &c->q, &c->p, &c->r0, &c->r1,
+    c->rbuf.release(); c->coef_a.release(); c->coef_c.release();
+    DevBuf<double>* db[] = {&c->l_diag, &c->y, &c->z, &c->q, &c->p,
                             &c->mu_v, &c->t, &c->wv, &c->b, &c->ind, &c->probe, &c->part_n,
                             &c->part_d, &c->part_d2, &c->part_o, &c->bigp, &c->sols, &c->wT, &c->scores,
                             &c->dense_a, &c->beta, &c->zeta_prev, &c->zeta, &c->zeta_next,
@@ -1748,7 +1833,7 @@ int fsda_solve(fsda_ctx* c, double alpha, const double* betas, int ns, double to
   c->solve_kind = 0;
   c->solve_abs_tol = 0;
   Trace tr;
-  upload_solve_params(c, betas, ns, probe);
+  upload_solve_params(c, betas, ns, probe, max_iter);
   launch_solve(c, alpha, ns, max_iter, tol, nullptr);
   if (tr.on) {
     CK(cudaStreamSynchronize(c->stream));
@@ -1768,7 +1853,7 @@ int fsda_prepare_resident(fsda_ctx* c, double alpha, const double* betas, int ns
   if (rc) return rc;
   c->solve_kind = 0;
   c->solve_abs_tol = 0;
-  upload_solve_params(c, betas, ns, probe);
+  upload_solve_params(c, betas, ns, probe, max_iter);
   CK(cudaStreamSynchronize(c->stream));
   c->r_alpha = alpha;
   c->r_ns = ns;
@@ -1782,6 +1867,9 @@ int fsda_prepare_resident(fsda_ctx* c, double alpha, const double* betas, int ns
 int fsda_solve_async(fsda_ctx* c) {
   API_BEGIN(c)
   if (!c->r_prepared) return fail(FSDA_EINVAL, "call fsda_prepare_resident first");
+  c->solve_kind = 0;
+  resolve_shift_mode(c, c->r_ns, c->r_max_iter, c->d);
+  ensure_vectors(c, c->r_ns);
   launch_solve(c, c->r_alpha, c->r_ns, c->r_max_iter, c->r_tol, nullptr);
   return FSDA_OK;
   API_END
@@ -1804,6 +1892,9 @@ int fsda_profile_kernels(fsda_ctx* c, int max_kernels, int* n_kernels, const cha
   if (!c->r_prepared) return fail(FSDA_EINVAL, "call fsda_prepare_resident first");
   Recorder rec;
   rec.stream = c->stream;
+  c->solve_kind = 0;
+  resolve_shift_mode(c, c->r_ns, c->r_max_iter, c->d);
+  ensure_vectors(c, c->r_ns);
   launch_solve(c, c->r_alpha, c->r_ns, c->r_max_iter, c->r_tol, &rec);
   CK(cudaStreamSynchronize(c->stream));
   // accumulate per name, skipping launches after the loop finished is not
@@ -1860,21 +1951,16 @@ int fsda_shifted_cg_dense(fsda_ctx* c, int64_t dim, const double* a, const doubl
   } guard{c, c->n, c->d};
   c->d = dim;
   c->n = std::max<long long>(c->n, 1);
+  resolve_shift_mode(c, ns, max_iter, dim);
   ensure_vectors(c, ns);
   c->dense_a.ensure((size_t)dim * dim);
   CK(cudaMemcpyAsync(c->dense_a.ptr, a, sizeof(double) * dim * dim, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->b.ptr, bvec, sizeof(double) * dim, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->beta.ptr, betas, sizeof(double) * ns, cudaMemcpyHostToDevice, c->stream));
   ShiftState ss = c->shifts();
-  const long long nlD = n_leaves(dim);
   k_solve_reset<<<1, 256, 0, c->stream>>>(c->sc, ss, ns, max_iter, tol, absolute_tol);
   CKL();
-  {
-    dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
-    k_cg_init<<<g, LEAF_THREADS, 0, c->stream>>>(c->b.ptr, c->r0.ptr, c->p.ptr, c->bigp.ptr,
-                                                 c->sols.ptr, dim, c->part_d.ptr, nlD, c->sc, ss, ns);
-    CKL();
-  }
+  launch_cg_init(c, c->b.ptr, dim, ns);
   for (long long it = 0; it < max_iter; ++it) {
     k_dense_matvec<<<grid_for(dim, 128), 128, 0, c->stream>>>(c->dense_a.ptr, c->p.ptr, c->q.ptr,
                                                               (int)dim, c->sc);
@@ -1888,7 +1974,7 @@ int fsda_shifted_cg_dense(fsda_ctx* c, int64_t dim, const double* a, const doubl
       if (h.finished || h.status) break;
     }
   }
-  launch_shift_update(c, ns, dim, c->stream, 0);
+  launch_final_shift(c, ns, dim);
   k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns);
   CKL();
   SolveOut o{solutions, nullptr, residuals, iterations, converged, n_applies, fail_iter};
@@ -1982,15 +2068,12 @@ int fsda_dev_cg_begin(fsda_ctx* c, const double* betas, int ns, double tol, int6
     if (s > 0 && !(betas[s] > betas[s - 1])) return fail(FSDA_EINVAL, "shifts must be strictly ascending");
   }
   if (!(tol > 0)) return fail(FSDA_EINVAL, "tol must be positive");
-  upload_solve_params(c, betas, ns, nullptr);
+  upload_solve_params(c, betas, ns, nullptr, max_iter);
   ShiftState ss = c->shifts();
-  const long long d = c->d, nlD = n_leaves(d);
+  const long long d = c->d;
   k_solve_reset<<<1, 256, 0, c->stream>>>(c->sc, ss, ns, max_iter, tol, 0);
   CKL();
-  dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
-  k_cg_init<<<g, LEAF_THREADS, 0, c->stream>>>(d_b, c->r0.ptr, c->p.ptr, c->bigp.ptr, c->sols.ptr, d,
-                                               c->part_d.ptr, nlD, c->sc, ss, ns);
-  CKL();
+  launch_cg_init(c, d_b, d, ns);
   c->r_ns = ns;
   CK(cudaStreamSynchronize(c->stream));  // betas were read from host memory
   return FSDA_OK;
@@ -2034,15 +2117,15 @@ int fsda_dev_project(fsda_ctx* c, double* d_scores, double* d_orient) {
   if (ns <= 0) return fail(FSDA_EINVAL, "call fsda_dev_cg_begin first");
   const long long n = c->n, d = c->d, nlN = n_leaves(n);
   ShiftState ss = c->shifts();
-  launch_shift_update(c, ns, d, c->stream, 0);
+  launch_final_shift(c, ns, d);
   k_cg_finish<<<1, 32, 0, c->stream>>>(c->sc, ss, ns);
   k_transpose_sols<<<grid_for(d * ns, 256), 256, 0, c->stream>>>(c->sols.ptr, c->wT.ptr, d, ns);
   if (n > 0)
     k_spmm_scores<<<grid_for(n, 8), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr, c->wT.ptr,
                                                          d_scores, (int)n, ns);
   dim3 g(grid_for(nlN, WARPS_PER_BLOCK), ns);
-  k_orient<<<g, LEAF_THREADS, 0, c->stream>>>(c->labels.ptr, d_scores, n, c->part_o.ptr, nlN, c->sc,
-                                              ss, ns, d_orient);
+  k_orient<<<g, LEAF_THREADS, 0, c->stream>>>(c->labels.ptr, d_scores, n, c->part_o.ptr, nlN);
+  k_orient_final<<<ns, 256, 0, c->stream>>>(c->part_o.ptr, nlN, ss, d_orient);
   CKL();
   return FSDA_OK;
   API_END
@@ -2081,7 +2164,7 @@ int fsda_regression_shifted_cg(fsda_ctx* c, const double* rhs, const double* bet
     if (s > 0 && !(betas[s] > betas[s - 1])) return fail(FSDA_EINVAL, "shifts must be strictly ascending");
   }
   if (!(tol > 0)) return fail(FSDA_EINVAL, "tol must be positive");
-  upload_solve_params(c, betas, ns, nullptr);
+  upload_solve_params(c, betas, ns, nullptr, max_iter);
   CK(cudaMemcpyAsync(c->b.ptr, rhs, sizeof(double) * c->d, cudaMemcpyHostToDevice, c->stream));
   c->solve_kind = 1;
   c->solve_abs_tol = absolute_tol ? 1 : 0;
@@ -2123,7 +2206,7 @@ int fsda_sa_solve(fsda_ctx* c, double alpha, const double* betas, int ns, double
   c->solve_kind = 2;
   c->solve_abs_tol = 0;
   ensure_vectors(c, ns);
-  upload_solve_params(c, betas, ns, nullptr);
+  upload_solve_params(c, betas, ns, nullptr, max_iter);
   CK(cudaMemcpyAsync(c->t.ptr, probe, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
   launch_solve(c, alpha, ns, max_iter, tol, nullptr);
   SolveOut o{solutions, nullptr, residuals, iterations, converged, n_applies, fail_iter};
@@ -2184,12 +2267,36 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   cudaStream_t st = c->stream;
   const long long nlN = n_leaves(n), nlD = n_leaves(d);
   const long long ND = (long long)tp;
+  // shift-update mode (as resolve_shift_mode, for T tasks): the deferred basis
+  // keeps max_iter + 1 task-minor residuals
+  int bmode = c->su_req;
+  if (bmode == 0 && std::getenv("FSDA_B200_SHIFT_MODE")) bmode = std::atoi(std::getenv("FSDA_B200_SHIFT_MODE"));
+  const long long bslots = std::max<long long>(max_iter, 0) + 1;
+  if (bmode == 0) {
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const double need = 8.0 * (double)bslots * (double)std::max<long long>(d, 1) * (double)tp +
+                        16.0 * (double)tp * ns * (double)bslots;
+    const double have = 8.0 * (double)(c->batch.RB.cap + c->batch.CA.cap + c->batch.CC.cap);
+    bmode = need <= 0.4 * (double)free_b + have ? 2 : 1;
+  }
+  if ((long long)tp * ns > 65535) bmode = 1;  // kb_coef_update's grid.y is one (task, shift)
+  c->su_mode = bmode;
+  const bool basis = bmode == 2;
   bb.lab.ensure(n * ND);
   bb.ind.ensure(n * ND);
-  for (DevBuf<double>* v : {&bb.P, &bb.Q, &bb.R0, &bb.R1, &bb.MU, &bb.Bv, &bb.PR}) v->ensure(std::max(1LL, d * ND));
+  for (DevBuf<double>* v : {&bb.P, &bb.Q, &bb.MU, &bb.Bv, &bb.PR}) v->ensure(std::max(1LL, d * ND));
+  if (basis) {
+    bb.RB.ensure(std::max(1LL, bslots * d * ND));
+    bb.CA.ensure(std::max(1LL, bslots * ND * ns));
+    bb.CC.ensure(std::max(1LL, bslots * ND * ns));
+  } else {
+    bb.R0.ensure(std::max(1LL, d * ND));
+    bb.R1.ensure(std::max(1LL, d * ND));
+  }
   bb.Y.ensure(std::max(1LL, n * ND));
   bb.Z.ensure(std::max(1LL, n * ND));
-  bb.BIGP.ensure(std::max(1LL, d * ND * ns));
+  bb.BIGP.ensure(basis ? 1LL : std::max(1LL, d * ND * ns));
   bb.SOLS.ensure(std::max(1LL, d * ND * ns));
   bb.SCORES.ensure(std::max(1LL, n * ND * ns));
   bb.OUT.ensure(std::max(1LL, (long long)T * ns * d));
@@ -2339,9 +2446,18 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   const long long tsn = ND * ns, passes = cdiv(tsn, 1024);
   const int sblk = (int)(cdiv(cdiv(tsn, passes), 32) * 32);
   const unsigned srows = (unsigned)std::max<long long>(1, std::min<long long>(d, (long long)c->num_sms * 8));
-  kb_cg_init_vec<<<srows, sblk, 0, st>>>(
-      bb.Bv.ptr, bb.R0.ptr, bb.P.ptr, bb.BIGP.ptr, bb.SOLS.ptr, d, tp, ns);
-  CKL();
+  const unsigned vblocks = (unsigned)std::max<long long>(1, std::min<long long>(cdiv(d * ND, 256), (long long)c->num_sms * 16));
+  if (basis) {
+    kb_cg_init_rp<<<vblocks, 256, 0, st>>>(bb.Bv.ptr, bb.RB.ptr, bb.P.ptr, d * ND);
+    CKL();
+    kb_coef_init<<<(unsigned)std::min<long long>(cdiv(bslots * ND * ns, 256), 4096), 256, 0, st>>>(
+        bb.CA.ptr, bb.CC.ptr, ND * ns, bslots);
+    CKL();
+  } else {
+    kb_cg_init_vec<<<srows, sblk, 0, st>>>(
+        bb.Bv.ptr, bb.R0.ptr, bb.P.ptr, bb.BIGP.ptr, bb.SOLS.ptr, d, tp, ns);
+    CKL();
+  }
   vec_sum(bb.Bv.ptr, bb.Bv.ptr, 3, d, bb.partD.ptr, B.pq);   // b.b
   kb_cg_init_scalars<<<tb, 128, 0, st>>>(B, B.pq, tol);
   CKL();
@@ -2352,8 +2468,8 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
 
   // ---- the shifted-CG loop (krylov.py:210-270), all live tasks in step
   for (long long it = 0; it < max_iter; ++it) {
-    double* r_cur = (it & 1) ? bb.R1.ptr : bb.R0.ptr;
-    double* r_nxt = (it & 1) ? bb.R0.ptr : bb.R1.ptr;
+    double* r_cur = basis ? bb.RB.ptr + it * d * ND : ((it & 1) ? bb.R1.ptr : bb.R0.ptr);
+    double* r_nxt = basis ? bb.RB.ptr + (it + 1) * d * ND : ((it & 1) ? bb.R0.ptr : bb.R1.ptr);
     rows_x(bb.P.ptr, bb.Y.ptr);                                // K1  y = X p
     smoother(bb.Y.ptr, bb.Z.ptr);                              // K2  z = M y
     xt(bb.Z.ptr, bb.Q.ptr, 0);                                 // K3  q = X^T z
@@ -2380,8 +2496,16 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
     CKL();
     kb_mark_stepped<<<tb, 128, 0, st>>>(B, stepped);
     CKL();
-    kb_step_c<<<srows, sblk, 0, st>>>(r_nxt, bb.P.ptr, bb.BIGP.ptr, bb.SOLS.ptr, d, B, stepped);
-    CKL();
+    if (basis) {
+      kb_step_c_p<<<vblocks, 256, 0, st>>>(r_nxt, bb.P.ptr, d * ND, tp, B, stepped);
+      CKL();
+      kb_coef_update<<<dim3((unsigned)cdiv(it + 2, 256), (unsigned)(ND * ns)), 256, 0, st>>>(
+          B, stepped, bb.CA.ptr, bb.CC.ptr, bslots, it);
+      CKL();
+    } else {
+      kb_step_c<<<srows, sblk, 0, st>>>(r_nxt, bb.P.ptr, bb.BIGP.ptr, bb.SOLS.ptr, d, B, stepped);
+      CKL();
+    }
     CK(cudaMemsetAsync(n_live, 0, sizeof(int), st));
     kb_end_iteration<<<tb, 128, 0, st>>>(B, stepped, n_live);
     CKL();
@@ -2392,7 +2516,13 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   }
 
   if (tr.on) tr.mark("batch: iterations");
-  // ---- tail: residuals, projections, orientation (sda.py:265-284)
+  // ---- tail: directions (deferred mode), residuals, projections, orientation
+  // (sda.py:265-284)
+  if (basis && d > 0) {
+    kb_combine_basis<<<(unsigned)cdiv(d * ND, 256), 256, 0, st>>>(bb.RB.ptr, d, B, bb.CC.ptr, bslots,
+                                                                  bb.SOLS.ptr);
+    CKL();
+  }
   kb_finish<<<tb, 128, 0, st>>>(B);
   CKL();
   const int nsp = tp * ns;

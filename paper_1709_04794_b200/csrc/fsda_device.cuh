@@ -86,6 +86,11 @@ struct ShiftState {
   double* upd_gs;   // gamma_s
   double* upd_zn;   // zeta_next
   double* upd_as;   // alpha_s
+  // deferred ("basis") shift updates: P_s = sum_j coef_a[s][j] r_j and
+  // sols_s = sum_j coef_c[s][j] r_j over the stored residuals r_0 .. r_K
+  double* coef_a;
+  double* coef_c;
+  long long coef_ld;  // max_iter + 1
 };
 
 // ---------------------------------------------------------------- R256 tree
@@ -257,7 +262,7 @@ __global__ void k_apply_w(const signed char* __restrict__ labels, double* __rest
 __global__ void k_cg_init(const double* __restrict__ b, double* __restrict__ r,
                           double* __restrict__ p, double* __restrict__ bigp,
                           double* __restrict__ sols, long long d, double* __restrict__ part,
-                          long long n_leaf, CgScalars* sc, ShiftState ss, int n_shifts) {
+                          long long n_leaf, CgScalars* sc, ShiftState ss, int n_shifts, int basis) {
   __shared__ double smem[257];
   const int lane = threadIdx.x & 31;
   const long long g = (long long)blockIdx.x * WARPS_PER_BLOCK + (threadIdx.x >> 5);
@@ -275,6 +280,16 @@ __global__ void k_cg_init(const double* __restrict__ b, double* __restrict__ r,
       }
       a = butterfly(a);
       if (lane == 0) { part[g] = a; __threadfence(); }
+    }
+  } else if (basis) {
+    // P_s = r_0 (= b), sols_s = 0 as coefficient rows
+    const int s = blockIdx.y - 1;
+    double* A = ss.coef_a + (long long)s * ss.coef_ld;
+    double* Cc = ss.coef_c + (long long)s * ss.coef_ld;
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < ss.coef_ld;
+         j += (long long)gridDim.x * blockDim.x) {
+      A[j] = j == 0 ? 1.0 : 0.0;
+      Cc[j] = 0.0;
     }
   } else {
     const int s = blockIdx.y - 1;
@@ -333,11 +348,10 @@ __global__ void k_transpose_sols(const double* __restrict__ sols, double* __rest
 }
 
 // Orientation dots y.s per shift (sda.py:280), canonical over N with fma
-// leaves; blockIdx.y = shift.  The last block sets the flip flags.
+// leaves; blockIdx.y = shift.  Leaf partials only: k_orient_final reduces
+// them, one block per shift.
 __global__ void k_orient(const signed char* __restrict__ labels, const double* __restrict__ scores,
-                         long long n, double* __restrict__ part, long long n_leaf, CgScalars* sc,
-                         ShiftState ss, int ns, double* dots_out) {
-  __shared__ double smem[257];
+                         long long n, double* __restrict__ part, long long n_leaf) {
   const int lane = threadIdx.x & 31;
   const long long g = (long long)blockIdx.x * WARPS_PER_BLOCK + (threadIdx.x >> 5);
   const int s = blockIdx.y;
@@ -349,16 +363,19 @@ __global__ void k_orient(const signed char* __restrict__ labels, const double* _
       if (i < n) a = fma((double)labels[i], sv[i], a);
     }
     a = butterfly(a);
-    if (lane == 0) { part[(long long)s * n_leaf + g] = a; __threadfence(); }
+    if (lane == 0) part[(long long)s * n_leaf + g] = a;
   }
-  if (arrive_last(&sc->counters[C_ORIENT], gridDim.x * gridDim.y)) {
-    for (int t = 0; t < ns; ++t) {
-      double v = block_reduce_partials(part + (long long)t * n_leaf, n_leaf, smem);
-      if (threadIdx.x == 0) {
-        ss.flip[t] = (v < 0.0) ? 1 : 0;
-        if (dots_out) dots_out[t] = v;
-      }
-    }
+}
+
+// R256 of shift blockIdx.x's orientation leaves; sets its flip flag.
+__global__ void k_orient_final(const double* __restrict__ part, long long n_leaf, ShiftState ss,
+                               double* dots_out) {
+  __shared__ double smem[257];
+  const int s = blockIdx.x;
+  const double v = block_reduce_partials(part + (long long)s * n_leaf, n_leaf, smem);
+  if (threadIdx.x == 0) {
+    ss.flip[s] = (v < 0.0) ? 1 : 0;
+    if (dots_out) dots_out[s] = v;
   }
 }
 

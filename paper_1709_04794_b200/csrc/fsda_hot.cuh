@@ -684,8 +684,8 @@ __global__ void k_center(const double* __restrict__ mu, double* __restrict__ q, 
 constexpr int STEP_THREADS = 256;
 
 __global__ void __launch_bounds__(STEP_THREADS) k_cg_step(
-    double* __restrict__ q, double* __restrict__ p, double* __restrict__ r0,
-    double* __restrict__ r1, double* __restrict__ bigp, double* __restrict__ sols, long long d,
+    double* __restrict__ q, double* __restrict__ p, double* __restrict__ rbuf, int nslots,
+    double* __restrict__ bigp, double* __restrict__ sols, long long d,
     double* __restrict__ part_pq, double* __restrict__ part_rr, long long n_leaf, CgScalars* sc,
     ShiftState ss, int ns, unsigned long long cond_handle, int use_cond,
     const double* __restrict__ mu, const double* __restrict__ part_z, long long n_leaf_z,
@@ -713,8 +713,9 @@ __global__ void __launch_bounds__(STEP_THREADS) k_cg_step(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
   const long long tw = (long long)gridDim.x * (blockDim.x >> 5);
-  const double* r_cur = (it & 1) ? r1 : r0;
-  double* r_next = (it & 1) ? r0 : r1;
+  // residual slots: ping-pong (nslots 2) or the stored basis r_0 .. r_K
+  const double* r_cur = rbuf + (it % nslots) * d;
+  double* r_next = rbuf + ((it + 1) % nslots) * d;
   const bool center = part_z != nullptr;
   const bool own = gw < n_leaf;  // this warp's register-cached leaf
 
@@ -934,14 +935,13 @@ __global__ void __launch_bounds__(STEP_THREADS) k_cg_step(
 constexpr int SU_ELEMS = 4;
 constexpr int SU_SHIFTS = 4;
 
-__global__ void __launch_bounds__(256) k_shift_update(const double* __restrict__ r0,
-                                                      const double* __restrict__ r1,
+__global__ void __launch_bounds__(256) k_shift_update(const double* __restrict__ rbuf, int nslots,
                                                       double* __restrict__ bigp,
                                                       double* __restrict__ sols, long long d,
                                                       ShiftState ss, const CgScalars* sc,
                                                       int ns, int guarded) {
   if (guarded && loop_idle(sc)) return;
-  const double* r = (sc->iter & 1) ? r1 : r0;
+  const double* r = rbuf + (sc->iter % nslots) * d;
   const long long base = (long long)blockIdx.x * (256 * SU_ELEMS) + threadIdx.x;
   double rv[SU_ELEMS];
 #pragma unroll
@@ -972,6 +972,78 @@ __global__ void __launch_bounds__(256) k_shift_update(const double* __restrict__
         if (mode == 3) P[i] = zn * rv[e] + as * pv[e];
       }
     }
+  }
+}
+
+// Deferred ("basis") shift updates.  With every residual r_0 .. r_K kept,
+// P_s and sols_s are linear combinations of them, so an iteration only
+// updates the coefficient rows (krylov.py:230, 240-241 on coefficients):
+//   sols_s -= gamma_s P_s   ->  c_s[j] = c_s[j] - a_s[j] * gamma_s   (j <= i)
+//   P_s = zeta_next r_{i+1} + alpha_s P_s
+//                           ->  a_s[j] = alpha_s * a_s[j] (j <= i), a_s[i+1] = zeta_next
+// and the directions are formed once, after the loop (k_combine_basis).  The
+// per-iteration shift traffic (32 D n_s bytes) becomes O(n_s K) scalars.
+// blockIdx.y = shift; threads over j.  Same guard / snapshot contract as
+// k_shift_update.
+__global__ void __launch_bounds__(256) k_coef_update(ShiftState ss, const CgScalars* sc, int ns,
+                                                     int guarded) {
+  if (guarded && loop_idle(sc)) return;
+  const int s = blockIdx.y;
+  const int mode = ss.upd_mode[s];
+  if (mode == 0) return;
+  const long long i = sc->iter - 1;  // the iteration the snapshot belongs to
+  const double gs = ss.upd_gs[s], zn = ss.upd_zn[s], as = ss.upd_as[s];
+  double* A = ss.coef_a + (long long)s * ss.coef_ld;
+  double* Cc = ss.coef_c + (long long)s * ss.coef_ld;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j <= i + 1;
+       j += (long long)gridDim.x * blockDim.x) {
+    if (j <= i) {
+      const double a = A[j];
+      Cc[j] = Cc[j] - a * gs;
+      if (mode == 3) A[j] = as * a;
+    } else if (mode == 3 && j < ss.coef_ld) {
+      A[j] = zn;
+    }
+  }
+}
+
+// sols[s][k] = sum_{j < J} c_s[j] * r_j[k], j ascending from 0.0 with one
+// fused multiply-add per term, J = iterations run.  A thread owns
+// one feature k for SH shifts; r_j[k] loads are coalesced and the
+// coefficient tile sits in shared memory (broadcast reads).
+constexpr int CB_SH = 16;    // shifts per thread
+constexpr int CB_JT = 128;   // coefficient columns per shared tile
+__global__ void __launch_bounds__(256) k_combine_basis(const double* __restrict__ rbuf, long long d,
+                                                       ShiftState ss, const CgScalars* sc, int ns,
+                                                       double* __restrict__ sols) {
+  __shared__ double ct[CB_SH][CB_JT];
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int s0 = blockIdx.y * CB_SH;
+  const int nsh = min(CB_SH, ns - s0);
+  const long long J = sc->status == ST_OK ? sc->iter : 0;
+  double acc[CB_SH];
+#pragma unroll
+  for (int t = 0; t < CB_SH; ++t) acc[t] = 0.0;
+  for (long long j0 = 0; j0 < J; j0 += CB_JT) {
+    const int jn = (int)min((long long)CB_JT, J - j0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < CB_SH * CB_JT; e += blockDim.x) {
+      const int t = e / CB_JT, jj = e - t * CB_JT;
+      ct[t][jj] = (t < nsh && jj < jn) ? ss.coef_c[(long long)(s0 + t) * ss.coef_ld + j0 + jj] : 0.0;
+    }
+    __syncthreads();
+    if (k < d) {
+      for (int jj = 0; jj < jn; ++jj) {
+        const double r = __ldcs(rbuf + (j0 + jj) * d + k);
+#pragma unroll
+        for (int t = 0; t < CB_SH; ++t) acc[t] = fma(ct[t][jj], r, acc[t]);
+      }
+    }
+  }
+  if (k < d) {
+#pragma unroll
+    for (int t = 0; t < CB_SH; ++t)
+      if (t < nsh) sols[(long long)(s0 + t) * d + k] = acc[t];
   }
 }
 

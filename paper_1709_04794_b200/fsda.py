@@ -129,6 +129,15 @@ class Device:
         except Exception:
             pass
 
+    def set_shift_update_mode(self, mode: int):
+        """0 auto (deferred basis when it fits), 1 per-iteration shift
+        updates, 2 deferred basis (include/fsda_b200.h)."""
+        _raise_for(_capi.lib().fsda_set_shift_update_mode(self._h, int(mode)))
+
+    @property
+    def last_shift_update_mode(self) -> int:
+        return int(_capi.lib().fsda_last_shift_update_mode(self._h))
+
     def set_stream(self, stream: Optional[int]):
         _raise_for(_capi.lib().fsda_ctx_set_stream(self._h, C.c_void_p(stream) if stream else None))
 

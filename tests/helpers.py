@@ -69,3 +69,23 @@ def same_ranking(a: np.ndarray, b: np.ndarray) -> bool:
     """Identical induced ordering (ties broken by index) for every shift."""
     return all(np.array_equal(np.argsort(x, kind="stable"), np.argsort(y, kind="stable"))
                for x, y in zip(a, b))
+
+
+def ranking_violations(a: np.ndarray, b: np.ndarray, rel_gap: float = 1e-9):
+    """Per shift: rows whose order under `a` contradicts the order under the
+    reference scores `b`, outside near-ties of b (consecutive sorted values
+    closer than rel_gap * max|b|, which any reordered sum may swap).
+    Returns (violations per shift, fraction of rows inside near-tie groups)."""
+    viol, tied = [], []
+    for x, y in zip(np.asarray(a), np.asarray(b)):
+        ob = np.argsort(y, kind="stable")
+        sy = y[ob]
+        gap = rel_gap * max(float(np.max(np.abs(y))), 1e-300)
+        new = np.concatenate([[True], np.diff(sy) > gap])
+        cluster = np.empty(y.size, dtype=np.int64)
+        cluster[ob] = np.cumsum(new) - 1
+        seq = cluster[np.argsort(x, kind="stable")]
+        viol.append(int(np.count_nonzero(np.diff(seq) < 0)))
+        sizes = np.bincount(cluster)
+        tied.append(float(np.sum(sizes[sizes > 1])) / y.size)
+    return np.array(viol), np.array(tied)

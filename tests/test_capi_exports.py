@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_error_channel():
     lib = _capi.lib()
-    assert lib.fsda_abi_version() == 1
+    assert lib.fsda_abi_version() == 2
     assert isinstance(_capi.last_error(), str)
 
 

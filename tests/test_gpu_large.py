@@ -1,17 +1,37 @@
-"""BASELINE configs[2] shape (cfg3: 1.5M x 500k, 75M nnz, Zipf 1.05, 30
-shifts) on the device: bitwise equal to the C oracle over the first Krylov
-iterations (the oracle needs ~1 s per iteration at this size on the host)."""
+"""BASELINE configs[2] (cfg3: 1.5M x 500k, 75M nnz, Zipf 1.05, random
+10-NN Laplacian, 30 shifts, K = 150) and configs[3] (cfg4: 64 label-mask
+tasks on the same matrix) on the device.
+
+Tolerances (north_star: fp64 directions within 1e-6, identical rankings and
+AUC per shift):
+* vs the reference's arithmetic (oracle/ref_numpy.py, pinned bit for bit to
+  the unmodified reference) at the measured stable Krylov dimension of cfg3,
+  K = 40 (tools/noise_floor.py -> profiles/r02_noise_floor_cfg3.json: the
+  reference moves by <= 1.1e-11 under ulp-level reordering up to K = 40,
+  6e-7 at K = 50): rel||dw|| <= 1e-6 per shift, identical labeled-row AUC,
+  identical full-row ranking outside near-ties (1e-9 relative);
+* vs the C oracle (device summation order) at the full K = 150: bitwise,
+  through the sha256 digest tests/golden/make_cfg3_digest.py committed (the
+  oracle needs minutes per cfg3 solve on the host).
+"""
+
+import hashlib
+import json
+from pathlib import Path
 
 import numpy as np
 import pytest
 
 import paper_1709_04794_b200 as fb
-from oracle import c_oracle
-from paper_1709_04794_b200.workloads import make_workload
+from oracle import c_oracle, ref_numpy
+from paper_1709_04794_b200.workloads import CONFIGS, make_workload, task_masks, workload_digest
 
-from helpers import problem_from_workload
+from helpers import labeled_aucs, problem_from_workload, ranking_violations, rel_rows
 
 pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+K_STABLE_CFG3 = 40
 
 
 @pytest.fixture(scope="module")
@@ -19,11 +39,86 @@ def cfg3():
     return make_workload("cfg3")
 
 
+def _stack(rep, betas, what):
+    if what == "dirs":
+        return np.stack([rep.directions[float(b)] for b in betas])
+    return np.stack([rep.ratings[float(b)].scores for b in betas])
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
 def test_cfg3_sweep_bitwise_vs_oracle(cfg3):
     k = 6
     rep = fb.fsda_solve(problem_from_workload(cfg3, max_iter=k))
     ref = c_oracle.fsda_solve_workload(cfg3, max_iter=k)
-    dirs = np.stack([rep.directions[float(b)] for b in cfg3.betas])
-    np.testing.assert_array_equal(dirs, ref["directions"])
+    np.testing.assert_array_equal(_stack(rep, cfg3.betas, "dirs"), ref["directions"])
     np.testing.assert_array_equal(rep.regression.residuals, ref["residuals"])
     assert rep.regression.operator_applications == k
+
+
+def test_cfg3_full_k_bitwise_vs_oracle_digest(cfg3):
+    """The headline configuration at the full K = 150: directions, scores and
+    residuals bit for bit equal to the C oracle's (committed digest)."""
+    dig = json.loads((GOLDEN / "cfg3_oracle_digest.json").read_text())
+    assert workload_digest(cfg3) == dig["workload_sha256"], "generator output changed"
+    dev = fb.Device(0)
+    dev.set_shift_update_mode(dig["shift_update_mode"])
+    rep = fb.fsda_solve(problem_from_workload(cfg3), device=dev)
+    assert dev.last_shift_update_mode == dig["shift_update_mode"]
+    dirs = _stack(rep, cfg3.betas, "dirs")
+    scores = _stack(rep, cfg3.betas, "scores")
+    assert rep.regression.operator_applications == dig["n_applies"] == 150
+    assert list(rep.regression.iterations) == dig["iterations"]
+    assert _sha(rep.regression.residuals) == dig["residuals_sha256"]
+    assert _sha(dirs) == dig["directions_sha256"], (
+        np.linalg.norm(dirs, axis=1)[:4], dig["direction_norms"][:4])
+    assert _sha(scores) == dig["scores_sha256"]
+
+
+def test_cfg3_stable_k_vs_reference_order(cfg3):
+    """cfg3 at its stable Krylov dimension against the reference's own
+    arithmetic: <= 1e-6 per shift, identical labeled AUC and full ranking."""
+    k = K_STABLE_CFG3
+    rep = fb.fsda_solve(problem_from_workload(cfg3, max_iter=k))
+    ref = ref_numpy.fsda_solve_workload(cfg3, max_iter=k)
+    dirs = _stack(rep, cfg3.betas, "dirs")
+    scores = _stack(rep, cfg3.betas, "scores")
+    rel = rel_rows(dirs, ref["directions"])
+    print(f"cfg3 K={k}: max rel||dw|| vs reference order {rel:.3e} (noise floor 1.1e-11 at K=40)")
+    assert rel <= 1e-6
+    np.testing.assert_array_equal(labeled_aucs(scores, cfg3.labels),
+                                  labeled_aucs(ref["scores"], cfg3.labels))
+    viol, tied = ranking_violations(scores, ref["scores"])
+    assert viol.sum() == 0, (viol, tied)
+    assert tied.max() < 0.01, tied       # near-ties are rare: the ranking check is real
+
+
+def test_cfg4_shape_batch_64_tasks(cfg3):
+    """cfg4's shape: 64 label-mask tasks (1% labeled, 10% positive, 20
+    shifts) on the cfg3 matrix in one batch; two tasks bitwise vs the C
+    oracle's solve of the same mask (few iterations: the oracle is slow)."""
+    c4 = CONFIGS["cfg4"]
+    k = 3
+    masks = task_masks(cfg3.n, c4["tasks"], c4["task_frac"], c4["task_pos"], seed=91)
+    betas = np.geomspace(c4["beta_lo"], c4["beta_hi"], c4["n_shifts"])
+    x = fb.SparseMatrix.binary(cfg3.n, cfg3.d, cfg3.x_offsets, cfg3.x_cols)
+    lap = fb.Laplacian(fb.SparseMatrix(cfg3.n, cfg3.n, cfg3.l_offsets, cfg3.l_cols, cfg3.l_vals),
+                       cfg3.degrees)
+    seeds = list(range(100, 100 + c4["tasks"]))
+    res = fb.solve_label_sets(x, lap, list(masks), cfg3.alpha, betas, cfg3.tol, k, seeds=seeds,
+                              scores=False)
+    assert len(res) == 64 and all(r.n_applies == k for r in res)
+    mode = fb.default_device().last_shift_update_mode
+    c_oracle.set_shift_mode(mode)
+    try:
+        for t in (0, 63):
+            probe = np.random.default_rng(seeds[t]).uniform(-1, 1, cfg3.d)
+            ref = c_oracle.fsda_solve(cfg3.x_offsets, cfg3.x_cols, cfg3.d, cfg3.l_offsets, cfg3.l_cols,
+                                      cfg3.l_vals, masks[t], cfg3.alpha, betas, cfg3.tol, k, probe,
+                                      scores=False)
+            np.testing.assert_array_equal(res[t].directions, ref["directions"])
+            np.testing.assert_array_equal(res[t].residuals, ref["residuals"])
+    finally:
+        c_oracle.set_shift_mode(2)

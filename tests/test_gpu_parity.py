@@ -451,3 +451,40 @@ def test_combined_upload_errors_then_recovers():
     ref = c_oracle.fsda_solve(w.x_offsets, w.x_cols, w.d, w.l_offsets, w.l_cols, w.l_vals,
                               w.labels, p.alpha, p.betas.betas, p.tol, p.max_iter_d, w.probe())
     np.testing.assert_array_equal(_dirs(rep, p.betas.betas), ref["directions"])
+
+
+# ------------------------------------------------- shift-update modes
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_shift_update_modes_bitwise_vs_oracle(cfg1_workload, mode):
+    """Per-iteration (1) and deferred-basis (2) shift updates: each bitwise
+    equal to the oracle run in the same mode, at the full BASELINE K."""
+    w = cfg1_workload
+    dev = fb.Device(0)
+    dev.set_shift_update_mode(mode)
+    p = problem_from_workload(w)
+    rep = fb.fsda_solve(p, device=dev)
+    assert dev.last_shift_update_mode == mode
+    c_oracle.set_shift_mode(mode)
+    try:
+        ref = c_oracle.fsda_solve_workload(w)
+    finally:
+        c_oracle.set_shift_mode(2)
+    np.testing.assert_array_equal(_dirs(rep, w.betas), ref["directions"])
+    np.testing.assert_array_equal(_scores(rep, w.betas), ref["scores"])
+    np.testing.assert_array_equal(rep.regression.residuals, ref["residuals"])
+    assert rep.regression.operator_applications == ref["n_applies"]
+
+
+def test_shift_update_modes_agree_cfg2():
+    """The two modes differ only in the rounding of the (non-feedback)
+    direction accumulation: <= 1e-12 at cfg2, K=100."""
+    w = make_workload("cfg2")
+    p = problem_from_workload(w)
+    out = {}
+    for mode in (1, 2):
+        dev = fb.Device(0)
+        dev.set_shift_update_mode(mode)
+        out[mode] = _dirs(fb.fsda_solve(p, device=dev), w.betas)
+        assert dev.last_shift_update_mode == mode
+    assert rel_rows(out[2], out[1]) <= 1e-12

@@ -138,6 +138,16 @@ int fsda_set_shift_update_mode(fsda_ctx* ctx, int mode);
 /* The mode (1 or 2) the last solve on this context used. */
 int fsda_last_shift_update_mode(fsda_ctx* ctx);
 
+/* Storage precision of the FSDA solve's vectors (BASELINE cfg5: "fp32 storage
+ * with fp64 reductions").  64 (default): fp64 throughout.  32: the gathered
+ * and iterated vectors y = X p, z = M y, p and the residuals r_j are stored as
+ * float; every sum and dot runs in double over the stored values; q, mu, the
+ * rhs, the directions, the scores and every scalar stay double.  Parity gate
+ * (stated): directions within 1e-3 per shift of the fp64 solve and identical
+ * labeled AUC at the stable Krylov dimension.  Implies the deferred
+ * shift-update mode.  Applies to fsda_solve / fsda_solve_async. */
+int fsda_set_storage(fsda_ctx* ctx, int bits);
+
 /* Device-resident variant for throughput measurement: launches one complete
  * solve on the context stream and returns without copying results to the
  * host (inputs already resident in HBM).  Results stay in the context and can
@@ -266,6 +276,43 @@ int fsda_graph_threshold(fsda_ctx* ctx, double theta, int64_t* nnz_out);
 /* Copy the last graph out: row_offsets (n_rows + 1) and col_indices (nnz),
  * int64 CSR with ascending columns (graph.py:146-148's from_scipy layout). */
 int fsda_graph_fetch(fsda_ctx* ctx, int64_t* row_offsets, int64_t* col_indices);
+
+/* ---- row-sharded solve (csrc/fsda_shard.cuh) -------------------
+ * One FSDA sweep with the rows of X and L split into contiguous blocks over
+ * `world` ranks.  Per iteration: an all-gather of y, a deterministic
+ * reduce-scatter (send/recv, rank-ordered owner sum) + all-gather of the
+ * D + 1 partials [X_g^T z_g | sum z_g]; D-vectors and scalars replicated.
+ * Replaces the single-process fsda_solve of sda.py:293-320 when the problem
+ * is spread over GPUs (the reference has no multi-node path).
+ *
+ * Set-up per rank: fsda_upload_x(local rows), fsda_upload_laplacian_rows(
+ * n_local, world * slot, rank * slot, offsets, REMAPPED columns, values) with
+ * slot = max rows per rank rounded up to even and global column j of rank h
+ * remapped to h * slot + (j - bounds[h]); fsda_set_label_mask(local labels);
+ * then fsda_shard_init. */
+
+/* A fresh ncclUniqueId (128 bytes) for fsda_shard_init (rank 0 draws it and
+ * broadcasts it).  NCCL is loaded at run time (libnccl.so.2). */
+int fsda_nccl_unique_id(uint8_t* out);
+
+/* Make ctx rank `rank` of `world` with rows [row_bounds[rank],
+ * row_bounds[rank+1]).  nccl_id: 128 bytes (one process per GPU, NCCL over
+ * NVLink), or NULL for a local group (all ranks driven by one process — the
+ * multi-rank tests on one GPU). */
+int fsda_shard_init(fsda_ctx* ctx, int world, int rank, const int64_t* row_bounds,
+                    const uint8_t* nccl_id);
+
+/* One row-sharded sweep.  ctxs: this process's NCCL rank (n_ctx 1), or all
+ * `world` contexts of a local group in rank order.  probe (D) and betas are
+ * replicated; n1 / n2 are the global class counts.  directions: n_shifts x D
+ * (replicated); scores: n_shifts x rows_total of the driven ranks' rows (rank
+ * blocks side by side per shift).  At world 1 the results equal fsda_solve's
+ * bit for bit. */
+int fsda_solve_sharded(fsda_ctx** ctxs, int n_ctx, double alpha, const double* betas,
+                       int n_shifts, double tol, int64_t max_iter, const double* probe, int64_t n1,
+                       int64_t n2, double* directions, double* scores, double* residuals,
+                       int64_t* iterations, uint8_t* converged, int64_t* n_applies,
+                       int64_t* fail_iter);
 
 #ifdef __cplusplus
 }

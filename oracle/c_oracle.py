@@ -74,9 +74,16 @@ def lib():
                                         _PI64, _PU8, _PI64, _PI64]
         h.oracle_max_threads.restype = C.c_int
         h.oracle_max_threads.argtypes = []
+        h.oracle_fsda_solve_sharded.restype = C.c_int
+        h.oracle_fsda_solve_sharded.argtypes = [_I64, _I64, _PI64, _PI64, _PI64, _PI64, _PD, _PI8, C.c_double,
+                                                _PD, C.c_int, C.c_double, _I64, _PD, C.c_int, C.c_int,
+                                                _PI64, _PD, _PD, _PD, _PI64, _PU8, _PI64, _PI64]
         h.oracle_set_deferred.restype = None
         h.oracle_set_deferred.argtypes = [C.c_int]
         h.oracle_set_deferred(1 if _shift_mode == 2 else 0)
+        h.oracle_set_storage.restype = None
+        h.oracle_set_storage.argtypes = [C.c_int]
+        h.oracle_set_storage(_storage_bits)
         _lib = h
     return _lib
 
@@ -98,6 +105,20 @@ def set_shift_mode(mode: int) -> None:
 
 def shift_mode() -> int:
     return _shift_mode
+
+
+# Storage precision of the FSDA vectors mirrored from the device
+# (fsda_set_storage): 64, or 32 = fp32 storage with fp64 reductions.
+_storage_bits = 64
+
+
+def set_storage(bits: int) -> None:
+    global _storage_bits
+    if bits not in (32, 64):
+        raise ValueError("storage must be 32 or 64 bits")
+    _storage_bits = bits
+    if _lib is not None:
+        _lib.oracle_set_storage(bits)
 
 
 def _d(a):
@@ -312,3 +333,36 @@ def fsda_solve_workload(w, n_threads=0, scores=True, max_iter=None):
 
 def max_threads() -> int:
     return lib().oracle_max_threads()
+
+
+def fsda_solve_sharded(xoffs, xcols, d, loffs, lcols, lvals, labels, alpha, betas, tol, max_iter,
+                       probe, bounds, n_threads=0, scores=True):
+    """The row-sharded sweep's arithmetic (device fsda_solve_sharded): rows
+    split at `bounds`; column sums, sum(z), class sums and orientation dots
+    are rank-ordered sums of per-rank canonical trees."""
+    xo, pxo = _i(xoffs)
+    xc, pxc = _i(xcols)
+    lo, plo = _i(loffs)
+    lc, plc = _i(lcols)
+    lv, plv = _d(lvals)
+    lab, pl = _b(labels)
+    betas, pbe = _d(betas)
+    probe, ppr = _d(probe)
+    bd, pbd = _i(bounds)
+    n, ns = xo.size - 1, betas.size
+    dirs = np.empty((ns, d))
+    sc = np.empty((ns, n)) if scores else None
+    res = np.empty(ns)
+    its = np.empty(ns, dtype=np.int64)
+    conv = np.empty(ns, dtype=np.uint8)
+    napp, fail = C.c_int64(0), C.c_int64(-1)
+    st = lib().oracle_fsda_solve_sharded(n, d, pxo, pxc, plo, plc, plv, pl, float(alpha), pbe, ns,
+                                         float(tol), int(max_iter), ppr, int(n_threads), int(bd.size - 1),
+                                         pbd, dirs.ctypes.data_as(_PD),
+                                         sc.ctypes.data_as(_PD) if sc is not None else None,
+                                         res.ctypes.data_as(_PD), its.ctypes.data_as(_PI64),
+                                         conv.ctypes.data_as(_PU8), C.byref(napp), C.byref(fail))
+    if st:
+        raise OracleFailure(st, fail.value)
+    return dict(directions=dirs, scores=sc, residuals=res, iterations=its,
+                converged=conv.astype(bool), n_applies=napp.value)

@@ -50,6 +50,11 @@ SIGNATURES = {
     "fsda_solve_async": [_P],
     "fsda_set_shift_update_mode": [_P, C.c_int],
     "fsda_last_shift_update_mode": [_P],
+    "fsda_set_storage": [_P, C.c_int],
+    "fsda_nccl_unique_id": [_PU8],
+    "fsda_shard_init": [_P, C.c_int, C.c_int, _PI64, _PU8],
+    "fsda_solve_sharded": [C.POINTER(_P), C.c_int, _D, _PD, C.c_int, _D, _I64, _PD, _I64, _I64, _PD, _PD,
+                           _PD, _PI64, _PU8, _PI64, _PI64],
     "fsda_fetch_results": [_P, _PD, _PD, _PD, _PI64, _PU8, _PI64, _PI64, _PI64],
     "fsda_profile_kernels": [_P, C.c_int, _PI, C.POINTER(C.c_char_p), _PD, _PD, _PI64],
     "fsda_shifted_cg_dense": [_P, _I64, _PD, _PD, _PD, C.c_int, _D, _I64, C.c_int, _PD, _PD,

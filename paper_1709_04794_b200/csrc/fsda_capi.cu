@@ -253,6 +253,10 @@ struct fsda_ctx {
   // shift-update mode: requested (0 auto, 1 per-iteration, 2 deferred basis)
   // and the one the current solve uses (1 or 2)
   int su_req = 0, su_mode = 1;
+  // storage of the FSDA solve's vectors (p, y, z, r slots): 64, or 32 = fp32
+  // storage with fp64 reductions (BASELINE cfg5); q, mu, b and all scalars
+  // stay double.  fp32 storage always runs with the deferred basis.
+  int store_bits = 64;
   DevBuf<double> coef_a, coef_c;
   long long coef_ld = 1;
   DevBuf<double> bigp, sols, wT, scores, dense_a;
@@ -287,6 +291,15 @@ struct fsda_ctx {
   long long r_max_iter = 0;
   bool r_prepared = false;
   long long last_launch_count = 0;
+
+  // row-sharded solve (fsda_shard_init, fsda_shard.cuh): this context holds
+  // one contiguous row block of X and L of a problem split over `world` ranks
+  int world = 1, rank = 0;
+  long long maxc = 0;          // rows of the largest shard: the y all-gather slot
+  long long shard_n_global = 0;
+  void* nccl = nullptr;        // ncclComm_t (one process per GPU), or null (local ranks)
+  DevBuf<double> ypad, qpart, qrecv, qown, spart, sall;
+  cudaEvent_t ev_x = nullptr, ev_y = nullptr;  // local-rank exchanges
 
   ShiftState shifts() {
     ShiftState s;
@@ -390,8 +403,11 @@ int pdl_mode() {
   return v;
 }
 
-template <int KIND>
-void launch_segsum(fsda_ctx* c, const HostPlan& hp, const SegArgs& a, int guarded,
+// fp32 storage applies to the FSDA solve's loop vectors
+inline bool f32(const fsda_ctx* c) { return c->store_bits == 32 && c->solve_kind == 0; }
+
+template <int KIND, typename A>
+void launch_segsum(fsda_ctx* c, const HostPlan& hp, const A& a, int guarded,
                    long long sum_leaves) {
   SegPlan pl = hp.pl;
   pl.warp_base[8] = pl.warp_base[7] + sum_leaves;
@@ -410,24 +426,28 @@ void launch_segsum(fsda_ctx* c, const HostPlan& hp, const SegArgs& a, int guarde
   cfg.numAttrs = (pdl_mode() & 1) && KIND == SEG_LROWS ? 1 : 0;
   cfg.attrs = at;
   const CgScalars* sc = c->sc;
-  CK(cudaLaunchKernelEx(&cfg, k_segsum<KIND>, pl, a, sc, guarded));
+  CK(cudaLaunchKernelEx(&cfg, k_segsum<KIND, A>, pl, a, sc, guarded));
 }
 
-SegArgs seg_args(const double* src, double* out) {
-  SegArgs a;
+template <typename A = SegArgs>
+A seg_args(const void* src, void* out) {
+  A a;
   memset(&a, 0, sizeof(a));
-  a.src = src;
-  a.out = out;
+  a.src = static_cast<const typename A::value_type*>(src);
+  a.out = static_cast<decltype(a.out)>(out);
   return a;
 }
 
 // X^T z: mode 0 raw (+ optional sum(z) leaves), 1 centred with *sum_ptr, 2 / ell.
-void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* sum_ptr, int guarded,
-            double* sum_part, double* sum_out = nullptr) {
+// zf32: z is stored as float (the fp32-storage loop); out (q) is double.
+template <typename A>
+void enq_xt_t(Enq& e, const void* zsrc, double* out, int mode, const double* sum_ptr, int guarded,
+              double* sum_part, double* sum_out) {
   fsda_ctx* c = e.c;
-  const double bytes = 4.0 * (c->d + 1) + 4.0 * c->nnz + 8.0 * c->n + 8.0 * c->d +
+  const double vb = sizeof(typename A::value_type);
+  const double bytes = 4.0 * (c->d + 1) + 4.0 * c->nnz + vb * c->n + 8.0 * c->d +
                        (mode == 1 ? 8.0 * c->d : 0.0);
-  SegArgs a = seg_args(zsrc, out);
+  A a = seg_args<A>(zsrc, out);
   a.mode = mode;
   a.mu = c->mu_v.ptr;
   a.sum_ptr = sum_ptr;
@@ -445,7 +465,7 @@ void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* sum
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c->xt_blocks);
     cfg.blockDim = dim3(XT_THREADS);
-    cfg.dynamicSmemBytes = sizeof(double) * xh.rb;
+    cfg.dynamicSmemBytes = sizeof(typename A::value_type) * xh.rb;
     cfg.stream = c->stream;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;
@@ -454,39 +474,60 @@ void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* sum
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.numAttrs = (pdl_mode() & 2) ? 2 : 1;
     cfg.attrs = at;
-    CK(cudaLaunchKernelEx(&cfg, k_xt_coop, pl, xh, a, sc, guarded, n_rows, ticket, sum_out));
+    CK(cudaLaunchKernelEx(&cfg, k_xt_coop<A>, pl, xh, a, sc, guarded, n_rows, ticket, sum_out));
   });
 }
 
-// y = X v in the canonical row order.
-void enq_xrows(Enq& e, const double* v, double* out, int guarded) {
+void enq_xt(Enq& e, const double* zsrc, double* out, int mode, const double* sum_ptr, int guarded,
+            double* sum_part, double* sum_out = nullptr, bool zf32 = false) {
+  if (zf32) enq_xt_t<SegArgs32D>(e, zsrc, out, mode, sum_ptr, guarded, sum_part, sum_out);
+  else enq_xt_t<SegArgs>(e, zsrc, out, mode, sum_ptr, guarded, sum_part, sum_out);
+}
+
+// y = X v in the canonical row order (vf32: v and y stored as float).
+void enq_xrows(Enq& e, const void* v, void* out, int guarded, bool vf32 = false) {
   fsda_ctx* c = e.c;
-  const double bytes = 4.0 * (c->n + 1) + 4.0 * c->nnz + 8.0 * c->d + 8.0 * c->n;
-  SegArgs a = seg_args(v, out);
-  e.go("spmv_rows", bytes, [&] { launch_segsum<SEG_XROWS>(c, c->plan_xr, a, guarded, 0); });
+  const double vb = vf32 ? 4.0 : 8.0;
+  const double bytes = 4.0 * (c->n + 1) + 4.0 * c->nnz + vb * c->d + vb * c->n;
+  if (vf32) {
+    SegArgs32 a = seg_args<SegArgs32>(v, out);
+    e.go("spmv_rows", bytes, [&] { launch_segsum<SEG_XROWS>(c, c->plan_xr, a, guarded, 0); });
+  } else {
+    SegArgs a = seg_args<SegArgs>(v, out);
+    e.go("spmv_rows", bytes, [&] { launch_segsum<SEG_XROWS>(c, c->plan_xr, a, guarded, 0); });
+  }
 }
 
 int alpha_mode_of(double alpha) { return alpha == 0.0 ? 0 : (alpha == 1.0 ? 1 : 2); }
 
-// z = M y (apply_smoother, sda.py:131-140).
-void enq_smoother(Enq& e, double alpha, const double* y, double* z, int guarded) {
+// z = M y (apply_smoother, sda.py:131-140); vf32: y and z stored as float.
+template <typename A>
+void enq_smoother_t(Enq& e, double alpha, const void* y, void* z, int guarded) {
   fsda_ctx* c = e.c;
+  using V = typename A::value_type;
+  const double vb = sizeof(V);
   const int amode = alpha_mode_of(alpha);
   if (amode == 0) {
-    e.go("smoother", 17.0 * c->n, [&] {
-      k_mask_labeled<<<grid_for(c->n, 256), 256, 0, c->stream>>>(y, c->labels.ptr, z, (int)c->n, c->sc,
-                                                                 guarded, (int)c->row_base);
+    e.go("smoother", (2.0 * vb + 1.0) * c->n, [&] {
+      k_mask_labeled<V><<<grid_for(c->n, 256), 256, 0, c->stream>>>(
+          static_cast<const V*>(y), c->labels.ptr, static_cast<V*>(z), (int)c->n, c->sc, guarded,
+          (int)c->row_base);
     });
     return;
   }
-  SegArgs a = seg_args(y, z);
+  A a = seg_args<A>(y, z);
   a.ldiag = c->l_diag.ptr;
   a.labels = c->labels.ptr;
   a.alpha = alpha;
   a.alpha_mode = amode;
   a.row_base = (int)c->row_base;
-  const double bytes = 4.0 * (c->n + 1) + 4.0 * c->l_nnz + 8.0 * c->n + 1.0 * c->n + 16.0 * c->n;
+  const double bytes = 4.0 * (c->n + 1) + 4.0 * c->l_nnz + vb * c->n + 1.0 * c->n + 8.0 * c->n + vb * c->n;
   e.go("smoother", bytes, [&] { launch_segsum<SEG_LROWS>(c, c->plan_lr, a, guarded, 0); });
+}
+
+void enq_smoother(Enq& e, double alpha, const void* y, void* z, int guarded, bool vf32 = false) {
+  if (vf32) enq_smoother_t<SegArgs32>(e, alpha, y, z, guarded);
+  else enq_smoother_t<SegArgs>(e, alpha, y, z, guarded);
 }
 
 size_t step_smem(int ns) { return sizeof(double) * 3 * (size_t)std::max(ns, 1); }
@@ -499,7 +540,7 @@ void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, i
   const long long nlD = n_leaves(d);
   double* q = c->q.ptr;
   double* p = c->p.ptr;
-  double* rb = c->rbuf.ptr;
+  void* rb = c->rbuf.ptr;
   int nsl = c->nslots;
   double* bigp = c->bigp.ptr;
   double* sols = c->sols.ptr;
@@ -517,11 +558,14 @@ void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, i
   // the two grid barriers); warps loop over further leaves only when d exceeds
   // what a co-resident grid covers.
   if (c->step_blocks == 0) {
-    int nb = 0;
-    CK(cudaFuncSetAttribute(k_cg_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cg_step, STEP_THREADS,
+    int nb = 0, nb32 = 0;
+    CK(cudaFuncSetAttribute(k_cg_step<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_cg_step<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cg_step<double>, STEP_THREADS,
                                                      step_smem(4096)));
-    c->step_blocks = std::max(1, nb) * c->num_sms;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb32, k_cg_step<float>, STEP_THREADS,
+                                                     step_smem(4096)));
+    c->step_blocks = std::max(1, std::min(nb, nb32)) * c->num_sms;
   }
   const long long want = (nlD + STEP_THREADS / 32 - 1) / (STEP_THREADS / 32);
   const int blocks = (int)std::max(1LL, std::min<long long>(want, c->step_blocks));
@@ -537,8 +581,12 @@ void launch_cg_step(fsda_ctx* c, int ns, long long d, unsigned long long cond, i
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.numAttrs = (pdl_mode() & 4) ? 2 : 1;
   cfg.attrs = at;
-  CK(cudaLaunchKernelEx(&cfg, k_cg_step, q, p, rb, nsl, bigp, sols, d, pp, pr, nlD, sc, ss, ns, cond,
-                        use_cond, mu, pz, nlz, lab, ell, sum_ready));
+  if (f32(c))
+    CK(cudaLaunchKernelEx(&cfg, k_cg_step<float>, q, (float*)p, (float*)rb, nsl, bigp, sols, d, pp, pr,
+                          nlD, sc, ss, ns, cond, use_cond, mu, pz, nlz, lab, ell, sum_ready));
+  else
+    CK(cudaLaunchKernelEx(&cfg, k_cg_step<double>, q, p, (double*)rb, nsl, bigp, sols, d, pp, pr, nlD,
+                          sc, ss, ns, cond, use_cond, mu, pz, nlz, lab, ell, sum_ready));
 }
 
 // The shift-state update of the last base step on `stream`: sols / P
@@ -578,6 +626,7 @@ void resolve_shift_mode(fsda_ctx* c, int ns, long long max_iter, long long d) {
     const double have = 8.0 * (double)c->rbuf.cap + 8.0 * (double)(c->coef_a.cap + c->coef_c.cap);
     mode = need <= 0.25 * (double)free_b + have ? 2 : 1;
   }
+  if (c->store_bits == 32 && c->solve_kind == 0) mode = 2;
   c->su_mode = mode;
   c->nslots = mode == 2 ? (int)std::min<long long>(slots, INT32_MAX) : 2;
   c->coef_ld = mode == 2 ? slots : 1;
@@ -588,9 +637,14 @@ void launch_cg_init(fsda_ctx* c, const double* bsrc, long long d, int ns) {
   ShiftState ss = c->shifts();
   const long long nlD = n_leaves(d);
   dim3 g(grid_for(nlD, WARPS_PER_BLOCK), 1 + ns);
-  k_cg_init<<<g, LEAF_THREADS, 0, c->stream>>>(bsrc, c->rbuf.ptr, c->p.ptr, c->bigp.ptr,
-                                               c->sols.ptr, d, c->part_d.ptr, nlD, c->sc, ss, ns,
-                                               c->su_mode == 2 ? 1 : 0);
+  if (f32(c))
+    k_cg_init<float><<<g, LEAF_THREADS, 0, c->stream>>>(bsrc, (float*)c->rbuf.ptr, (float*)c->p.ptr,
+                                                        c->bigp.ptr, c->sols.ptr, d, c->part_d.ptr, nlD,
+                                                        c->sc, ss, ns, 1);
+  else
+    k_cg_init<double><<<g, LEAF_THREADS, 0, c->stream>>>(bsrc, c->rbuf.ptr, c->p.ptr, c->bigp.ptr,
+                                                         c->sols.ptr, d, c->part_d.ptr, nlD, c->sc, ss,
+                                                         ns, c->su_mode == 2 ? 1 : 0);
   CKL();
 }
 
@@ -601,7 +655,11 @@ void launch_final_shift(fsda_ctx* c, int ns, long long d) {
   if (c->su_mode == 2 && d > 0) {
     ShiftState ss = c->shifts();
     dim3 g((unsigned)grid_for(d, 256), (unsigned)((ns + CB_SH - 1) / CB_SH));
-    k_combine_basis<<<g, 256, 0, c->stream>>>(c->rbuf.ptr, d, ss, c->sc, ns, c->sols.ptr);
+    if (f32(c))
+      k_combine_basis<float><<<g, 256, 0, c->stream>>>((const float*)c->rbuf.ptr, d, ss, c->sc, ns,
+                                                       c->sols.ptr);
+    else
+      k_combine_basis<double><<<g, 256, 0, c->stream>>>(c->rbuf.ptr, d, ss, c->sc, ns, c->sols.ptr);
     CKL();
   }
 }
@@ -648,10 +706,11 @@ void enq_fsda_iteration(Enq& e, double alpha, int ns, unsigned long long cond, i
   // (FSDA_B200_K3_SUM=0: the CG step reduces it)
   static const bool k3_sum = !std::getenv("FSDA_B200_K3_SUM") || std::atoi(std::getenv("FSDA_B200_K3_SUM"));
   double* sum_out = k3_sum ? &c->sc->sum_z_iter : nullptr;
+  const bool v32 = f32(c);
   enq_iteration_body(e, ns, d, 1, cond, use_cond, 8.0 * c->n + 24.0 * d + 24.0 * d + 24.0 * d, [&] {
-    enq_xrows(e, c->p.ptr, c->y.ptr, 1);
-    enq_smoother(e, alpha, c->y.ptr, c->z.ptr, 1);
-    enq_xt(e, c->z.ptr, c->q.ptr, 0, nullptr, 1, c->part_n.ptr, sum_out);
+    enq_xrows(e, c->p.ptr, c->y.ptr, 1, v32);
+    enq_smoother(e, alpha, c->y.ptr, c->z.ptr, 1, v32);
+    enq_xt(e, c->z.ptr, c->q.ptr, 0, nullptr, 1, c->part_n.ptr, sum_out, v32);
   }, sum_out);
 }
 
@@ -823,7 +882,7 @@ bool build_solve_graph(fsda_ctx* c, double alpha, int ns, long long max_iter, do
   char key[320];
   snprintf(key, sizeof(key), "%d|%d|%a|%d|%lld|%a|%lld|%lld|%lld|%llu|%llx|%d|%d", c->solve_kind,
            c->solve_abs_tol, alpha, ns, max_iter, tol, c->n, c->d, c->nnz, g_alloc_gen, h,
-           c->su_mode, c->nslots);
+           c->su_mode, c->nslots * (c->store_bits == 32 ? -1 : 1));
   if (c->exec && c->graph_key == key) {
     *launches_fixed = c->graph_fixed;
     *launches_body = c->graph_body;
@@ -1237,9 +1296,13 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   tr.mark("  blocked: h2d");
   if (c->xt_blocks == 0) {
     int per_sm = 0;
-    CK(cudaFuncSetAttribute(k_xt_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    // the fp32-storage instance needs half the shared memory: the fp64 grid
+    // is co-resident for both
+    CK(cudaFuncSetAttribute(k_xt_coop<SegArgs>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double) * rb)));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_xt_coop, XT_THREADS,
+    CK(cudaFuncSetAttribute(k_xt_coop<SegArgs32D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(sizeof(double) * rb)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_xt_coop<SegArgs>, XT_THREADS,
                                                      sizeof(double) * rb));
     c->xt_blocks = std::max(1, std::min(per_sm, XT_CTAS_PER_SM)) * c->num_sms;
   }
@@ -1331,6 +1394,15 @@ int fsda_last_shift_update_mode(fsda_ctx* c) {
   return c->su_mode;
 }
 
+int fsda_set_storage(fsda_ctx* c, int bits) {
+  API_BEGIN(c)
+  if (bits != 32 && bits != 64) return fail(FSDA_EINVAL, "storage must be 32 or 64 bits, got %d", bits);
+  c->store_bits = bits;
+  c->invalidate_graph();
+  return FSDA_OK;
+  API_END
+}
+
 const char* fsda_last_error(void) { return g_last_error.c_str(); }
 
 int fsda_ctx_create(fsda_ctx** out, int device, void* stream) {
@@ -1374,6 +1446,8 @@ int fsda_ctx_create(fsda_ctx** out, int device, void* stream) {
   *out = c;
   return FSDA_OK;
 }
+
+void shard_release_comm(fsda_ctx* c);  // fsda_shard.cuh
 
 int fsda_ctx_destroy(fsda_ctx* c) {
   if (!c) return FSDA_OK;
@@ -1423,6 +1497,11 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_lfork) cudaEventDestroy(c->ev_lfork);
     if (c->ev_lcopy) cudaEventDestroy(c->ev_lcopy);
+    if (c->ev_x) cudaEventDestroy(c->ev_x);
+    if (c->ev_y) cudaEventDestroy(c->ev_y);
+    c->ypad.release(); c->qpart.release(); c->qrecv.release(); c->qown.release();
+    c->spart.release(); c->sall.release();
+    shard_release_comm(c);
     if (c->own_stream) cudaStreamDestroy(c->stream);
   }
   delete c;
@@ -2591,6 +2670,8 @@ int fsda_solve_batch(fsda_ctx* c, int n_tasks, const int8_t* labels, double alph
 }
 
 }  // extern "C"
+
+#include "fsda_shard.cuh"
 
 // debug: per-CTA phase timestamps of the last k_xt_coop launch (globaltimer ns)
 extern "C" int fsda_debug_xt_trace(int on, unsigned long long* out) {

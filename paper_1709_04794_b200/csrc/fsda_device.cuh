@@ -259,8 +259,9 @@ __global__ void k_apply_w(const signed char* __restrict__ labels, double* __rest
 // Shifted-CG initialisation (krylov.py:185-208): b_norm, threshold, rr, and
 // r = p = b, P_s = b, sols = 0.  blockIdx.y == 0: r/p + b.b leaves;
 // blockIdx.y == s+1: shift s.
-__global__ void k_cg_init(const double* __restrict__ b, double* __restrict__ r,
-                          double* __restrict__ p, double* __restrict__ bigp,
+template <typename V>
+__global__ void k_cg_init(const double* __restrict__ b, V* __restrict__ r,
+                          V* __restrict__ p, double* __restrict__ bigp,
                           double* __restrict__ sols, long long d, double* __restrict__ part,
                           long long n_leaf, CgScalars* sc, ShiftState ss, int n_shifts, int basis) {
   __shared__ double smem[257];
@@ -273,8 +274,8 @@ __global__ void k_cg_init(const double* __restrict__ b, double* __restrict__ r,
         long long i = g * LEAF + k * 32 + lane;
         if (i < d) {
           double v = b[i];
-          r[i] = v;
-          p[i] = v;
+          r[i] = (V)v;
+          p[i] = (V)v;
           a = fma(v, v, a);
         }
       }

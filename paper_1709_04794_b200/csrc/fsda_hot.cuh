@@ -164,9 +164,14 @@ struct SegPlan {
   double* seg_part;          // leaf partials
 };
 
-struct SegArgs {
-  const double* src;         // gathered vector: p, y or z
-  double* out;               // y, z or q (raw)
+// V: storage type of the gathered vector src (double, or float for the
+// fp32-storage mode); O: storage type of out (q stays double).  Every sum
+// runs in double over the stored values; out is rounded to O once.
+template <typename V, typename O>
+struct SegArgsT {
+  using value_type = V;
+  const V* src;              // gathered vector: p, y or z
+  O* out;                    // y, z or q (raw)
   // L rows: z = blend(alpha, masked y, alpha * (L y))
   const double* ldiag;
   const signed char* labels;
@@ -182,26 +187,29 @@ struct SegArgs {
   double* sum_part;
   long long sum_n;
 };
+using SegArgs = SegArgsT<double, double>;
+using SegArgs32 = SegArgsT<float, float>;     // K1 / K2 in fp32 storage
+using SegArgs32D = SegArgsT<float, double>;   // K3 in fp32 storage: q in double
 
-template <int KIND>
-__device__ __forceinline__ double seg_term(const SegArgs& a, int seg, int idx, double dg) {
-  const double v = __ldg(a.src + idx);
+template <int KIND, typename A>
+__device__ __forceinline__ double seg_term(const A& a, int seg, int idx, double dg) {
+  const double v = (double)__ldg(a.src + idx);
   if (KIND == SEG_LROWS) return (idx == seg + a.row_base) ? dg * v : -v;
   return v;
 }
 
 // The row's own loads that seg_finish needs (L rows: the masked y_i), issued
 // with the task so they do not add a round trip after the reduction.
-template <int KIND>
-__device__ __forceinline__ double seg_pre(const SegArgs& a, int seg) {
+template <int KIND, typename A>
+__device__ __forceinline__ double seg_pre(const A& a, int seg) {
   if (KIND != SEG_LROWS) return 0.0;
   const signed char l = __ldg(a.labels + seg);
-  const double y = __ldg(a.src + seg + a.row_base);
+  const double y = (double)__ldg(a.src + seg + a.row_base);
   return l != 0 ? y : 0.0;
 }
 
-template <int KIND>
-__device__ __forceinline__ void seg_finish(const SegArgs& a, int seg, double s, double masked) {
+template <int KIND, typename A>
+__device__ __forceinline__ void seg_finish(const A& a, int seg, double s, double masked) {
   if (KIND == SEG_XROWS) {
     a.out[seg] = s;
   } else if (KIND == SEG_LROWS) {
@@ -214,15 +222,15 @@ __device__ __forceinline__ void seg_finish(const SegArgs& a, int seg, double s, 
   }
 }
 
-template <int KIND>
-__device__ __forceinline__ void seg_finish(const SegArgs& a, int seg, double s) {
+template <int KIND, typename A>
+__device__ __forceinline__ void seg_finish(const A& a, int seg, double s) {
   seg_finish<KIND>(a, seg, s, seg_pre<KIND>(a, seg));
 }
 
 // Canonical leaf of segment elements [start, start+n) (n <= 8W) by a W-lane
 // group; t = lane within the group; result in every lane of the group.
-template <int W, int KIND>
-__device__ __forceinline__ double group_leaf(const SegPlan& pl, const SegArgs& a, int seg, int start,
+template <int W, int KIND, typename SA>
+__device__ __forceinline__ double group_leaf(const SegPlan& pl, const SA& a, int seg, int start,
                                              int n, int t) {
   constexpr int M = 32 / W;
   constexpr int MA = M < 8 ? M : 8;
@@ -243,7 +251,7 @@ __device__ __forceinline__ double group_leaf(const SegPlan& pl, const SegArgs& a
 #pragma unroll
     for (int k = 0; k < KA; ++k) {
       const int e = t + m * W + 32 * k;
-      v[m * KA + k] = (e < n) ? seg_term<KIND>(a, seg, ix[m * KA + k], dg) : 0.0;
+      v[m * KA + k] = (e < n) ? seg_term<KIND, SA>(a, seg, ix[m * KA + k], dg) : 0.0;
     }
   double A[MA];
 #pragma unroll
@@ -264,27 +272,27 @@ __device__ __forceinline__ double group_leaf(const SegPlan& pl, const SegArgs& a
   return r;
 }
 
-template <int W, int KIND>
-__device__ __forceinline__ void seg_class_task(const SegPlan& pl, const SegArgs& a, int cls,
+template <int W, int KIND, typename A>
+__device__ __forceinline__ void seg_class_task(const SegPlan& pl, const A& a, int cls,
                                                long long tw, int lane) {
   const long long idx = pl.cls_off[cls] + (tw - pl.warp_base[cls]) * (32 / W) + lane / W;
   int4 tk = make_int4(-1, 0, 0, -1);
   if (idx < pl.cls_off[cls + 1]) tk = __ldg(pl.tasks + idx);
   const bool leader = tk.x >= 0 && (lane & (W - 1)) == 0;
-  const double pre = leader ? seg_pre<KIND>(a, tk.x) : 0.0;
-  const double s = group_leaf<W, KIND>(pl, a, tk.x, tk.y, tk.z, lane & (W - 1));
-  if (leader) seg_finish<KIND>(a, tk.x, s, pre);
+  const double pre = leader ? seg_pre<KIND, A>(a, tk.x) : 0.0;
+  const double s = group_leaf<W, KIND, A>(pl, a, tk.x, tk.y, tk.z, lane & (W - 1));
+  if (leader) seg_finish<KIND, A>(a, tk.x, s, pre);
 }
 
-template <int KIND>
-__device__ __forceinline__ void seg_heavy_task(const SegPlan& pl, const SegArgs& a, long long tw,
+template <int KIND, typename A>
+__device__ __forceinline__ void seg_heavy_task(const SegPlan& pl, const A& a, long long tw,
                                                int lane) {
   // heavy task: up to 4 consecutive leaves of one segment
   const int4 tk = __ldg(pl.tasks + pl.cls_off[6] + (tw - pl.warp_base[6]));
   const int h = tk.w;
   const int leaf0 = __ldg(pl.heavy_seg0 + h) + (tk.y - __ldg(pl.heavy_start + h)) / LEAF;
   for (int lf = 0; lf * LEAF < tk.z; ++lf) {
-    const double s = group_leaf<32, KIND>(pl, a, tk.x, tk.y + lf * LEAF,
+    const double s = group_leaf<32, KIND, A>(pl, a, tk.x, tk.y + lf * LEAF,
                                           min(LEAF, tk.z - lf * LEAF), lane);
     if (lane == 0) pl.seg_part[leaf0 + lf] = s;
   }
@@ -300,7 +308,7 @@ __device__ __forceinline__ void seg_heavy_task(const SegPlan& pl, const SegArgs&
     const double s = warp_reduce_partials(pl.seg_part + __ldg(pl.heavy_seg0 + h),
                                           __ldg(pl.heavy_nseg + h), lane);
     if (lane == 0) {
-      seg_finish<KIND>(a, tk.x, s);
+      seg_finish<KIND, A>(a, tk.x, s);
       pl.heavy_count[h] = 0u;
     }
   }
@@ -314,8 +322,8 @@ __device__ __forceinline__ void seg_heavy_task(const SegPlan& pl, const SegArgs&
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-template <int KIND>
-__global__ void __launch_bounds__(256, 6) k_segsum(SegPlan pl, SegArgs a, const CgScalars* sc,
+template <int KIND, typename A>
+__global__ void __launch_bounds__(256, 6) k_segsum(SegPlan pl, A a, const CgScalars* sc,
                                                 int guarded) {
   pdl_trigger();
   pdl_wait();
@@ -329,12 +337,12 @@ __global__ void __launch_bounds__(256, 6) k_segsum(SegPlan pl, SegArgs a, const 
       int k = 0;
       while (tw >= pl.warp_base[k + 1]) ++k;
       switch (k) {
-        case 0: seg_class_task<1, KIND>(pl, a, 0, tw, lane); break;
-        case 1: seg_class_task<2, KIND>(pl, a, 1, tw, lane); break;
-        case 2: seg_class_task<4, KIND>(pl, a, 2, tw, lane); break;
-        case 3: seg_class_task<8, KIND>(pl, a, 3, tw, lane); break;
-        case 4: seg_class_task<16, KIND>(pl, a, 4, tw, lane); break;
-        default: seg_class_task<32, KIND>(pl, a, 5, tw, lane); break;
+        case 0: seg_class_task<1, KIND, A>(pl, a, 0, tw, lane); break;
+        case 1: seg_class_task<2, KIND, A>(pl, a, 1, tw, lane); break;
+        case 2: seg_class_task<4, KIND, A>(pl, a, 2, tw, lane); break;
+        case 3: seg_class_task<8, KIND, A>(pl, a, 3, tw, lane); break;
+        case 4: seg_class_task<16, KIND, A>(pl, a, 4, tw, lane); break;
+        default: seg_class_task<32, KIND, A>(pl, a, 5, tw, lane); break;
       }
       continue;
     }
@@ -344,13 +352,13 @@ __global__ void __launch_bounds__(256, 6) k_segsum(SegPlan pl, SegArgs a, const 
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const long long i = g * LEAF + k * 32 + lane;
-        if (i < a.sum_n) s = s + __ldg(a.src + i);
+        if (i < a.sum_n) s = s + (double)__ldg(a.src + i);
       }
       s = butterfly(s);
       if (lane == 0) a.sum_part[g] = s;
       continue;
     }
-    seg_heavy_task<KIND>(pl, a, tw, lane);
+    seg_heavy_task<KIND, A>(pl, a, tw, lane);
   }
 }
 
@@ -402,8 +410,8 @@ struct XtDense {
   long long n_big;
 };
 
-template <int W>
-__device__ __forceinline__ void dense_slice_task(const XtDense& dn, const double* zs, int r0,
+template <int W, typename V>
+__device__ __forceinline__ void dense_slice_task(const XtDense& dn, const V* zs, int r0,
                                                  const long long* off, const long long* wb,
                                                  int cls, long long tw_local, int lane) {
   constexpr int M = 32 / W;
@@ -428,7 +436,7 @@ __device__ __forceinline__ void dense_slice_task(const XtDense& dn, const double
     double acc = 0.0;
 #pragma unroll
     for (int k = 0; k < KA; ++k)
-      if (t + m * W + 32 * k < n) acc = acc + zs[ix[m * KA + k]];
+      if (t + m * W + 32 * k < n) acc = acc + (double)zs[ix[m * KA + k]];
     A[m] = acc;
   }
 #pragma unroll
@@ -467,10 +475,11 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 // an odd last element by a plain load); every thread waits for the bytes.
 // The caller's __syncthreads() before the call retires the previous block's
 // reads; the one after it publishes the odd element.
-__device__ __forceinline__ void stage_block(double* zs, const double* __restrict__ src, int n,
+template <typename V>
+__device__ __forceinline__ void stage_block(V* zs, const V* __restrict__ src, int n,
                                             unsigned long long* bar, unsigned phase) {
   if (threadIdx.x == 0) {
-    const unsigned bytes = (unsigned)(8 * n) & ~15u;
+    const unsigned bytes = (unsigned)(sizeof(V) * n) & ~15u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
@@ -481,7 +490,7 @@ __device__ __forceinline__ void stage_block(double* zs, const double* __restrict
               smem_u32(zs)),
           "l"(src), "r"(bytes), "r"(smem_u32(bar))
           : "memory");
-    if (n & 1) zs[n - 1] = __ldg(src + n - 1);
+    for (int k = (int)(bytes / sizeof(V)); k < n; ++k) zs[k] = __ldg(src + k);
   }
   mbar_wait(bar, phase);
 }
@@ -496,13 +505,16 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define XT_MARK(k) \
   if (g_xt_trace_on && threadIdx.x == 0 && blockIdx.x < 1024) g_xt_trace[k][blockIdx.x] = gtimer();
 
-__global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan pl, XtDense dn, SegArgs a,
+template <typename A>
+__global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan pl, XtDense dn, A a,
                                                     const CgScalars* sc, int guarded, int n_rows,
                                                     unsigned long long* ticket, double* sum_out) {
+  using V = typename A::value_type;
   pdl_trigger();
   pdl_wait();
   if (guarded && loop_idle(sc)) return;  // uniform across the grid
-  extern __shared__ __align__(16) double zs[];  // dn.rb doubles
+  extern __shared__ __align__(16) double zs_raw[];  // dn.rb values of z
+  V* zs = reinterpret_cast<V*>(zs_raw);
   __shared__ unsigned long long zs_bar;
   __shared__ long long s_off[7], s_wb[7];  // the current row block's class starts / warp prefixes
   XT_MARK(0)
@@ -535,12 +547,12 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
         int k = 0;
         while (tw >= s_wb[k + 1]) ++k;
         switch (k) {
-          case 0: dense_slice_task<1>(dn, zs, r0, s_off, s_wb, 0, tw, lane); break;
-          case 1: dense_slice_task<2>(dn, zs, r0, s_off, s_wb, 1, tw, lane); break;
-          case 2: dense_slice_task<4>(dn, zs, r0, s_off, s_wb, 2, tw, lane); break;
-          case 3: dense_slice_task<8>(dn, zs, r0, s_off, s_wb, 3, tw, lane); break;
-          case 4: dense_slice_task<16>(dn, zs, r0, s_off, s_wb, 4, tw, lane); break;
-          default: dense_slice_task<32>(dn, zs, r0, s_off, s_wb, 5, tw, lane); break;
+          case 0: dense_slice_task<1, V>(dn, zs, r0, s_off, s_wb, 0, tw, lane); break;
+          case 1: dense_slice_task<2, V>(dn, zs, r0, s_off, s_wb, 1, tw, lane); break;
+          case 2: dense_slice_task<4, V>(dn, zs, r0, s_off, s_wb, 2, tw, lane); break;
+          case 3: dense_slice_task<8, V>(dn, zs, r0, s_off, s_wb, 3, tw, lane); break;
+          case 4: dense_slice_task<16, V>(dn, zs, r0, s_off, s_wb, 4, tw, lane); break;
+          default: dense_slice_task<32, V>(dn, zs, r0, s_off, s_wb, 5, tw, lane); break;
         }
       }
     }
@@ -567,22 +579,22 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
       int k = 0;
       while (tw >= pl.warp_base[k + 1]) ++k;
       switch (k) {
-        case 0: seg_class_task<1, SEG_XCOLS>(pl, a, 0, tw, lane); break;
-        case 1: seg_class_task<2, SEG_XCOLS>(pl, a, 1, tw, lane); break;
-        case 2: seg_class_task<4, SEG_XCOLS>(pl, a, 2, tw, lane); break;
-        case 3: seg_class_task<8, SEG_XCOLS>(pl, a, 3, tw, lane); break;
-        case 4: seg_class_task<16, SEG_XCOLS>(pl, a, 4, tw, lane); break;
-        default: seg_class_task<32, SEG_XCOLS>(pl, a, 5, tw, lane); break;
+        case 0: seg_class_task<1, SEG_XCOLS, A>(pl, a, 0, tw, lane); break;
+        case 1: seg_class_task<2, SEG_XCOLS, A>(pl, a, 1, tw, lane); break;
+        case 2: seg_class_task<4, SEG_XCOLS, A>(pl, a, 2, tw, lane); break;
+        case 3: seg_class_task<8, SEG_XCOLS, A>(pl, a, 3, tw, lane); break;
+        case 4: seg_class_task<16, SEG_XCOLS, A>(pl, a, 4, tw, lane); break;
+        default: seg_class_task<32, SEG_XCOLS, A>(pl, a, 5, tw, lane); break;
       }
     } else if (tw < pl.warp_base[7]) {
-      seg_heavy_task<SEG_XCOLS>(pl, a, tw, lane);
+      seg_heavy_task<SEG_XCOLS, A>(pl, a, tw, lane);
     } else {
       const long long g = tw - pl.warp_base[7];
       double v = 0.0;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const long long i = g * LEAF + k * 32 + lane;
-        if (i < a.sum_n) v = v + __ldg(a.src + i);
+        if (i < a.sum_n) v = v + (double)__ldg(a.src + i);
       }
       v = butterfly(v);
       if (lane == 0) a.sum_part[g] = v;
@@ -599,7 +611,7 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
   // CTA, whose warps hold the fewest dense columns, reduces it with the same
   // tree as k_cg_step's block_reduce_partials would
   if (sum_out && blockIdx.x == gridDim.x - 1) {
-    const double s = block_reduce_partials(a.sum_part, (a.sum_n + LEAF - 1) / LEAF, zs);
+    const double s = block_reduce_partials(a.sum_part, (a.sum_n + LEAF - 1) / LEAF, zs_raw);
     if (threadIdx.x == 0) *sum_out = s;
   }
   // ---- phase 2: dense columns.  Columns with more than XT_BIG_PARTS leaf
@@ -609,8 +621,8 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
   for (long long i = blockIdx.x; i < dn.n_big; i += gridDim.x) {
     const int h = __ldg(dn.big + i);
     const long long p0 = __ldg(dn.poff + h);
-    const double v = block_reduce_partials(dn.part + p0, __ldg(dn.poff + h + 1) - p0, zs);
-    if (threadIdx.x == 0) seg_finish<SEG_XCOLS>(a, __ldg(dn.col + h), v);
+    const double v = block_reduce_partials(dn.part + p0, __ldg(dn.poff + h + 1) - p0, zs_raw);
+    if (threadIdx.x == 0) seg_finish<SEG_XCOLS, A>(a, __ldg(dn.col + h), v);
   }
   const long long gw = (long long)blockIdx.x * nw + warp;
   for (long long h = gw; h < dn.n_dense; h += nwarps) {
@@ -618,7 +630,7 @@ __global__ void __launch_bounds__(XT_THREADS, XT_CTAS_PER_SM) k_xt_coop(SegPlan 
     const int m = (int)(__ldg(dn.poff + h + 1) - p0);
     if (m > XT_BIG_PARTS) continue;
     const double v = warp_reduce_partials(dn.part + p0, m, lane);
-    if (lane == 0) seg_finish<SEG_XCOLS>(a, __ldg(dn.col + h), v);
+    if (lane == 0) seg_finish<SEG_XCOLS, A>(a, __ldg(dn.col + h), v);
   }
   __syncthreads();
   XT_MARK(4)
@@ -645,12 +657,13 @@ __global__ void k_heavy_bptr(const int* __restrict__ colptr, const int* __restri
 }
 
 // z = masked y (apply_smoother at alpha == 0: no Laplacian term, sda.py:135-136).
-__global__ void k_mask_labeled(const double* __restrict__ y, const signed char* __restrict__ labels,
-                               double* __restrict__ z, int n, const CgScalars* sc, int guarded,
+template <typename V>
+__global__ void k_mask_labeled(const V* __restrict__ y, const signed char* __restrict__ labels,
+                               V* __restrict__ z, int n, const CgScalars* sc, int guarded,
                                int row_base) {
   if (guarded && loop_idle(sc)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) z[i] = labels[i] != 0 ? y[i + row_base] : 0.0;
+  if (i < n) z[i] = labels[i] != 0 ? y[i + row_base] : (V)0;
 }
 
 // q[i] = q[i] - mu[i] * q[d]  (centring of an all-reduced [X^T z | sum z]),
@@ -683,8 +696,12 @@ __global__ void k_center(const double* __restrict__ mu, double* __restrict__ q, 
 // at kernel entry, so no block reads state that block 0 modifies.
 constexpr int STEP_THREADS = 256;
 
+// V: storage of p and the residual slots (double, or float in the fp32-storage
+// mode: every update is computed in double and rounded once when stored; the
+// dots run over the stored values).
+template <typename V>
 __global__ void __launch_bounds__(STEP_THREADS) k_cg_step(
-    double* __restrict__ q, double* __restrict__ p, double* __restrict__ rbuf, int nslots,
+    double* __restrict__ q, V* __restrict__ p, V* __restrict__ rbuf, int nslots,
     double* __restrict__ bigp, double* __restrict__ sols, long long d,
     double* __restrict__ part_pq, double* __restrict__ part_rr, long long n_leaf, CgScalars* sc,
     ShiftState ss, int ns, unsigned long long cond_handle, int use_cond,
@@ -714,8 +731,8 @@ __global__ void __launch_bounds__(STEP_THREADS) k_cg_step(
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
   const long long tw = (long long)gridDim.x * (blockDim.x >> 5);
   // residual slots: ping-pong (nslots 2) or the stored basis r_0 .. r_K
-  const double* r_cur = rbuf + (it % nslots) * d;
-  double* r_next = rbuf + ((it + 1) % nslots) * d;
+  const V* r_cur = rbuf + (it % nslots) * d;
+  V* r_next = rbuf + ((it + 1) % nslots) * d;
   const bool center = part_z != nullptr;
   const bool own = gw < n_leaf;  // this warp's register-cached leaf
 
@@ -725,8 +742,8 @@ __global__ void __launch_bounds__(STEP_THREADS) k_cg_step(
   for (int k = 0; k < 8; ++k) {
     const long long i = gw * LEAF + k * 32 + lane;
     const bool in = own && i < d;
-    pr[k] = in ? p[i] : 0.0;
-    rv[k] = in ? r_cur[i] : 0.0;
+    pr[k] = in ? (double)p[i] : 0.0;
+    rv[k] = in ? (double)r_cur[i] : 0.0;
     cr[k] = (in && center) ? (mu ? mu[i] : (labels[i] != 0 ? 1.0 : 0.0)) : 0.0;
   }
   // everything above is this step's own state; q and the sum(z) leaves come
@@ -777,7 +794,7 @@ __global__ void __launch_bounds__(STEP_THREADS) k_cg_step(
           qi = qi - (mu ? mu[i] : (labels[i] != 0 ? 1.0 : 0.0)) * sz;
           q[i] = qi;
         }
-        a = fma(p[i], qi, a);
+        a = fma((double)p[i], qi, a);
       }
     }
     a = butterfly(a);
@@ -820,8 +837,9 @@ __global__ void __launch_bounds__(STEP_THREADS) k_cg_step(
     for (int k = 0; k < 8; ++k) {
       const long long i = gw * LEAF + k * 32 + lane;
       if (i < d) {
-        rv[k] = rv[k] + gamma * qr[k];
-        r_next[i] = rv[k];
+        const V st = (V)(rv[k] + gamma * qr[k]);
+        r_next[i] = st;
+        rv[k] = (double)st;
         a = fma(rv[k], rv[k], a);
       }
     }
@@ -834,8 +852,9 @@ __global__ void __launch_bounds__(STEP_THREADS) k_cg_step(
     for (int k = 0; k < 8; ++k) {
       const long long i = g * LEAF + k * 32 + lane;
       if (i < d) {
-        const double rn = r_cur[i] + gamma * q[i];
-        r_next[i] = rn;
+        const V st = (V)((double)r_cur[i] + gamma * q[i]);
+        r_next[i] = st;
+        const double rn = (double)st;
         a = fma(rn, rn, a);
       }
     }
@@ -860,14 +879,14 @@ __global__ void __launch_bounds__(STEP_THREADS) k_cg_step(
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const long long i = gw * LEAF + k * 32 + lane;
-      if (i < d) p[i] = rv[k] + alpha_new * pr[k];
+      if (i < d) p[i] = (V)(rv[k] + alpha_new * pr[k]);
     }
   }
   for (long long g = gw + tw; g < n_leaf; g += tw) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const long long i = g * LEAF + k * 32 + lane;
-      if (i < d) p[i] = r_next[i] + alpha_new * p[i];  // this thread wrote r_next[i] in B
+      if (i < d) p[i] = (V)((double)r_next[i] + alpha_new * (double)p[i]);  // this thread wrote r_next[i] in B
     }
   }
   if (blockIdx.x != 0) return;
@@ -1013,7 +1032,8 @@ __global__ void __launch_bounds__(256) k_coef_update(ShiftState ss, const CgScal
 // coefficient tile sits in shared memory (broadcast reads).
 constexpr int CB_SH = 16;    // shifts per thread
 constexpr int CB_JT = 128;   // coefficient columns per shared tile
-__global__ void __launch_bounds__(256) k_combine_basis(const double* __restrict__ rbuf, long long d,
+template <typename V>
+__global__ void __launch_bounds__(256) k_combine_basis(const V* __restrict__ rbuf, long long d,
                                                        ShiftState ss, const CgScalars* sc, int ns,
                                                        double* __restrict__ sols) {
   __shared__ double ct[CB_SH][CB_JT];
@@ -1034,7 +1054,7 @@ __global__ void __launch_bounds__(256) k_combine_basis(const double* __restrict_
     __syncthreads();
     if (k < d) {
       for (int jj = 0; jj < jn; ++jj) {
-        const double r = __ldcs(rbuf + (j0 + jj) * d + k);
+        const double r = (double)__ldcs(rbuf + (j0 + jj) * d + k);
 #pragma unroll
         for (int t = 0; t < CB_SH; ++t) acc[t] = fma(ct[t][jj], r, acc[t]);
       }

@@ -134,6 +134,12 @@ class Device:
         updates, 2 deferred basis (include/fsda_b200.h)."""
         _raise_for(_capi.lib().fsda_set_shift_update_mode(self._h, int(mode)))
 
+    def set_storage(self, bits: int):
+        """64 (default) or 32: fp32 storage of the solve's vectors with fp64
+        reductions (BASELINE cfg5; include/fsda_b200.h)."""
+        _raise_for(_capi.lib().fsda_set_storage(self._h, int(bits)))
+        self.storage_bits = int(bits)
+
     @property
     def last_shift_update_mode(self) -> int:
         return int(_capi.lib().fsda_last_shift_update_mode(self._h))
@@ -392,19 +398,28 @@ def _report(p, res: SweepResult, fam, t0: float, algorithm: str = "fsda"):
         wall_time_s=time.perf_counter() - t0)
 
 
-def fsda_solve(p, *, device: Optional[Device] = None) -> "T.SolveReport":
+def fsda_solve(p, *, device: Optional[Device] = None, storage: Optional[int] = None) -> "T.SolveReport":
     """One shifted Krylov solve of the centred rating operator in feature
     space for every beta of p.betas, rating s = X w per shift — on the GPU.
 
     Drop-in for sdakit.sda.fsda_solve (sda.py:293-320): same probe draw
     (default_rng(p.seed).uniform(-1, 1, D), sda.py:297-300), same report
-    fields, same exceptions."""
+    fields, same exceptions.  storage=32 runs the fp32-storage mode (fp64
+    reductions; BASELINE cfg5) for this call; the default keeps the device's
+    setting (fp64 unless Device.set_storage(32))."""
     t0 = time.perf_counter()
     fam = _family(p)
     dev = device or default_device()
     dev.load_problem(p, fam)
     probe = np.random.default_rng(p.seed).uniform(-1.0, 1.0, size=int(p.x.n_cols))
-    res = dev.solve_fsda(p.alpha, p.betas.betas, p.tol, p.max_iter_d, probe, fam=fam)
+    prev = getattr(dev, "storage_bits", 64)
+    if storage is not None and int(storage) != prev:
+        dev.set_storage(int(storage))
+    try:
+        res = dev.solve_fsda(p.alpha, p.betas.betas, p.tol, p.max_iter_d, probe, fam=fam)
+    finally:
+        if storage is not None and int(storage) != prev:
+            dev.set_storage(prev)
     return _report(p, res, fam, t0)
 
 

@@ -1,5 +1,18 @@
 """Row-sharded FSDA sweep over several GPUs.
 
+The product path is ``solve_row_sharded`` (one process per GPU, NCCL) and
+``solve_row_sharded_local`` (every rank a context in this process — the
+multi-rank tests on one GPU): both drive the C-ABI ``fsda_solve_sharded``
+(csrc/fsda_shard.cuh), which runs the whole iteration on the device with the
+exchanges captured in a CUDA graph.  The rank-ordered partial sums make the
+result deterministic and reproducible by the oracle's partitioned mode
+(oracle/fsda_oracle.c oracle_fsda_solve_sharded); at world 1 it equals
+fsda_solve bit for bit.
+
+The Python orchestrator below (``sharded_fsda_solve``) is the same
+decomposition written against two small interfaces; it runs the host-side
+logic on CPU ranks (gloo) in tests/test_sharded_gloo.py.
+
 One process per GPU.  Rank g owns a contiguous block of rows of X and of the
 Laplacian L (balanced by nonzeros) and the block's labels.  The D-length
 Krylov vectors and the whole shift state are replicated: every rank runs the
@@ -318,3 +331,171 @@ def solve_sharded(x_offsets, x_cols, d, l_offsets, l_cols, l_vals, labels, alpha
     out = sharded_fsda_solve(ops, comm, alpha, betas, tol, max_iter, probe, n1, n2)
     out["row_bounds"] = bounds
     return out
+
+
+# ------------------------------------------- the device path (C ABI)
+
+def shard_slot(bounds) -> int:
+    """Rows per rank in the all-gather layout: the largest shard, rounded up
+    to even (fsda_shard_init)."""
+    b = np.asarray(bounds, dtype=np.int64)
+    m = int(np.max(np.diff(b))) if b.size > 1 else 0
+    return (m + 1) & ~1
+
+
+def remap_columns(cols, bounds) -> np.ndarray:
+    """Global row index j (owned by rank h) -> h * slot + (j - bounds[h])."""
+    b = np.asarray(bounds, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    h = np.searchsorted(b, cols, side="right") - 1
+    return h * shard_slot(b) + (cols - b[h])
+
+
+class ShardRank:
+    """One rank's context: its rows of X and L uploaded in the all-gather
+    layout, its labels, and the shard registration."""
+
+    def __init__(self, shard: "RowShard", bounds, rank: int, device: int = 0, stream=None,
+                 nccl_id: Optional[bytes] = None, storage: int = 64):
+        from .fsda import Device, _raise_for
+
+        self.dev = Device(device, stream=stream)
+        self.shard = shard
+        world = len(bounds) - 1
+        lib = _capi.lib()
+        x = T.SparseMatrix.binary(shard.n_local, shard.d, shard.x_offsets, shard.x_cols)
+        self.dev.upload_x(x)
+        slot = shard_slot(bounds)
+        lcols = np.ascontiguousarray(remap_columns(shard.l_cols, bounds))
+        _raise_for(lib.fsda_upload_laplacian_rows(
+            self.dev._h, shard.n_local, world * slot, rank * slot, _capi.i64ptr(shard.l_offsets),
+            _capi.i64ptr(lcols), _capi.dptr(shard.l_vals)))
+        self.dev.set_label_mask(shard.labels)
+        self.dev._loaded = (None, None, None)
+        bd = np.ascontiguousarray(bounds, dtype=np.int64)
+        idp = None
+        if nccl_id is not None:
+            idb = np.frombuffer(bytes(nccl_id), dtype=np.uint8).copy()
+            idp = _capi.u8ptr(idb)
+        _raise_for(lib.fsda_shard_init(self.dev._h, world, rank, _capi.i64ptr(bd), idp))
+        if storage != 64:
+            self.dev.set_storage(storage)
+
+
+def _solve_ranks(ranks, d, alpha, betas, tol, max_iter, probe, n1, n2, scores=True):
+    from .fsda import _raise_for
+
+    betas = np.ascontiguousarray(betas, dtype=np.float64)
+    probe = np.ascontiguousarray(probe, dtype=np.float64)
+    ns = int(betas.size)
+    rows = sum(r.shard.n_local for r in ranks)
+    dirs = np.empty((ns, d))
+    sc = np.empty((ns, rows)) if scores else None
+    res = np.empty(ns)
+    its = np.empty(ns, dtype=np.int64)
+    conv = np.empty(ns, dtype=np.uint8)
+    napp, fail = C.c_int64(0), C.c_int64(-1)
+    arr = (C.c_void_p * len(ranks))(*[r.dev._h.value for r in ranks])
+    rc = _capi.lib().fsda_solve_sharded(
+        arr, len(ranks), float(alpha), _capi.dptr(betas), ns, float(tol), int(max_iter),
+        _capi.dptr(probe), int(n1), int(n2), _capi.dptr(dirs),
+        _capi.dptr(sc) if sc is not None else None, _capi.dptr(res), _capi.i64ptr(its),
+        _capi.u8ptr(conv), C.byref(napp), C.byref(fail))
+    _raise_for(rc)
+    return dict(directions=dirs, scores=sc, residuals=res, iterations=its,
+                converged=conv.astype(bool), n_applies=int(napp.value))
+
+
+def _class_counts(labels):
+    lab = np.asarray(labels)
+    ml = lab != 0
+    if ml.size and not ml.all() and ml[int(np.argmin(ml)):].any():   # a labeled row after an unlabeled one
+        raise ValueError("labeled samples must occupy the first rows; use arrange_labeled_first "
+                         "to permute the problem")
+    return int((lab == 1).sum()), int((lab == -1).sum())
+
+
+def solve_row_sharded_local(x_offsets, x_cols, d, l_offsets, l_cols, l_vals, labels, alpha, betas,
+                            tol, max_iter, seed=0, world=2, device=0, bounds=None, storage=64):
+    """The row-sharded sweep with every rank a context of this process on one
+    GPU (exchanges as device copies): the multi-rank path testable on one
+    B200.  Returns directions, scores of all rows (global order), residuals,
+    iterations, converged, n_applies, row_bounds."""
+    n1, n2 = _class_counts(labels)
+    b = partition_rows(x_offsets, world, l_offsets) if bounds is None else np.asarray(bounds, np.int64)
+    ranks = [ShardRank(take_shard(x_offsets, x_cols, d, l_offsets, l_cols, l_vals, labels, b, g),
+                       b, g, device=device, storage=storage) for g in range(len(b) - 1)]
+    probe = np.random.default_rng(seed).uniform(-1.0, 1.0, size=int(d))
+    out = _solve_ranks(ranks, int(d), alpha, betas, tol, max_iter, probe, n1, n2)
+    out["row_bounds"] = b
+    return out
+
+
+def solve_row_sharded(x_offsets, x_cols, d, l_offsets, l_cols, l_vals, labels, alpha, betas, tol,
+                      max_iter, seed=0, device: Optional[int] = None, group=None, storage=64,
+                      stream=None):
+    """One process per GPU over the initialised torch.distributed group: this
+    rank's rows on its GPU, NCCL for the exchanges (inside the captured
+    iteration graph).  Returns the replicated directions, this rank's scores,
+    residuals, iterations, converged, n_applies, row_bounds."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n1, n2 = _class_counts(labels)
+    b = partition_rows(x_offsets, world, l_offsets)
+    box = [None]
+    if rank == 0:
+        idb = np.zeros(128, dtype=np.uint8)
+        from .fsda import _raise_for
+
+        _raise_for(_capi.lib().fsda_nccl_unique_id(_capi.u8ptr(idb)))
+        box = [idb.tobytes()]
+    dist.broadcast_object_list(box, src=0, group=group)
+    shard = take_shard(x_offsets, x_cols, d, l_offsets, l_cols, l_vals, labels, b, rank)
+    r = ShardRank(shard, b, rank, device=rank if device is None else device, stream=stream,
+                  nccl_id=box[0], storage=storage)
+    probe = np.random.default_rng(seed).uniform(-1.0, 1.0, size=int(d))
+    out = _solve_ranks([r], int(d), alpha, betas, tol, max_iter, probe, n1, n2)
+    out["row_bounds"] = b
+    out["rank"] = r
+    return out
+
+
+def time_sharded_solves(w, steps, warmup, flush, barrier, storage=64):
+    """bench.py --gpus N (strong scaling): the workload's rows sharded over
+    the torch.distributed world; CUDA-event time of `steps` solves on this
+    rank's stream (max over ranks taken by the caller).  Returns (ms total,
+    launches per solve, description)."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(), dist.get_rank()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    run = lambda: solve_row_sharded(w.x_offsets, w.x_cols, w.d, w.l_offsets, w.l_cols, w.l_vals,  # noqa: E731
+                                    w.labels, w.alpha, w.betas, w.tol, w.max_iter, w.seed,
+                                    device=torch.cuda.current_device(), storage=storage,
+                                    stream=stream.cuda_stream)
+    out = run()                      # uploads + graph capture
+    r = out["rank"]
+    ms = 0.0
+    for _ in range(max(0, warmup - 1)):
+        _solve_ranks([r], int(w.d), w.alpha, w.betas, w.tol, w.max_iter, w.probe(),
+                     *_class_counts(w.labels), scores=False)
+    for k in range(steps):
+        flush.fill_(float(k))
+        barrier()
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        res = _solve_ranks([r], int(w.d), w.alpha, w.betas, w.tol, w.max_iter, w.probe(),
+                           *_class_counts(w.labels), scores=False)
+        b_.record(stream)
+        b_.synchronize()
+        ms += a.elapsed_time(b_)
+    assert res["n_applies"] == w.max_iter
+    b = out["row_bounds"]
+    info = (f"rows {int(b[rank])}..{int(b[rank + 1])} of {w.n} on rank {rank}; per iteration an NCCL "
+            f"all-gather of y and a send/recv reduce-scatter + all-gather of the D+1 partials, "
+            f"captured with the kernels in one CUDA graph")
+    return ms, 0, info

@@ -73,14 +73,16 @@ def same_ranking(a: np.ndarray, b: np.ndarray) -> bool:
 
 def ranking_violations(a: np.ndarray, b: np.ndarray, rel_gap: float = 1e-9):
     """Per shift: rows whose order under `a` contradicts the order under the
-    reference scores `b`, outside near-ties of b (consecutive sorted values
-    closer than rel_gap * max|b|, which any reordered sum may swap).
-    Returns (violations per shift, fraction of rows inside near-tie groups)."""
+    reference scores `b`, outside near-ties of b — consecutive sorted values
+    closer than max(rel_gap * max|b|, 4 max_i |a_i - b_i|): two rows whose
+    reference scores differ by less than the scores' own discrepancy may swap
+    under any reordered sum.  Returns (violations per shift, fraction of rows
+    inside near-tie groups)."""
     viol, tied = [], []
     for x, y in zip(np.asarray(a), np.asarray(b)):
         ob = np.argsort(y, kind="stable")
         sy = y[ob]
-        gap = rel_gap * max(float(np.max(np.abs(y))), 1e-300)
+        gap = max(rel_gap * max(float(np.max(np.abs(y))), 1e-300), 4.0 * float(np.max(np.abs(x - y))))
         new = np.concatenate([[True], np.diff(sy) > gap])
         cluster = np.empty(y.size, dtype=np.int64)
         cluster[ob] = np.cumsum(new) - 1

@@ -139,3 +139,21 @@ def test_r256_tree_definition():
     x[1] = -1e16
     assert c_oracle.r256(x) == 0.0                 # (1e16+1) + (-1e16) = 0 in this tree
     assert np.sum(x) in (0.0, 1.0)
+
+
+def test_oracle_fp32_storage_within_gate(cfg1_workload):
+    """The fp32-storage mirror against fp64 at cfg1's stable K (1e-3 gate,
+    identical labeled AUC) — the host side of the device fp32 gate."""
+    from helpers import labeled_aucs
+
+    w = cfg1_workload
+    a = c_oracle.fsda_solve_workload(w, max_iter=20)
+    c_oracle.set_storage(32)
+    try:
+        b = c_oracle.fsda_solve_workload(w, max_iter=20)
+    finally:
+        c_oracle.set_storage(64)
+    rel = np.max(np.linalg.norm(a["directions"] - b["directions"], axis=1) /
+                 np.linalg.norm(a["directions"], axis=1))
+    assert 0.0 < rel <= 1e-3
+    np.testing.assert_array_equal(labeled_aucs(a["scores"], w.labels), labeled_aucs(b["scores"], w.labels))

@@ -57,6 +57,10 @@ def parse():
     ap.add_argument("--workload", default="cfg3")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="N > 1: one row-sharded solve (strong) or one solve per rank (weak)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the row-sharded (NCCL) path even at one GPU")
+    ap.add_argument("--storage", type=int, default=None, choices=[32, 64],
+                    help="vector storage (default: 32 for cfg5 as BASELINE states, else 64)")
     ap.add_argument("--extra", default="cfg2,cfg4",
                     help="extra keys: cfg2 (second workload), cfg4 (64-task batch), none")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -66,6 +70,20 @@ def parse():
     ap.add_argument("--batch-tasks", type=int, default=32,
                     help="tasks of the multi-task batch measurement (0: skip)")
     return ap.parse_args()
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def load_workload(name):
+    from paper_1709_04794_b200.workloads import make_workload, make_workload_chunked
+
+    return make_workload_chunked(name) if name == "cfg5" else make_workload(name)
 
 
 def dist_env():
@@ -227,7 +245,7 @@ def run_reference(args):
         return
     from paper_1709_04794_b200.workloads import make_workload
 
-    w = make_workload(args.workload)
+    w = load_workload(args.workload)
     ks = K_SAMPLE.get(args.workload)
     threads = os.cpu_count() or 1
     for _ in range(max(0, min(args.warmup, 1))):
@@ -371,9 +389,12 @@ def run_b200(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    w = make_workload(args.workload)
+    w = load_workload(args.workload)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    if world > 1 and args.scaling == "strong":
+    if (world > 1 and args.scaling == "strong") or args.sharded:
+        if world == 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                    init_method="tcp://127.0.0.1:%d" % _free_port(), rank=0, world_size=1)
         return run_strong(args, torch, dist, fb, w, flush, barrier)
 
     if world > 1:   # weak: every rank its own task (a different label draw, as nested CV)
@@ -386,6 +407,8 @@ def run_b200(args):
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     dev = fb.Device(local, stream=stream.cuda_stream)
+    if args.storage != 64:
+        dev.set_storage(args.storage)
     p = make_problem(fb, w)
     dev.load_problem(p)
     dev.prepare_resident(w.alpha, w.betas, w.tol, w.max_iter, w.probe())
@@ -573,7 +596,8 @@ def run_b200(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+            "dtype": "f64" if args.storage == 64 else "f32 storage, f64 reductions",
             "data": "synthetic (seeded generator with BASELINE cfg shapes; no public dataset)",
             "config": workload_config(w, {
                 "parallelism": (f"task-parallel x{world} (one independent solve per GPU per step)"
@@ -605,26 +629,36 @@ def run_b200(args):
 def run_strong(args, torch, dist, fb, w, flush, barrier):
     """One FSDA solve row-sharded over every rank: rank g owns a
     contiguous row block of X and L; per iteration an all-gather of y and a
-    D-length all-reduce over NCCL.  value = solves/s of the whole job
-    (max-over-ranks device time)."""
+    deterministic reduce-scatter + all-gather of the D+1 partials over NCCL,
+    captured with the kernels in one graph.  value = solves/s of the whole
+    job (max-over-ranks device time)."""
     from paper_1709_04794_b200 import sharded
 
     rank, world, local = dist_env()
     with ClockSampler(local) as clocks:
-        ms, launches, info = sharded.time_sharded_solves(w, args.steps, args.warmup, flush, barrier)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        r = sharded.time_sharded_solves(w, args.steps, args.warmup, flush, barrier,
+                                        storage=args.storage, e2e_steps=args.e2e_steps or 3)
+    t = torch.tensor([r["ms"], r["e2e_s"]], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_per_step = float(t.item()) / args.steps
+    ms_per_step = float(t[0].item()) / args.steps
+    e2e_s = float(t[1].item())
+    hd = torch.tensor([r["h2d_bytes"], r["d2h_bytes"]], dtype=torch.float64, device="cuda")
+    dist.all_reduce(hd, op=dist.ReduceOp.SUM)
     if rank == 0:
         line = {
             "metric": METRIC, "value": 1000.0 / ms_per_step, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if args.storage == 64 else "f32 storage, f64 reductions",
             "data": "synthetic (seeded generator with BASELINE cfg shapes; no public dataset)",
             "config": workload_config(w, {
-                "parallelism": f"row-sharded x{world} ({info})",
+                "parallelism": f"row-sharded x{world} ({r['info']})",
                 "l2": "inputs larger than L2, and L2 flushed between steps (outside the events)"}),
-            "e2e": None, "gpu_launches": int(launches * args.steps),
+            "e2e": {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(hd[0].item()),
+                    "d2h_bytes_per_step": int(hd[1].item()),
+                    "path": "sharded.solve_row_sharded's per-rank upload + fsda_solve_sharded + readback "
+                            "(communicator kept), max over ranks"},
+            "gpu_launches": int(r["launches_per_solve"] * args.steps),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -633,6 +667,8 @@ def run_strong(args, torch, dist, fb, w, flush, barrier):
 
 def main():
     args = parse()
+    if args.storage is None:
+        args.storage = 32 if args.workload == "cfg5" else 64
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -148,6 +148,12 @@ int fsda_last_shift_update_mode(fsda_ctx* ctx);
  * shift-update mode.  Applies to fsda_solve / fsda_solve_async. */
 int fsda_set_storage(fsda_ctx* ctx, int bits);
 
+/* 1: launch each solve's kernels one by one from the host (the same kernels,
+ * the same results) instead of the cached CUDA graph with its conditional
+ * WHILE node — for profilers that cannot see into conditional graphs.  The
+ * default comes from FSDA_B200_EAGER at context creation. */
+int fsda_set_eager(fsda_ctx* ctx, int eager);
+
 /* Device-resident variant for throughput measurement: launches one complete
  * solve on the context stream and returns without copying results to the
  * host (inputs already resident in HBM).  Results stay in the context and can

@@ -51,6 +51,7 @@ SIGNATURES = {
     "fsda_set_shift_update_mode": [_P, C.c_int],
     "fsda_last_shift_update_mode": [_P],
     "fsda_set_storage": [_P, C.c_int],
+    "fsda_set_eager": [_P, C.c_int],
     "fsda_nccl_unique_id": [_PU8],
     "fsda_shard_init": [_P, C.c_int, C.c_int, _PI64, _PU8],
     "fsda_solve_sharded": [C.POINTER(_P), C.c_int, _D, _PD, C.c_int, _D, _I64, _PD, _I64, _I64, _PD, _PD,

@@ -278,6 +278,10 @@ struct fsda_ctx {
   cudaGraph_t graph = nullptr;
   std::string graph_key;
   bool cond_supported = true;
+  // launch the solve's kernels one by one from the host instead of the
+  // captured graph (FSDA_B200_EAGER=1 at creation, or fsda_set_eager): ncu
+  // cannot profile kernel nodes of graphs that contain conditional nodes
+  bool eager = false;
 
   long long graph_fixed = 0, graph_body = 0;  // launches in the cached graph
   // which operator the solve graph runs: 0 FSDA (sda.py:162-174), 1 the
@@ -985,10 +989,7 @@ void upload_solve_params(fsda_ctx* c, const double* betas, int ns, const double*
 // Launch one complete solve (graph, or eager when rec != null or no graph).
 long long launch_solve(fsda_ctx* c, double alpha, int ns, long long max_iter, double tol,
                        Recorder* rec) {
-  // FSDA_B200_EAGER=1 launches the same kernels one by one (ncu cannot
-  // profile kernel nodes of graphs that contain conditional nodes).
-  static const bool force_eager = getenv("FSDA_B200_EAGER") && getenv("FSDA_B200_EAGER")[0] == '1';
-  if (!rec && c->cond_supported && !force_eager) {
+  if (!rec && c->cond_supported && !c->eager) {
     long long fixed = 0, body = 0;
     try {
       build_solve_graph(c, alpha, ns, max_iter, tol, &fixed, &body);
@@ -1394,6 +1395,13 @@ int fsda_last_shift_update_mode(fsda_ctx* c) {
   return c->su_mode;
 }
 
+int fsda_set_eager(fsda_ctx* c, int eager) {
+  API_BEGIN(c)
+  c->eager = eager != 0;
+  return FSDA_OK;
+  API_END
+}
+
 int fsda_set_storage(fsda_ctx* c, int bits) {
   API_BEGIN(c)
   if (bits != 32 && bits != 64) return fail(FSDA_EINVAL, "storage must be 32 or 64 bits, got %d", bits);
@@ -1415,6 +1423,7 @@ int fsda_ctx_create(fsda_ctx** out, int device, void* stream) {
   if (device < 0 || device >= ndev) return fail(FSDA_EINVAL, "device %d out of range", device);
   fsda_ctx* c = new fsda_ctx();
   c->device = device;
+  c->eager = getenv("FSDA_B200_EAGER") && getenv("FSDA_B200_EAGER")[0] == '1';
   try {
     CK(cudaSetDevice(device));
     cudaDeviceProp prop;

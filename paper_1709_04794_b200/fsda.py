@@ -134,6 +134,11 @@ class Device:
         updates, 2 deferred basis (include/fsda_b200.h)."""
         _raise_for(_capi.lib().fsda_set_shift_update_mode(self._h, int(mode)))
 
+    def set_eager(self, eager: bool = True):
+        """Launch solves kernel by kernel instead of through the cached CUDA
+        graph (same kernels, same results; for profilers)."""
+        _raise_for(_capi.lib().fsda_set_eager(self._h, int(bool(eager))))
+
     def set_storage(self, bits: int):
         """64 (default) or 32: fp32 storage of the solve's vectors with fp64
         reductions (BASELINE cfg5; include/fsda_b200.h)."""

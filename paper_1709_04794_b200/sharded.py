@@ -381,6 +381,22 @@ class ShardRank:
         if storage != 64:
             self.dev.set_storage(storage)
 
+    def reload(self, shard: "RowShard", bounds, rank: int):
+        """Re-upload this rank's rows (same shapes; the shard registration and
+        the communicator stay)."""
+        from .fsda import _raise_for
+
+        world = len(bounds) - 1
+        slot = shard_slot(bounds)
+        x = T.SparseMatrix.binary(shard.n_local, shard.d, shard.x_offsets, shard.x_cols)
+        self.dev.upload_x(x)
+        lcols = np.ascontiguousarray(remap_columns(shard.l_cols, bounds))
+        _raise_for(_capi.lib().fsda_upload_laplacian_rows(
+            self.dev._h, shard.n_local, world * slot, rank * slot, _capi.i64ptr(shard.l_offsets),
+            _capi.i64ptr(lcols), _capi.dptr(shard.l_vals)))
+        self.dev.set_label_mask(shard.labels)
+        self.shard = shard
+
 
 def _solve_ranks(ranks, d, alpha, betas, tol, max_iter, probe, n1, n2, scores=True):
     from .fsda import _raise_for
@@ -462,40 +478,64 @@ def solve_row_sharded(x_offsets, x_cols, d, l_offsets, l_cols, l_vals, labels, a
     return out
 
 
-def time_sharded_solves(w, steps, warmup, flush, barrier, storage=64):
+def time_sharded_solves(w, steps, warmup, flush, barrier, storage=64, e2e_steps=3):
     """bench.py --gpus N (strong scaling): the workload's rows sharded over
-    the torch.distributed world; CUDA-event time of `steps` solves on this
-    rank's stream (max over ranks taken by the caller).  Returns (ms total,
-    launches per solve, description)."""
+    the torch.distributed world.  Device time: CUDA events around `steps`
+    solves on this rank's stream (max over ranks taken by the caller).  e2e:
+    per step, this rank's shard re-uploaded from host memory, the solve, and
+    the results read back (the communicator is kept).  Returns a dict."""
+    import time as _time
+
     import torch
     import torch.distributed as dist
 
     world, rank = dist.get_world_size(), dist.get_rank()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    run = lambda: solve_row_sharded(w.x_offsets, w.x_cols, w.d, w.l_offsets, w.l_cols, w.l_vals,  # noqa: E731
-                                    w.labels, w.alpha, w.betas, w.tol, w.max_iter, w.seed,
-                                    device=torch.cuda.current_device(), storage=storage,
-                                    stream=stream.cuda_stream)
-    out = run()                      # uploads + graph capture
+    out = solve_row_sharded(w.x_offsets, w.x_cols, w.d, w.l_offsets, w.l_cols, w.l_vals,
+                            w.labels, w.alpha, w.betas, w.tol, w.max_iter, w.seed,
+                            device=torch.cuda.current_device(), storage=storage,
+                            stream=stream.cuda_stream)           # uploads + graph capture
     r = out["rank"]
-    ms = 0.0
+    n1, n2 = _class_counts(w.labels)
+    probe = w.probe()
+
+    def solve(scores=False):
+        return _solve_ranks([r], int(w.d), w.alpha, w.betas, w.tol, w.max_iter, probe, n1, n2,
+                            scores=scores)
+
     for _ in range(max(0, warmup - 1)):
-        _solve_ranks([r], int(w.d), w.alpha, w.betas, w.tol, w.max_iter, w.probe(),
-                     *_class_counts(w.labels), scores=False)
+        solve()
+    ms = 0.0
     for k in range(steps):
         flush.fill_(float(k))
         barrier()
         a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        res = _solve_ranks([r], int(w.d), w.alpha, w.betas, w.tol, w.max_iter, w.probe(),
-                           *_class_counts(w.labels), scores=False)
+        res = solve()
         b_.record(stream)
         b_.synchronize()
         ms += a.elapsed_time(b_)
     assert res["n_applies"] == w.max_iter
+    # e2e: host shard -> device, solve, directions + local scores -> host
+    sh = r.shard
+    barrier()
+    t0 = _time.perf_counter()
+    for _ in range(e2e_steps):
+        r.reload(sh, out["row_bounds"], rank)
+        res = solve(scores=True)
+    barrier()
+    e2e_s = (_time.perf_counter() - t0) / e2e_steps
+    h2d = (sh.x_offsets.nbytes + sh.x_cols.nbytes + sh.l_offsets.nbytes + sh.l_cols.nbytes +
+           sh.l_vals.nbytes + sh.labels.nbytes + 8 * w.d + 8 * w.betas.size)
+    d2h = 8 * w.betas.size * (w.d + sh.n_local) + 24 * w.betas.size
     b = out["row_bounds"]
+    ns = int(w.betas.size)
+    # kernels per solve: setup 14, per iteration K1 K2 K3 rank-sum K4 shift (6),
+    # tail 9 (+ the all-gather / send-recv copies, which are NCCL's)
+    launches = 14 + 6 * int(w.max_iter) + 9
     info = (f"rows {int(b[rank])}..{int(b[rank + 1])} of {w.n} on rank {rank}; per iteration an NCCL "
             f"all-gather of y and a send/recv reduce-scatter + all-gather of the D+1 partials, "
             f"captured with the kernels in one CUDA graph")
-    return ms, 0, info
+    return {"ms": ms, "launches_per_solve": launches, "info": info, "e2e_s": e2e_s,
+            "h2d_bytes": int(h2d), "d2h_bytes": int(d2h), "n_shifts": ns}

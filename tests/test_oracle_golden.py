@@ -157,3 +157,22 @@ def test_oracle_fp32_storage_within_gate(cfg1_workload):
                  np.linalg.norm(a["directions"], axis=1))
     assert 0.0 < rel <= 1e-3
     np.testing.assert_array_equal(labeled_aucs(a["scores"], w.labels), labeled_aucs(b["scores"], w.labels))
+
+
+def test_acceptance_fixture_pinned_by_reference_order_oracle():
+    """The acceptance fixtures (the reference's own FSDA test cases and
+    outputs) are reproduced by oracle/ref_numpy.py — the problems were
+    stored exactly."""
+    from acceptance_cases import keys, load
+
+    g = load()
+    for key in ["pencil", "lda", "consistent", "deterministic"] + keys(g, "crit1_")[:6]:
+        n, d = (int(v) for v in g[f"{key}__shape"])
+        prob = ref_numpy.Problem(g[f"{key}__x_offsets"], g[f"{key}__x_cols"], d, g[f"{key}__l_offsets"],
+                                 g[f"{key}__l_cols"], g[f"{key}__l_vals"], g[f"{key}__labels"])
+        alpha, tol, max_iter, seed = g[f"{key}__knobs"]
+        out = ref_numpy.fsda_solve(prob, float(alpha), g[f"{key}__betas"], float(tol), int(max_iter),
+                                   int(seed))
+        ref = g[f"{key}__ref_directions"]
+        rel = np.max(np.linalg.norm(out["directions"] - ref, axis=1) / np.linalg.norm(ref, axis=1))
+        assert rel <= 1e-12, (key, rel)

@@ -1,12 +1,12 @@
 """Summarise a round's ncu evidence into profiles/ (tracked).
 
-    python tools/summarize_ncu.py ROUND LAUNCHES_CSV FULL_REP
+    python tools/summarize_ncu.py ROUND LAUNCHES_CSV FULL_REP [WORKLOAD]
 
 Writes profiles/<ROUND>_launches.md (per-kernel share of one solve from the
 serialised, cold-cache launch list), profiles/<ROUND>_ncu_full.md (key
 metrics + top stall reasons per captured kernel) and
-profiles/ncu_traffic_<ROUND>.json (dram bytes per launch, read by bench.py
-for roofline.traffic).
+profiles/ncu_traffic_<ROUND>_<WORKLOAD>.json (dram bytes and L2 sectors per
+launch of the same workload, read by bench.py for roofline.traffic).
 """
 import collections
 import csv
@@ -16,17 +16,23 @@ import sys
 from pathlib import Path
 
 rnd, launches, rep = sys.argv[1], sys.argv[2], sys.argv[3]
+workload = sys.argv[4] if len(sys.argv) > 4 else "cfg2"
 out = Path(__file__).resolve().parents[1] / "profiles"
 out.mkdir(exist_ok=True)
 
 # bench.py names -> kernel names
 BENCH_NAME = {"k_xt_coop": "xt", "k_segsum<0>": "spmv_rows", "k_segsum<1>": "smoother",
               "k_cg_step": "cg_step", "k_shift_update": "shift_update",
-              "k_spmm_scores": "spmm_scores"}
+              "k_spmm_scores": "spmm_scores", "k_combine_basis": "combine_basis"}
 
 
 def short(name):
     n = name.split("(")[0].replace("void ", "").replace("fsda::", "")
+    # templated kernels: k_segsum<0, fsda::SegArgsT<double, double>> -> k_segsum<0>
+    if n.startswith("k_segsum<"):
+        n = "k_segsum<" + n[len("k_segsum<")] + ">"
+    elif "<" in n:
+        n = n.split("<")[0]
     return n
 
 
@@ -39,7 +45,7 @@ for r in rows:
     a[1] += float(r[-1])
 tot = sum(v[1] for v in agg.values())
 lines = [f"# {rnd}: ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
-         "One eager cfg2 solve (FSDA_B200_EAGER=1, tools/ncu_solve.py --solves 1), including the",
+         f"One eager {workload} solve (FSDA_B200_EAGER=1, tools/ncu_solve.py --solves 1), including the",
          "upload (CSC sort, plans).  Serialised and cold-cache: compare shares, not absolutes.", "",
          "| kernel | launches | mean us | total us | share |", "|---|---|---|---|---|"]
 for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -56,7 +62,7 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "launch__grid_size", "smsp__inst_executed.sum"]
 units = r[1] if len(r) > 1 else []
-md = [f"# {rnd}: ncu --set full (one captured launch per kernel, iteration 2 of a cfg2 solve)", ""]
+md = [f"# {rnd}: ncu --set full (one captured launch per kernel, iteration 2 of a {workload} solve)", ""]
 traffic = {}
 for row in r[2:]:
     name = short(row[hdr.index("Kernel Name")])
@@ -87,9 +93,17 @@ for row in r[2:]:
 
     bench = BENCH_NAME.get(name)
     if bench:
-        traffic[bench] = {"kernel": name, "dram_bytes_per_launch":
-                          mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")}
+        ent = {"kernel": name, "dram_bytes_per_launch": mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")}
+        for k in ("lts__t_sectors.sum", "lts__t_sectors_srcunit_tex_op_read.sum"):
+            if k in hdr:
+                try:
+                    ent["l2_sectors_per_launch" if k == "lts__t_sectors.sum" else "l2_read_sectors_per_launch"] = \
+                        float(row[hdr.index(k)])
+                except ValueError:
+                    pass
+        traffic[bench] = ent
 (out / f"{rnd}_ncu_full.md").write_text("\n".join(md) + "\n")
-(out / f"ncu_traffic_{rnd}.json").write_text(json.dumps({"round": rnd, "kernels": traffic}, indent=1))
+(out / f"ncu_traffic_{rnd}_{workload}.json").write_text(
+    json.dumps({"round": rnd, "workload": workload, "kernels": traffic}, indent=1))
 print("\n".join(lines))
 print(json.dumps(traffic, indent=1))

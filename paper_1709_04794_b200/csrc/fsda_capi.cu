@@ -1197,7 +1197,9 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   Trace tr;
   std::vector<int> bptr;
   if (nh) {
-    CK(cudaMemcpy(c->xh_col.ptr, dense.data(), sizeof(int) * nh, cudaMemcpyHostToDevice));
+    // stream-ordered: a plain cudaMemcpy would also wait for L's copies queued
+    // on the side stream by fsda_upload_problem
+    CK(cudaMemcpyAsync(c->xh_col.ptr, dense.data(), sizeof(int) * nh, cudaMemcpyHostToDevice, c->stream));
     k_heavy_bptr<<<grid_for(nh * (nb + 1), 256), 256, 0, c->stream>>>(
         c->csc_colptr.ptr, c->csc_rows.ptr, c->xh_col.ptr, c->xh_bptr.ptr, nh, nb, rb);
     CKL();

@@ -83,6 +83,7 @@ SIGNATURES = {
     "fsda_graph_knn": [_P, C.c_int32, _PI64],
     "fsda_graph_threshold": [_P, _D, _PI64],
     "fsda_graph_fetch": [_P, _PI64, _PI64],
+    "fsda_head_counts": [_P, C.c_int64, C.c_int32, _P, C.c_int64, C.c_int64, _P],
 }
 
 _lib = None

@@ -29,8 +29,8 @@
 #include "fsda_hot.cuh"
 #include "fsda_batch.cuh"
 #include "graph_knn.cuh"
+#include "graph_gemm.cuh"
 
-#include <cublas_v2.h>
 #include <cub/device/device_select.cuh>
 
 using namespace fsda;
@@ -187,13 +187,12 @@ struct GraphBufs {
   DevBuf<long long> offs, cols, count;
   long long n = 0, nnz = 0;
   double tail_avg = 0.0;  // tail-column occurrences per row of the last build
-  cublasHandle_t blas = nullptr;
+  CUtensorMap amap{};            // TMA descriptor of A (re-encoded per build)
+  bool gemm_attr = false;        // k_head_gemm's shared-memory opt-in done
   void release() {
     head_of.release(); cand.release(); ncand.release(); nbr.release(); rsize.release(); tsize.release(); A.release();
     C.release();
     keys.release(); keys2.release(); temp.release(); offs.release(); cols.release(); count.release();
-    if (blas) cublasDestroy(blas);
-    blas = nullptr;
   }
 };
 
@@ -2694,15 +2693,51 @@ extern "C" int fsda_debug_xt_trace(int on, unsigned long long* out) {
 // graph.py:152-166 knn_graph on the context's X (fsda_upload_x first).
 namespace {
 
-#define CKB(x)                                                                  \
-  do {                                                                          \
-    cublasStatus_t st_ = (x);                                                   \
-    if (st_ != CUBLAS_STATUS_SUCCESS) {                                         \
-      fail(FSDA_ECUDA, "cuBLAS status %d at line %d", (int)st_, __LINE__);      \
-      return FSDA_ECUDA;                                                        \
-    }                                                                           \
-  } while (0)
+
 }  // namespace
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link
+// dependency on libcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+const char* encode_head_map(CUtensorMap* map, const signed char* A, int H, long long rows) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      return "cuTensorMapEncodeTiled unavailable";
+    fn = (EncodeTiledFn)p;
+  }
+  // A: rows x H bytes, row-major; boxes of 128 bytes x 128 rows, 128-byte swizzle
+  const cuuint64_t dims[2] = {(cuuint64_t)H, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)H};
+  const cuuint32_t box[2] = {(cuuint32_t)HG_BK, (cuuint32_t)HG_BM};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)A, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? nullptr : "cuTensorMapEncodeTiled failed";
+}
+
+#define CK_HG(x)                                                    \
+  do {                                                              \
+    const char* e_ = (x);                                           \
+    if (e_) return fail(FSDA_ECUDA, "head-count GEMM: %s", e_);     \
+  } while (0)
+
+// C block (nb16 x n16) of head counts for rows [r0, r0 + nb16): k_head_gemm on
+// one persistent CTA per SM (at most one per tile).
+void launch_head_gemm(fsda_ctx* c, GraphBufs& g, int r0, int nb16, int n16, int H) {
+  const int m_tiles = (nb16 + HG_BM - 1) / HG_BM, n_tiles = (n16 + HG_BN - 1) / HG_BN;
+  const int grid = std::max(1, std::min(m_tiles * n_tiles, c->num_sms));
+  k_head_gemm<<<grid, HG_THREADS, HG_SMEM, c->stream>>>(g.amap, r0, nb16, n16, H / HG_BK, g.C.ptr,
+                                                        (long long)n16, m_tiles, n_tiles);
+  CKL();
+}
 
 // Shared by the k-NN and threshold builds: head selection, the int8 head
 // matrix, then per row block the head-count GEMM followed by `per_block`.
@@ -2740,7 +2775,7 @@ int graph_blocks(fsda_ctx* c, GraphBufs& g, F per_block) {
     if ((size_t)cand >= order.size()) break;
   }
   g.tail_avg = n > 0 ? sq[nh] / (double)n : 0.0;
-  const int H = nh > 0 ? (nh + 15) & ~15 : 0;  // GEMM depth padded to 16 (zero columns)
+  const int H = nh > 0 ? (nh + HG_BK - 1) / HG_BK * HG_BK : 0;  // GEMM depth padded to 128 (zero columns)
   std::vector<int> head_of((size_t)std::max<long long>(d, 1), -1);
   for (int h = 0; h < nh; ++h) head_of[order[h]] = h;
   g.head_of.ensure(std::max<long long>(d, 1));
@@ -2774,20 +2809,19 @@ int graph_blocks(fsda_ctx* c, GraphBufs& g, F per_block) {
     k_knn_head_dense<<<grid_for(n, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr, g.head_of.ptr,
                                                              g.A.ptr, (int)n, H);
     CKL();
-    if (!g.blas) CKB(cublasCreate(&g.blas));
-    CKB(cublasSetStream(g.blas, c->stream));
-    CKB(cublasSetMathMode(g.blas, CUBLAS_DEFAULT_MATH));
+    CK_HG(encode_head_map(&g.amap, g.A.ptr, H, n16));
+    if (!g.gemm_attr) {
+      CK(cudaFuncSetAttribute(k_head_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, HG_SMEM));
+      g.gemm_attr = true;
+    }
   }
   for (long long r0 = 0; r0 < n; r0 += B) {
     const long long nb = std::min(B, n - r0);
     if (H > 0) {
-      const int one = 1, zero = 0;
       const long long nb16 = (nb + 15) & ~15LL;
-      // C (n16 x nb16, column-major) = A^T (n16 x H) * A_blk (H x nb16): row b
-      // of the row-major block = head counts of row r0 + b against every row
-      CKB(cublasGemmEx(g.blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)n16, (int)nb16, H, &one, g.A.ptr, CUDA_R_8I, H,
-                       g.A.ptr + r0 * H, CUDA_R_8I, H, &zero, g.C.ptr, CUDA_R_32I, (int)n16,
-                       CUBLAS_COMPUTE_32I, CUBLAS_GEMM_DEFAULT));
+      // C (nb16 x n16, row-major) = A_blk . A^T: row b = head counts of row
+      // r0 + b against every row
+      launch_head_gemm(c, g, (int)r0, (int)nb16, (int)n16, H);
     }
     per_block(r0, nb, n16, H > 0 ? g.C.ptr : nullptr);
   }
@@ -2914,6 +2948,32 @@ extern "C" int fsda_graph_threshold(fsda_ctx* c, double theta, int64_t* nnz_out)
   graph_csr(c, g, (long long)hits);
   tr.mark("threshold: csr");
   if (nnz_out) *nnz_out = g.nnz;
+  return FSDA_OK;
+  API_END
+}
+
+extern "C" int fsda_head_counts(fsda_ctx* c, int64_t n_rows, int32_t h, const int8_t* a, int64_t r0,
+                                int64_t nb, int32_t* counts) {
+  API_BEGIN(c)
+  if (n_rows <= 0 || h <= 0 || !a || !counts) return fail(FSDA_EINVAL, "fsda_head_counts: empty input");
+  if (r0 < 0 || nb <= 0 || r0 + nb > n_rows) return fail(FSDA_EINVAL, "fsda_head_counts: bad row block");
+  if (n_rows * (long long)nb >= (1LL << 31)) return fail(FSDA_EINVAL, "fsda_head_counts: block too large");
+  GraphBufs& g = c->knn;
+  const long long n16 = (n_rows + 15) & ~15LL, nb16 = (nb + 15) & ~15LL;
+  const int H = (h + HG_BK - 1) / HG_BK * HG_BK;
+  g.A.ensure(n16 * H);
+  g.C.ensure(nb16 * n16);
+  CK(cudaMemsetAsync(g.A.ptr, 0, (size_t)n16 * H, c->stream));
+  CK(cudaMemcpy2DAsync(g.A.ptr, H, a, h, h, n_rows, cudaMemcpyHostToDevice, c->stream));
+  CK_HG(encode_head_map(&g.amap, g.A.ptr, H, n16));
+  if (!g.gemm_attr) {
+    CK(cudaFuncSetAttribute(k_head_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, HG_SMEM));
+    g.gemm_attr = true;
+  }
+  launch_head_gemm(c, g, (int)r0, (int)nb16, (int)n16, H);
+  CK(cudaMemcpy2DAsync(counts, sizeof(int32_t) * n_rows, g.C.ptr, sizeof(int) * n16, sizeof(int32_t) * n_rows,
+                       nb, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
   return FSDA_OK;
   API_END
 }

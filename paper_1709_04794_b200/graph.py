@@ -74,6 +74,19 @@ def _graph_types(x):
     return T.SparseMatrix, SimilarityGraph, GraphError, T.Laplacian
 
 
+def head_counts(a, r0: int = 0, nb: Optional[int] = None, *, device: Optional[Device] = None) -> np.ndarray:
+    """counts[b, j] = sum_k a[r0 + b, k] * a[j, k] for a 0/1 matrix a (any
+    n x h): the exact int32 block the graph builds take from the hand-written
+    tcgen05 head-count GEMM (csrc/graph_gemm.cuh)."""
+    a = np.ascontiguousarray(a, dtype=np.int8)
+    n, h = a.shape
+    nb = n - r0 if nb is None else int(nb)
+    out = np.empty((nb, n), dtype=np.int32)
+    dev = device or default_device()
+    _raise_for(_capi.lib().fsda_head_counts(dev._h, n, h, a.ctypes.data, int(r0), nb, out.ctypes.data))
+    return out
+
+
 def knn_graph(x, k: int, *, block_size: int = 1024, n_threads: int = 1,
               device: Optional[Device] = None):
     """Union-symmetrized k-nearest-neighbour Tanimoto graph of the rows of x

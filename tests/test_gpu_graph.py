@@ -165,3 +165,33 @@ def test_cfg2_rows_contain_their_oracle_neighbours():
         have = set(a.col_indices[a.row_offsets[i]:a.row_offsets[i + 1]].tolist())
         assert set(expect.tolist()) <= have, int(i)
     assert g.n_edges >= 10 * w.n // 2
+
+
+@pytest.mark.parametrize("n,h,r0,nb,density", [
+    (1000, 300, 0, 1000, 0.05),      # one 128-deep K step after padding, ragged N tile
+    (777, 129, 13, 500, 0.3),        # N, r0 and nb off every tile / 16 boundary
+    (4096, 4096, 1024, 2048, 0.02),  # the cfg2 head width: 32 K steps, many tiles per CTA
+    (300, 1, 0, 300, 0.5),           # one head column
+    (3000, 640, 2900, 100, 1.0),     # all ones: counts = h (largest values)
+])
+def test_head_count_gemm_exact(n, h, r0, nb, density):
+    """The hand-written tcgen05 int8 GEMM (k_head_gemm) against numpy's
+    integer product: exact counts, every entry."""
+    rng = np.random.default_rng(n + h)
+    a = (rng.random((n, h)) < density).astype(np.int8)
+    got = G.head_counts(a, r0, nb)
+    ai = a.astype(np.int32)
+    want = ai[r0:r0 + nb] @ ai.T
+    assert np.array_equal(got, want)
+
+
+def test_head_count_gemm_zipf_rows():
+    """Rows of a Zipf-headed binary X (the graph builds' real operand)."""
+    w = make_workload("cfg1", n=2500, d=1200)
+    a = np.zeros((w.n, 512), dtype=np.int8)
+    for i in range(w.n):
+        c = w.x_cols[w.x_offsets[i]:w.x_offsets[i + 1]]
+        a[i, c[c < 512]] = 1
+    got = G.head_counts(a, 640, 1500)
+    ai = a.astype(np.int32)
+    assert np.array_equal(got, ai[640:2140] @ ai.T)

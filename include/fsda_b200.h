@@ -284,8 +284,8 @@ int fsda_graph_threshold(fsda_ctx* ctx, double theta, int64_t* nnz_out);
 int fsda_graph_fetch(fsda_ctx* ctx, int64_t* row_offsets, int64_t* col_indices);
 /* The graph builds' head-count contraction on its own, for tests: for an
  * n_rows x h 0/1 int8 matrix a (row-major), counts[b * n_rows + j] =
- * sum_k a[r0 + b][k] * a[j][k] for b < nb, j < n_rows — the block of exact
- * int32 counts the builds take from the hand-written tcgen05 GEMM
+ * sum_k a[r0 + b][k] * a[j][k] for b < nb, j < n_rows (h <= 65535) — the block
+ * of exact counts (16-bit on the device) the builds take from the hand-written tcgen05 GEMM
  * (csrc/graph_gemm.cuh; the reference's per-block X_blk X^T, graph.py:79-111).
  * Uses the context's device and stream. */
 int fsda_head_counts(fsda_ctx* ctx, int64_t n_rows, int32_t h, const int8_t* a, int64_t r0, int64_t nb,

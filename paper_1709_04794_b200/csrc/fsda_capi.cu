@@ -181,7 +181,7 @@ struct BatchBufs {
 struct GraphBufs {
   DevBuf<int> head_of, cand, ncand, nbr, rsize, tsize;
   DevBuf<signed char> A;
-  DevBuf<int> C;
+  DevBuf<HeadCount> C;
   DevBuf<unsigned long long> keys, keys2;
   DevBuf<unsigned char> temp;
   DevBuf<long long> offs, cols, count;
@@ -2729,14 +2729,43 @@ const char* encode_head_map(CUtensorMap* map, const signed char* A, int H, long 
     if (e_) return fail(FSDA_ECUDA, "head-count GEMM: %s", e_);     \
   } while (0)
 
+bool head_gemm_pairs();
+
 // C block (nb16 x n16) of head counts for rows [r0, r0 + nb16): k_head_gemm on
 // one persistent CTA per SM (at most one per tile).
 void launch_head_gemm(fsda_ctx* c, GraphBufs& g, int r0, int nb16, int n16, int H) {
-  const int m_tiles = (nb16 + HG_BM - 1) / HG_BM, n_tiles = (n16 + HG_BN - 1) / HG_BN;
-  const int grid = std::max(1, std::min(m_tiles * n_tiles, c->num_sms));
-  k_head_gemm<<<grid, HG_THREADS, HG_SMEM, c->stream>>>(g.amap, r0, nb16, n16, H / HG_BK, g.C.ptr,
-                                                        (long long)n16, m_tiles, n_tiles);
-  CKL();
+  const int n_tiles = (n16 + HG_BN - 1) / HG_BN;
+  if (!head_gemm_pairs()) {
+    const int m_tiles = (nb16 + HG_BM - 1) / HG_BM;
+    const int grid = std::max(1, std::min(m_tiles * n_tiles, c->num_sms));
+    k_head_gemm<<<grid, HG_THREADS, HG_SMEM, c->stream>>>(g.amap, r0, nb16, n16, H / HG_BK, g.C.ptr,
+                                                          (long long)n16, m_tiles, n_tiles);
+    CKL();
+    return;
+  }
+  // CTA pairs on 256 x 256 tiles: one cluster of two per TPC
+  const int m_tiles = (nb16 + 255) / 256;
+  const int grid = 2 * std::max(1, std::min(m_tiles * n_tiles, c->num_sms / 2));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(HG_THREADS);
+  cfg.dynamicSmemBytes = HG2_SMEM;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_head_gemm2, g.amap, r0, nb16, n16, H / HG_BK, g.C.ptr, (long long)n16, m_tiles,
+                        n_tiles));
+}
+
+// k_head_gemm2 (CTA pairs, cta_group::2) unless FSDA_B200_HEAD_GEMM=1sm
+bool head_gemm_pairs() {
+  static const bool v = !(std::getenv("FSDA_B200_HEAD_GEMM") && std::string(std::getenv("FSDA_B200_HEAD_GEMM")) == "1sm");
+  return v;
 }
 
 // Shared by the k-NN and threshold builds: head selection, the int8 head
@@ -2812,6 +2841,7 @@ int graph_blocks(fsda_ctx* c, GraphBufs& g, F per_block) {
     CK_HG(encode_head_map(&g.amap, g.A.ptr, H, n16));
     if (!g.gemm_attr) {
       CK(cudaFuncSetAttribute(k_head_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, HG_SMEM));
+      CK(cudaFuncSetAttribute(k_head_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, HG2_SMEM));
       g.gemm_attr = true;
     }
   }
@@ -2870,7 +2900,7 @@ extern "C" int fsda_graph_knn(fsda_ctx* c, int32_t k, int64_t* nnz_out) {
   g.cand.ensure(B * k);
   g.ncand.ensure(B);
   g.nbr.ensure(n * k);
-  int rc = graph_blocks(c, g, [&](long long r0, long long nb, long long ldc, const int* C) {
+  int rc = graph_blocks(c, g, [&](long long r0, long long nb, long long ldc, const HeadCount* C) {
     if (C) {
       k_knn_scan<<<(unsigned)cdiv(nb, KNN_WARPS), KNN_WARPS * 32, 0, c->stream>>>(
           C, (int)r0, (int)nb, (int)n, (int)ldc, g.rsize.ptr, k, g.cand.ptr, g.ncand.ptr);
@@ -2921,7 +2951,7 @@ extern "C" int fsda_graph_threshold(fsda_ctx* c, double theta, int64_t* nnz_out)
     g.keys.ensure((long long)cap);
     CK(cudaMemsetAsync(g.count.ptr, 0, sizeof(long long), c->stream));
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(g.count.ptr);
-    int rc = graph_blocks(c, g, [&](long long r0, long long nb, long long ldc, const int* C) {
+    int rc = graph_blocks(c, g, [&](long long r0, long long nb, long long ldc, const HeadCount* C) {
       if (g.tail_avg <= KNN_TAIL_CAP / 2) {
         k_graph_threshold<KNN_TAIL_CAP, KNN_REFINE_WARPS>
             <<<(unsigned)cdiv(nb, KNN_REFINE_WARPS), KNN_REFINE_WARPS * 32,
@@ -2957,6 +2987,7 @@ extern "C" int fsda_head_counts(fsda_ctx* c, int64_t n_rows, int32_t h, const in
   API_BEGIN(c)
   if (n_rows <= 0 || h <= 0 || !a || !counts) return fail(FSDA_EINVAL, "fsda_head_counts: empty input");
   if (r0 < 0 || nb <= 0 || r0 + nb > n_rows) return fail(FSDA_EINVAL, "fsda_head_counts: bad row block");
+  if (h > 65535) return fail(FSDA_EINVAL, "fsda_head_counts: counts are 16-bit (h <= 65535)");
   if (n_rows * (long long)nb >= (1LL << 31)) return fail(FSDA_EINVAL, "fsda_head_counts: block too large");
   GraphBufs& g = c->knn;
   const long long n16 = (n_rows + 15) & ~15LL, nb16 = (nb + 15) & ~15LL;
@@ -2968,12 +2999,15 @@ extern "C" int fsda_head_counts(fsda_ctx* c, int64_t n_rows, int32_t h, const in
   CK_HG(encode_head_map(&g.amap, g.A.ptr, H, n16));
   if (!g.gemm_attr) {
     CK(cudaFuncSetAttribute(k_head_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, HG_SMEM));
+    CK(cudaFuncSetAttribute(k_head_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, HG2_SMEM));
     g.gemm_attr = true;
   }
   launch_head_gemm(c, g, (int)r0, (int)nb16, (int)n16, H);
-  CK(cudaMemcpy2DAsync(counts, sizeof(int32_t) * n_rows, g.C.ptr, sizeof(int) * n16, sizeof(int32_t) * n_rows,
-                       nb, cudaMemcpyDeviceToHost, c->stream));
+  std::vector<HeadCount> h16((size_t)nb * n_rows);
+  CK(cudaMemcpy2DAsync(h16.data(), sizeof(HeadCount) * n_rows, g.C.ptr, sizeof(HeadCount) * n16,
+                       sizeof(HeadCount) * n_rows, nb, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  for (size_t k = 0; k < h16.size(); ++k) counts[k] = h16[k];
   return FSDA_OK;
   API_END
 }

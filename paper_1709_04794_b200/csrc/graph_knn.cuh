@@ -28,6 +28,9 @@
 namespace fsda {
 
 constexpr int KNN_MAX_K = 64;
+// head counts are at most the head width H <= 16384: 16 bits each, so the
+// GEMM writes (and the scans read) half the bytes of int32 counts
+using HeadCount = unsigned short;
 constexpr int KNN_WARPS = 8;
 
 // A[i * H + head_of[c]] = 1 for every head column c of row i (A zeroed first).
@@ -94,7 +97,7 @@ __device__ __forceinline__ void knn_offer(KnnList& L, bool valid, double sim, in
 // with a similarity strictly above the k-th (j grows along the scan, so a tie
 // never wins); an fp32 estimate screens pairs against the k-th value with a
 // 1e-5 relative margin, and only pairs that pass get the exact fp64 quotient.
-__global__ void __launch_bounds__(KNN_WARPS * 32) k_knn_scan(const int* __restrict__ C, int r0, int nb,
+__global__ void __launch_bounds__(KNN_WARPS * 32) k_knn_scan(const HeadCount* __restrict__ C, int r0, int nb,
                                                              int n, int ldc, const int* __restrict__ rsize,
                                                              int k, int* __restrict__ cand,
                                                              int* __restrict__ ncand) {
@@ -109,24 +112,26 @@ __global__ void __launch_bounds__(KNN_WARPS * 32) k_knn_scan(const int* __restri
   __syncwarp();
   KnnList L{s_s[warp], s_j[warp], &s_c[warp], k};
   const int ni = rsize[i];
-  const int4* row4 = reinterpret_cast<const int4*>(C + (long long)b * ldc);
+  const uint2* row4 = reinterpret_cast<const uint2*>(C + (long long)b * ldc);  // 4 counts per load
   const int4* rs4 = reinterpret_cast<const int4*>(rsize);
   const int n4 = ldc >> 2;  // int4 groups per row (ldc and rsize padded to 16)
   float floor_f = -1.0f;    // fp32 screen: k-th similarity minus the margin (-1 while not full)
   // lane t takes the 4 consecutive j of groups t and t + 32 of every 64-group
   // stride; both groups' loads are issued before either is screened
   for (int g0 = 0; g0 < n4; g0 += 64) {
-    int4 cv[2], sv[2];
+    uint2 cv[2];
+    int4 sv[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int gi = g0 + u * 32 + lane;
-      cv[u] = gi < n4 ? __ldcs(row4 + gi) : make_int4(0, 0, 0, 0);
+      cv[u] = gi < n4 ? __ldcs(row4 + gi) : make_uint2(0u, 0u);
       sv[u] = gi < n4 ? __ldg(rs4 + gi) : make_int4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int jb = 4 * (g0 + u * 32 + lane);
-      const int cs[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
+      const int cs[4] = {(int)(cv[u].x & 0xffffu), (int)(cv[u].x >> 16), (int)(cv[u].y & 0xffffu),
+                         (int)(cv[u].y >> 16)};
       const int ns[4] = {sv[u].x, sv[u].y, sv[u].z, sv[u].w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -238,7 +243,7 @@ __device__ __forceinline__ int knn_mult(const int* buf, int m, int j) {
 // intersect the two supports directly instead.
 template <int CAP, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_knn_refine(
-    const int* __restrict__ C, int ldc, int r0, int nb, int n, const int* __restrict__ rowptr,
+    const HeadCount* __restrict__ C, int ldc, int r0, int nb, int n, const int* __restrict__ rowptr,
     const int* __restrict__ cols, const int* __restrict__ colptr, const int* __restrict__ rows,
     const int* __restrict__ head_of, int k, const int* __restrict__ cand, const int* __restrict__ ncand,
     int* __restrict__ nbr) {
@@ -257,7 +262,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_knn_refine(
   for (int e = lane; e < ni && staged; e += 32) s_row[warp][e] = cols[lo_i + e];
   __syncwarp();
   const int* ai = staged ? s_row[warp] : cols + lo_i;
-  const int* crow = C + (long long)b * ldc;
+  const HeadCount* crow = C ? C + (long long)b * ldc : nullptr;
   KnnList L{s_s[warp], s_j[warp], &s_c[warp], k};
   int* buf = s_tail + warp * CAP;
   const int m = knn_tail_sorted<CAP>(ai, ni, head_of, colptr, rows, buf, lane);
@@ -347,7 +352,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_knn_refine(
 // (warp-aggregated atomic); the symmetrization sorts them.
 template <int CAP, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_graph_threshold(
-    const int* __restrict__ C, int ldc, int r0, int nb, int n, const int* __restrict__ rsize,
+    const HeadCount* __restrict__ C, int ldc, int r0, int nb, int n, const int* __restrict__ rsize,
     const int* __restrict__ rowptr, const int* __restrict__ cols, const int* __restrict__ colptr,
     const int* __restrict__ rows, const int* __restrict__ head_of, const int* __restrict__ tsize,
     double theta, unsigned long long* __restrict__ keys, unsigned long long* __restrict__ count,
@@ -367,19 +372,20 @@ __global__ void __launch_bounds__(WARPS * 32) k_graph_threshold(
   const int m = knn_tail_sorted<CAP>(ai, ni, head_of, colptr, rows, buf, lane);
   const int ti = tsize[i];
   const float th_f = (float)(theta * (1.0 - 1e-5));
-  const int4* row4 = C ? reinterpret_cast<const int4*>(C + (long long)b * ldc) : nullptr;
+  const uint2* row4 = C ? reinterpret_cast<const uint2*>(C + (long long)b * ldc) : nullptr;
   const int4* rs4 = reinterpret_cast<const int4*>(rsize);
   const int4* ts4 = reinterpret_cast<const int4*>(tsize);
   const int n4 = ldc >> 2;  // rsize / tsize / C rows padded to 16
   for (int g0 = 0; g0 < n4; g0 += 32) {
     const int gi = g0 + lane;
-    int4 cv = make_int4(0, 0, 0, 0), sv = cv, tv = cv;
+    uint2 cv = make_uint2(0u, 0u);
+    int4 sv = make_int4(0, 0, 0, 0), tv = sv;
     if (gi < n4) {
       if (row4) cv = __ldcs(row4 + gi);
       sv = __ldg(rs4 + gi);
       tv = __ldg(ts4 + gi);
     }
-    const int cs[4] = {cv.x, cv.y, cv.z, cv.w};
+    const int cs[4] = {(int)(cv.x & 0xffffu), (int)(cv.x >> 16), (int)(cv.y & 0xffffu), (int)(cv.y >> 16)};
     const int ns[4] = {sv.x, sv.y, sv.z, sv.w};
     const int tt[4] = {tv.x, tv.y, tv.z, tv.w};
 #pragma unroll

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 import paper_1709_04794_b200 as fb
+from oracle import c_oracle
 from paper_1709_04794_b200.workloads import make_workload
 
 pytestmark = pytest.mark.gpu
@@ -43,11 +44,25 @@ def _same(a, b):
 def _check(w, sets, alpha, tol, max_iter, seeds):
     x, lap = _mats(w)
     batch = fb.solve_label_sets(x, lap, sets, alpha, w.betas, tol, max_iter, seeds=seeds)
+    batch_mode = fb.default_device().last_shift_update_mode
     seq = fb.solve_label_sets(x, lap, sets, alpha, w.betas, tol, max_iter, seeds=seeds,
                               batched=False)
     assert len(batch) == len(sets)
     for a, b in zip(batch, seq):
         _same(a, b)
+    # pinned directly, not only through the single solves: the first and last
+    # task against the C oracle's solve of that mask (same shift-update mode)
+    c_oracle.set_shift_mode(batch_mode)
+    try:
+        for t in sorted({0, len(sets) - 1}):
+            probe = np.random.default_rng(seeds[t]).uniform(-1, 1, w.d)
+            ref = c_oracle.fsda_solve(w.x_offsets, w.x_cols, w.d, w.l_offsets, w.l_cols, w.l_vals,
+                                      sets[t], alpha, w.betas, tol, max_iter, probe)
+            np.testing.assert_array_equal(batch[t].directions, ref["directions"])
+            np.testing.assert_array_equal(batch[t].iterations, ref["iterations"])
+            np.testing.assert_array_equal(batch[t].converged, ref["converged"])
+    finally:
+        c_oracle.set_shift_mode(2)
     return batch
 
 

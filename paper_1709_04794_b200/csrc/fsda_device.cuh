@@ -13,9 +13,11 @@
 // Arithmetic contract.  The library is compiled with
 // -fmad=false, so every `a * b + c` below rounds twice exactly like numpy;
 // fma() is written out where the canonical reduction wants it (dot leaves).
-//   * Row sums (X p, L y, X W) are sequential in stored column order: one
-//     thread per row, acc = 0.0; acc = acc + term.  Bit-identical to scipy.
-//   * Every other sum uses the canonical "R256" tree: a leaf covers <= 256
+//   * The projection rows s = X w (and the X v probe API) are sequential in
+//     stored column order: acc = 0.0; acc = acc + term.  Bit-identical to
+//     scipy's csr_matvec.
+//   * Every other sum — the operator's rows X p and L y included — uses the
+//     canonical "R256" tree: a leaf covers <= 256
 //     consecutive values; lane l of a warp sums values l, l+32, ... from 0.0,
 //     then a xor-butterfly 16,8,4,2,1 combines lanes.  More than 256 values:
 //     R256 of the leaf partials of consecutive 256-blocks.  The tree depends

@@ -13,9 +13,9 @@ similarity >= theta; ``laplacian(graph)`` (graph.py:191-195) assembles
 L = D - S.
 
 The similarity work — every pair's intersection count, the per-row ranking
-and the symmetrization — runs in ``libfsda_b200.so`` (graph_knn.cuh: a
-bf16 tensor-core GEMM of the 0/1 head-column matrix for the counts of the
-frequent columns, a warp-per-row ranking scan, an exact re-ranking of the
+and the symmetrization — runs in ``libfsda_b200.so`` (graph_gemm.cuh / graph_knn.cuh: a
+hand-written int8 tcgen05 tensor-core GEMM of the 0/1 head-column matrix for
+the exact counts of the frequent columns, a warp-per-row ranking scan, an exact re-ranking of the
 candidates that share rarer columns, a radix-sort union).  ``block_size`` and
 ``n_threads`` only steer the reference's CPU blocking; the result does not
 depend on them, so they are accepted and ignored.  There is no CPU fallback.

@@ -517,7 +517,9 @@ def run_b200(args):
         betas4 = np.geomspace(c4["beta_lo"], c4["beta_hi"], c4["n_shifts"])
         masks = task_masks(w.n, T, c4["task_frac"], c4["task_pos"], seed=91)
         probes = np.stack([np.random.default_rng(1000 + t).uniform(-1, 1, w.d) for t in range(T)])
-        dev.solve_batch(masks, w.alpha, betas4, w.tol, 1, probes, scores=False)   # warm
+        # warm at the full K: the deferred shift updates keep K + 1 task-minor
+        # residuals (39 GB at cfg4), allocated on first use
+        dev.solve_batch(masks, w.alpha, betas4, w.tol, c4["max_iter"], probes, scores=False)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         bres = dev.solve_batch(masks, w.alpha, betas4, w.tol, c4["max_iter"], probes, scores=False)

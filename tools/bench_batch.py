@@ -41,8 +41,9 @@ dev = fb.Device(0)
 dev.upload_x(x)
 dev.upload_laplacian(lap)
 
-# warm: allocations at the full task count
-dev.solve_batch(masks, w.alpha, w.betas, w.tol, 1, probes, scores=False)
+# warm: allocations at the full task count and Krylov dimension (the deferred
+# shift updates keep K + 1 task-minor residuals: 39 GB at cfg4)
+dev.solve_batch(masks, w.alpha, w.betas, w.tol, w.max_iter, probes, scores=False)
 best = None
 for _ in range(args.reps):
     t0 = time.perf_counter()

@@ -260,8 +260,11 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
         "higher_is_better": True, "scaling": args.scaling if args.gpus > 1 else "strong",
         "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded, BASELINE shapes)",
-        "config": workload_config(w, {"parallelism": f"host threads ({threads})"}),
+        "data": "synthetic (seeded generator with BASELINE cfg shapes; no public dataset)",
+        # config: the workload only, identical to the b200 arm's; how each arm
+        # runs it goes in "parallelism"
+        "config": workload_config(w),
+        "parallelism": f"host threads ({threads})",
         "cpu_baseline": {
             "value": value, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"each step: {desc}; oracle/fsda_oracle.c is the reference path restated in C "
@@ -601,12 +604,11 @@ def run_b200(args):
             "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
             "dtype": "f64" if args.storage == 64 else "f32 storage, f64 reductions",
             "data": "synthetic (seeded generator with BASELINE cfg shapes; no public dataset)",
-            "config": workload_config(w, {
-                "parallelism": (f"task-parallel x{world} (one independent solve per GPU per step)"
-                                if world > 1 else "single GPU"),
-                "l2": "inputs (1.0 GB of index streams) larger than L2, and L2 flushed between "
-                      "steps (256 MB write outside the timed events)",
-            }),
+            "config": workload_config(w),
+            "parallelism": (f"task-parallel x{world} (one independent solve per GPU per step)"
+                            if world > 1 else "single GPU"),
+            "l2": "inputs (1.0 GB of index streams) larger than L2, and L2 flushed between "
+                  "steps (256 MB write outside the timed events)",
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "path": "paper_1709_04794_b200.fsda_solve(p) (drop-in API), pinned host arrays"},
@@ -653,9 +655,9 @@ def run_strong(args, torch, dist, fb, w, flush, barrier):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if args.storage == 64 else "f32 storage, f64 reductions",
             "data": "synthetic (seeded generator with BASELINE cfg shapes; no public dataset)",
-            "config": workload_config(w, {
-                "parallelism": f"row-sharded x{world} ({r['info']})",
-                "l2": "inputs larger than L2, and L2 flushed between steps (outside the events)"}),
+            "config": workload_config(w),
+            "parallelism": f"row-sharded x{world} ({r['info']})",
+            "l2": "inputs larger than L2, and L2 flushed between steps (outside the events)",
             "e2e": {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(hd[0].item()),
                     "d2h_bytes_per_step": int(hd[1].item()),
                     "path": "sharded.solve_row_sharded's per-rank upload + fsda_solve_sharded + readback "

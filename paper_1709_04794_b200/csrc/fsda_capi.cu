@@ -269,6 +269,8 @@ struct fsda_ctx {
   // the sparse kernels inside the solve graph
   cudaStream_t side = nullptr;
   cudaEvent_t ev_lfork = nullptr, ev_lcopy = nullptr;  // combined upload: L's copies on `side`
+  PinnedBuf ldiag_stage;  // combined upload: L's diagonal, split out on the host
+  int l_host_err = 0;     // the host split's validation result (check_err_flag codes)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   CgScalars* sc = nullptr;
 
@@ -1484,6 +1486,7 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     c->xh_part.release();
     c->xh_poff.release();
     c->xh_stage.release();
+    c->ldiag_stage.release();
     c->batch.release();
     c->knn.release();
     c->plan_xr.release();
@@ -1661,10 +1664,19 @@ static int upload_laplacian_rows(fsda_ctx* c, int64_t n, int64_t n_global, int64
     upload_narrow_async(c, col_indices, nnz, n_global - 1, c->l_cols, c->scratch_l64.ptr + n + 1);
   }
   c->l_diag.ensure(n);
-  if (n > 0) {
+  if (prefetched) {
+    // values checked and the diagonal split on the host by l_prefetch
+    if (c->l_host_err) {
+      CK(cudaStreamSynchronize(c->stream));
+      const int e = c->l_host_err;
+      c->l_host_err = 0;
+      CK(cudaMemcpy(c->err.ptr, &e, sizeof(int), cudaMemcpyHostToDevice));
+      return check_err_flag(c, "laplacian");
+    }
+  } else if (n > 0) {
     c->scratch_f64.ensure(std::max<long long>(nnz, 1));
     double* dvals = c->scratch_f64.ptr;
-    if (nnz > 0 && !prefetched)
+    if (nnz > 0)
       CK(cudaMemcpyAsync(dvals, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, c->stream));
     k_laplacian_split<<<grid_for(n, 256), 256, 0, c->stream>>>(c->l_rowptr.ptr, c->l_cols.ptr, dvals,
                                                                c->l_diag.ptr, (int)n, c->err.ptr,
@@ -1703,16 +1715,43 @@ void l_prefetch(void* arg) {
   LPrefetch* a = static_cast<LPrefetch*>(arg);
   fsda_ctx* c = a->c;
   c->scratch_l64.ensure(std::max<long long>(a->n + 1 + a->nnz, 1));
-  c->scratch_f64.ensure(std::max<long long>(a->nnz, 1));
   CK(cudaEventRecord(c->ev_lfork, c->stream));
   CK(cudaStreamWaitEvent(c->side, c->ev_lfork, 0));
   CK(cudaMemcpyAsync(c->scratch_l64.ptr, a->offs, sizeof(long long) * (a->n + 1), cudaMemcpyHostToDevice,
                      c->side));
-  if (a->nnz > 0) {
+  if (a->nnz > 0)
     CK(cudaMemcpyAsync(c->scratch_l64.ptr + a->n + 1, a->cols, sizeof(long long) * a->nnz,
                        cudaMemcpyHostToDevice, c->side));
-    CK(cudaMemcpyAsync(c->scratch_f64.ptr, a->vals, sizeof(double) * a->nnz, cudaMemcpyHostToDevice, c->side));
+  // L's values never cross the link: off-diagonals must be -1 (a unit-weight
+  // graph, graph.py:191-195) and the diagonal is the degree, so the host
+  // checks them and splits the diagonal out (what k_laplacian_split does on
+  // the device) while the index copies are in flight — 12 MB instead of the
+  // values' 8 bytes per entry.
+  const long long n = a->n, nnz = a->nnz;
+  const int64_t* offs = a->offs;
+  const int64_t* cols = a->cols;
+  const double* vals = a->vals;
+  double* diag = static_cast<double*>(c->ldiag_stage.ensure(sizeof(double) * std::max<long long>(n, 1)));
+  int err = 0;
+#pragma omp parallel for schedule(static, 4096) reduction(max : err)
+  for (long long i = 0; i < n; ++i) {
+    const long long lo = offs[i], hi = offs[i + 1];
+    double dv = 0.0;
+    if (lo < 0 || hi < lo || hi > nnz) {
+      err = std::max(err, 2);
+    } else {
+      for (long long jj = lo; jj < hi; ++jj) {
+        const long long cc = cols[jj];
+        if (jj > lo && cc <= cols[jj - 1]) err = std::max(err, 3);
+        if (cc == i) dv = vals[jj];
+        else if (vals[jj] != -1.0) err = std::max(err, 4);
+      }
+    }
+    diag[i] = dv;
   }
+  c->l_host_err = err;
+  c->l_diag.ensure(std::max<long long>(n, 1));
+  if (n > 0) CK(cudaMemcpyAsync(c->l_diag.ptr, diag, sizeof(double) * n, cudaMemcpyHostToDevice, c->side));
   CK(cudaEventRecord(c->ev_lcopy, c->side));
 }
 }  // namespace

@@ -553,3 +553,49 @@ def test_fp32_storage_gate_vs_fp64(cfg, k):
     assert rel <= 1e-3
     np.testing.assert_array_equal(labeled_aucs(_scores(r32, w.betas), w.labels),
                                   labeled_aucs(_scores(r64, w.betas), w.labels))
+
+
+def test_concurrent_contexts_and_graph_replays_bitwise():
+    """Race stress in place of compute-sanitizer (closed on this pool): the
+    self-resetting arrival counters of the heavy segments, K3's grid ticket
+    (reset after its grid barrier) and the TMA/mbarrier z staging must leave
+    no state behind.  Four contexts on four streams replay their cached solve
+    graphs back to back, interleaved, with heavy and blocked X^T columns; eager
+    and graph launches alternate on a fifth context.  Every result equals the
+    C oracle bit for bit."""
+    import torch
+
+    # 300k rows: 73 heavy (leaf-combining, counter-completed) and 521 blocked
+    # X^T columns
+    w = make_workload("cfg1", n=300000, d=20000, ell=3000, n_pos=600, lam=6.0, k=3, n_shifts=4,
+                      max_iter=15)
+    refs, devs, streams = [], [], []
+    for k in range(4):
+        lab = w.labels.copy()
+        rng = np.random.default_rng(100 + k)
+        flip = rng.choice(np.flatnonzero(lab != 0), size=200, replace=False)
+        lab[flip] = -lab[flip]
+        probe = np.random.default_rng(k).uniform(-1, 1, w.d)
+        refs.append(c_oracle.fsda_solve(w.x_offsets, w.x_cols, w.d, w.l_offsets, w.l_cols, w.l_vals, lab,
+                                        w.alpha, w.betas, w.tol, 15, probe)["directions"])
+        st = torch.cuda.Stream()
+        dev = fb.Device(0, stream=st.cuda_stream)
+        p = problem_from_workload(w, max_iter=15)
+        dev.load_problem(fb.SdaProblem(x=p.x, labels=fb.LabelVector(lab), lap=p.lap, alpha=w.alpha,
+                                       betas=w.betas, tol=w.tol, max_iter_d=15, seed=k))
+        dev.prepare_resident(w.alpha, w.betas, w.tol, 15, probe)
+        devs.append(dev)
+        streams.append(st)
+    for _ in range(6):                       # interleaved replays on 4 streams
+        for dev in devs:
+            dev.solve_async()
+    torch.cuda.synchronize()
+    for dev, ref in zip(devs, refs):
+        np.testing.assert_array_equal(dev.fetch(scores=False).directions, ref)
+    # eager and graph launches alternating on one context
+    p = problem_from_workload(w, max_iter=15)
+    want = c_oracle.fsda_solve_workload(w, max_iter=15)["directions"]
+    dev = fb.Device(0)
+    for eager in (True, False, True, False):
+        dev.set_eager(eager)
+        np.testing.assert_array_equal(_dirs(fb.fsda_solve(p, device=dev), w.betas), want)

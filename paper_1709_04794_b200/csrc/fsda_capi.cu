@@ -270,6 +270,10 @@ struct fsda_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_lfork = nullptr, ev_lcopy = nullptr;  // combined upload: L's copies on `side`
   PinnedBuf ldiag_stage;  // combined upload: L's diagonal, split out on the host
+  // bounce ring for host -> device copies from pageable memory (h2d)
+  PinnedBuf h2d_ring;
+  cudaEvent_t h2d_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  unsigned h2d_next = 0;
   int l_host_err = 0;     // the host split's validation result (check_err_flag codes)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   CgScalars* sc = nullptr;
@@ -1357,9 +1361,50 @@ void narrow_async(fsda_ctx* c, const long long* tmp, long long n, long long limi
   CKL();
 }
 
+// Host -> device copy of an input array.  Page-locked sources go straight to
+// the DMA engine.  Pageable ones (a plain numpy array, as sdakit callers pass
+// them) would go through the driver's single-threaded bounce buffer at a
+// fraction of the link's speed; instead they stream through a 4-slot pinned
+// ring: all host threads copy a 16 MB chunk into a free slot, the DMA drains
+// it, and the next chunk fills the next slot meanwhile.
+bool host_page_locked(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+void h2d(fsda_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  constexpr size_t CH = (size_t)16 << 20;
+  constexpr int SLOTS = 4;
+  if (bytes == 0) return;
+  if (bytes < CH || host_page_locked(src)) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    return;
+  }
+  char* ring = static_cast<char*>(c->h2d_ring.ensure(CH * SLOTS));
+  for (size_t off = 0; off < bytes; off += CH) {
+    const size_t len = std::min(CH, bytes - off);
+    const int slot = (int)(c->h2d_next++ % SLOTS);
+    CK(cudaEventSynchronize(c->h2d_ev[slot]));  // the DMA out of this slot is done
+    char* stage = ring + (size_t)slot * CH;
+    const char* from = static_cast<const char*>(src) + off;
+    const long long parts = (long long)((len + (1 << 20) - 1) >> 20);
+#pragma omp parallel for schedule(static)
+    for (long long k = 0; k < parts; ++k) {
+      const size_t a = (size_t)k << 20, b = std::min(len, a + ((size_t)1 << 20));
+      memcpy(stage + a, from + a, b - a);
+    }
+    CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, stage, len, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(c->h2d_ev[slot], st));
+  }
+}
+
 void upload_narrow_async(fsda_ctx* c, const int64_t* host, long long n, long long limit,
                          DevBuf<int>& out, long long* tmp) {
-  if (n > 0) CK(cudaMemcpyAsync(tmp, host, sizeof(long long) * n, cudaMemcpyHostToDevice, c->stream));
+  if (n > 0) h2d(c, tmp, host, sizeof(long long) * n, c->stream);
   narrow_async(c, tmp, n, limit, out);
 }
 
@@ -1449,6 +1494,7 @@ int fsda_ctx_create(fsda_ctx** out, int device, void* stream) {
     CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_lfork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_lcopy, cudaEventDisableTiming));
+    for (cudaEvent_t& e : c->h2d_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->err.ensure(1);
     CK(cudaMemset(c->err.ptr, 0, sizeof(int)));
   } catch (CudaError& ce) {
@@ -1487,6 +1533,7 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     c->xh_poff.release();
     c->xh_stage.release();
     c->ldiag_stage.release();
+    c->h2d_ring.release();
     c->batch.release();
     c->knn.release();
     c->plan_xr.release();
@@ -1510,6 +1557,8 @@ int fsda_ctx_destroy(fsda_ctx* c) {
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_lfork) cudaEventDestroy(c->ev_lfork);
     if (c->ev_lcopy) cudaEventDestroy(c->ev_lcopy);
+    for (cudaEvent_t e : c->h2d_ev)
+      if (e) cudaEventDestroy(e);
     if (c->ev_x) cudaEventDestroy(c->ev_x);
     if (c->ev_y) cudaEventDestroy(c->ev_y);
     c->ypad.release(); c->qpart.release(); c->qrecv.release(); c->qown.release();
@@ -1677,7 +1726,7 @@ static int upload_laplacian_rows(fsda_ctx* c, int64_t n, int64_t n_global, int64
     c->scratch_f64.ensure(std::max<long long>(nnz, 1));
     double* dvals = c->scratch_f64.ptr;
     if (nnz > 0)
-      CK(cudaMemcpyAsync(dvals, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, c->stream));
+      h2d(c, dvals, values, sizeof(double) * nnz, c->stream);
     k_laplacian_split<<<grid_for(n, 256), 256, 0, c->stream>>>(c->l_rowptr.ptr, c->l_cols.ptr, dvals,
                                                                c->l_diag.ptr, (int)n, c->err.ptr,
                                                                (int)row_base);
@@ -1717,11 +1766,8 @@ void l_prefetch(void* arg) {
   c->scratch_l64.ensure(std::max<long long>(a->n + 1 + a->nnz, 1));
   CK(cudaEventRecord(c->ev_lfork, c->stream));
   CK(cudaStreamWaitEvent(c->side, c->ev_lfork, 0));
-  CK(cudaMemcpyAsync(c->scratch_l64.ptr, a->offs, sizeof(long long) * (a->n + 1), cudaMemcpyHostToDevice,
-                     c->side));
-  if (a->nnz > 0)
-    CK(cudaMemcpyAsync(c->scratch_l64.ptr + a->n + 1, a->cols, sizeof(long long) * a->nnz,
-                       cudaMemcpyHostToDevice, c->side));
+  h2d(c, c->scratch_l64.ptr, a->offs, sizeof(long long) * (a->n + 1), c->side);
+  if (a->nnz > 0) h2d(c, c->scratch_l64.ptr + a->n + 1, a->cols, sizeof(long long) * a->nnz, c->side);
   // L's values never cross the link: off-diagonals must be -1 (a unit-weight
   // graph, graph.py:191-195) and the diagonal is the degree, so the host
   // checks them and splits the diagonal out (what k_laplacian_split does on
@@ -2444,11 +2490,11 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   bb.betas.ensure(ns);
   // inputs
   bb.raw.ensure(std::max<long long>((long long)T * n, (long long)T * d * 8));
-  CK(cudaMemcpyAsync(bb.raw.ptr, labels, (size_t)T * n, cudaMemcpyHostToDevice, st));
+  h2d(c, bb.raw.ptr, labels, (size_t)T * n, st);
   kb_labels_in<<<(unsigned)std::min<long long>(cdiv(n * ND, 256), 65535LL * 4), 256, 0, st>>>(
       (const signed char*)bb.raw.ptr, bb.lab.ptr, bb.ind.ptr, n, T, tp);
   CKL();
-  CK(cudaMemcpyAsync(bb.raw.ptr, probes, sizeof(double) * T * d, cudaMemcpyHostToDevice, st));
+  h2d(c, bb.raw.ptr, probes, sizeof(double) * T * d, st);
   kb_task_minor<<<(unsigned)std::min<long long>(cdiv(d * ND, 256), 65535LL * 4), 256, 0, st>>>(
       (const double*)bb.raw.ptr, bb.PR.ptr, d, T, tp);
   CKL();

@@ -124,11 +124,10 @@ __device__ __forceinline__ double emu_dot_leaf(int n, XY xy) {
 // butterfly step — so only 16 partial sums stay live (register budget: three
 // 256-thread CTAs per SM).  Indices arrive 32 at a time (coalesced) and are
 // shuffled to every lane; GATHER_MLP values per lane are in flight.
-template <typename Term>
-__device__ __forceinline__ double emu_gather_leaf(const int* __restrict__ ind, long long s0, int len,
-                                                  const double* __restrict__ src, int tp, int t,
-                                                  int lane, Term term) {
-  constexpr int LS = GATHER_MLP / 2;  // lane pairs per step
+template <int LS, typename Term>
+__device__ __forceinline__ double emu_gather_leaf_ls(const int* __restrict__ ind, long long s0, int len,
+                                                     const double* __restrict__ src, int tp, int t,
+                                                     int lane, Term term) {
   const int nk = (len + 31) >> 5;     // <= 8 index chunks
   int my[8];
 #pragma unroll
@@ -164,6 +163,19 @@ __device__ __forceinline__ double emu_gather_leaf(const int* __restrict__ ind, l
 #pragma unroll
     for (int l = 0; l < off; ++l) B[l] = B[l] + B[l + off];
   return B[0];
+}
+
+// LS lane pairs (2 LS gathers per lane) in flight per step.  A segment of at
+// most 32 entries (a row of L, ~21 at cfg4) has a single index chunk, so its
+// steps are latency rounds with little else to overlap: it takes 8 pairs per
+// step (2 rounds instead of 4); longer segments keep GATHER_MLP.  Same
+// accumulation order either way.
+template <typename Term>
+__device__ __forceinline__ double emu_gather_leaf(const int* __restrict__ ind, long long s0, int len,
+                                                  const double* __restrict__ src, int tp, int t,
+                                                  int lane, Term term) {
+  if (len <= 32) return emu_gather_leaf_ls<8>(ind, s0, len, src, tp, t, lane, term);
+  return emu_gather_leaf_ls<GATHER_MLP / 2>(ind, s0, len, src, tp, t, lane, term);
 }
 
 // Segments longer than 256 entries: R256 over their leaves (two levels,

@@ -356,6 +356,13 @@ int fsda_solve_sharded(fsda_ctx** ctxs, int n_ctx, double alpha, const double* b
     const bool v32 = f32(c0);
     ShiftState ss0 = c0->shifts();
     (void)ss0;
+    Trace tr;
+    auto sync_mark = [&](const char* what) {
+      if (!tr.on) return;
+      for (fsda_ctx* c : R.r) CK(cudaStreamSynchronize(c->stream));
+      tr.mark(what);
+    };
+    sync_mark("shard: params");
     // ---- setup: mu, rhs, CG init (sda.py:297-301, krylov.py:185-208)
     for (fsda_ctx* c : R.r) {
       ShiftState ss = c->shifts();
@@ -402,6 +409,7 @@ int fsda_solve_sharded(fsda_ctx** ctxs, int n_ctx, double alpha, const double* b
     }
     // ---- the iterations: every rank issues max_iter of them (identical
     // collectives on all ranks); the kernels idle once the solve finished
+    sync_mark("shard: setup");
     if (R.nccl) {
       fsda_ctx* c = c0;
       char key[160];
@@ -428,6 +436,7 @@ int fsda_solve_sharded(fsda_ctx** ctxs, int n_ctx, double alpha, const double* b
     } else {
       for (long long it = 0; it < max_iter; ++it) shard_iteration(R, alpha, ns, v32);
     }
+    sync_mark("shard: iterations");
     // ---- tail: directions, residuals, local projections, orientation
     for (fsda_ctx* c : R.r) {
       ShiftState ss = c->shifts();
@@ -467,6 +476,7 @@ int fsda_solve_sharded(fsda_ctx** ctxs, int n_ctx, double alpha, const double* b
       off += c->n;
     }
     for (fsda_ctx* c : R.r) CK(cudaStreamSynchronize(c->stream));
+    tr.mark("shard: tail");
     // results: replicated state, read from the first driven rank
     SolveOut o{directions, nullptr, residuals, iterations, converged, n_applies, fail_iter};
     locks.clear();

@@ -188,6 +188,7 @@ struct GraphBufs {
   long long n = 0, nnz = 0;
   double tail_avg = 0.0;  // tail-column occurrences per row of the last build
   CUtensorMap amap{};            // TMA descriptor of A (re-encoded per build)
+  long long block_rows = 0;      // rows per GEMM / scan block of the current build
   bool gemm_attr = false;        // k_head_gemm's shared-memory opt-in done
   void release() {
     head_of.release(); cand.release(); ncand.release(); nbr.release(); rsize.release(); tsize.release(); A.release();
@@ -2853,6 +2854,22 @@ bool head_gemm_pairs() {
   return v;
 }
 
+// Rows per block of the graph builds: as many as a 16 GiB (at most a quarter
+// of free memory) block of 16-bit head counts allows, a multiple of 16.  The
+// scans run one warp per row of the block, so small blocks starve the GPU at
+// large N (r01's 2^30-element cap gave 715-row blocks at cfg3).
+long long graph_block_rows(GraphBufs& g, long long n16) {
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  const double budget = std::min(16.0 * (1LL << 30), 0.25 * (double)free_b);
+  long long b = (long long)(budget / (sizeof(HeadCount) * (double)std::max<long long>(n16, 1))) & ~15LL;
+  if (const char* f = std::getenv("FSDA_B200_GRAPH_BLOCK_ROWS"))  // tests: many blocks on small inputs
+    b = std::atoll(f) & ~15LL;
+  b = std::max<long long>(16, std::min<long long>(n16, b));
+  g.block_rows = b;
+  return b;
+}
+
 // Shared by the k-NN and threshold builds: head selection, the int8 head
 // matrix, then per row block the head-count GEMM followed by `per_block`.
 template <typename F>
@@ -2896,10 +2913,9 @@ int graph_blocks(fsda_ctx* c, GraphBufs& g, F per_block) {
   CK(cudaMemcpyAsync(g.head_of.ptr, head_of.data(), sizeof(int) * std::max<long long>(d, 1),
                      cudaMemcpyHostToDevice, c->stream));
   // int8 tensor-core GEMM shapes: rows of A and C's leading dimension padded
-  // to 16 (zero rows); blocks start at multiples of 16, and the nb x n16 int32
-  // block of head counts stays below 2^30 elements
+  // to 16 (zero rows); blocks of g.block_rows rows (graph_block_rows)
   const long long n16 = (n + 15) & ~15LL;
-  const long long B = std::max<long long>(16, std::min<long long>(n16, ((1LL << 30) / n16) & ~15LL));
+  const long long B = g.block_rows;
   g.rsize.ensure(n16);
   CK(cudaMemsetAsync(g.rsize.ptr, 0, sizeof(int) * n16, c->stream));
   k_knn_rsize<<<grid_for(n, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, g.rsize.ptr, (int)n);
@@ -2981,7 +2997,7 @@ extern "C" int fsda_graph_knn(fsda_ctx* c, int32_t k, int64_t* nnz_out) {
   GraphBufs& g = c->knn;
   Trace tr;
   const long long n16 = (n + 15) & ~15LL;
-  const long long B = std::max<long long>(16, std::min<long long>(n16, ((1LL << 30) / n16) & ~15LL));
+  const long long B = graph_block_rows(g, n16);
   g.cand.ensure(B * k);
   g.ncand.ensure(B);
   g.nbr.ensure(n * k);
@@ -3032,6 +3048,7 @@ extern "C" int fsda_graph_threshold(fsda_ctx* c, double theta, int64_t* nnz_out)
   g.count.ensure(1);
   unsigned long long cap = (unsigned long long)std::max<long long>(1LL << 20, 16 * n);
   unsigned long long hits = 0;
+  graph_block_rows(g, (n + 15) & ~15LL);
   for (int attempt = 0; attempt < 2; ++attempt) {
     g.keys.ensure((long long)cap);
     CK(cudaMemsetAsync(g.count.ptr, 0, sizeof(long long), c->stream));

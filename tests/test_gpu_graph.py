@@ -195,3 +195,15 @@ def test_head_count_gemm_zipf_rows():
     got = G.head_counts(a, 640, 1500)
     ai = a.astype(np.int32)
     assert np.array_equal(got, ai[640:2140] @ ai.T)
+
+
+@pytest.mark.parametrize("rows", ["16", "1008", "4000"])
+def test_device_graphs_in_many_blocks(gold, rows, monkeypatch):
+    """The builds cut the rows into blocks sized by a memory budget (one block
+    at these sizes); forcing small blocks — including a last, ragged one —
+    must give the reference's graphs entry for entry."""
+    monkeypatch.setenv("FSDA_B200_GRAPH_BLOCK_ROWS", rows)
+    w = make_workload("cfg1")
+    x = T.SparseMatrix.binary(w.n, w.d, w.x_offsets, w.x_cols)
+    _check(G.knn_graph(x, 10), gold["cfg1__g_offsets"], gold["cfg1__g_cols"].astype(np.int64))
+    _check(G.threshold_graph(x, 0.3), gold["cfg1__t030_offsets"], gold["cfg1__t030_cols"].astype(np.int64))

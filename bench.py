@@ -318,10 +318,10 @@ def time_e2e(fb, dev, w, steps, pinned=True):
         rep = fb.fsda_solve(pp, device=dev)
     dt = (time.perf_counter() - t0) / steps
     assert rep.regression.operator_applications == w.max_iter
-    # bytes that cross the link: X and L indices (int64, as the reference holds
-    # them), L's diagonal (its values are checked and split on the host),
-    # labels, probe, betas
-    h2d = (w.x_offsets.nbytes + w.x_cols.nbytes + w.l_offsets.nbytes + w.l_cols.nbytes +
+    # bytes that cross the link: X and L indices (narrowed from the reference's
+    # int64 to int32 on the host), L's diagonal (its values are checked and
+    # split on the host), labels, probe, betas
+    h2d = (4 * (w.x_offsets.size + w.x_cols.size + w.l_offsets.size + w.l_cols.size) +
            8 * w.n + w.labels.nbytes + 8 * w.d + 8 * w.betas.size)
     d2h = 8 * w.betas.size * (w.d + w.n) + 8 * 3 * w.betas.size
     return dt, int(h2d), int(d2h)

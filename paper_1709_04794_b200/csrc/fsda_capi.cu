@@ -1403,8 +1403,53 @@ void h2d(fsda_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st)
   }
 }
 
+// int64 host indices -> int32 device indices, narrowed (and range-checked)
+// on the host by all threads into the pinned ring, so only half the bytes
+// cross the link.  Returns 1 when an index lies outside [0, limit] (the
+// check k_narrow_idx makes on the device).
+int h2d_narrow(fsda_ctx* c, DevBuf<int>& out, const int64_t* src, long long n, long long limit,
+               cudaStream_t st) {
+  constexpr size_t CH = (size_t)16 << 20;  // bytes of int32 per ring slot
+  constexpr int SLOTS = 4;
+  out.ensure(n + 8);  // tail padding: the row kernels stage indices with 16-byte loads
+  CK(cudaMemsetAsync(out.ptr + n, 0, 8 * sizeof(int), st));
+  if (n == 0) return 0;
+  char* ring = static_cast<char*>(c->h2d_ring.ensure(CH * SLOTS));
+  const long long che = (long long)(CH / sizeof(int));
+  int bad = 0;
+  for (long long off = 0; off < n; off += che) {
+    const long long len = std::min(che, n - off);
+    const int slot = (int)(c->h2d_next++ % SLOTS);
+    CK(cudaEventSynchronize(c->h2d_ev[slot]));
+    int* stage = reinterpret_cast<int*>(ring + (size_t)slot * CH);
+    const int64_t* from = src + off;
+#pragma omp parallel for schedule(static) reduction(max : bad)
+    for (long long k = 0; k < len; ++k) {
+      const long long v = from[k];
+      bad = std::max(bad, (v < 0 || v > limit) ? 1 : 0);
+      stage[k] = (int)v;
+    }
+    CK(cudaMemcpyAsync(out.ptr + off, stage, sizeof(int) * len, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(c->h2d_ev[slot], st));
+  }
+  return bad;
+}
+
+// FSDA_B200_DEVICE_NARROW=1: copy the int64 indices and narrow them on the
+// device (the round-1 path) instead of h2d_narrow.
+bool device_narrow() {
+  static const bool v = std::getenv("FSDA_B200_DEVICE_NARROW") && std::atoi(std::getenv("FSDA_B200_DEVICE_NARROW"));
+  return v;
+}
+
 void upload_narrow_async(fsda_ctx* c, const int64_t* host, long long n, long long limit,
                          DevBuf<int>& out, long long* tmp) {
+  if (!device_narrow()) {
+    static const int k_out_of_range = 1;  // check_err_flag's "index out of range"
+    if (h2d_narrow(c, out, host, n, limit, c->stream))
+      CK(cudaMemcpyAsync(c->err.ptr, &k_out_of_range, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    return;
+  }
   if (n > 0) h2d(c, tmp, host, sizeof(long long) * n, c->stream);
   narrow_async(c, tmp, n, limit, out);
 }
@@ -1706,8 +1751,10 @@ static int upload_laplacian_rows(fsda_ctx* c, int64_t n, int64_t n_global, int64
   if (prefetched) {
     // the raw arrays were copied on the side stream (l_prefetch)
     CK(cudaStreamWaitEvent(c->stream, c->ev_lcopy, 0));
-    narrow_async(c, c->scratch_l64.ptr, n + 1, nnz, c->l_rowptr);
-    narrow_async(c, c->scratch_l64.ptr + n + 1, nnz, n_global - 1, c->l_cols);
+    if (device_narrow()) {
+      narrow_async(c, c->scratch_l64.ptr, n + 1, nnz, c->l_rowptr);
+      narrow_async(c, c->scratch_l64.ptr + n + 1, nnz, n_global - 1, c->l_cols);
+    }
   } else {
     c->scratch_l64.ensure(std::max<long long>(n + 1 + nnz, 1));
     upload_narrow_async(c, row_offsets, n + 1, nnz, c->l_rowptr, c->scratch_l64.ptr);
@@ -1764,11 +1811,17 @@ struct LPrefetch {
 void l_prefetch(void* arg) {
   LPrefetch* a = static_cast<LPrefetch*>(arg);
   fsda_ctx* c = a->c;
-  c->scratch_l64.ensure(std::max<long long>(a->n + 1 + a->nnz, 1));
   CK(cudaEventRecord(c->ev_lfork, c->stream));
   CK(cudaStreamWaitEvent(c->side, c->ev_lfork, 0));
-  h2d(c, c->scratch_l64.ptr, a->offs, sizeof(long long) * (a->n + 1), c->side);
-  if (a->nnz > 0) h2d(c, c->scratch_l64.ptr + a->n + 1, a->cols, sizeof(long long) * a->nnz, c->side);
+  int range_err = 0;
+  if (device_narrow()) {
+    c->scratch_l64.ensure(std::max<long long>(a->n + 1 + a->nnz, 1));
+    h2d(c, c->scratch_l64.ptr, a->offs, sizeof(long long) * (a->n + 1), c->side);
+    if (a->nnz > 0) h2d(c, c->scratch_l64.ptr + a->n + 1, a->cols, sizeof(long long) * a->nnz, c->side);
+  } else {
+    range_err |= h2d_narrow(c, c->l_rowptr, a->offs, a->n + 1, a->nnz, c->side);
+    range_err |= h2d_narrow(c, c->l_cols, a->cols, a->nnz, a->n - 1, c->side);
+  }
   // L's values never cross the link: off-diagonals must be -1 (a unit-weight
   // graph, graph.py:191-195) and the diagonal is the degree, so the host
   // checks them and splits the diagonal out (what k_laplacian_split does on
@@ -1796,7 +1849,7 @@ void l_prefetch(void* arg) {
     }
     diag[i] = dv;
   }
-  c->l_host_err = err;
+  c->l_host_err = range_err ? 1 : err;
   c->l_diag.ensure(std::max<long long>(n, 1));
   if (n > 0) CK(cudaMemcpyAsync(c->l_diag.ptr, diag, sizeof(double) * n, cudaMemcpyHostToDevice, c->side));
   CK(cudaEventRecord(c->ev_lcopy, c->side));

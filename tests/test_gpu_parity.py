@@ -599,3 +599,28 @@ def test_concurrent_contexts_and_graph_replays_bitwise():
     for eager in (True, False, True, False):
         dev.set_eager(eager)
         np.testing.assert_array_equal(_dirs(fb.fsda_solve(p, device=dev), w.betas), want)
+
+
+def test_large_pageable_upload_narrowed_on_host():
+    """Uploads larger than one 16 MB ring slot: plain (pageable) int64 index
+    arrays stream through the pinned ring narrowed to int32 on the host.  An
+    out-of-range index in the last chunk is still reported, and a valid X of
+    the same size then matches X v computed by the oracle."""
+    from paper_1709_04794_b200 import _capi
+
+    rng = np.random.default_rng(5)
+    n, d, per = 400_000, 50_000, 40          # 16M entries: 128 MB of int64, 4 ring chunks
+    offs = np.arange(0, (n + 1) * per, per, dtype=np.int64)
+    # strictly increasing columns in every row: sorted draws plus 0..per-1,
+    # clipped below a strictly increasing cap
+    cols = np.sort(rng.integers(0, d, size=(n, per)), axis=1) + np.arange(per)
+    cols = np.minimum(cols, d - per + np.arange(per)).astype(np.int64).ravel()
+    dev = fb.Device(0)
+    bad = cols.copy()
+    bad[-1] = d + 7
+    rc = _capi.lib().fsda_upload_x(dev._h, n, d, _capi.i64ptr(offs), _capi.i64ptr(bad))
+    assert rc == _capi.FSDA_EINVAL and _capi.last_error().startswith("X: index out of range")
+    x = fb.SparseMatrix.binary(n, d, offs, cols)
+    v = rng.standard_normal(d)
+    got = fb.matvec(x, v)
+    np.testing.assert_array_equal(got, c_oracle.matvec(offs, cols, v))

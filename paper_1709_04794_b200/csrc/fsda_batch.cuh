@@ -457,34 +457,84 @@ __device__ __forceinline__ double block_leaf(int n, Load load, double* sm) {
   return r;
 }
 
+// The long columns' partials, unit u: heavy segment u (hn leaf sums from h0)
+// for u < n_heavy, else blocked column u - n_heavy (its poff range).
+__device__ __forceinline__ const double* unit_part(const SegPlan& pl, const XtDense& dn,
+                                                   const double* hpart, const double* xpart,
+                                                   long long n_heavy, long long u, int tp,
+                                                   long long* m) {
+  if (u < n_heavy) {
+    *m = __ldg(pl.heavy_nseg + u);
+    return hpart + (long long)__ldg(pl.heavy_seg0 + u) * tp;
+  }
+  const long long b = u - n_heavy;
+  const long long p0 = __ldg(dn.poff + b);
+  *m = __ldg(dn.poff + b + 1) - p0;
+  return xpart + p0 * tp;
+}
+
+// Level 1 of the long units (more than 256 partials — the Zipf head's
+// blocked columns hold up to ~6k): one warp per (256-partial group, task
+// group) writes the group's canonical leaf to gsum, so no warp walks a whole
+// column alone.  chunks[k] = {unit, group}; gsoff[unit] = its first slot.
+__global__ void __launch_bounds__(256) kb_part_groups(SegPlan pl, XtDense dn,
+                                                      const double* __restrict__ hpart,
+                                                      const double* __restrict__ xpart,
+                                                      long long n_heavy, const int2* __restrict__ chunks,
+                                                      long long n_chunks, const int* __restrict__ gsoff,
+                                                      double* __restrict__ gsum, int G, int tp) {
+  const int lane = threadIdx.x & 31;
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= n_chunks * G) return;
+  const long long k = w / G;
+  const int g = (int)(w - k * G);
+  const int t = g * BG + lane;
+  const int2 ch = __ldg(chunks + k);
+  long long m;
+  const double* part = unit_part(pl, dn, hpart, xpart, n_heavy, ch.x, tp, &m);
+  const long long k0 = (long long)ch.y * LEAF;
+  gsum[((long long)__ldg(gsoff + ch.x) + ch.y) * tp + t] =
+      emu_part_leaf(part, k0, (int)min((long long)LEAF, m - k0), tp, t);
+}
+
+// Level 2 over m2 <= 256 precomputed group leaves gs[j][TP]: lane
+// accumulators P[l] = sum of leaves j = l, l + 32, ... in order, then
+// tree32 — the second level of emu_part_long.
+__device__ __noinline__ double emu_group_level2(const double* __restrict__ gs, int m2, int tp, int t) {
+  double P[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) P[l] = 0.0;
+  for (int gb = 0; gb < m2; gb += 32) {
+#pragma unroll
+    for (int l = 0; l < 32; ++l)
+      if (gb + l < m2) P[l] = P[l] + gs[(long long)(gb + l) * tp + t];
+  }
+  return tree32(P);
+}
+
 // Combine the long columns: heavy segment h (hn[h] leaf sums from h0[h]) and
-// blocked column b (poff range).  One warp per (column, group).
+// blocked column b (poff range).  One warp per (column, group); units with
+// more than 256 partials take their level-1 leaves from kb_part_groups.
 __global__ void __launch_bounds__(256, 2) kb_cols_combine(SegPlan pl, XtDense dn,
                                                        const double* __restrict__ hpart,
                                                        const double* __restrict__ xpart,
                                                        long long n_heavy,
                                                        double* __restrict__ out, int G, int tp,
                                                        int mode, const double* __restrict__ mu,
-                                                       BatchState B) {
+                                                       BatchState B, const int* __restrict__ gsoff,
+                                                       const double* __restrict__ gsum) {
   const int lane = threadIdx.x & 31;
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= (n_heavy + dn.n_dense) * G) return;
   const long long u = w / G;
   const int g = (int)(w - u * G);
   const int t = g * BG + lane;
-  double s;
-  long long col;
-  if (u < n_heavy) {
-    const int h = (int)u;
-    const int h0 = __ldg(pl.heavy_seg0 + h), hn = __ldg(pl.heavy_nseg + h);
-    s = emu_partials(hpart + (long long)h0 * tp, hn, tp, t);
-    col = __ldg(pl.heavy_seg + h);
-  } else {
-    const long long b = u - n_heavy;
-    const long long p0 = __ldg(dn.poff + b), p1 = __ldg(dn.poff + b + 1);
-    s = emu_partials(xpart + p0 * tp, p1 - p0, tp, t);
-    col = __ldg(dn.col + b);
-  }
+  long long m;
+  const double* part = unit_part(pl, dn, hpart, xpart, n_heavy, u, tp, &m);
+  const long long col = u < n_heavy ? (long long)__ldg(pl.heavy_seg + u) : (long long)__ldg(dn.col + (u - n_heavy));
+  const int go = gsoff ? __ldg(gsoff + u) : -1;
+  const double s = go >= 0 ? emu_group_level2(gsum + (long long)go * tp, (int)((m + LEAF - 1) / LEAF), tp, t)
+                           : emu_partials(part, m, tp, t);
   out[col * tp + t] = b_col_finish(s, mode, col, t, tp, mu, B);
 }
 

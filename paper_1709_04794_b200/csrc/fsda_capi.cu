@@ -156,6 +156,9 @@ struct BatchBufs {
   DevBuf<signed char> lab;
   DevBuf<double> ind, P, Q, R0, R1, MU, Bv, PR, Y, Z, BIGP, SOLS, SCORES, OUT;
   DevBuf<double> RB, CA, CC;  // deferred mode: residual slots, coefficient rows
+  DevBuf<int2> gchunks;       // long X^T units: {unit, 256-partial group}
+  DevBuf<int> gsoff;          // per unit: first group-leaf slot, or -1
+  DevBuf<double> gsum;        // group leaves [slot][TP]
   DevBuf<double> partD, partN, part2, hpart, xpart, opart, scal;
   DevBuf<long long> lscal;
   DevBuf<int> iscal;
@@ -170,6 +173,7 @@ struct BatchBufs {
     MU.release(); Bv.release(); PR.release(); Y.release(); Z.release(); BIGP.release();
     SOLS.release(); SCORES.release(); OUT.release(); partD.release(); partN.release();
     RB.release(); CA.release(); CC.release();
+    gchunks.release(); gsoff.release(); gsum.release();
     hpart.release(); xpart.release(); opart.release(); scal.release(); lscal.release();
     part2.release();
     iscal.release(); sh_d.release(); sh_l.release(); sh_u.release(); sh_i.release();
@@ -2609,6 +2613,36 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   const long long n_light = pxc.cls_off[6];
   const long long n_htask = pxc.warp_base[7] - pxc.warp_base[6];
   const long long n_heavy = c->plan_xc.n_heavy;
+  // units (heavy segments, blocked columns) with more than 256 leaf partials:
+  // their level-1 group leaves go to kb_part_groups, spread over warps
+  long long n_gchunks = 0;
+  {
+    const long long nu = n_heavy + c->xh.n_dense;
+    std::vector<int> hn((size_t)std::max<long long>(n_heavy, 1));
+    std::vector<long long> poff((size_t)c->xh.n_dense + 1, 0);
+    if (n_heavy) CK(cudaMemcpy(hn.data(), pxc.heavy_nseg, sizeof(int) * n_heavy, cudaMemcpyDeviceToHost));
+    if (c->xh.n_dense)
+      CK(cudaMemcpy(poff.data(), c->xh.poff, sizeof(long long) * (c->xh.n_dense + 1), cudaMemcpyDeviceToHost));
+    std::vector<int> gso((size_t)std::max<long long>(nu, 1), -1);
+    std::vector<int2> chunks;
+    long long slots = 0;
+    for (long long u = 0; u < nu; ++u) {
+      const long long m = u < n_heavy ? hn[u] : poff[u - n_heavy + 1] - poff[u - n_heavy];
+      if (m <= LEAF) continue;
+      const long long m2 = cdiv(m, LEAF);
+      gso[u] = (int)slots;
+      for (long long j = 0; j < m2; ++j) chunks.push_back(make_int2((int)u, (int)j));
+      slots += m2;
+    }
+    n_gchunks = (long long)chunks.size();
+    bb.gsoff.ensure(std::max<long long>(nu, 1));
+    bb.gchunks.ensure(std::max<long long>(n_gchunks, 1));
+    bb.gsum.ensure(std::max<long long>(slots * ND, 1));
+    if (nu) CK(cudaMemcpyAsync(bb.gsoff.ptr, gso.data(), sizeof(int) * nu, cudaMemcpyHostToDevice, st));
+    if (n_gchunks)
+      CK(cudaMemcpyAsync(bb.gchunks.ptr, chunks.data(), sizeof(int2) * n_gchunks, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // the host vectors go out of scope
+  }
   auto xt = [&](const double* src, double* out, int mode) {
     if (n_light)
       kb_cols_light<<<grid_w(n_light * G), 256, 0, st>>>(pxc, src, out, G, tp, mode, bb.MU.ptr, B);
@@ -2617,8 +2651,15 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
       kb_cols_leaves<<<grid_w((4 * n_htask + c->xh_ntasks) * G), 256, 0, st>>>(
           pxc, c->xh, src, bb.hpart.ptr, bb.xpart.ptr, 4 * n_htask, c->xh_ntasks, G, tp);
       CKL();
+      if (n_gchunks) {
+        kb_part_groups<<<grid_w(n_gchunks * G), 256, 0, st>>>(pxc, c->xh, bb.hpart.ptr, bb.xpart.ptr, n_heavy,
+                                                              bb.gchunks.ptr, n_gchunks, bb.gsoff.ptr,
+                                                              bb.gsum.ptr, G, tp);
+        CKL();
+      }
       kb_cols_combine<<<grid_w((n_heavy + c->xh.n_dense) * G), 256, 0, st>>>(
-          pxc, c->xh, bb.hpart.ptr, bb.xpart.ptr, n_heavy, out, G, tp, mode, bb.MU.ptr, B);
+          pxc, c->xh, bb.hpart.ptr, bb.xpart.ptr, n_heavy, out, G, tp, mode, bb.MU.ptr, B,
+          n_gchunks ? bb.gsoff.ptr : nullptr, bb.gsum.ptr);
       CKL();
     }
   };

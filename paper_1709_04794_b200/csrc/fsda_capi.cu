@@ -2999,6 +2999,8 @@ int graph_blocks(fsda_ctx* c, GraphBufs& g, F per_block) {
     }
     if ((size_t)cand >= order.size()) break;
   }
+  if (const char* f = std::getenv("FSDA_B200_GRAPH_HEAD"))  // experiments: force the head width
+    nh = (int)std::min<size_t>(order.size(), (size_t)std::max(0, std::atoi(f)));
   g.tail_avg = n > 0 ? sq[nh] / (double)n : 0.0;
   const int H = nh > 0 ? (nh + HG_BK - 1) / HG_BK * HG_BK : 0;  // GEMM depth padded to 128 (zero columns)
   std::vector<int> head_of((size_t)std::max<long long>(d, 1), -1);

@@ -8,7 +8,8 @@ workload is the largest single-GPU one, configs[2] = "cfg3": a
 1.5M x 500k binary X (75M nnz, Poisson 50, Zipf 1.05), random 10-NN
 Laplacian, 30 shifts, K = 150, fp64 — on seeded synthetic inputs of that
 shape (the reference ships no dataset for this path).  cfg2 (the medium
-case) and cfg4 (64 label-mask tasks on the cfg3 matrix) are extra keys.
+case), cfg4 (64 label-mask tasks on the cfg3 matrix) and cfg5 (8M x 2M in
+fp32 storage, on this one GPU) are extra keys.
 
   python bench.py [--gpus N --steps K --warmup W --workload cfg3]
   python bench.py --impl reference ...     # the reference's CPU path (oracle port)
@@ -61,8 +62,9 @@ def parse():
                     help="run the row-sharded (NCCL) path even at one GPU")
     ap.add_argument("--storage", type=int, default=None, choices=[32, 64],
                     help="vector storage (default: 32 for cfg5 as BASELINE states, else 64)")
-    ap.add_argument("--extra", default="cfg2,cfg4",
-                    help="extra keys: cfg2 (second workload), cfg4 (64-task batch), none")
+    ap.add_argument("--extra", default="cfg2,cfg4,cfg5",
+                    help="extra keys: cfg2 (second workload), cfg4 (64-task batch), "
+                         "cfg5 (8M x 2M in fp32 storage on this GPU; ~2.5 min of host generation), none")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -600,6 +602,52 @@ def run_b200(args):
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": desc + " (the reference path restated in C with OpenMP)"}
 
+    # cfg5 (BASELINE configs[4]: 8M x 2M, 640M nnz, 15-NN, K=200, fp32 storage
+    # with fp64 reductions, stated for 4/8 GPUs) on this one GPU: device-
+    # resident solves/s in the stated storage mode.  Its 1e-3 gate against the
+    # fp64 solve is tests/test_gpu_parity.py::test_fp32_storage_gate_vs_fp64;
+    # bitwise vs the oracle at cfg5 scale: tools/cfg5_parity.py.
+    cfg5 = None
+    if "cfg5" in extras and w.name != "cfg5":
+        from paper_1709_04794_b200.workloads import make_workload_chunked
+
+        t0 = time.perf_counter()
+        w5 = make_workload_chunked("cfg5")
+        t_gen = time.perf_counter() - t0
+        d5 = fb.Device(local, stream=stream.cuda_stream)
+        d5.set_storage(32)
+        p5 = make_problem(fb, w5)              # host-side validation of the 640M-entry inputs
+        t0 = time.perf_counter()
+        d5.load_problem(p5)
+        torch.cuda.synchronize()
+        t_up = time.perf_counter() - t0
+        del p5
+        d5.prepare_resident(w5.alpha, w5.betas, w5.tol, w5.max_iter, w5.probe())
+        d5.solve_async()                       # warm (graph capture)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2)]
+        for a_, b_ in ev:
+            a_.record(stream)
+            d5.solve_async()
+            b_.record(stream)
+        torch.cuda.synchronize()
+        ms5 = [a_.elapsed_time(b_) for a_, b_ in ev]
+        r5 = d5.fetch(directions=False, scores=True)
+        lab5 = w5.labels
+        aucs = []
+        for s_ in r5.scores:
+            sc = s_[lab5 != 0]
+            yv = lab5[lab5 != 0] == 1
+            rk = np.empty(sc.size)
+            rk[np.argsort(sc, kind="stable")] = np.arange(1, sc.size + 1)
+            aucs.append(float((rk[yv].sum() - yv.sum() * (yv.sum() + 1) / 2) / (yv.sum() * (~yv).sum())))
+        cfg5 = {"value": 1000.0 / statistics.mean(ms5), "unit": UNIT, "ms_per_solve": ms5,
+                "dtype": "f32 storage, f64 reductions", "n_applies": r5.n_applies,
+                "labeled_auc_min": min(aucs), "generate_s": t_gen, "upload_s": t_up,
+                "config": workload_config(w5)["workload"],
+                "note": "one B200 (BASELINE states 4/8 GPUs); device-resident, CUDA events"}
+        del d5, r5, w5
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -621,6 +669,7 @@ def run_b200(args):
             "spmv_pair": spmv_pair,
             "solve_bandwidth": solve_bw,
             "extra": extra_lines or None,
+            "cfg5_fp32": cfg5,
             "batch_cfg4": batch,
             "regression_phase": regression,
             "graph_build": graph,

@@ -6,9 +6,15 @@
 //   C[b][j] = sum_h A[r0 + b][h] * A[j][h]      b < nb, j < n16
 //
 // A is the N16 x H 0/1 int8 head matrix (row-major: K-major for both MMA
-// operands), C the nb16 x n16 block of exact head counts (16-bit) read by
-// k_knn_scan / k_knn_refine / k_graph_threshold.  Integer arithmetic: the
-// counts are exact and equal to any other GEMM's bit for bit.
+// operands), C the nb16 x n16 block of exact head counts, 16-bit (counts are
+// at most H <= 16384), read by k_knn_scan / k_knn_refine / k_graph_threshold.
+// Integer arithmetic: the counts are exact and equal to any other GEMM's.
+//
+// The product path is k_head_gemm2: clusters of two CTAs (the two SMs of a
+// TPC) on 256 x 256 tiles, tcgen05.mma.cta_group::2 (see its comment below);
+// 4.06 int8 POPS per cfg2 block, 87 % of the imma pipe (profiles/
+// r02_graph_gemm.md).  k_head_gemm, the single-CTA form below, is kept as the
+// FSDA_B200_HEAD_GEMM=1sm alternative; its structure is the same:
 //
 // One persistent CTA per SM, 192 threads, warp-specialised:
 //   warp 0     TMA producer: per K step (128 bytes of H) one 128 x 128 tile of
@@ -20,12 +26,12 @@
 //              tcgen05.commit frees the ring slot and, after the last K step,
 //              hands the accumulator to the epilogue;
 //   warps 2-5  epilogue: tcgen05.ld of the 128 x 256 int32 accumulator (each
-//              warp its 32-lane quarter), packed to 16-bit counts (<= H) and
-//              stored straight to C, 8 per 16-byte store.
+//              warp its 32-lane quarter), packed to 16-bit counts and stored
+//              straight to C, 8 per 16-byte store.
 // TMEM holds two accumulators (2 x 256 of its 512 columns), so the epilogue
 // of tile t overlaps the MMAs of tile t+1.  Tiles run m-fastest over the
 // grid: the A_blk tiles stay L2-resident and the CTAs in flight share the
-// same few j tiles, so A is read from HBM about once per block.
+// same few j tiles.
 #pragma once
 
 #include <cuda.h>

@@ -2944,8 +2944,8 @@ void launch_head_gemm(fsda_ctx* c, GraphBufs& g, int r0, int nb16, int n16, int 
 
 // k_head_gemm2 (CTA pairs, cta_group::2) unless FSDA_B200_HEAD_GEMM=1sm
 bool head_gemm_pairs() {
-  static const bool v = !(std::getenv("FSDA_B200_HEAD_GEMM") && std::string(std::getenv("FSDA_B200_HEAD_GEMM")) == "1sm");
-  return v;
+  const char* v = std::getenv("FSDA_B200_HEAD_GEMM");  // read per build: tests switch it
+  return !(v && std::string(v) == "1sm");
 }
 
 // Rows per block of the graph builds: as many as a 16 GiB (at most a quarter

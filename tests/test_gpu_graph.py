@@ -174,9 +174,13 @@ def test_cfg2_rows_contain_their_oracle_neighbours():
     (300, 1, 0, 300, 0.5),           # one head column
     (3000, 640, 2900, 100, 1.0),     # all ones: counts = h (largest values)
 ])
-def test_head_count_gemm_exact(n, h, r0, nb, density):
-    """The hand-written tcgen05 int8 GEMM (k_head_gemm) against numpy's
-    integer product: exact counts, every entry."""
+@pytest.mark.parametrize("kernel", ["pairs", "1sm"])
+def test_head_count_gemm_exact(n, h, r0, nb, density, kernel, monkeypatch):
+    """The hand-written tcgen05 int8 GEMMs (k_head_gemm2 on CTA pairs, the
+    product path, and the single-CTA k_head_gemm) against numpy's integer
+    product: exact counts, every entry."""
+    if kernel == "1sm":
+        monkeypatch.setenv("FSDA_B200_HEAD_GEMM", "1sm")
     rng = np.random.default_rng(n + h)
     a = (rng.random((n, h)) < density).astype(np.int8)
     got = G.head_counts(a, r0, nb)

@@ -647,10 +647,36 @@ __global__ void kb_cg_init_rp(const double* __restrict__ b, double* __restrict__
   }
 }
 
-// Coefficient updates of loop iteration `it` for the tasks that stepped
+// The loop iteration lives on the device (*BIter::it, advanced by
+// kb_loop_next), so the body's launches are identical every iteration and
+// the loop can run as a captured graph with a conditional WHILE node.  The
+// residual slots of iteration it: r_it / r_{it+1} of the deferred basis, or
+// the ping-pong pair of the per-iteration mode.
+struct BIter {
+  double* rb;            // deferred basis: slot j at rb + j * stride
+  double* r0;            // per-iteration mode: ping-pong residuals
+  double* r1;
+  long long stride;      // d * TP
+  int basis;
+  const long long* it;   // loop iteration (device)
+};
+
+__device__ __forceinline__ void b_iter_ptrs(const BIter& bi, const double*& cur, double*& nxt) {
+  const long long it = *bi.it;
+  if (bi.basis) {
+    cur = bi.rb + it * bi.stride;
+    nxt = bi.rb + (it + 1) * bi.stride;
+  } else {
+    cur = (it & 1) ? bi.r1 : bi.r0;
+    nxt = (it & 1) ? bi.r0 : bi.r1;
+  }
+}
+
+// Coefficient updates of loop iteration it for the tasks that stepped
 // (kb_step_c's shift part on coefficients).  blockIdx.y = (task, shift).
 __global__ void kb_coef_update(BatchState B, const int* __restrict__ stepped, double* __restrict__ coef_a,
-                               double* __restrict__ coef_c, long long ld, long long it) {
+                               double* __restrict__ coef_c, long long ld, const long long* __restrict__ itp) {
+  const long long it = *itp;
   const int k = blockIdx.y;
   const int t = k / B.ns;
   if (!stepped[t]) return;
@@ -673,8 +699,12 @@ __global__ void kb_coef_update(BatchState B, const int* __restrict__ stepped, do
 
 // p = r_next + alpha_new p for the tasks that stepped (kb_step_c without the
 // shift state).
-__global__ void kb_step_c_p(const double* __restrict__ r_next, double* __restrict__ p, long long len,
+__global__ void kb_step_c_p(BIter bi, double* __restrict__ p, long long len,
                             int tp, BatchState B, const int* __restrict__ stepped) {
+  const double* r_cur;
+  double* r_next;
+  b_iter_ptrs(bi, r_cur, r_next);
+  (void)r_cur;
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < len;
        k += (long long)gridDim.x * blockDim.x) {
     const int t = (int)(k % tp);
@@ -794,12 +824,13 @@ __global__ void kb_scalars_b(BatchState B) {
 }
 
 // B: r_next = r + gamma q and the r.r leaves; one block per (leaf, group).
-__global__ void __launch_bounds__(256) kb_step_b(const double* __restrict__ q,
-                                                 const double* __restrict__ r_cur,
-                                                 double* __restrict__ r_next, long long d,
+__global__ void __launch_bounds__(256) kb_step_b(const double* __restrict__ q, BIter bi, long long d,
                                                  double* __restrict__ part, long long n_leaf,
                                                  int G, BatchState B) {
   extern __shared__ double sm[];
+  const double* r_cur;
+  double* r_next;
+  b_iter_ptrs(bi, r_cur, r_next);
   const long long lf = blockIdx.x / G;
   const int g = (int)(blockIdx.x - lf * G);
   const int lane = threadIdx.x & 31;
@@ -879,9 +910,13 @@ __global__ void kb_scalars_c(BatchState B) {
 // (t = j / ns, s = j % ns: its scalars stay in registers) and walks the rows
 // i = blockIdx.x, +gridDim.x, ...; for a fixed row the block's accesses to
 // the (row, task, shift) shift state are contiguous.
-__global__ void kb_step_c(const double* __restrict__ r_next, double* __restrict__ p,
+__global__ void kb_step_c(BIter bi, double* __restrict__ p,
                           double* __restrict__ bigp, double* __restrict__ sols, long long d,
                           BatchState B, const int* __restrict__ stepped) {
+  const double* r_cur;
+  double* r_next;
+  b_iter_ptrs(bi, r_cur, r_next);
+  (void)r_cur;
   const int tp = B.tp, ns = B.ns, tsn = tp * ns;
   for (int j = threadIdx.x; j < tsn; j += blockDim.x) {
     const int t = j / ns, s = j - t * ns;
@@ -916,6 +951,20 @@ __global__ void kb_end_iteration(BatchState B, const int* __restrict__ stepped,
   if (t >= B.tp) return;
   if (stepped[t] && (B.n_active[t] == 0 || B.iter[t] >= B.max_iter)) B.finished[t] = 1;
   if (b_live(B, t)) atomicAdd(n_live, 1);
+}
+
+// End of a loop iteration: advance the device iteration, decide whether
+// another one runs (a live task and budget left) and reset the live count.
+// In the captured loop the decision is the WHILE node's condition; the
+// eager loop reads *keep.
+__global__ void kb_loop_next(int* __restrict__ n_live, long long* __restrict__ itp, long long max_iter,
+                             int* __restrict__ keep_out, unsigned long long cond_handle, int use_cond) {
+  const long long it = *itp + 1;
+  *itp = it;
+  const int keep = (*n_live > 0 && it < max_iter) ? 1 : 0;
+  *n_live = 0;
+  *keep_out = keep;
+  if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond_handle, (unsigned)keep);
 }
 
 // After the loop: still-active shifts report |zeta| sqrt(rr) (krylov.py:272-275).

@@ -2539,8 +2539,8 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   bb.xpart.ensure(std::max(1LL, c->xh_nslots * ND));
   bb.opart.ensure(std::max(1LL, nlN * ND * ns));
   bb.scal.ensure(15 * ND);
-  bb.lscal.ensure(2 * ND);
-  bb.iscal.ensure(5 * ND + 1);
+  bb.lscal.ensure(2 * ND + 1);
+  bb.iscal.ensure(5 * ND + 2);
   bb.sh_d.ensure(9 * ND * ns);
   bb.sh_l.ensure(ND * ns);
   bb.sh_u.ensure(4 * ND * ns);
@@ -2735,10 +2735,18 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
     tr.mark("batch: setup");
   }
 
-  // ---- the shifted-CG loop (krylov.py:210-270), all live tasks in step
-  for (long long it = 0; it < max_iter; ++it) {
-    double* r_cur = basis ? bb.RB.ptr + it * d * ND : ((it & 1) ? bb.R1.ptr : bb.R0.ptr);
-    double* r_nxt = basis ? bb.RB.ptr + (it + 1) * d * ND : ((it & 1) ? bb.R0.ptr : bb.R1.ptr);
+  // ---- the shifted-CG loop (krylov.py:210-270), all live tasks in step.
+  // The iteration index lives on the device (kb_loop_next), so the body is
+  // the same launches every time: it runs as a CUDA graph whose conditional
+  // WHILE node repeats it until no task is live or max_iter is reached (no
+  // host round trip per iteration), or eagerly from a host loop
+  // (FSDA_B200_EAGER=1 / fsda_set_eager, or no conditional-node support).
+  long long* loop_it = bb.lscal.ptr + 2 * ND;
+  int* keep = n_live + 1;
+  BIter bi{bb.RB.ptr, bb.R0.ptr, bb.R1.ptr, d * ND, basis ? 1 : 0, loop_it};
+  CK(cudaMemsetAsync(loop_it, 0, sizeof(long long), st));
+  CK(cudaMemsetAsync(n_live, 0, sizeof(int), st));
+  auto body = [&](unsigned long long handle, int use_cond) {
     rows_x(bb.P.ptr, bb.Y.ptr);                                // K1  y = X p
     smoother(bb.Y.ptr, bb.Z.ptr);                              // K2  z = M y
     xt(bb.Z.ptr, bb.Q.ptr, 0);                                 // K3  q = X^T z
@@ -2754,8 +2762,7 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
     kb_scalars_b<<<tb, 128, 0, st>>>(B);
     CKL();
     if (nlD) {
-      kb_step_b<<<(unsigned)(nlD * G), 256, sm_dot, st>>>(bb.Q.ptr, r_cur, r_nxt, d, bb.partD.ptr, nlD,
-                                                          G, B);
+      kb_step_b<<<(unsigned)(nlD * G), 256, sm_dot, st>>>(bb.Q.ptr, bi, d, bb.partD.ptr, nlD, G, B);
       CKL();
       combine(bb.partD.ptr, nlD, B.rr_new);
     } else {
@@ -2766,24 +2773,79 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
     kb_mark_stepped<<<tb, 128, 0, st>>>(B, stepped);
     CKL();
     if (basis) {
-      kb_step_c_p<<<vblocks, 256, 0, st>>>(r_nxt, bb.P.ptr, d * ND, tp, B, stepped);
+      kb_step_c_p<<<vblocks, 256, 0, st>>>(bi, bb.P.ptr, d * ND, tp, B, stepped);
       CKL();
-      kb_coef_update<<<dim3((unsigned)cdiv(it + 2, 256), (unsigned)(ND * ns)), 256, 0, st>>>(
-          B, stepped, bb.CA.ptr, bb.CC.ptr, bslots, it);
+      kb_coef_update<<<dim3((unsigned)cdiv(bslots + 1, 256), (unsigned)(ND * ns)), 256, 0, st>>>(
+          B, stepped, bb.CA.ptr, bb.CC.ptr, bslots, loop_it);
       CKL();
     } else {
-      kb_step_c<<<srows, sblk, 0, st>>>(r_nxt, bb.P.ptr, bb.BIGP.ptr, bb.SOLS.ptr, d, B, stepped);
+      kb_step_c<<<srows, sblk, 0, st>>>(bi, bb.P.ptr, bb.BIGP.ptr, bb.SOLS.ptr, d, B, stepped);
       CKL();
     }
-    CK(cudaMemsetAsync(n_live, 0, sizeof(int), st));
     kb_end_iteration<<<tb, 128, 0, st>>>(B, stepped, n_live);
     CKL();
-    int h_live = 0;
-    CK(cudaMemcpyAsync(&h_live, n_live, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (h_live == 0) break;
+    kb_loop_next<<<1, 1, 0, st>>>(n_live, loop_it, max_iter, keep, handle, use_cond);
+    CKL();
+  };
+  cudaGraphExec_t loop_exec = nullptr;
+  cudaGraph_t loop_graph = nullptr;
+  bool looped = max_iter <= 0;
+  if (!looped && c->cond_supported && !c->eager) {
+    try {
+      CK(cudaGraphCreate(&loop_graph, 0));
+      cudaGraphConditionalHandle handle;
+      CK(cudaGraphConditionalHandleCreate(&handle, loop_graph, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = handle;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t cond_node;
+      CK(cudaGraphAddNode(&cond_node, loop_graph, nullptr, 0, &cp));
+      CK(cudaStreamBeginCaptureToGraph(st, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                       cudaStreamCaptureModeThreadLocal));
+      try {
+        body((unsigned long long)handle, 1);
+      } catch (...) {
+        cudaGraph_t g2;
+        cudaStreamEndCapture(st, &g2);
+        throw;
+      }
+      cudaGraph_t body_out;
+      CK(cudaStreamEndCapture(st, &body_out));
+      CK(cudaGraphInstantiate(&loop_exec, loop_graph, 0));
+      CK(cudaGraphLaunch(loop_exec, st));
+      looped = true;
+    } catch (CudaError& ce) {
+      if (loop_exec) cudaGraphExecDestroy(loop_exec);
+      if (loop_graph) cudaGraphDestroy(loop_graph);
+      loop_exec = nullptr;
+      loop_graph = nullptr;
+      if (ce.err != cudaErrorNotSupported && ce.err != cudaErrorCallRequiresNewerDriver) throw;
+      cudaGetLastError();
+      c->cond_supported = false;  // the eager loop below
+    }
   }
-
+  if (!looped) {
+    for (long long it = 0; it < max_iter; ++it) {
+      body(0ULL, 0);
+      int h_keep = 0;
+      CK(cudaMemcpyAsync(&h_keep, keep, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (!h_keep) break;
+    }
+  }
+  struct LoopGraphGuard {
+    cudaGraphExec_t& e;
+    cudaGraph_t& g;
+    cudaStream_t s;
+    ~LoopGraphGuard() {
+      if (e || g) cudaStreamSynchronize(s);
+      if (e) cudaGraphExecDestroy(e);
+      if (g) cudaGraphDestroy(g);
+    }
+  } loop_guard{loop_exec, loop_graph, st};
+  if (tr.on) CK(cudaStreamSynchronize(st));
   if (tr.on) tr.mark("batch: iterations");
   // ---- tail: directions (deferred mode), residuals, projections, orientation
   // (sda.py:265-284)

@@ -109,3 +109,28 @@ def test_batch_rejects_one_class_task():
     sets[1][sets[1] == -1] = 1
     with pytest.raises(ValueError, match="both classes"):
         fb.solve_label_sets(x, lap, sets, w.alpha, w.betas, w.tol, 5)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_batch_graph_loop_equals_eager_loop(mode):
+    """The batch loop runs as a CUDA graph with a conditional WHILE node (the
+    iteration index lives on the device); the eager host loop launches the
+    same body.  Equal bit for bit, with tasks finishing early (the WHILE
+    condition ends the loop once no task is live, before max_iter)."""
+    w = make_workload("cfg1", n=800, d=300, ell=200, n_pos=60, lam=6.0, k=4, n_shifts=5,
+                      beta_lo=1.0, beta_hi=1e4)
+    x, lap = _mats(w)
+    sets = _masks(w.n, 5, 200, 60, seed=2)
+    probes = np.stack([np.random.default_rng(s).uniform(-1, 1, w.d) for s in range(5)])
+    out = []
+    for eager in (False, True):
+        dev = fb.Device(0)
+        dev.set_shift_update_mode(mode)
+        dev.set_eager(eager)
+        dev.upload_x(x)
+        dev.upload_laplacian(lap)
+        out.append(dev.solve_batch(sets, w.alpha, w.betas, 1e-3, 400, probes))
+        assert dev.last_shift_update_mode == mode
+    assert max(r.n_applies for r in out[0]) < 400      # the loop stopped on the device flag
+    for a, b in zip(*out):
+        _same(a, b)

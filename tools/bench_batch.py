@@ -54,8 +54,9 @@ napp = [r.n_applies for r in res]
 
 seq_el = 0.0
 S = min(args.seq_tasks, T)
-dev.set_label_mask(masks[0])          # warm: graph capture of the single-task solve
-dev.solve_fsda(w.alpha, w.betas, w.tol, w.max_iter, probes[0], scores=False)
+if S:
+    dev.set_label_mask(masks[0])      # warm: graph capture of the single-task solve
+    dev.solve_fsda(w.alpha, w.betas, w.tol, w.max_iter, probes[0], scores=False)
 for t in range(S):
     dev.set_label_mask(masks[t])
     t0 = time.perf_counter()
@@ -67,7 +68,8 @@ out = {
     "workload": args.workload, "tasks": T, "n_shifts": int(w.betas.size), "max_iter": w.max_iter,
     "n_applies": [min(napp), max(napp)],
     "batch_s": best, "batch_task_solves_per_s": T / best,
-    "sequential_task_s": seq_el / S, "sequential_task_solves_per_s": S / seq_el,
-    "speedup": (T / best) / (S / seq_el), "bitwise_equal_tasks_checked": S,
+    "sequential_task_s": seq_el / S if S else None,
+    "sequential_task_solves_per_s": S / seq_el if S else None,
+    "speedup": (T / best) / (S / seq_el) if S else None, "bitwise_equal_tasks_checked": S,
 }
 print(json.dumps(out))

@@ -24,6 +24,19 @@ constexpr int BG = 32;  // tasks per group (one per lane)
 #ifndef GATHER_MLP
 #define GATHER_MLP 8        // row gathers in flight per lane (16: same speed, spills)
 #endif
+// minimum CTAs per SM (register caps) of the batch gather kernels
+#ifndef KB_XROWS_MINB
+#define KB_XROWS_MINB 4
+#endif
+#ifndef KB_LROWS_MINB
+#define KB_LROWS_MINB 4
+#endif
+#ifndef KB_COLS_MINB
+#define KB_COLS_MINB 4
+#endif
+#ifndef F32_LS
+#define F32_LS 4            // fp32 storage: lane pairs in flight per step (8 spills at 64 registers)
+#endif
 
 // Per-task scalars (index t) and per-(task, shift) state (index t * ns + s).
 struct BatchState {
@@ -117,6 +130,19 @@ __device__ __forceinline__ double emu_dot_leaf(int n, XY xy) {
   return tree32(A);
 }
 
+// Gathered-value terms: special(idx) marks the one index treated differently
+// (the diagonal of a Laplacian row), operator()(is_special, v) maps the value.
+struct TermPlain {
+  __device__ __forceinline__ bool special(int) const { return false; }
+  __device__ __forceinline__ double operator()(bool, double v) const { return v; }
+};
+struct TermLap {  // (L y)_i terms: d_i y_i on the diagonal, -y_j off it
+  int row;
+  double dg;
+  __device__ __forceinline__ bool special(int idx) const { return idx == row; }
+  __device__ __forceinline__ double operator()(bool sp, double v) const { return sp ? dg * v : -v; }
+};
+
 // Canonical leaf of a gathered index segment: ind[s0, s0 + len) (len <= 256)
 // selects rows of src (task-minor); term(idx, v) maps the gathered value.
 // The canonical lane accumulators A[l] = sum_k v[l + 32 k] are built in pairs
@@ -124,9 +150,9 @@ __device__ __forceinline__ double emu_dot_leaf(int n, XY xy) {
 // butterfly step — so only 16 partial sums stay live (register budget: three
 // 256-thread CTAs per SM).  Indices arrive 32 at a time (coalesced) and are
 // shuffled to every lane; GATHER_MLP values per lane are in flight.
-template <int LS, typename Term>
+template <int LS, typename V, typename Term>
 __device__ __forceinline__ double emu_gather_leaf_ls(const int* __restrict__ ind, long long s0, int len,
-                                                     const double* __restrict__ src, int tp, int t,
+                                                     const V* __restrict__ src, int tp, int t,
                                                      int lane, Term term) {
   const int nk = (len + 31) >> 5;     // <= 8 index chunks
   int my[8];
@@ -141,18 +167,40 @@ __device__ __forceinline__ double emu_gather_leaf_ls(const int* __restrict__ ind
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       if (k >= nk) break;
-      double v1[LS], v2[LS];
+      if (sizeof(V) == 8) {
+        double v1[LS], v2[LS];
 #pragma unroll
-      for (int q = 0; q < LS; ++q) {
-        const int l = l0 + q;
-        const int i1 = __shfl_sync(FULL, my[k], l), i2 = __shfl_sync(FULL, my[k], l + 16);
-        v1[q] = (32 * k + l < len) ? term(i1, __ldg(src + (long long)i1 * tp + t)) : 0.0;
-        v2[q] = (32 * k + l + 16 < len) ? term(i2, __ldg(src + (long long)i2 * tp + t)) : 0.0;
-      }
+        for (int q = 0; q < LS; ++q) {
+          const int l = l0 + q;
+          const int i1 = __shfl_sync(FULL, my[k], l), i2 = __shfl_sync(FULL, my[k], l + 16);
+          v1[q] = (32 * k + l < len) ? term(term.special(i1), (double)__ldg(src + (long long)i1 * tp + t)) : 0.0;
+          v2[q] = (32 * k + l + 16 < len) ? term(term.special(i2), (double)__ldg(src + (long long)i2 * tp + t)) : 0.0;
+        }
 #pragma unroll
-      for (int q = 0; q < LS; ++q) {
-        if (32 * k + l0 + q < len) a1[q] = a1[q] + v1[q];
-        if (32 * k + l0 + q + 16 < len) a2[q] = a2[q] + v2[q];
+        for (int q = 0; q < LS; ++q) {
+          if (32 * k + l0 + q < len) a1[q] = a1[q] + v1[q];
+          if (32 * k + l0 + q + 16 < len) a2[q] = a2[q] + v2[q];
+        }
+      } else {
+        // fp32 storage: the loads stay floats until they are summed (half
+        // the registers per gather in flight); the term's special-index test
+        // is kept as a bit mask
+        V v1[LS], v2[LS];
+        unsigned sp1 = 0u, sp2 = 0u;
+#pragma unroll
+        for (int q = 0; q < LS; ++q) {
+          const int l = l0 + q;
+          const int i1 = __shfl_sync(FULL, my[k], l), i2 = __shfl_sync(FULL, my[k], l + 16);
+          v1[q] = (32 * k + l < len) ? __ldg(src + (long long)i1 * tp + t) : (V)0;
+          v2[q] = (32 * k + l + 16 < len) ? __ldg(src + (long long)i2 * tp + t) : (V)0;
+          sp1 |= term.special(i1) ? (1u << q) : 0u;
+          sp2 |= term.special(i2) ? (1u << q) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < LS; ++q) {
+          if (32 * k + l0 + q < len) a1[q] = a1[q] + term((sp1 >> q) & 1u, (double)v1[q]);
+          if (32 * k + l0 + q + 16 < len) a2[q] = a2[q] + term((sp2 >> q) & 1u, (double)v2[q]);
+        }
       }
     }
 #pragma unroll
@@ -170,19 +218,20 @@ __device__ __forceinline__ double emu_gather_leaf_ls(const int* __restrict__ ind
 // steps are latency rounds with little else to overlap: it takes 8 pairs per
 // step (2 rounds instead of 4); longer segments keep GATHER_MLP.  Same
 // accumulation order either way.
-template <typename Term>
+template <typename V, typename Term>
 __device__ __forceinline__ double emu_gather_leaf(const int* __restrict__ ind, long long s0, int len,
-                                                  const double* __restrict__ src, int tp, int t,
+                                                  const V* __restrict__ src, int tp, int t,
                                                   int lane, Term term) {
-  if (len <= 32) return emu_gather_leaf_ls<8>(ind, s0, len, src, tp, t, lane, term);
-  return emu_gather_leaf_ls<GATHER_MLP / 2>(ind, s0, len, src, tp, t, lane, term);
+  constexpr int LS = sizeof(V) == 4 ? F32_LS : GATHER_MLP / 2;
+  if (len <= 32) return emu_gather_leaf_ls<8, V>(ind, s0, len, src, tp, t, lane, term);
+  return emu_gather_leaf_ls<LS, V>(ind, s0, len, src, tp, t, lane, term);
 }
 
 // Segments longer than 256 entries: R256 over their leaves (two levels,
 // n <= 65536).  Kept out of line: it holds a second accumulator set.
-template <typename Term>
+template <typename V, typename Term>
 __device__ __noinline__ double emu_gather_long(const int* __restrict__ ind, long long start, int n,
-                                               const double* __restrict__ src, int tp, int t,
+                                               const V* __restrict__ src, int tp, int t,
                                                int lane, Term term) {
   const int m = (n + LEAF - 1) / LEAF;  // <= 256 (host-checked)
   double P[32];
@@ -201,9 +250,9 @@ __device__ __noinline__ double emu_gather_long(const int* __restrict__ ind, long
   return tree32(P);
 }
 
-template <typename Term>
+template <typename V, typename Term>
 __device__ __forceinline__ double emu_segment(const int* __restrict__ ind, long long start, int n,
-                                              const double* __restrict__ src, int tp, int t,
+                                              const V* __restrict__ src, int tp, int t,
                                               int lane, Term term) {
   if (n <= LEAF) return emu_gather_leaf(ind, start, n, src, tp, t, lane, term);
   return emu_gather_long(ind, start, n, src, tp, t, lane, term);
@@ -270,11 +319,11 @@ __global__ void kb_reset(BatchState B, int T, double tol) {
 
 // Row sums over a CSR pattern for every task: K1 (y = X p) and K2 (z = M y).
 // One warp per (row, task group).
-template <int KIND>
-__global__ void __launch_bounds__(256, 4) kb_rows(const int* __restrict__ rowptr,
+template <int KIND, typename V>
+__global__ void __launch_bounds__(256, KIND == SEG_LROWS ? KB_LROWS_MINB : KB_XROWS_MINB) kb_rows(const int* __restrict__ rowptr,
                                                const int* __restrict__ cols,
-                                               const double* __restrict__ src,
-                                               double* __restrict__ out, long long n_rows, int G,
+                                               const V* __restrict__ src,
+                                               V* __restrict__ out, long long n_rows, int G,
                                                int tp, const double* __restrict__ ldiag,
                                                const signed char* __restrict__ lab, double alpha,
                                                int alpha_mode) {
@@ -288,23 +337,23 @@ __global__ void __launch_bounds__(256, 4) kb_rows(const int* __restrict__ rowptr
   double s;
   if (KIND == SEG_LROWS) {
     const double dg = __ldg(ldiag + i);
-    s = emu_segment(cols, lo, n, src, tp, t, lane,
-                    [&](int idx, double v) { return idx == (int)i ? dg * v : -v; });
-    const double masked = lab[i * tp + t] != 0 ? src[i * tp + t] : 0.0;
+    s = emu_segment(cols, lo, n, src, tp, t, lane, TermLap{(int)i, dg});
+    const double masked = lab[i * tp + t] != 0 ? (double)src[i * tp + t] : 0.0;
     const double smoothed = alpha * s;
     s = (alpha_mode == 1) ? smoothed : (1.0 - alpha) * masked + smoothed;
   } else {
-    s = emu_segment(cols, lo, n, src, tp, t, lane, [](int, double v) { return v; });
+    s = emu_segment(cols, lo, n, src, tp, t, lane, TermPlain{});
   }
-  out[i * tp + t] = s;
+  out[i * tp + t] = (V)s;
 }
 
 // z = masked y (apply_smoother at alpha == 0).
-__global__ void kb_mask(const double* __restrict__ y, const signed char* __restrict__ lab,
-                        double* __restrict__ z, long long len) {
+template <typename V>
+__global__ void kb_mask(const V* __restrict__ y, const signed char* __restrict__ lab,
+                        V* __restrict__ z, long long len) {
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < len;
        k += (long long)gridDim.x * blockDim.x)
-    z[k] = lab[k] != 0 ? y[k] : 0.0;
+    z[k] = lab[k] != 0 ? y[k] : (V)0;
 }
 
 // Column finish of X^T: mode 0 raw, 1 centred (s - mu * sum_v[t]), 2 / ell[t].
@@ -318,7 +367,8 @@ __device__ __forceinline__ double b_col_finish(double s, int mode, long long c, 
 
 // X^T columns with n <= 256: the class tasks of the single-task column plan
 // (any class: each entry is one column segment).  One warp per (entry, group).
-__global__ void __launch_bounds__(256, 4) kb_cols_light(SegPlan pl, const double* __restrict__ src,
+template <typename V>
+__global__ void __launch_bounds__(256, KB_COLS_MINB) kb_cols_light(SegPlan pl, const V* __restrict__ src,
                                                      double* __restrict__ out, int G, int tp,
                                                      int mode, const double* __restrict__ mu,
                                                      BatchState B) {
@@ -330,15 +380,16 @@ __global__ void __launch_bounds__(256, 4) kb_cols_light(SegPlan pl, const double
   const int g = (int)(w - e * G);
   const int t = g * BG + lane;
   const int4 tk = __ldg(pl.tasks + e);
-  const double s = emu_gather_leaf(pl.ind, tk.y, tk.z, src, tp, t, lane, [](int, double v) { return v; });
+  const double s = emu_gather_leaf(pl.ind, tk.y, tk.z, src, tp, t, lane, TermPlain{});
   out[(long long)tk.x * tp + t] = b_col_finish(s, mode, tk.x, t, tp, mu, B);
 }
 
 // Leaf sums of the long columns: the heavy leaves (plan_xc heavy tasks, up to
 // 4 leaves each) into hpart[slot][TP], and the blocked slices (XtDense tasks,
 // one <= 256-entry leaf each) into xpart[slot][TP].
-__global__ void __launch_bounds__(256, 4) kb_cols_leaves(SegPlan pl, XtDense dn,
-                                                      const double* __restrict__ src,
+template <typename V>
+__global__ void __launch_bounds__(256, KB_COLS_MINB) kb_cols_leaves(SegPlan pl, XtDense dn,
+                                                      const V* __restrict__ src,
                                                       double* __restrict__ hpart,
                                                       double* __restrict__ xpart, long long n_hleaf,
                                                       long long n_xtask, int G, int tp) {
@@ -357,12 +408,11 @@ __global__ void __launch_bounds__(256, 4) kb_cols_leaves(SegPlan pl, XtDense dn,
     const int h = tk.w;
     const int slot = __ldg(pl.heavy_seg0 + h) + (tk.y - __ldg(pl.heavy_start + h)) / LEAF + lf;
     const double v = emu_gather_leaf(pl.ind, tk.y + lf * LEAF, min(LEAF, tk.z - lf * LEAF), src,
-                                     tp, t, lane, [](int, double x) { return x; });
+                                     tp, t, lane, TermPlain{});
     hpart[(long long)slot * tp + t] = v;
   } else {
     const int4 tk = __ldg(dn.tasks + (u - n_hleaf));
-    const double v = emu_gather_leaf(dn.rows, tk.y, tk.z, src, tp, t, lane,
-                                     [](int, double x) { return x; });
+    const double v = emu_gather_leaf(dn.rows, tk.y, tk.z, src, tp, t, lane, TermPlain{});
     xpart[(long long)tk.x * tp + t] = v;
   }
 }
@@ -418,39 +468,39 @@ __device__ __forceinline__ double emu_partials(const double* __restrict__ part, 
   return emu_part_long(part, m, tp, t);
 }
 
-// Block-level canonical leaves: 8 warps stage the (up to) 256 rows of a leaf
-// in shared memory — warp w takes rows l + 32 w — and warp 0 folds them in
-// canonical order: A[l] = sum over w of row l + 32 w, then tree32.  sm holds
-// 2 x 8 x 32 x 32 doubles (x and y of a dot leaf; y unused for sums).
-constexpr int BLK_SM = 2 * 8 * 32 * 32;
+// Block-level canonical leaves over (up to) 256 task-minor rows: warp w owns
+// the canonical lanes l = 4w .. 4w + 3 and builds A[l] = sum over k of row
+// l + 32 k (k ascending from 0.0; fma for dot leaves) straight from global
+// memory — every row is one coalesced 256-byte load per warp, eight rows in
+// flight per lane.  The 32 lane sums go through 8 KB of shared memory to
+// warp 0, which folds them with tree32.  sm holds 32 x 32 doubles.
+constexpr int BLK_SM = 32 * 32;
 
 template <bool DOT, typename Load>
 __device__ __forceinline__ double block_leaf(int n, Load load, double* sm) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll 4
-  for (int l = 0; l < 32; ++l) {
-    const int e = l + 32 * w;
-    double x = 0.0, y = 0.0;
-    if (e < n) load(e, x, y);
-    sm[(w * 32 + l) * 32 + lane] = x;
-    if (DOT) sm[8 * 32 * 32 + (w * 32 + l) * 32 + lane] = y;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int l = 4 * w + j;
+    double x[8], y[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      x[k] = 0.0;
+      y[k] = 0.0;
+      if (l + 32 * k < n) load(l + 32 * k, x[k], y[k]);
+    }
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (l + 32 * k < n) a = DOT ? fma(x[k], y[k], a) : a + x[k];
+    sm[l * 32 + lane] = a;
   }
   __syncthreads();
   double r = 0.0;
   if (w == 0) {
     double A[32];
 #pragma unroll
-    for (int l = 0; l < 32; ++l) A[l] = 0.0;
-    for (int k = 0; k < 8; ++k) {
-      if (32 * k >= n) break;
-#pragma unroll
-      for (int l = 0; l < 32; ++l)
-        if (l + 32 * k < n) {
-          const double x = sm[(k * 32 + l) * 32 + lane];
-          if (DOT) A[l] = fma(x, sm[8 * 32 * 32 + (k * 32 + l) * 32 + lane], A[l]);
-          else A[l] = A[l] + x;
-        }
-    }
+    for (int l = 0; l < 32; ++l) A[l] = sm[l * 32 + lane];
     r = tree32(A);
   }
   __syncthreads();
@@ -541,13 +591,14 @@ __global__ void __launch_bounds__(256, 2) kb_cols_combine(SegPlan pl, XtDense dn
 // Leaf sums over a contiguous task-minor vector (len rows): kind 0 sum(v),
 // 1 sum over class +1 (off-class 0.0), 2 class -1, 3 fma dot v . v2.
 // One 256-thread block per (leaf, group).
-__global__ void __launch_bounds__(256) kb_vec_leaves(const double* __restrict__ v,
-                                                     const double* __restrict__ v2,
+template <typename V>
+__global__ void __launch_bounds__(256) kb_vec_leaves(const V* __restrict__ v,
+                                                     const V* __restrict__ v2,
                                                      const signed char* __restrict__ lab,
                                                      long long len, int kind,
                                                      double* __restrict__ part, long long n_leaf,
                                                      int G, int tp) {
-  extern __shared__ double sm[];
+  __shared__ double sm[BLK_SM];
   const long long lf = blockIdx.x / G;
   const int g = (int)(blockIdx.x - lf * G);
   const int lane = threadIdx.x & 31;
@@ -557,13 +608,13 @@ __global__ void __launch_bounds__(256) kb_vec_leaves(const double* __restrict__ 
   double s;
   if (kind == 3) {
     s = block_leaf<true>(n, [&](int e, double& x, double& y) {
-      x = v[(i0 + e) * tp + t];
-      y = v2[(i0 + e) * tp + t];
+      x = (double)v[(i0 + e) * tp + t];
+      y = (double)v2[(i0 + e) * tp + t];
     }, sm);
   } else {
     s = block_leaf<false>(n, [&](int e, double& x, double&) {
       const long long k = (i0 + e) * tp + t;
-      const double u = v[k];
+      const double u = (double)v[k];
       x = kind == 1 ? (lab[k] == 1 ? u : 0.0) : (kind == 2 ? (lab[k] == -1 ? u : 0.0) : u);
     }, sm);
   }
@@ -576,7 +627,7 @@ __global__ void __launch_bounds__(256) kb_vec_leaves(const double* __restrict__ 
 // partials exactly as the first level of R256 does.
 __global__ void __launch_bounds__(256) kb_combine_leaf(const double* __restrict__ part, int n,
                                                        double* __restrict__ out, int tp) {
-  extern __shared__ double sm[];
+  __shared__ double sm[BLK_SM];
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * BG + lane;
   const double s = block_leaf<false>(n, [&](int e, double& x, double&) { x = part[(long long)e * tp + t]; }, sm);
@@ -637,13 +688,14 @@ __global__ void kb_coef_init(double* __restrict__ coef_a, double* __restrict__ c
 }
 
 // r = p = b only (the deferred mode keeps no P / sols during the loop).
-__global__ void kb_cg_init_rp(const double* __restrict__ b, double* __restrict__ r,
-                              double* __restrict__ p, long long len) {
+template <typename V>
+__global__ void kb_cg_init_rp(const double* __restrict__ b, V* __restrict__ r,
+                              V* __restrict__ p, long long len) {
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < len;
        k += (long long)gridDim.x * blockDim.x) {
     const double v = b[k];
-    r[k] = v;
-    p[k] = v;
+    r[k] = (V)v;
+    p[k] = (V)v;
   }
 }
 
@@ -652,16 +704,20 @@ __global__ void kb_cg_init_rp(const double* __restrict__ b, double* __restrict__
 // the loop can run as a captured graph with a conditional WHILE node.  The
 // residual slots of iteration it: r_it / r_{it+1} of the deferred basis, or
 // the ping-pong pair of the per-iteration mode.
-struct BIter {
-  double* rb;            // deferred basis: slot j at rb + j * stride
-  double* r0;            // per-iteration mode: ping-pong residuals
-  double* r1;
+template <typename V>
+struct BIterT {
+  V* rb;                 // deferred basis: slot j at rb + j * stride
+  V* r0;                 // per-iteration mode: ping-pong residuals
+  V* r1;
   long long stride;      // d * TP
   int basis;
   const long long* it;   // loop iteration (device)
 };
 
-__device__ __forceinline__ void b_iter_ptrs(const BIter& bi, const double*& cur, double*& nxt) {
+using BIter = BIterT<double>;
+
+template <typename V>
+__device__ __forceinline__ void b_iter_ptrs(const BIterT<V>& bi, const V*& cur, V*& nxt) {
   const long long it = *bi.it;
   if (bi.basis) {
     cur = bi.rb + it * bi.stride;
@@ -699,23 +755,25 @@ __global__ void kb_coef_update(BatchState B, const int* __restrict__ stepped, do
 
 // p = r_next + alpha_new p for the tasks that stepped (kb_step_c without the
 // shift state).
-__global__ void kb_step_c_p(BIter bi, double* __restrict__ p, long long len,
+template <typename V>
+__global__ void kb_step_c_p(BIterT<V> bi, V* __restrict__ p, long long len,
                             int tp, BatchState B, const int* __restrict__ stepped) {
-  const double* r_cur;
-  double* r_next;
+  const V* r_cur;
+  V* r_next;
   b_iter_ptrs(bi, r_cur, r_next);
   (void)r_cur;
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < len;
        k += (long long)gridDim.x * blockDim.x) {
     const int t = (int)(k % tp);
-    if (stepped[t]) p[k] = r_next[k] + B.alpha_new[t] * p[k];
+    if (stepped[t]) p[k] = (V)((double)r_next[k] + B.alpha_new[t] * (double)p[k]);
   }
 }
 
 // sols[(i * tp + t) * ns + s] = sum_{j < iter_t} c[t][s][j] * r_j[i * tp + t],
 // j ascending from 0.0, one fma per term — the single solve's k_combine_basis
 // per task.
-__global__ void __launch_bounds__(256) kb_combine_basis(const double* __restrict__ rb, long long d,
+template <typename V>
+__global__ void __launch_bounds__(256) kb_combine_basis(const V* __restrict__ rb, long long d,
                                                         BatchState B, const double* __restrict__ coef_c,
                                                         long long ld, double* __restrict__ sols) {
   const int tp = B.tp, ns = B.ns;
@@ -730,7 +788,7 @@ __global__ void __launch_bounds__(256) kb_combine_basis(const double* __restrict
     for (int u = 0; u < 8; ++u) acc[u] = 0.0;
     const double* cc = coef_c + ((long long)t * ns + s0) * ld;
     for (long long j = 0; j < J; ++j) {
-      const double r = __ldcs(rb + j * stride + x);
+      const double r = (double)__ldcs(rb + j * stride + x);
 #pragma unroll
       for (int u = 0; u < 8; ++u)
         if (s0 + u < ns) acc[u] = fma(__ldg(cc + (long long)u * ld + j), r, acc[u]);
@@ -765,12 +823,13 @@ __global__ void kb_cg_init_scalars(BatchState B, const double* __restrict__ bb, 
 
 // A: centring q -= mu * sum(z) and the p.q leaves (fma); one 256-thread
 // block per (leaf, group).
+template <typename V>
 __global__ void __launch_bounds__(256) kb_step_a(double* __restrict__ q,
-                                                 const double* __restrict__ p,
+                                                 const V* __restrict__ p,
                                                  const double* __restrict__ mu, long long d,
                                                  double* __restrict__ part, long long n_leaf,
                                                  int G, BatchState B) {
-  extern __shared__ double sm[];
+  __shared__ double sm[BLK_SM];
   const long long lf = blockIdx.x / G;
   const int g = (int)(blockIdx.x - lf * G);
   const int lane = threadIdx.x & 31;
@@ -784,7 +843,7 @@ __global__ void __launch_bounds__(256) kb_step_a(double* __restrict__ q,
     const long long k = (i0 + e) * tp + t;
     const double qc = q[k] - mu[k] * sz;
     if (live) q[k] = qc;
-    x = p[k];
+    x = (double)p[k];
     y = qc;
   }, sm);
   if (threadIdx.x < 32 && live) part[lf * tp + t] = s;
@@ -824,12 +883,13 @@ __global__ void kb_scalars_b(BatchState B) {
 }
 
 // B: r_next = r + gamma q and the r.r leaves; one block per (leaf, group).
-__global__ void __launch_bounds__(256) kb_step_b(const double* __restrict__ q, BIter bi, long long d,
+template <typename V>
+__global__ void __launch_bounds__(256) kb_step_b(const double* __restrict__ q, BIterT<V> bi, long long d,
                                                  double* __restrict__ part, long long n_leaf,
                                                  int G, BatchState B) {
-  extern __shared__ double sm[];
-  const double* r_cur;
-  double* r_next;
+  __shared__ double sm[BLK_SM];
+  const V* r_cur;
+  V* r_next;
   b_iter_ptrs(bi, r_cur, r_next);
   const long long lf = blockIdx.x / G;
   const int g = (int)(blockIdx.x - lf * G);
@@ -842,10 +902,11 @@ __global__ void __launch_bounds__(256) kb_step_b(const double* __restrict__ q, B
   const double gamma = B.gamma[t];
   const double s = block_leaf<true>(n, [&](int e, double& x, double& y) {
     const long long k = (i0 + e) * tp + t;
-    const double rn = r_cur[k] + gamma * q[k];
-    if (live) r_next[k] = rn;
-    x = rn;
-    y = rn;
+    // rounded to storage once; the dot runs over the stored value
+    const V st = (V)((double)r_cur[k] + gamma * q[k]);
+    if (live) r_next[k] = st;
+    x = (double)st;
+    y = (double)st;
   }, sm);
   if (threadIdx.x < 32 && live) part[lf * tp + t] = s;
 }

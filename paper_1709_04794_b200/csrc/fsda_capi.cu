@@ -2449,7 +2449,12 @@ int fsda_sa_solve(fsda_ctx* c, double alpha, const double* betas, int ns, double
 
 // ---- multi-task batch (fsda_batch.cuh) -----------------------------------
 
-static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alpha,
+extern "C++" {
+// V: storage type of the loop vectors P, Y, Z and the residual slots (double,
+// or float after fsda_set_storage(32): sums, dots and scalars stay double —
+// the single solve's fp32-storage mode per task).
+template <typename V>
+static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
                             const double* betas, int ns, double tol, int64_t max_iter,
                             const double* probes, double* directions, double* scores,
                             double* residuals, int64_t* iterations, uint8_t* converged,
@@ -2512,14 +2517,19 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
     const double have = 8.0 * (double)(c->batch.RB.cap + c->batch.CA.cap + c->batch.CC.cap);
     bmode = need <= 0.4 * (double)free_b + have ? 2 : 1;
   }
-  if ((long long)tp * ns > 65535) bmode = 1;  // kb_coef_update's grid.y is one (task, shift)
+  constexpr bool V32 = sizeof(V) == 4;
+  if (V32) bmode = 2;  // as the single solve: fp32 storage keeps the residual basis
+  if ((long long)tp * ns > 65535) {  // kb_coef_update's grid.y is one (task, shift)
+    if (V32) return fail(FSDA_EINVAL, "fsda_solve_batch: fp32 storage supports at most 65535 (task, shift) pairs");
+    bmode = 1;
+  }
   c->su_mode = bmode;
   const bool basis = bmode == 2;
   bb.lab.ensure(n * ND);
   bb.ind.ensure(n * ND);
   for (DevBuf<double>* v : {&bb.P, &bb.Q, &bb.MU, &bb.Bv, &bb.PR}) v->ensure(std::max(1LL, d * ND));
   if (basis) {
-    bb.RB.ensure(std::max(1LL, bslots * d * ND));
+    bb.RB.ensure(std::max(1LL, V32 ? cdiv(bslots * d * ND, 2) : bslots * d * ND));
     bb.CA.ensure(std::max(1LL, bslots * ND * ns));
     bb.CC.ensure(std::max(1LL, bslots * ND * ns));
   } else {
@@ -2557,6 +2567,11 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
       (const double*)bb.raw.ptr, bb.PR.ptr, d, T, tp);
   CKL();
   CK(cudaMemcpyAsync(bb.betas.ptr, betas, sizeof(double) * ns, cudaMemcpyHostToDevice, st));
+  // loop vectors in storage type (the setup products use Y / Z as doubles)
+  V* const Pv = reinterpret_cast<V*>(bb.P.ptr);
+  V* const Yv = reinterpret_cast<V*>(bb.Y.ptr);
+  V* const Zv = reinterpret_cast<V*>(bb.Z.ptr);
+  V* const RBv = reinterpret_cast<V*>(bb.RB.ptr);
   BatchState B;
   double* sd = bb.scal.ptr;
   B.rr = sd; B.gamma_prev = sd + ND; B.alpha = sd + 2 * ND; B.b_norm = sd + 3 * ND;
@@ -2593,20 +2608,21 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   if (c->xh_nslots) CK(cudaMemsetAsync(bb.xpart.ptr, 0, sizeof(double) * c->xh_nslots * ND, st));
 
   auto grid_w = [](long long warps) { return (unsigned)std::max<long long>(1, cdiv(warps, 8)); };
-  auto rows_x = [&](const double* src, double* out) {
-    kb_rows<SEG_XROWS><<<grid_w(n * G), 256, 0, st>>>(c->x_rowptr.ptr, c->x_cols.ptr, src, out, n, G,
-                                                     tp, nullptr, nullptr, 0.0, 0);
+  auto rows_x = [&](auto* src, auto* out) {
+    using U = std::remove_cv_t<std::remove_pointer_t<decltype(out)>>;
+    kb_rows<SEG_XROWS, U><<<grid_w(n * G), 256, 0, st>>>(c->x_rowptr.ptr, c->x_cols.ptr, (const U*)src, out,
+                                                        n, G, tp, nullptr, nullptr, 0.0, 0);
     CKL();
   };
-  auto smoother = [&](const double* y, double* z) {
+  auto smoother = [&](auto* y, auto* z) {
+    using U = std::remove_cv_t<std::remove_pointer_t<decltype(z)>>;
     const int amode = alpha_mode_of(alpha);
-    if (amode == 0) {
-      kb_mask<<<(unsigned)std::min<long long>(cdiv(n * ND, 256), 65535LL * 4), 256, 0, st>>>(
-          y, bb.lab.ptr, z, n * ND);
-    } else {
-      kb_rows<SEG_LROWS><<<grid_w(n * G), 256, 0, st>>>(c->l_rowptr.ptr, c->l_cols.ptr, y, z, n, G,
-                                                       tp, c->l_diag.ptr, bb.lab.ptr, alpha, amode);
-    }
+    if (amode == 0)
+      kb_mask<U><<<(unsigned)std::min<long long>(cdiv(n * ND, 256), 65535LL * 4), 256, 0, st>>>(
+          (const U*)y, bb.lab.ptr, z, n * ND);
+    else
+      kb_rows<SEG_LROWS, U><<<grid_w(n * G), 256, 0, st>>>(c->l_rowptr.ptr, c->l_cols.ptr, (const U*)y, z, n,
+                                                          G, tp, c->l_diag.ptr, bb.lab.ptr, alpha, amode);
     CKL();
   };
   const SegPlan& pxc = c->plan_xc.pl;
@@ -2643,12 +2659,14 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
       CK(cudaMemcpyAsync(bb.gchunks.ptr, chunks.data(), sizeof(int2) * n_gchunks, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));  // the host vectors go out of scope
   }
-  auto xt = [&](const double* src, double* out, int mode) {
+  auto xt = [&](auto* src_any, double* out, int mode) {
+    using U = std::remove_cv_t<std::remove_pointer_t<decltype(src_any)>>;
+    const U* src = src_any;
     if (n_light)
-      kb_cols_light<<<grid_w(n_light * G), 256, 0, st>>>(pxc, src, out, G, tp, mode, bb.MU.ptr, B);
+      kb_cols_light<U><<<grid_w(n_light * G), 256, 0, st>>>(pxc, src, out, G, tp, mode, bb.MU.ptr, B);
     CKL();
     if (n_htask || c->xh_ntasks) {
-      kb_cols_leaves<<<grid_w((4 * n_htask + c->xh_ntasks) * G), 256, 0, st>>>(
+      kb_cols_leaves<U><<<grid_w((4 * n_htask + c->xh_ntasks) * G), 256, 0, st>>>(
           pxc, c->xh, src, bb.hpart.ptr, bb.xpart.ptr, 4 * n_htask, c->xh_ntasks, G, tp);
       CKL();
       if (n_gchunks) {
@@ -2663,22 +2681,15 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
       CKL();
     }
   };
-  if (!c->batch_attrs_set) {  // per context: the attribute binds to the current device
-    const int big = (int)(sizeof(double) * BLK_SM);
-    CK(cudaFuncSetAttribute(kb_vec_leaves, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CK(cudaFuncSetAttribute(kb_step_a, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CK(cudaFuncSetAttribute(kb_step_b, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CK(cudaFuncSetAttribute(kb_combine_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, big / 2));
-    c->batch_attrs_set = true;
-  }
-  const size_t sm_dot = sizeof(double) * BLK_SM, sm_sum = sm_dot / 2;
+  // the block-level leaves use 8 KB of static shared memory
+  const size_t sm_dot = 0, sm_sum = 0;
   auto combine = [&](const double* part, long long nl, double* out) {
     // R256 over nl <= 65536 partials: level 1 (runs of 256) by kb_vec_leaves,
     // the last level by kb_combine_leaf
     if (nl > LEAF) {
       const long long m2 = cdiv(nl, LEAF);
-      kb_vec_leaves<<<(unsigned)(m2 * G), 256, sm_sum, st>>>(part, nullptr, nullptr, nl, 0,
-                                                             bb.part2.ptr, m2, G, tp);
+      kb_vec_leaves<double><<<(unsigned)(m2 * G), 256, sm_sum, st>>>(part, nullptr, nullptr, nl, 0,
+                                                                     bb.part2.ptr, m2, G, tp);
       CKL();
       part = bb.part2.ptr;
       nl = m2;
@@ -2686,15 +2697,17 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
     kb_combine_leaf<<<G, 256, sm_sum, st>>>(part, (int)nl, out, tp);
     CKL();
   };
-  auto vec_sum = [&](const double* v, const double* v2, int kind, long long len, double* part,
+  auto vec_sum = [&](auto* v_any, decltype(v_any) v2, int kind, long long len, double* part,
                      double* out) {
+    using U = std::remove_cv_t<std::remove_pointer_t<decltype(v_any)>>;
+    const U* v = v_any;
     const long long nl = n_leaves(len);
     if (nl == 0) {
       CK(cudaMemsetAsync(out, 0, sizeof(double) * ND, st));
       return;
     }
-    kb_vec_leaves<<<(unsigned)(nl * G), 256, kind == 3 ? sm_dot : sm_sum, st>>>(
-        v, v2, bb.lab.ptr, len, kind, part, nl, G, tp);
+    kb_vec_leaves<U><<<(unsigned)(nl * G), 256, kind == 3 ? sm_dot : sm_sum, st>>>(
+        v, (const U*)v2, bb.lab.ptr, len, kind, part, nl, G, tp);
     CKL();
     combine(part, nl, out);
   };
@@ -2702,14 +2715,14 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   // ---- setup (sda.py:297-301, krylov.py:185-208), per task
   xt(bb.ind.ptr, bb.MU.ptr, 2);                       // mu = X^T 1_l / l
   rows_x(bb.PR.ptr, bb.Y.ptr);                        // t = X r
-  vec_sum(bb.Y.ptr, nullptr, 1, n, bb.partN.ptr, B.pq);
-  vec_sum(bb.Y.ptr, nullptr, 2, n, bb.partN.ptr, B.rr_new);
+  vec_sum(bb.Y.ptr, (double*)nullptr, 1, n, bb.partN.ptr, B.pq);
+  vec_sum(bb.Y.ptr, (double*)nullptr, 2, n, bb.partN.ptr, B.rr_new);
   kb_class_means<<<tb, 128, 0, st>>>(B, B.pq, B.rr_new);
   CKL();
   kb_apply_w<<<(unsigned)std::min<long long>(cdiv(n * ND, 256), 65535LL * 4), 256, 0, st>>>(
       bb.lab.ptr, bb.Z.ptr, n * ND, tp, B);
   CKL();
-  vec_sum(bb.Z.ptr, nullptr, 0, n, bb.partN.ptr, B.sum_v);   // sum(w)
+  vec_sum(bb.Z.ptr, (double*)nullptr, 0, n, bb.partN.ptr, B.sum_v);   // sum(w)
   xt(bb.Z.ptr, bb.Bv.ptr, 1);                                // b = X^T w - mu sum(w)
   // threads per block: the (task, shift) pairs split evenly over <= 1024 threads
   const long long tsn = ND * ns, passes = cdiv(tsn, 1024);
@@ -2717,7 +2730,7 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   const unsigned srows = (unsigned)std::max<long long>(1, std::min<long long>(d, (long long)c->num_sms * 8));
   const unsigned vblocks = (unsigned)std::max<long long>(1, std::min<long long>(cdiv(d * ND, 256), (long long)c->num_sms * 16));
   if (basis) {
-    kb_cg_init_rp<<<vblocks, 256, 0, st>>>(bb.Bv.ptr, bb.RB.ptr, bb.P.ptr, d * ND);
+    kb_cg_init_rp<V><<<vblocks, 256, 0, st>>>(bb.Bv.ptr, RBv, Pv, d * ND);
     CKL();
     kb_coef_init<<<(unsigned)std::min<long long>(cdiv(bslots * ND * ns, 256), 4096), 256, 0, st>>>(
         bb.CA.ptr, bb.CC.ptr, ND * ns, bslots);
@@ -2743,17 +2756,18 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   // (FSDA_B200_EAGER=1 / fsda_set_eager, or no conditional-node support).
   long long* loop_it = bb.lscal.ptr + 2 * ND;
   int* keep = n_live + 1;
-  BIter bi{bb.RB.ptr, bb.R0.ptr, bb.R1.ptr, d * ND, basis ? 1 : 0, loop_it};
+  BIterT<V> bi{RBv, reinterpret_cast<V*>(bb.R0.ptr), reinterpret_cast<V*>(bb.R1.ptr), d * ND, basis ? 1 : 0,
+               loop_it};
   CK(cudaMemsetAsync(loop_it, 0, sizeof(long long), st));
   CK(cudaMemsetAsync(n_live, 0, sizeof(int), st));
   auto body = [&](unsigned long long handle, int use_cond) {
-    rows_x(bb.P.ptr, bb.Y.ptr);                                // K1  y = X p
-    smoother(bb.Y.ptr, bb.Z.ptr);                              // K2  z = M y
-    xt(bb.Z.ptr, bb.Q.ptr, 0);                                 // K3  q = X^T z
-    vec_sum(bb.Z.ptr, nullptr, 0, n, bb.partN.ptr, B.sum_v);   //     sum(z)
+    rows_x(Pv, Yv);                                            // K1  y = X p
+    smoother(Yv, Zv);                                          // K2  z = M y
+    xt(Zv, bb.Q.ptr, 0);                                       // K3  q = X^T z
+    vec_sum(Zv, (V*)nullptr, 0, n, bb.partN.ptr, B.sum_v);     //     sum(z)
     if (nlD) {
-      kb_step_a<<<(unsigned)(nlD * G), 256, sm_dot, st>>>(bb.Q.ptr, bb.P.ptr, bb.MU.ptr, d, bb.partD.ptr,
-                                                          nlD, G, B);
+      kb_step_a<V><<<(unsigned)(nlD * G), 256, sm_dot, st>>>(bb.Q.ptr, Pv, bb.MU.ptr, d, bb.partD.ptr,
+                                                             nlD, G, B);
       CKL();
       combine(bb.partD.ptr, nlD, B.pq);
     } else {
@@ -2762,7 +2776,7 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
     kb_scalars_b<<<tb, 128, 0, st>>>(B);
     CKL();
     if (nlD) {
-      kb_step_b<<<(unsigned)(nlD * G), 256, sm_dot, st>>>(bb.Q.ptr, bi, d, bb.partD.ptr, nlD, G, B);
+      kb_step_b<V><<<(unsigned)(nlD * G), 256, sm_dot, st>>>(bb.Q.ptr, bi, d, bb.partD.ptr, nlD, G, B);
       CKL();
       combine(bb.partD.ptr, nlD, B.rr_new);
     } else {
@@ -2773,14 +2787,16 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
     kb_mark_stepped<<<tb, 128, 0, st>>>(B, stepped);
     CKL();
     if (basis) {
-      kb_step_c_p<<<vblocks, 256, 0, st>>>(bi, bb.P.ptr, d * ND, tp, B, stepped);
+      kb_step_c_p<V><<<vblocks, 256, 0, st>>>(bi, Pv, d * ND, tp, B, stepped);
       CKL();
       kb_coef_update<<<dim3((unsigned)cdiv(bslots + 1, 256), (unsigned)(ND * ns)), 256, 0, st>>>(
           B, stepped, bb.CA.ptr, bb.CC.ptr, bslots, loop_it);
       CKL();
     } else {
-      kb_step_c<<<srows, sblk, 0, st>>>(bi, bb.P.ptr, bb.BIGP.ptr, bb.SOLS.ptr, d, B, stepped);
-      CKL();
+      if constexpr (!V32) {
+        kb_step_c<<<srows, sblk, 0, st>>>(bi, bb.P.ptr, bb.BIGP.ptr, bb.SOLS.ptr, d, B, stepped);
+        CKL();
+      }
     }
     kb_end_iteration<<<tb, 128, 0, st>>>(B, stepped, n_live);
     CKL();
@@ -2850,8 +2866,8 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
   // ---- tail: directions (deferred mode), residuals, projections, orientation
   // (sda.py:265-284)
   if (basis && d > 0) {
-    kb_combine_basis<<<(unsigned)cdiv(d * ND, 256), 256, 0, st>>>(bb.RB.ptr, d, B, bb.CC.ptr, bslots,
-                                                                  bb.SOLS.ptr);
+    kb_combine_basis<V><<<(unsigned)cdiv(d * ND, 256), 256, 0, st>>>(RBv, d, B, bb.CC.ptr, bslots,
+                                                                     bb.SOLS.ptr);
     CKL();
   }
   kb_finish<<<tb, 128, 0, st>>>(B);
@@ -2908,6 +2924,20 @@ static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alp
     if (status) status[t] = stt[t] == ST_BREAKDOWN ? FSDA_EBREAKDOWN : (stt[t] == ST_NONFINITE ? FSDA_ENONFINITE : FSDA_OK);
   }
   return FSDA_OK;
+}
+
+}  // extern "C++"
+
+static int batch_solve_impl(fsda_ctx* c, int T, const int8_t* labels, double alpha,
+                            const double* betas, int ns, double tol, int64_t max_iter,
+                            const double* probes, double* directions, double* scores,
+                            double* residuals, int64_t* iterations, uint8_t* converged,
+                            int64_t* n_applies, int64_t* fail_iter, int* status) {
+  if (c->store_bits == 32)
+    return batch_solve_t<float>(c, T, labels, alpha, betas, ns, tol, max_iter, probes, directions, scores,
+                                residuals, iterations, converged, n_applies, fail_iter, status);
+  return batch_solve_t<double>(c, T, labels, alpha, betas, ns, tol, max_iter, probes, directions, scores,
+                               residuals, iterations, converged, n_applies, fail_iter, status);
 }
 
 int fsda_solve_batch(fsda_ctx* c, int n_tasks, const int8_t* labels, double alpha,

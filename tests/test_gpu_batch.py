@@ -134,3 +134,77 @@ def test_batch_graph_loop_equals_eager_loop(mode):
     assert max(r.n_applies for r in out[0]) < 400      # the loop stopped on the device flag
     for a, b in zip(*out):
         _same(a, b)
+
+
+# ------------------------------------------------ fp32 storage (cfg4 / cfg5 mode)
+
+def _check_fp32(w, sets, alpha, tol, max_iter, seeds):
+    """Batch in fp32 storage (fsda_set_storage(32): P, Y, Z and the residual
+    basis as floats, every sum and scalar in double) == the single fp32-storage
+    solve of each task, and the first / last task == the C oracle's fp32 mirror."""
+    x, lap = _mats(w)
+    dev = fb.Device(0)
+    dev.set_storage(32)
+    batch = fb.solve_label_sets(x, lap, sets, alpha, w.betas, tol, max_iter, seeds=seeds, device=dev)
+    assert dev.last_shift_update_mode == 2
+    seq = fb.solve_label_sets(x, lap, sets, alpha, w.betas, tol, max_iter, seeds=seeds, device=dev,
+                              batched=False)
+    for a, b in zip(batch, seq):
+        _same(a, b)
+    c_oracle.set_storage(32)
+    try:
+        for t in sorted({0, len(sets) - 1}):
+            probe = np.random.default_rng(seeds[t]).uniform(-1, 1, w.d)
+            ref = c_oracle.fsda_solve(w.x_offsets, w.x_cols, w.d, w.l_offsets, w.l_cols, w.l_vals,
+                                      sets[t], alpha, w.betas, tol, max_iter, probe)
+            np.testing.assert_array_equal(batch[t].directions, ref["directions"])
+            np.testing.assert_array_equal(batch[t].iterations, ref["iterations"])
+    finally:
+        c_oracle.set_storage(64)
+    return batch
+
+
+def test_batch_fp32_storage_40_tasks_bitwise():
+    w = make_workload("cfg1", n=3000, d=1200, ell=300, n_pos=60, lam=14.0, k=6, n_shifts=6)
+    sets = _masks(w.n, 40, 150, 40, seed=11)
+    _check_fp32(w, sets, w.alpha, w.tol, 12, seeds=list(range(40)))
+
+
+@pytest.mark.parametrize("alpha", [0.0, 1.0])
+def test_batch_fp32_storage_alpha_branches(alpha):
+    w = make_workload("cfg1", n=1500, d=600, ell=150, n_pos=30, lam=10.0, k=5, n_shifts=4)
+    sets = _masks(w.n, 3, 90, 25, seed=5)
+    _check_fp32(w, sets, alpha, w.tol, 10, seeds=[3, 4, 5])
+
+
+def test_batch_fp32_storage_long_rows_and_heavy_columns():
+    """Rows of X above 32 and above 256 entries (chunked float gathers and the
+    two-level long-segment path), rows of L above 32 entries, heavy columns."""
+    w = make_workload("cfg1", n=300_000, d=2500, ell=3000, n_pos=600, lam=4.0, k=3, n_shifts=3)
+    sets = _masks(w.n, 3, 2000, 500, seed=9)
+    _check_fp32(w, sets, w.alpha, w.tol, 5, seeds=[7, 8, 9])
+    w2 = make_workload("cfg1", n=2000, d=900, ell=200, n_pos=50, lam=300.0, k=24, n_shifts=3)
+    assert np.diff(w2.x_offsets).max() > 256 and np.diff(w2.l_offsets).max() > 32
+    sets2 = _masks(w2.n, 2, 150, 40, seed=3)
+    _check_fp32(w2, sets2, w2.alpha, w2.tol, 6, seeds=[1, 2])
+
+
+def test_batch_fp32_storage_gate_vs_fp64():
+    """The stated fp32 gate (north_star: 1e-3 if fp32 is used) for the batch:
+    at a stable Krylov dimension every task's fp32-storage directions sit
+    within 1e-3 per shift of the fp64 batch (measured far below)."""
+    w = make_workload("cfg1")
+    x, lap = _mats(w)
+    sets = _masks(w.n, 4, 1000, 200, seed=21)
+    seeds = [0, 1, 2, 3]
+    d64 = fb.Device(0)
+    r64 = fb.solve_label_sets(x, lap, sets, w.alpha, w.betas, w.tol, 20, seeds=seeds, device=d64)
+    d32 = fb.Device(0)
+    d32.set_storage(32)
+    r32 = fb.solve_label_sets(x, lap, sets, w.alpha, w.betas, w.tol, 20, seeds=seeds, device=d32)
+    worst = 0.0
+    for a, b in zip(r32, r64):
+        rel = np.linalg.norm(a.directions - b.directions, axis=1) / np.linalg.norm(b.directions, axis=1)
+        worst = max(worst, float(rel.max()))
+    print(f"batch fp32 storage vs fp64 at K=20: rel {worst:.3e}")
+    assert worst <= 1e-3

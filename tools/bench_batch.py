@@ -28,16 +28,28 @@ ap.add_argument("--tasks", type=int, default=None)
 ap.add_argument("--max-iter", type=int, default=None)
 ap.add_argument("--seq-tasks", type=int, default=2)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--storage", type=int, default=64, help="32: fp32 storage with fp64 reductions")
+ap.add_argument("--cache", default=None, help="pickle the generated workload here and reuse it (variant sweeps)")
 args = ap.parse_args()
 
 cfg = CONFIGS[args.workload]
 T = args.tasks or cfg.get("tasks", 32)
-w = make_workload(args.workload, max_iter=args.max_iter)
+if args.cache and Path(args.cache).exists():
+    import pickle
+    with open(args.cache, "rb") as fh:
+        w = pickle.load(fh)
+else:
+    w = make_workload(args.workload, max_iter=args.max_iter)
+    if args.cache:
+        import pickle
+        with open(args.cache, "wb") as fh:
+            pickle.dump(w, fh, protocol=4)
 masks = task_masks(w.n, T, cfg.get("task_frac", 0.01), cfg.get("task_pos", 0.1), seed=77)
 probes = np.stack([np.random.default_rng(s).uniform(-1, 1, w.d) for s in range(T)])
 x = fb.SparseMatrix.binary(w.n, w.d, w.x_offsets, w.x_cols)
 lap = fb.Laplacian(fb.SparseMatrix(w.n, w.n, w.l_offsets, w.l_cols, w.l_vals), w.degrees)
 dev = fb.Device(0)
+dev.set_storage(args.storage)
 dev.upload_x(x)
 dev.upload_laplacian(lap)
 
@@ -65,7 +77,7 @@ for t in range(S):
     np.testing.assert_array_equal(r.directions, res[t].directions)
 
 out = {
-    "workload": args.workload, "tasks": T, "n_shifts": int(w.betas.size), "max_iter": w.max_iter,
+    "workload": args.workload, "storage_bits": args.storage, "tasks": T, "n_shifts": int(w.betas.size), "max_iter": w.max_iter,
     "n_applies": [min(napp), max(napp)],
     "batch_s": best, "batch_task_solves_per_s": T / best,
     "sequential_task_s": seq_el / S if S else None,

@@ -538,6 +538,25 @@ def run_b200(args):
                  "task_solves_per_s": T / t_b, "seconds": t_b,
                  "n_applies": [min(r.n_applies for r in bres), max(r.n_applies for r in bres)],
                  "note": "host-timed fsda_solve_batch: masks + probes H2D, directions D2H"}
+        # the same batch in fp32 storage (fsda_set_storage(32): P, Y, Z and the
+        # residual basis as floats, every sum in double; the 1e-3 gate of
+        # tests/test_gpu_batch.py) -- reported beside the fp64 number, not instead
+        dev.set_storage(32)
+        try:
+            dev.solve_batch(masks, w.alpha, betas4, w.tol, c4["max_iter"], probes, scores=False)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            b32 = dev.solve_batch(masks, w.alpha, betas4, w.tol, c4["max_iter"], probes, scores=False)
+            t_b32 = time.perf_counter() - t0
+            rel = max(float(np.max(np.linalg.norm(a.directions - b.directions, axis=1) /
+                                   np.linalg.norm(b.directions, axis=1))) for a, b in zip(b32, bres))
+            batch["fp32_storage"] = {"task_solves_per_s": T / t_b32, "seconds": t_b32,
+                                     "max_rel_vs_fp64_at_full_K": rel,
+                                     "note": "full K=150 is past the Krylov stability horizon; the stated "
+                                             "1e-3 gate is checked at the stable K (tests/test_gpu_batch.py)"}
+            del b32
+        finally:
+            dev.set_storage(64)
         del bres
         dev.load_problem(p)
 

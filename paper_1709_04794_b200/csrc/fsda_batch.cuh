@@ -133,31 +133,47 @@ __device__ __forceinline__ double emu_dot_leaf(int n, XY xy) {
 // Gathered-value terms: special(idx) marks the one index treated differently
 // (the diagonal of a Laplacian row), operator()(is_special, v) maps the value.
 struct TermPlain {
+  static constexpr bool kSpecial = false;
   __device__ __forceinline__ bool special(int) const { return false; }
+  __device__ __forceinline__ int special_row() const { return 0; }
   __device__ __forceinline__ double operator()(bool, double v) const { return v; }
 };
 struct TermLap {  // (L y)_i terms: d_i y_i on the diagonal, -y_j off it
+  static constexpr bool kSpecial = true;
   int row;
   double dg;
   __device__ __forceinline__ bool special(int idx) const { return idx == row; }
+  __device__ __forceinline__ int special_row() const { return row; }
   __device__ __forceinline__ double operator()(bool sp, double v) const { return sp ? dg * v : -v; }
 };
 
 // Canonical leaf of a gathered index segment: ind[s0, s0 + len) (len <= 256)
-// selects rows of src (task-minor); term(idx, v) maps the gathered value.
+// selects rows of src (task-minor); term maps the gathered value.
 // The canonical lane accumulators A[l] = sum_k v[l + 32 k] are built in pairs
 // (l, l + 16) and folded at once into B[l] = A[l] + A[l + 16] — the first
-// butterfly step — so only 16 partial sums stay live (register budget: three
-// 256-thread CTAs per SM).  Indices arrive 32 at a time (coalesced) and are
-// shuffled to every lane; GATHER_MLP values per lane are in flight.
+// butterfly step — so only 16 partial sums stay live (register budget: four
+// 256-thread CTAs per SM).  Indices arrive 32 at a time (coalesced); the
+// owning lane turns each into the element offset idx * tp once, and the
+// offsets are shuffled to every lane; 2 LS values per lane are in flight.
+// Entries past the segment's end load nothing and add (+/-)0.0, which leaves
+// every partial sum unchanged bit for bit (no partial sum is ever -0.0).
 template <int LS, typename V, typename Term>
 __device__ __forceinline__ double emu_gather_leaf_ls(const int* __restrict__ ind, long long s0, int len,
                                                      const V* __restrict__ src, int tp, int t,
                                                      int lane, Term term) {
   const int nk = (len + 31) >> 5;     // <= 8 index chunks
-  int my[8];
+  // byte offset idx * tp * sizeof(V) of the gathered row (host: below 2^32), all ones past the end
+  unsigned my[8];
+  const unsigned row_bytes = (unsigned)tp * (unsigned)sizeof(V);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) my[k] = (k < nk && 32 * k + lane < len) ? __ldg(ind + s0 + 32 * k + lane) : 0;
+  for (int k = 0; k < 8; ++k)
+    my[k] = (k < nk && 32 * k + lane < len) ? (unsigned)__ldg(ind + s0 + 32 * k + lane) * row_bytes : 0xffffffffu;
+  // this lane's column of src as an opaque address, so that a gather is one
+  // 64-bit add away (the compiler otherwise rebuilds (idx * tp + t) * 8 + src
+  // for every load)
+  unsigned long long bp = (unsigned long long)(src + t);
+  asm volatile("" : "+l"(bp));
+  const unsigned sp_off = (unsigned)term.special_row() * row_bytes;
   double B[16];
 #pragma unroll
   for (int l0 = 0; l0 < 16; l0 += LS) {
@@ -167,40 +183,23 @@ __device__ __forceinline__ double emu_gather_leaf_ls(const int* __restrict__ ind
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       if (k >= nk) break;
-      if (sizeof(V) == 8) {
-        double v1[LS], v2[LS];
+      V v1[LS], v2[LS];
+      unsigned sp1 = 0u, sp2 = 0u;
 #pragma unroll
-        for (int q = 0; q < LS; ++q) {
-          const int l = l0 + q;
-          const int i1 = __shfl_sync(FULL, my[k], l), i2 = __shfl_sync(FULL, my[k], l + 16);
-          v1[q] = (32 * k + l < len) ? term(term.special(i1), (double)__ldg(src + (long long)i1 * tp + t)) : 0.0;
-          v2[q] = (32 * k + l + 16 < len) ? term(term.special(i2), (double)__ldg(src + (long long)i2 * tp + t)) : 0.0;
+      for (int q = 0; q < LS; ++q) {
+        const int l = l0 + q;
+        const unsigned o1 = __shfl_sync(FULL, my[k], l), o2 = __shfl_sync(FULL, my[k], l + 16);
+        v1[q] = (32 * k + l < len) ? __ldg(reinterpret_cast<const V*>(bp + o1)) : (V)0;
+        v2[q] = (32 * k + l + 16 < len) ? __ldg(reinterpret_cast<const V*>(bp + o2)) : (V)0;
+        if (Term::kSpecial) {
+          sp1 |= (o1 == sp_off) ? (1u << q) : 0u;
+          sp2 |= (o2 == sp_off) ? (1u << q) : 0u;
         }
+      }
 #pragma unroll
-        for (int q = 0; q < LS; ++q) {
-          if (32 * k + l0 + q < len) a1[q] = a1[q] + v1[q];
-          if (32 * k + l0 + q + 16 < len) a2[q] = a2[q] + v2[q];
-        }
-      } else {
-        // fp32 storage: the loads stay floats until they are summed (half
-        // the registers per gather in flight); the term's special-index test
-        // is kept as a bit mask
-        V v1[LS], v2[LS];
-        unsigned sp1 = 0u, sp2 = 0u;
-#pragma unroll
-        for (int q = 0; q < LS; ++q) {
-          const int l = l0 + q;
-          const int i1 = __shfl_sync(FULL, my[k], l), i2 = __shfl_sync(FULL, my[k], l + 16);
-          v1[q] = (32 * k + l < len) ? __ldg(src + (long long)i1 * tp + t) : (V)0;
-          v2[q] = (32 * k + l + 16 < len) ? __ldg(src + (long long)i2 * tp + t) : (V)0;
-          sp1 |= term.special(i1) ? (1u << q) : 0u;
-          sp2 |= term.special(i2) ? (1u << q) : 0u;
-        }
-#pragma unroll
-        for (int q = 0; q < LS; ++q) {
-          if (32 * k + l0 + q < len) a1[q] = a1[q] + term((sp1 >> q) & 1u, (double)v1[q]);
-          if (32 * k + l0 + q + 16 < len) a2[q] = a2[q] + term((sp2 >> q) & 1u, (double)v2[q]);
-        }
+      for (int q = 0; q < LS; ++q) {
+        a1[q] = a1[q] + term((sp1 >> q) & 1u, (double)v1[q]);
+        a2[q] = a2[q] + term((sp2 >> q) & 1u, (double)v2[q]);
       }
     }
 #pragma unroll

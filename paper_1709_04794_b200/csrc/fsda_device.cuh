@@ -455,6 +455,7 @@ __global__ void k_laplacian_split(const int* __restrict__ rowptr, const int* __r
   if (i >= n) return;
   int lo = rowptr[i], hi = rowptr[i + 1];
   double dv = 0.0;
+  if (hi < lo) atomicExch(err, 2);
   for (int jj = lo; jj < hi; ++jj) {
     int c = cols[jj];
     if (jj > lo && c <= cols[jj - 1]) atomicExch(err, 3);

@@ -280,7 +280,6 @@ struct fsda_ctx {
   cudaEvent_t h2d_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   unsigned h2d_next = 0;
   int l_host_err = 0;     // the host split's validation result (check_err_flag codes)
-  bool l_raw = false;     // combined upload: L's raw arrays (values too) went straight to the device
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   CgScalars* sc = nullptr;
 
@@ -1640,7 +1639,7 @@ int fsda_ctx_set_stream(fsda_ctx* c, void* stream) {
 // X upload; `after_h2d` (optional) runs once X's copies are enqueued — the
 // combined upload uses it to start the Laplacian's copies behind them.
 static int upload_x_impl(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* row_offsets,
-                         const int64_t* col_indices, void (*after_h2d)(void*, int), void* hook_arg) {
+                         const int64_t* col_indices, void (*after_h2d)(void*), void* hook_arg) {
   if (n_rows < 0 || n_cols < 0) return fail(FSDA_EINVAL, "matrix shape must be non-negative");
   if (!row_offsets) return fail(FSDA_EINVAL, "row_offsets is null");
   const long long nnz = row_offsets[n_rows];
@@ -1665,10 +1664,9 @@ static int upload_x_impl(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int6
   // H2D + narrowing run on the stream while the host builds the row plan
   // (it needs only the host offsets).
   c->scratch_i64.ensure(std::max<long long>(n_rows + 1 + nnz, 1));
-  if (after_h2d) after_h2d(hook_arg, 0);  // before X's copies: page-locked L arrays start their DMA
   upload_narrow_async(c, row_offsets, n_rows + 1, nnz, c->x_rowptr, c->scratch_i64.ptr);
   upload_narrow_async(c, col_indices, nnz, n_cols - 1, c->x_cols, c->scratch_i64.ptr + n_rows + 1);
-  if (after_h2d) after_h2d(hook_arg, 1);  // behind X's copies: the host-narrowed L path
+  if (after_h2d) after_h2d(hook_arg);
   build_seg_plan(c->plan_xr, c->stream, row_offsets, n_rows, c->x_cols.ptr);
   tr.mark("x: row plan (host)");
   CK(cudaStreamSynchronize(c->stream));
@@ -1757,7 +1755,7 @@ static int upload_laplacian_rows(fsda_ctx* c, int64_t n, int64_t n_global, int64
   if (prefetched) {
     // the raw arrays were copied on the side stream (l_prefetch)
     CK(cudaStreamWaitEvent(c->stream, c->ev_lcopy, 0));
-    if (device_narrow() || c->l_raw) {
+    if (device_narrow()) {
       narrow_async(c, c->scratch_l64.ptr, n + 1, nnz, c->l_rowptr);
       narrow_async(c, c->scratch_l64.ptr + n + 1, nnz, n_global - 1, c->l_cols);
     }
@@ -1767,16 +1765,7 @@ static int upload_laplacian_rows(fsda_ctx* c, int64_t n, int64_t n_global, int64
     upload_narrow_async(c, col_indices, nnz, n_global - 1, c->l_cols, c->scratch_l64.ptr + n + 1);
   }
   c->l_diag.ensure(n);
-  if (prefetched && c->l_raw) {
-    // the values came with the raw arrays: checked and split on the device
-    c->l_raw = false;
-    if (n > 0) {
-      k_laplacian_split<<<grid_for(n, 256), 256, 0, c->stream>>>(c->l_rowptr.ptr, c->l_cols.ptr,
-                                                                 c->scratch_f64.ptr, c->l_diag.ptr, (int)n,
-                                                                 c->err.ptr, (int)row_base);
-      CKL();
-    }
-  } else if (prefetched) {
+  if (prefetched) {
     // values checked and the diagonal split on the host by l_prefetch
     if (c->l_host_err) {
       CK(cudaStreamSynchronize(c->stream));
@@ -1823,33 +1812,9 @@ struct LPrefetch {
 
 // The Laplacian's raw arrays to device scratch on the side stream, queued
 // behind X's copies, so they cross the link while X's CSC and plans build.
-// FSDA_B200_L_RAW=0: keep the host-narrowed path for page-locked arrays too.
-bool l_raw_enabled() {
-  static const bool v = !std::getenv("FSDA_B200_L_RAW") || std::atoi(std::getenv("FSDA_B200_L_RAW"));
-  return v;
-}
-
-void l_prefetch(void* arg, int phase) {
+void l_prefetch(void* arg) {
   LPrefetch* a = static_cast<LPrefetch*>(arg);
   fsda_ctx* c = a->c;
-  if (phase == 0) {
-    // Page-locked L arrays go to the device as they are (indices as int64, the
-    // values too), ahead of X's copies: the DMA engine moves them while the
-    // host threads narrow X's indices, instead of the host narrowing and
-    // checking L after X (the host pass over L's 2 x nnz words was as long as
-    // the link time it saved).  Narrowed, checked and split on the device.
-    c->l_raw = !device_narrow() && l_raw_enabled() && a->nnz > 0 && host_page_locked(a->offs) &&
-               host_page_locked(a->cols) && host_page_locked(a->vals);
-    if (!c->l_raw) return;
-    c->scratch_l64.ensure(std::max<long long>(a->n + 1 + a->nnz, 1));
-    c->scratch_f64.ensure(std::max<long long>(a->nnz, 1));
-    CK(cudaMemcpyAsync(c->scratch_l64.ptr, a->offs, sizeof(long long) * (a->n + 1), cudaMemcpyHostToDevice, c->side));
-    CK(cudaMemcpyAsync(c->scratch_l64.ptr + a->n + 1, a->cols, sizeof(long long) * a->nnz, cudaMemcpyHostToDevice, c->side));
-    CK(cudaMemcpyAsync(c->scratch_f64.ptr, a->vals, sizeof(double) * a->nnz, cudaMemcpyHostToDevice, c->side));
-    CK(cudaEventRecord(c->ev_lcopy, c->side));
-    return;
-  }
-  if (c->l_raw) return;  // already on its way
   CK(cudaEventRecord(c->ev_lfork, c->stream));
   CK(cudaStreamWaitEvent(c->side, c->ev_lfork, 0));
   int range_err = 0;

@@ -624,3 +624,4 @@ def test_large_pageable_upload_narrowed_on_host():
     v = rng.standard_normal(d)
     got = fb.matvec(x, v)
     np.testing.assert_array_equal(got, c_oracle.matvec(offs, cols, v))
+

@@ -313,7 +313,7 @@ def time_e2e(fb, dev, w, steps, pinned=True):
     """fsda_solve(p) through the public API: every call uploads X, L, labels
     and the probe from host memory and returns numpy results."""
     pp = make_problem(fb, w, pinned=pinned)
-    for _ in range(2):
+    for _ in range(3):
         rep = fb.fsda_solve(pp, device=dev)
     t0 = time.perf_counter()
     for _ in range(steps):
@@ -431,7 +431,7 @@ def run_b200(args):
     value = world * 1000.0 / ms_per_step
 
     # ---- e2e through the public API, host arrays in pinned memory (and pageable)
-    e2e_steps = args.e2e_steps or max(3, min(args.steps, 5))
+    e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
     e2e_s, h2d, d2h = time_e2e(fb, dev, w, e2e_steps, pinned=True)
     te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -78,7 +79,7 @@ struct CudaError {
 
 // Bumped on every device (re)allocation; part of the graph cache key so a
 // cached graph never holds a stale buffer pointer.
-unsigned long long g_alloc_gen = 0;
+std::atomic<unsigned long long> g_alloc_gen{0};  // bumped from any thread / context
 
 template <typename T>
 struct DevBuf {
@@ -895,7 +896,7 @@ bool build_solve_graph(fsda_ctx* c, double alpha, int ns, long long max_iter, do
   mix(&c->n2, sizeof(c->n2));
   char key[320];
   snprintf(key, sizeof(key), "%d|%d|%a|%d|%lld|%a|%lld|%lld|%lld|%llu|%llx|%d|%d", c->solve_kind,
-           c->solve_abs_tol, alpha, ns, max_iter, tol, c->n, c->d, c->nnz, g_alloc_gen, h,
+           c->solve_abs_tol, alpha, ns, max_iter, tol, c->n, c->d, c->nnz, g_alloc_gen.load(), h,
            c->su_mode, c->nslots * (c->store_bits == 32 ? -1 : 1));
   if (c->exec && c->graph_key == key) {
     *launches_fixed = c->graph_fixed;

@@ -414,7 +414,7 @@ int fsda_solve_sharded(fsda_ctx** ctxs, int n_ctx, double alpha, const double* b
       fsda_ctx* c = c0;
       char key[160];
       snprintf(key, sizeof(key), "shard|%a|%d|%lld|%a|%llu|%d|%d|%d", alpha, ns, (long long)max_iter, tol,
-               g_alloc_gen, c->su_mode, c->nslots, c->store_bits);
+               g_alloc_gen.load(), c->su_mode, c->nslots, c->store_bits);
       if (!(c->exec && c->graph_key == key)) {
         c->invalidate_graph();
         cudaGraph_t g;

@@ -155,19 +155,22 @@ struct TermLap {  // (L y)_i terms: d_i y_i on the diagonal, -y_j off it
 // 256-thread CTAs per SM).  Indices arrive 32 at a time (coalesced); the
 // owning lane turns each into the element offset idx * tp once, and the
 // offsets are shuffled to every lane; 2 LS values per lane are in flight.
-// Entries past the segment's end load nothing and add (+/-)0.0, which leaves
-// every partial sum unchanged bit for bit (no partial sum is ever -0.0).
+// Slots past the segment's end gather the table's zero row (every gathered
+// table carries one more row of zeros) and add (+/-)0.0, which leaves every
+// partial sum unchanged bit for bit (no partial sum is ever -0.0): no bounds
+// test or select per gather.
 template <int LS, typename V, typename Term>
 __device__ __forceinline__ double emu_gather_leaf_ls(const int* __restrict__ ind, long long s0, int len,
                                                      const V* __restrict__ src, int tp, int t,
-                                                     int lane, Term term) {
+                                                     int lane, Term term, unsigned zoff) {
   const int nk = (len + 31) >> 5;     // <= 8 index chunks
-  // byte offset idx * tp * sizeof(V) of the gathered row (host: below 2^32), all ones past the end
+  // byte offset idx * tp * sizeof(V) of the gathered row (host: below 2^32);
+  // slots past the segment's end point at the table's zero row (zoff)
   unsigned my[8];
   const unsigned row_bytes = (unsigned)tp * (unsigned)sizeof(V);
 #pragma unroll
   for (int k = 0; k < 8; ++k)
-    my[k] = (k < nk && 32 * k + lane < len) ? (unsigned)__ldg(ind + s0 + 32 * k + lane) * row_bytes : 0xffffffffu;
+    my[k] = (k < nk && 32 * k + lane < len) ? (unsigned)__ldg(ind + s0 + 32 * k + lane) * row_bytes : zoff;
   // this lane's column of src as an opaque address, so that a gather is one
   // 64-bit add away (the compiler otherwise rebuilds (idx * tp + t) * 8 + src
   // for every load)
@@ -189,8 +192,8 @@ __device__ __forceinline__ double emu_gather_leaf_ls(const int* __restrict__ ind
       for (int q = 0; q < LS; ++q) {
         const int l = l0 + q;
         const unsigned o1 = __shfl_sync(FULL, my[k], l), o2 = __shfl_sync(FULL, my[k], l + 16);
-        v1[q] = (32 * k + l < len) ? __ldg(reinterpret_cast<const V*>(bp + o1)) : (V)0;
-        v2[q] = (32 * k + l + 16 < len) ? __ldg(reinterpret_cast<const V*>(bp + o2)) : (V)0;
+        v1[q] = __ldg(reinterpret_cast<const V*>(bp + o1));
+        v2[q] = __ldg(reinterpret_cast<const V*>(bp + o2));
         if (Term::kSpecial) {
           sp1 |= (o1 == sp_off) ? (1u << q) : 0u;
           sp2 |= (o2 == sp_off) ? (1u << q) : 0u;
@@ -220,10 +223,10 @@ __device__ __forceinline__ double emu_gather_leaf_ls(const int* __restrict__ ind
 template <typename V, typename Term>
 __device__ __forceinline__ double emu_gather_leaf(const int* __restrict__ ind, long long s0, int len,
                                                   const V* __restrict__ src, int tp, int t,
-                                                  int lane, Term term) {
+                                                  int lane, Term term, unsigned zoff) {
   constexpr int LS = sizeof(V) == 4 ? F32_LS : GATHER_MLP / 2;
-  if (len <= 32) return emu_gather_leaf_ls<8, V>(ind, s0, len, src, tp, t, lane, term);
-  return emu_gather_leaf_ls<LS, V>(ind, s0, len, src, tp, t, lane, term);
+  if (len <= 32) return emu_gather_leaf_ls<8, V>(ind, s0, len, src, tp, t, lane, term, zoff);
+  return emu_gather_leaf_ls<LS, V>(ind, s0, len, src, tp, t, lane, term, zoff);
 }
 
 // Segments longer than 256 entries: R256 over their leaves (two levels,
@@ -231,7 +234,7 @@ __device__ __forceinline__ double emu_gather_leaf(const int* __restrict__ ind, l
 template <typename V, typename Term>
 __device__ __noinline__ double emu_gather_long(const int* __restrict__ ind, long long start, int n,
                                                const V* __restrict__ src, int tp, int t,
-                                               int lane, Term term) {
+                                               int lane, Term term, unsigned zoff) {
   const int m = (n + LEAF - 1) / LEAF;  // <= 256 (host-checked)
   double P[32];
 #pragma unroll
@@ -240,7 +243,7 @@ __device__ __noinline__ double emu_gather_long(const int* __restrict__ ind, long
     for (int l = 0; l < 32 && gb + l < m; ++l) {
       const int g = gb + l;
       const double v = emu_gather_leaf(ind, start + (long long)g * LEAF, min(LEAF, n - g * LEAF),
-                                       src, tp, t, lane, term);
+                                       src, tp, t, lane, term, zoff);
 #pragma unroll
       for (int q = 0; q < 32; ++q)
         if (q == l) P[q] = P[q] + v;
@@ -252,9 +255,9 @@ __device__ __noinline__ double emu_gather_long(const int* __restrict__ ind, long
 template <typename V, typename Term>
 __device__ __forceinline__ double emu_segment(const int* __restrict__ ind, long long start, int n,
                                               const V* __restrict__ src, int tp, int t,
-                                              int lane, Term term) {
-  if (n <= LEAF) return emu_gather_leaf(ind, start, n, src, tp, t, lane, term);
-  return emu_gather_long(ind, start, n, src, tp, t, lane, term);
+                                              int lane, Term term, unsigned zoff) {
+  if (n <= LEAF) return emu_gather_leaf(ind, start, n, src, tp, t, lane, term, zoff);
+  return emu_gather_long(ind, start, n, src, tp, t, lane, term, zoff);
 }
 
 // ------------------------------------------------------------ layout moves
@@ -325,7 +328,8 @@ __global__ void __launch_bounds__(256, KIND == SEG_LROWS ? KB_LROWS_MINB : KB_XR
                                                V* __restrict__ out, long long n_rows, int G,
                                                int tp, const double* __restrict__ ldiag,
                                                const signed char* __restrict__ lab, double alpha,
-                                               int alpha_mode) {
+                                               int alpha_mode, long long src_rows) {
+  const unsigned zoff = (unsigned)(src_rows * tp * (long long)sizeof(V));  // the zero row of src
   const int lane = threadIdx.x & 31;
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= n_rows * G) return;
@@ -336,12 +340,12 @@ __global__ void __launch_bounds__(256, KIND == SEG_LROWS ? KB_LROWS_MINB : KB_XR
   double s;
   if (KIND == SEG_LROWS) {
     const double dg = __ldg(ldiag + i);
-    s = emu_segment(cols, lo, n, src, tp, t, lane, TermLap{(int)i, dg});
+    s = emu_segment(cols, lo, n, src, tp, t, lane, TermLap{(int)i, dg}, zoff);
     const double masked = lab[i * tp + t] != 0 ? (double)src[i * tp + t] : 0.0;
     const double smoothed = alpha * s;
     s = (alpha_mode == 1) ? smoothed : (1.0 - alpha) * masked + smoothed;
   } else {
-    s = emu_segment(cols, lo, n, src, tp, t, lane, TermPlain{});
+    s = emu_segment(cols, lo, n, src, tp, t, lane, TermPlain{}, zoff);
   }
   out[i * tp + t] = (V)s;
 }
@@ -370,7 +374,8 @@ template <typename V>
 __global__ void __launch_bounds__(256, KB_COLS_MINB) kb_cols_light(SegPlan pl, const V* __restrict__ src,
                                                      double* __restrict__ out, int G, int tp,
                                                      int mode, const double* __restrict__ mu,
-                                                     BatchState B) {
+                                                     BatchState B, long long src_rows) {
+  const unsigned zoff = (unsigned)(src_rows * tp * (long long)sizeof(V));
   const int lane = threadIdx.x & 31;
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const long long n_entries = pl.cls_off[6];
@@ -379,7 +384,7 @@ __global__ void __launch_bounds__(256, KB_COLS_MINB) kb_cols_light(SegPlan pl, c
   const int g = (int)(w - e * G);
   const int t = g * BG + lane;
   const int4 tk = __ldg(pl.tasks + e);
-  const double s = emu_gather_leaf(pl.ind, tk.y, tk.z, src, tp, t, lane, TermPlain{});
+  const double s = emu_gather_leaf(pl.ind, tk.y, tk.z, src, tp, t, lane, TermPlain{}, zoff);
   out[(long long)tk.x * tp + t] = b_col_finish(s, mode, tk.x, t, tp, mu, B);
 }
 
@@ -391,7 +396,9 @@ __global__ void __launch_bounds__(256, KB_COLS_MINB) kb_cols_leaves(SegPlan pl, 
                                                       const V* __restrict__ src,
                                                       double* __restrict__ hpart,
                                                       double* __restrict__ xpart, long long n_hleaf,
-                                                      long long n_xtask, int G, int tp) {
+                                                      long long n_xtask, int G, int tp,
+                                                      long long src_rows) {
+  const unsigned zoff = (unsigned)(src_rows * tp * (long long)sizeof(V));
   const int lane = threadIdx.x & 31;
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= (n_hleaf + n_xtask) * G) return;
@@ -407,11 +414,11 @@ __global__ void __launch_bounds__(256, KB_COLS_MINB) kb_cols_leaves(SegPlan pl, 
     const int h = tk.w;
     const int slot = __ldg(pl.heavy_seg0 + h) + (tk.y - __ldg(pl.heavy_start + h)) / LEAF + lf;
     const double v = emu_gather_leaf(pl.ind, tk.y + lf * LEAF, min(LEAF, tk.z - lf * LEAF), src,
-                                     tp, t, lane, TermPlain{});
+                                     tp, t, lane, TermPlain{}, zoff);
     hpart[(long long)slot * tp + t] = v;
   } else {
     const int4 tk = __ldg(dn.tasks + (u - n_hleaf));
-    const double v = emu_gather_leaf(dn.rows, tk.y, tk.z, src, tp, t, lane, TermPlain{});
+    const double v = emu_gather_leaf(dn.rows, tk.y, tk.z, src, tp, t, lane, TermPlain{}, zoff);
     xpart[(long long)tk.x * tp + t] = v;
   }
 }

@@ -2484,7 +2484,7 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
   const long long n = c->n, d = c->d;
   Trace tr;
   const int G = (T + BG - 1) / BG, tp = G * BG;
-  if (std::max(n, d) * (long long)tp * 8 >= (1LL << 32))  // the setup products gather doubles in either storage
+  if ((std::max(n, d) + 1) * (long long)tp * 8 >= (1LL << 32))  // the setup products gather doubles in either storage
     return fail(FSDA_EINVAL, "fsda_solve_batch: a task-minor vector must stay below 4 GiB (32-bit gather offsets)");
   std::vector<double> ell(tp, 1.0), n1v(tp, 1.0), n2v(tp, 1.0);
   std::vector<int> bad(T, 0);
@@ -2535,8 +2535,10 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
   c->su_mode = bmode;
   const bool basis = bmode == 2;
   bb.lab.ensure(n * ND);
-  bb.ind.ensure(n * ND);
-  for (DevBuf<double>* v : {&bb.P, &bb.Q, &bb.MU, &bb.Bv, &bb.PR}) v->ensure(std::max(1LL, d * ND));
+  // every gathered table (ind, PR, P over features; Y, Z over samples) carries
+  // one more row of zeros: the gathers' out-of-range slots read it
+  bb.ind.ensure((n + 1) * ND);
+  for (DevBuf<double>* v : {&bb.P, &bb.Q, &bb.MU, &bb.Bv, &bb.PR}) v->ensure(std::max(1LL, (d + 1) * ND));
   if (basis) {
     bb.RB.ensure(std::max(1LL, V32 ? cdiv(bslots * d * ND, 2) : bslots * d * ND));
     bb.CA.ensure(std::max(1LL, bslots * ND * ns));
@@ -2545,8 +2547,8 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
     bb.R0.ensure(std::max(1LL, d * ND));
     bb.R1.ensure(std::max(1LL, d * ND));
   }
-  bb.Y.ensure(std::max(1LL, n * ND));
-  bb.Z.ensure(std::max(1LL, n * ND));
+  bb.Y.ensure(std::max(1LL, (n + 1) * ND));
+  bb.Z.ensure(std::max(1LL, (n + 1) * ND));
   bb.BIGP.ensure(basis ? 1LL : std::max(1LL, d * ND * ns));
   bb.SOLS.ensure(std::max(1LL, d * ND * ns));
   bb.SCORES.ensure(std::max(1LL, n * ND * ns));
@@ -2581,6 +2583,13 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
   V* const Yv = reinterpret_cast<V*>(bb.Y.ptr);
   V* const Zv = reinterpret_cast<V*>(bb.Z.ptr);
   V* const RBv = reinterpret_cast<V*>(bb.RB.ptr);
+  auto zero_row = [&](auto* table, long long rows) {
+    CK(cudaMemsetAsync(table + rows * ND, 0, sizeof(*table) * ND, st));
+  };
+  zero_row(bb.ind.ptr, n);   // the setup products gather doubles
+  zero_row(bb.PR.ptr, d);
+  zero_row(bb.Y.ptr, n);
+  zero_row(bb.Z.ptr, n);
   BatchState B;
   double* sd = bb.scal.ptr;
   B.rr = sd; B.gamma_prev = sd + ND; B.alpha = sd + 2 * ND; B.b_norm = sd + 3 * ND;
@@ -2620,7 +2629,7 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
   auto rows_x = [&](auto* src, auto* out) {
     using U = std::remove_cv_t<std::remove_pointer_t<decltype(out)>>;
     kb_rows<SEG_XROWS, U><<<grid_w(n * G), 256, 0, st>>>(c->x_rowptr.ptr, c->x_cols.ptr, (const U*)src, out,
-                                                        n, G, tp, nullptr, nullptr, 0.0, 0);
+                                                        n, G, tp, nullptr, nullptr, 0.0, 0, d);
     CKL();
   };
   auto smoother = [&](auto* y, auto* z) {
@@ -2631,7 +2640,7 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
           (const U*)y, bb.lab.ptr, z, n * ND);
     else
       kb_rows<SEG_LROWS, U><<<grid_w(n * G), 256, 0, st>>>(c->l_rowptr.ptr, c->l_cols.ptr, (const U*)y, z, n,
-                                                          G, tp, c->l_diag.ptr, bb.lab.ptr, alpha, amode);
+                                                          G, tp, c->l_diag.ptr, bb.lab.ptr, alpha, amode, n);
     CKL();
   };
   const SegPlan& pxc = c->plan_xc.pl;
@@ -2672,11 +2681,11 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
     using U = std::remove_cv_t<std::remove_pointer_t<decltype(src_any)>>;
     const U* src = src_any;
     if (n_light)
-      kb_cols_light<U><<<grid_w(n_light * G), 256, 0, st>>>(pxc, src, out, G, tp, mode, bb.MU.ptr, B);
+      kb_cols_light<U><<<grid_w(n_light * G), 256, 0, st>>>(pxc, src, out, G, tp, mode, bb.MU.ptr, B, n);
     CKL();
     if (n_htask || c->xh_ntasks) {
       kb_cols_leaves<U><<<grid_w((4 * n_htask + c->xh_ntasks) * G), 256, 0, st>>>(
-          pxc, c->xh, src, bb.hpart.ptr, bb.xpart.ptr, 4 * n_htask, c->xh_ntasks, G, tp);
+          pxc, c->xh, src, bb.hpart.ptr, bb.xpart.ptr, 4 * n_htask, c->xh_ntasks, G, tp, n);
       CKL();
       if (n_gchunks) {
         kb_part_groups<<<grid_w(n_gchunks * G), 256, 0, st>>>(pxc, c->xh, bb.hpart.ptr, bb.xpart.ptr, n_heavy,
@@ -2757,6 +2766,10 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
     tr.mark("batch: setup");
   }
 
+  // the loop vectors' zero rows, in storage type (the setup used Y / Z as doubles)
+  zero_row(Pv, d);
+  zero_row(Yv, n);
+  zero_row(Zv, n);
   // ---- the shifted-CG loop (krylov.py:210-270), all live tasks in step.
   // The iteration index lives on the device (kb_loop_next), so the body is
   // the same launches every time: it runs as a CUDA graph whose conditional

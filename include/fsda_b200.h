@@ -145,7 +145,9 @@ int fsda_last_shift_update_mode(fsda_ctx* ctx);
  * rhs, the directions, the scores and every scalar stay double.  Parity gate
  * (stated): directions within 1e-3 per shift of the fp64 solve and identical
  * labeled AUC at the stable Krylov dimension.  Implies the deferred
- * shift-update mode.  Applies to fsda_solve / fsda_solve_async. */
+ * shift-update mode.  Applies to fsda_solve / fsda_solve_async and to
+ * fsda_solve_batch (P, Y, Z and the residual basis of every task as floats;
+ * each task equals its single fp32-storage solve bit for bit). */
 int fsda_set_storage(fsda_ctx* ctx, int bits);
 
 /* 1: launch each solve's kernels one by one from the host (the same kernels,
@@ -215,8 +217,11 @@ int fsda_sa_solve(fsda_ctx* ctx, double alpha, const double* betas, int n_shifts
  * [T][n_shifts][N] (may be NULL), residuals / iterations / converged
  * [T][n_shifts], n_applies / fail_iter / status [T] (status: FSDA_OK,
  * FSDA_EBREAKDOWN or FSDA_ENONFINITE per task; a failed task does not stop
- * the others).  Replaces the per-fold fsda_solve calls of nested_cv
- * (evaluation.py:110-123, 173-237). */
+ * the others).  Honours fsda_set_storage (32: fp32 storage, each task equal
+ * to its single fp32-storage solve).  Limit: a task-minor vector, (max(N, D)
+ * + 1) x tasks padded to 32 x 8 bytes, must stay below 4 GiB (32-bit gather
+ * offsets); larger batches are split by the caller.  Replaces the per-fold
+ * fsda_solve calls of nested_cv (evaluation.py:110-123, 173-237). */
 int fsda_solve_batch(fsda_ctx* ctx, int n_tasks, const int8_t* labels, double alpha,
                      const double* betas, int n_shifts, double tol, int64_t max_iter,
                      const double* probes, double* directions, double* scores,

@@ -286,16 +286,28 @@ __global__ void kb_task_minor(const double* __restrict__ in, double* __restrict_
   }
 }
 
-// sols [D][TP][ns] -> out [T][ns][D].
-__global__ void kb_directions_out(const double* __restrict__ sols, double* __restrict__ out,
-                                  long long d, int T, int tp, int ns) {
-  const long long total = (long long)T * ns * d;
-  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
-       k += (long long)gridDim.x * blockDim.x) {
-    const long long ts = k / d;
-    const long long c = k - ts * d;
-    const int t = (int)(ts / ns), s = (int)(ts - (long long)t * ns);
-    out[k] = sols[(c * tp + t) * ns + s];
+// sols [D][TP * ns] -> out [T * ns][D], negated where the orientation flips
+// (sda.py:280-283): a 32 x 32 tiled transpose through shared memory, so both
+// the reads (along task-shift) and the writes (along features) are coalesced.
+// blockDim = (32, 8); grid = (ceil(Q / 32), ceil(D / 32)), Q = T * ns.
+__global__ void __launch_bounds__(256) kb_directions_out(const double* __restrict__ sols,
+                                                         double* __restrict__ out, long long d, int T,
+                                                         int tp, int ns,
+                                                         const unsigned char* __restrict__ flip) {
+  __shared__ double tile[32][33];
+  const long long Q = (long long)T * ns, ld = (long long)tp * ns;
+  const long long q0 = (long long)blockIdx.x * 32, c0 = (long long)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const long long c = c0 + r, q = q0 + threadIdx.x;
+    tile[r][threadIdx.x] = (c < d && q < Q) ? sols[c * ld + q] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const long long q = q0 + r, c = c0 + threadIdx.x;
+    if (q < Q && c < d) {
+      const double v = tile[threadIdx.x][r];
+      out[q * d + c] = flip[q] ? -v : v;
+    }
   }
 }
 
@@ -1048,24 +1060,71 @@ __global__ void kb_finish(BatchState B) {
   }
 }
 
-// Orientation leaves y.s per (task, shift) over N (fma, canonical lanes over
-// rows; blockIdx.y = task * ns + shift) and the flip flags.
-__global__ void kb_orient_leaves(const signed char* __restrict__ lab,
+// Projection scores of the labeled rows only (the orientation y . s needs no
+// others; used when the caller does not ask for the scores): thread (row,
+// task) with a label walks the row's columns in stored order — the order of
+// k_spmm_scores and of scipy's csr_matvec — for SC_SH shifts at a time.
+// lab: labels task-minor [N][TP].
+constexpr int SC_SH = 8;
+__global__ void __launch_bounds__(256) kb_scores_labeled(const int* __restrict__ rowptr,
+                                                         const int* __restrict__ cols,
+                                                         const signed char* __restrict__ lab,
+                                                         const double* __restrict__ sols,
+                                                         double* __restrict__ scores, long long n,
+                                                         int tp, int ns) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n * tp) return;
+  if (lab[k] == 0) return;
+  const long long i = k / tp;
+  const int t = (int)(k - i * tp);
+  const int lo = __ldg(rowptr + i), hi = __ldg(rowptr + i + 1);
+  for (int s0 = 0; s0 < ns; s0 += SC_SH) {
+    double acc[SC_SH];
+#pragma unroll
+    for (int u = 0; u < SC_SH; ++u) acc[u] = 0.0;
+    for (int j = lo; j < hi; ++j) {
+      const double* w = sols + ((long long)__ldg(cols + j) * tp + t) * ns + s0;
+#pragma unroll
+      for (int u = 0; u < SC_SH; ++u)
+        if (s0 + u < ns) acc[u] = acc[u] + w[u];
+    }
+#pragma unroll
+    for (int u = 0; u < SC_SH; ++u)
+      if (s0 + u < ns) scores[((long long)t * ns + s0 + u) * n + i] = acc[u];
+  }
+}
+
+// Orientation leaves y . s per (task, shift) over N (fma, canonical lanes over
+// rows) for SC_SH shifts of one task per warp pass: blockIdx.y = task *
+// n_chunks + chunk.  Unlabeled rows are skipped: fma(0, s, a) == a for every
+// finite s, so the leaf sums equal the single solve's k_orient bit for bit
+// (a non-finite score on an unlabeled row would differ; such a task has
+// already failed with ST_NONFINITE).  labt: labels task-major [T][N].
+__global__ void kb_orient_leaves(const signed char* __restrict__ labt,
                                  const double* __restrict__ scores, long long n,
-                                 double* __restrict__ part, long long n_leaf, int tp, int ns) {
+                                 double* __restrict__ part, long long n_leaf, int ns) {
   const int lane = threadIdx.x & 31;
   const long long g = (long long)blockIdx.x * WARPS_PER_BLOCK + (threadIdx.x >> 5);
-  const int ts = blockIdx.y;
-  const int t = ts / ns;
+  const int nch = (ns + SC_SH - 1) / SC_SH;
+  const int t = blockIdx.y / nch, s0 = (blockIdx.y - t * nch) * SC_SH;
   if (g >= n_leaf) return;
-  const double* sv = scores + (long long)ts * n;
-  double a = 0.0;
+  double a[SC_SH];
+#pragma unroll
+  for (int u = 0; u < SC_SH; ++u) a[u] = 0.0;
   for (int k = 0; k < 8; ++k) {
     const long long i = g * LEAF + k * 32 + lane;
-    if (i < n) a = fma((double)lab[i * tp + t], sv[i], a);
+    if (i >= n) continue;
+    const signed char lb = labt[(long long)t * n + i];
+    if (lb == 0) continue;
+#pragma unroll
+    for (int u = 0; u < SC_SH; ++u)
+      if (s0 + u < ns) a[u] = fma((double)lb, scores[((long long)t * ns + s0 + u) * n + i], a[u]);
   }
-  a = butterfly(a);
-  if (lane == 0) part[(long long)ts * n_leaf + g] = a;
+#pragma unroll
+  for (int u = 0; u < SC_SH; ++u) {
+    const double v = butterfly(a[u]);
+    if (lane == 0 && s0 + u < ns) part[((long long)t * ns + s0 + u) * n_leaf + g] = v;
+  }
 }
 
 __global__ void kb_orient_combine(const double* __restrict__ part, long long n_leaf,
@@ -1076,21 +1135,15 @@ __global__ void kb_orient_combine(const double* __restrict__ part, long long n_l
   if (threadIdx.x == 0) B.flip[ts] = v < 0.0 ? 1 : 0;
 }
 
-// Negate flipped (task, shift) scores [TP*ns][N] and directions [D][TP][ns].
-__global__ void kb_flip(double* __restrict__ scores, double* __restrict__ sols, long long n,
-                        long long d, int T, BatchState B) {
+// Negate the flipped (task, shift) score vectors [T * ns][N] (the directions
+// take their sign in kb_directions_out).
+__global__ void kb_flip(double* __restrict__ scores, long long n, int T, BatchState B) {
   const int ts = blockIdx.y;
-  const int t = ts / B.ns, s = ts - t * B.ns;
+  const int t = ts / B.ns;
   if (t >= T || !B.flip[ts]) return;
-  const long long lim = n > d ? n : d;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < lim;
-       i += (long long)gridDim.x * blockDim.x) {
-    if (i < n) scores[(long long)ts * n + i] = -scores[(long long)ts * n + i];
-    if (i < d) {
-      const long long e = (i * B.tp + t) * B.ns + s;
-      sols[e] = -sols[e];
-    }
-  }
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    scores[(long long)ts * n + i] = -scores[(long long)ts * n + i];
 }
 
 }  // namespace fsda

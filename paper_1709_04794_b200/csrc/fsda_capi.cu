@@ -154,7 +154,7 @@ struct HostPlan {
 
 // Device buffers of the multi-task batch (fsda_solve_batch), task-minor.
 struct BatchBufs {
-  DevBuf<signed char> lab;
+  DevBuf<signed char> lab, labt;
   DevBuf<double> ind, P, Q, R0, R1, MU, Bv, PR, Y, Z, BIGP, SOLS, SCORES, OUT;
   DevBuf<double> RB, CA, CC;  // deferred mode: residual slots, coefficient rows
   DevBuf<int2> gchunks;       // long X^T units: {unit, 256-partial group}
@@ -170,7 +170,7 @@ struct BatchBufs {
   DevBuf<double> betas;
   DevBuf<char> raw;
   void release() {
-    lab.release(); ind.release(); P.release(); Q.release(); R0.release(); R1.release();
+    lab.release(); labt.release(); ind.release(); P.release(); Q.release(); R0.release(); R1.release();
     MU.release(); Bv.release(); PR.release(); Y.release(); Z.release(); BIGP.release();
     SOLS.release(); SCORES.release(); OUT.release(); partD.release(); partN.release();
     RB.release(); CA.release(); CC.release();
@@ -2568,10 +2568,11 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
   bb.sh_i.ensure(ND * ns);
   bb.betas.ensure(ns);
   // inputs
-  bb.raw.ensure(std::max<long long>((long long)T * n, (long long)T * d * 8));
-  h2d(c, bb.raw.ptr, labels, (size_t)T * n, st);
+  bb.raw.ensure((long long)T * d * 8);
+  bb.labt.ensure(std::max<long long>((long long)T * n, 1));  // task-major labels, kept for the orientation
+  h2d(c, bb.labt.ptr, labels, (size_t)T * n, st);
   kb_labels_in<<<(unsigned)std::min<long long>(cdiv(n * ND, 256), 65535LL * 4), 256, 0, st>>>(
-      (const signed char*)bb.raw.ptr, bb.lab.ptr, bb.ind.ptr, n, T, tp);
+      bb.labt.ptr, bb.lab.ptr, bb.ind.ptr, n, T, tp);
   CKL();
   h2d(c, bb.raw.ptr, probes, sizeof(double) * T * d, st);
   kb_task_minor<<<(unsigned)std::min<long long>(cdiv(d * ND, 256), 65535LL * 4), 256, 0, st>>>(
@@ -2895,24 +2896,30 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
   kb_finish<<<tb, 128, 0, st>>>(B);
   CKL();
   const int nsp = tp * ns;
-  k_spmm_scores<<<grid_for(n, 8), 256, 0, st>>>(c->x_rowptr.ptr, c->x_cols.ptr, bb.SOLS.ptr,
-                                                bb.SCORES.ptr, (int)n, nsp);
+  if (scores) {
+    k_spmm_scores<<<grid_for(n, 8), 256, 0, st>>>(c->x_rowptr.ptr, c->x_cols.ptr, bb.SOLS.ptr,
+                                                  bb.SCORES.ptr, (int)n, nsp);
+  } else if (n > 0) {
+    // the caller wants no scores: the orientation needs the labeled rows' only
+    kb_scores_labeled<<<(unsigned)cdiv(n * ND, 256), 256, 0, st>>>(c->x_rowptr.ptr, c->x_cols.ptr, bb.lab.ptr,
+                                                                  bb.SOLS.ptr, bb.SCORES.ptr, n, tp, ns);
+  }
   CKL();
   if (nlN) {
-    dim3 g((unsigned)grid_for(nlN, WARPS_PER_BLOCK), (unsigned)nsp);
-    kb_orient_leaves<<<g, LEAF_THREADS, 0, st>>>(bb.lab.ptr, bb.SCORES.ptr, n, bb.opart.ptr, nlN, tp, ns);
+    dim3 g((unsigned)grid_for(nlN, WARPS_PER_BLOCK), (unsigned)(T * cdiv(ns, SC_SH)));
+    kb_orient_leaves<<<g, LEAF_THREADS, 0, st>>>(bb.labt.ptr, bb.SCORES.ptr, n, bb.opart.ptr, nlN, ns);
     CKL();
-    kb_orient_combine<<<nsp, 256, 0, st>>>(bb.opart.ptr, nlN, B);
+    kb_orient_combine<<<T * ns, 256, 0, st>>>(bb.opart.ptr, nlN, B);
     CKL();
   }
-  {
-    dim3 g((unsigned)std::min<long long>(grid_for(std::max(n, d), 256), 1024), (unsigned)nsp);
-    kb_flip<<<g, 256, 0, st>>>(bb.SCORES.ptr, bb.SOLS.ptr, n, d, T, B);
+  if (scores && n > 0) {
+    dim3 g((unsigned)std::min<long long>(grid_for(n, 256), 1024), (unsigned)(T * ns));
+    kb_flip<<<g, 256, 0, st>>>(bb.SCORES.ptr, n, T, B);
     CKL();
   }
   if (d > 0) {
-    kb_directions_out<<<(unsigned)std::min<long long>(cdiv((long long)T * ns * d, 256), 65535LL * 4), 256, 0, st>>>(
-        bb.SOLS.ptr, bb.OUT.ptr, d, T, tp, ns);
+    dim3 g((unsigned)cdiv((long long)T * ns, 32), (unsigned)cdiv(d, 32));
+    kb_directions_out<<<g, dim3(32, 8), 0, st>>>(bb.SOLS.ptr, bb.OUT.ptr, d, T, tp, ns, B.flip);
     CKL();
   }
   if (tr.on) {

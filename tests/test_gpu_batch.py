@@ -208,3 +208,28 @@ def test_batch_fp32_storage_gate_vs_fp64():
         worst = max(worst, float(rel.max()))
     print(f"batch fp32 storage vs fp64 at K=20: rel {worst:.3e}")
     assert worst <= 1e-3
+
+
+@pytest.mark.parametrize("storage", [64, 32])
+def test_batch_without_scores_orients_from_labeled_rows(storage):
+    """scores=False: only the labeled rows are projected for the orientation
+    (kb_scores_labeled); the directions (sign included) equal the batch that
+    computes every score, and the single solves."""
+    w = make_workload("cfg1", n=3000, d=1200, ell=300, n_pos=60, lam=14.0, k=6, n_shifts=11)
+    x, lap = _mats(w)
+    sets = _masks(w.n, 35, 150, 40, seed=4)
+    seeds = list(range(35))
+    dev = fb.Device(0)
+    dev.set_storage(storage)
+    full = fb.solve_label_sets(x, lap, sets, w.alpha, w.betas, w.tol, 12, seeds=seeds, device=dev)
+    lean = fb.solve_label_sets(x, lap, sets, w.alpha, w.betas, w.tol, 12, seeds=seeds, device=dev,
+                               scores=False)
+    seq = fb.solve_label_sets(x, lap, sets, w.alpha, w.betas, w.tol, 12, seeds=seeds, device=dev,
+                              scores=False, batched=False)
+    flipped = 0
+    for a, b, c in zip(full, lean, seq):
+        assert b.scores is None
+        np.testing.assert_array_equal(a.directions, b.directions)
+        np.testing.assert_array_equal(c.directions, b.directions)
+        flipped += 1
+    assert flipped == 35

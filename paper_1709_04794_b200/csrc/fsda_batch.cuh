@@ -88,6 +88,12 @@ struct BatchState {
 
 constexpr int ST_PAD = 7;
 
+// w / G for the (item, task group) decomposition of a warp index: a shift when
+// G is a power of two (the 64-bit division costs ~50 instructions per warp).
+__device__ __forceinline__ long long div_groups(long long w, int G) {
+  return (G & (G - 1)) == 0 ? (w >> (31 - __clz(G))) : w / G;
+}
+
 __device__ __forceinline__ bool b_live(const BatchState& B, int t) {
   return B.status[t] == ST_OK && !B.finished[t];
 }
@@ -162,18 +168,18 @@ struct TermLap {  // (L y)_i terms: d_i y_i on the diagonal, -y_j off it
 // table carries one more row of zeros) and add (+/-)0.0, which leaves every
 // partial sum unchanged bit for bit (no partial sum is ever -0.0): no bounds
 // test or select per gather.
-template <int LS, typename V, typename Term>
+template <int LS, int NK, typename V, typename Term>
 __device__ __forceinline__ double emu_gather_leaf_ls(const int* __restrict__ ind, long long s0, int len,
                                                      const V* __restrict__ src, int tp, int t,
                                                      int lane, Term term, unsigned zoff) {
-  const int nk = (len + 31) >> 5;     // <= 8 index chunks
+  const int nk = (len + 31) >> 5;     // <= NK index chunks of 32 (NK = 1, 2 or 8: len <= 32 NK)
   // byte offset idx * tp * sizeof(V) of the gathered row (host: below 2^32);
   // slots past the segment's end point at the table's zero row (zoff)
-  unsigned my[8];
+  unsigned my[NK];
   const unsigned row_bytes = (unsigned)tp * (unsigned)sizeof(V);
 #pragma unroll
-  for (int k = 0; k < 8; ++k)
-    my[k] = (k < nk && 32 * k + lane < len) ? (unsigned)__ldg(ind + s0 + 32 * k + lane) * row_bytes : zoff;
+  for (int k = 0; k < NK; ++k)
+    my[k] = (32 * k + lane < len) ? (unsigned)__ldg(ind + s0 + 32 * k + lane) * row_bytes : zoff;
   // this lane's column of src as an opaque address, so that a gather is one
   // 64-bit add away (the compiler otherwise rebuilds (idx * tp + t) * 8 + src
   // for every load)
@@ -196,8 +202,8 @@ __device__ __forceinline__ double emu_gather_leaf_ls(const int* __restrict__ ind
 #pragma unroll
       for (int q = 0; q < LS; ++q) a1[q] = a2[q] = 0.0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (k >= nk) break;
+      for (int k = 0; k < NK; ++k) {
+        if (NK > 2 && k >= nk) break;  // NK <= 2: a chunk past the end gathers the zero row
         V v1[LS], v2[LS];
         unsigned sp1 = 0u, sp2 = 0u;
 #pragma unroll
@@ -240,8 +246,9 @@ __device__ __forceinline__ double emu_gather_leaf(const int* __restrict__ ind, l
                                                   const V* __restrict__ src, int tp, int t,
                                                   int lane, Term term, unsigned zoff) {
   constexpr int LS = sizeof(V) == 4 ? F32_LS : GATHER_MLP / 2;
-  if (len <= 32) return emu_gather_leaf_ls<8, V>(ind, s0, len, src, tp, t, lane, term, zoff);
-  return emu_gather_leaf_ls<LS, V>(ind, s0, len, src, tp, t, lane, term, zoff);
+  if (len <= 32) return emu_gather_leaf_ls<8, 1, V>(ind, s0, len, src, tp, t, lane, term, zoff);
+  if (len <= 64) return emu_gather_leaf_ls<LS, 2, V>(ind, s0, len, src, tp, t, lane, term, zoff);
+  return emu_gather_leaf_ls<LS, 8, V>(ind, s0, len, src, tp, t, lane, term, zoff);
 }
 
 // Segments longer than 256 entries: R256 over their leaves (two levels,
@@ -361,7 +368,7 @@ __global__ void __launch_bounds__(256, (KIND == SEG_LROWS ? KB_LROWS_MINB : KB_X
   const int lane = threadIdx.x & 31;
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= n_rows * G) return;
-  const long long i = w / G;
+  const long long i = div_groups(w, G);
   const int g = (int)(w - i * G);
   const int t = g * BG + lane;
   const int lo = __ldg(rowptr + i), n = __ldg(rowptr + i + 1) - lo;
@@ -408,7 +415,7 @@ __global__ void __launch_bounds__(256, KB_COLS_MINB) kb_cols_light(SegPlan pl, c
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const long long n_entries = pl.cls_off[6];
   if (w >= n_entries * G) return;
-  const long long e = w / G;
+  const long long e = div_groups(w, G);
   const int g = (int)(w - e * G);
   const int t = g * BG + lane;
   const int4 tk = __ldg(pl.tasks + e);
@@ -430,7 +437,7 @@ __global__ void __launch_bounds__(256, KB_COLS_MINB) kb_cols_leaves(SegPlan pl, 
   const int lane = threadIdx.x & 31;
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= (n_hleaf + n_xtask) * G) return;
-  const long long u = w / G;
+  const long long u = div_groups(w, G);
   const int g = (int)(w - u * G);
   const int t = g * BG + lane;
   // one gather call for both kinds of leaf (a single inlined copy of the loop)
@@ -579,7 +586,7 @@ __global__ void __launch_bounds__(256) kb_part_groups(SegPlan pl, XtDense dn,
   const int lane = threadIdx.x & 31;
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= n_chunks * G) return;
-  const long long k = w / G;
+  const long long k = div_groups(w, G);
   const int g = (int)(w - k * G);
   const int t = g * BG + lane;
   const int2 ch = __ldg(chunks + k);
@@ -619,7 +626,7 @@ __global__ void __launch_bounds__(256, 2) kb_cols_combine(SegPlan pl, XtDense dn
   const int lane = threadIdx.x & 31;
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= (n_heavy + dn.n_dense) * G) return;
-  const long long u = w / G;
+  const long long u = div_groups(w, G);
   const int g = (int)(w - u * G);
   const int t = g * BG + lane;
   long long m;

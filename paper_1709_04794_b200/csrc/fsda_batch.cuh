@@ -1093,36 +1093,37 @@ __global__ void kb_finish(BatchState B) {
 }
 
 // Projection scores of the labeled rows only (the orientation y . s needs no
-// others; used when the caller does not ask for the scores): thread (row,
-// task) with a label walks the row's columns in stored order — the order of
-// k_spmm_scores and of scipy's csr_matvec — for SC_SH shifts at a time.
-// lab: labels task-minor [N][TP].
-constexpr int SC_SH = 8;
+// others; used when the caller does not ask for the scores).  A warp covers 32
+// tasks of one row; for each labeled (row, task) among them the whole warp
+// walks the row's columns in stored order — the order of k_spmm_scores and of
+// scipy's csr_matvec — with lane = shift, so the W row reads are coalesced.
+// lab: labels task-minor [N][TP] (TP a multiple of 32).
+constexpr int SC_SH = 8;  // shifts per pass of kb_orient_leaves
 __global__ void __launch_bounds__(256) kb_scores_labeled(const int* __restrict__ rowptr,
                                                          const int* __restrict__ cols,
                                                          const signed char* __restrict__ lab,
                                                          const double* __restrict__ sols,
                                                          double* __restrict__ scores, long long n,
                                                          int tp, int ns) {
-  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n * tp) return;
-  if (lab[k] == 0) return;
-  const long long i = k / tp;
-  const int t = (int)(k - i * tp);
+  const int lane = threadIdx.x & 31;
+  const long long k0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) - lane;  // warp's first (row, task)
+  if (k0 >= n * tp) return;
+  unsigned m = __ballot_sync(FULL, lab[k0 + lane] != 0);
+  if (m == 0u) return;
+  const long long i = k0 / tp;
+  const int t0 = (int)(k0 - i * tp);
   const int lo = __ldg(rowptr + i), hi = __ldg(rowptr + i + 1);
-  for (int s0 = 0; s0 < ns; s0 += SC_SH) {
-    double acc[SC_SH];
-#pragma unroll
-    for (int u = 0; u < SC_SH; ++u) acc[u] = 0.0;
-    for (int j = lo; j < hi; ++j) {
-      const double* w = sols + ((long long)__ldg(cols + j) * tp + t) * ns + s0;
-#pragma unroll
-      for (int u = 0; u < SC_SH; ++u)
-        if (s0 + u < ns) acc[u] = acc[u] + w[u];
+  while (m) {
+    const int b = __ffs(m) - 1;
+    m &= m - 1;
+    const int t = t0 + b;
+    for (int s0 = 0; s0 < ns; s0 += 32) {
+      const int sh = s0 + lane;
+      double acc = 0.0;
+      if (sh < ns)
+        for (int j = lo; j < hi; ++j) acc = acc + sols[((long long)__ldg(cols + j) * tp + t) * ns + sh];
+      if (sh < ns) scores[((long long)t * ns + sh) * n + i] = acc;
     }
-#pragma unroll
-    for (int u = 0; u < SC_SH; ++u)
-      if (s0 + u < ns) scores[((long long)t * ns + s0 + u) * n + i] = acc[u];
   }
 }
 

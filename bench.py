@@ -529,15 +529,17 @@ def run_b200(args):
         # residuals (39 GB at cfg4), allocated on first use
         dev.solve_batch(masks, w.alpha, betas4, w.tol, c4["max_iter"], probes, scores=False)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        bres = dev.solve_batch(masks, w.alpha, betas4, w.tol, c4["max_iter"], probes, scores=False)
-        t_b = time.perf_counter() - t0
+        with ClockSampler(local) as bclocks:   # the batch runs at the board's power cap
+            t0 = time.perf_counter()
+            bres = dev.solve_batch(masks, w.alpha, betas4, w.tol, c4["max_iter"], probes, scores=False)
+            t_b = time.perf_counter() - t0
         batch = {"workload": f"cfg4: the {args.workload} X and graph, {T} tasks each labeling a random "
                              f"{c4['task_frac']:.0%} of rows ({c4['task_pos']:.0%} positive), "
                              f"{c4['n_shifts']} shifts, K={c4['max_iter']}",
                  "task_solves_per_s": T / t_b, "seconds": t_b,
                  "n_applies": [min(r.n_applies for r in bres), max(r.n_applies for r in bres)],
-                 "note": "host-timed fsda_solve_batch: masks + probes H2D, directions D2H"}
+                 "note": "host-timed fsda_solve_batch: masks + probes H2D, directions D2H",
+                 "clocks": bclocks.summary()}
         # the same batch in fp32 storage (fsda_set_storage(32): P, Y, Z and the
         # residual basis as floats, every sum in double; the 1e-3 gate of
         # tests/test_gpu_batch.py) -- reported beside the fp64 number, not instead

@@ -206,16 +206,27 @@ __device__ __forceinline__ double emu_gather_leaf_ls(const int* __restrict__ ind
         if (NK > 2 && k >= nk) break;  // NK <= 2: a chunk past the end gathers the zero row
         V v1[LS], v2[LS];
         unsigned sp1 = 0u, sp2 = 0u;
+        // the step's second half (slots l + 16) lies wholly past the end: its
+        // loads would all read the zero row, so they are skipped (warp-uniform;
+        // adding the zeros below is the same sum)
+        const bool second = 32 * k + l0 + 16 < len;
 #pragma unroll
         for (int q = 0; q < LS; ++q) {
           const int l = l0 + q;
-          const unsigned o1 = __shfl_sync(FULL, my[k], l), o2 = __shfl_sync(FULL, my[k], l + 16);
+          const unsigned o1 = __shfl_sync(FULL, my[k], l);
           v1[q] = __ldg(reinterpret_cast<const V*>(bp + o1));
-          v2[q] = __ldg(reinterpret_cast<const V*>(bp + o2));
-          if (Term::kSpecial) {
-            sp1 |= (o1 == sp_off) ? (1u << q) : 0u;
-            sp2 |= (o2 == sp_off) ? (1u << q) : 0u;
+          if (Term::kSpecial) sp1 |= (o1 == sp_off) ? (1u << q) : 0u;
+        }
+        if (second) {
+#pragma unroll
+          for (int q = 0; q < LS; ++q) {
+            const unsigned o2 = __shfl_sync(FULL, my[k], l0 + q + 16);
+            v2[q] = __ldg(reinterpret_cast<const V*>(bp + o2));
+            if (Term::kSpecial) sp2 |= (o2 == sp_off) ? (1u << q) : 0u;
           }
+        } else {
+#pragma unroll
+          for (int q = 0; q < LS; ++q) v2[q] = (V)0;
         }
 #pragma unroll
         for (int q = 0; q < LS; ++q) {

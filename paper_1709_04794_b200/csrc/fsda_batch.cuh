@@ -322,14 +322,15 @@ __global__ void kb_task_minor(const double* __restrict__ in, double* __restrict_
 // sols [D][TP * ns] -> out [T * ns][D], negated where the orientation flips
 // (sda.py:280-283): a 32 x 32 tiled transpose through shared memory, so both
 // the reads (along task-shift) and the writes (along features) are coalesced.
-// blockDim = (32, 8); grid = (ceil(Q / 32), ceil(D / 32)), Q = T * ns.
+// blockDim = (32, 8); grid = (ceil(D / 32), ceil(Q / 32)), Q = T * ns (the
+// long dimension on grid.x).
 __global__ void __launch_bounds__(256) kb_directions_out(const double* __restrict__ sols,
                                                          double* __restrict__ out, long long d, int T,
                                                          int tp, int ns,
                                                          const unsigned char* __restrict__ flip) {
   __shared__ double tile[32][33];
   const long long Q = (long long)T * ns, ld = (long long)tp * ns;
-  const long long q0 = (long long)blockIdx.x * 32, c0 = (long long)blockIdx.y * 32;
+  const long long q0 = (long long)blockIdx.y * 32, c0 = (long long)blockIdx.x * 32;
   for (int r = threadIdx.y; r < 32; r += 8) {
     const long long c = c0 + r, q = q0 + threadIdx.x;
     tile[r][threadIdx.x] = (c < d && q < Q) ? sols[c * ld + q] : 0.0;
@@ -1146,11 +1147,13 @@ __global__ void __launch_bounds__(256) kb_scores_labeled(const int* __restrict__
 // already failed with ST_NONFINITE).  labt: labels task-major [T][N].
 __global__ void kb_orient_leaves(const signed char* __restrict__ labt,
                                  const double* __restrict__ scores, long long n,
-                                 double* __restrict__ part, long long n_leaf, int ns) {
+                                 double* __restrict__ part, long long n_leaf, int ns,
+                                 int t_base) {
   const int lane = threadIdx.x & 31;
   const long long g = (long long)blockIdx.x * WARPS_PER_BLOCK + (threadIdx.x >> 5);
   const int nch = (ns + SC_SH - 1) / SC_SH;
-  const int t = blockIdx.y / nch, s0 = (blockIdx.y - t * nch) * SC_SH;
+  const int tl = blockIdx.y / nch, s0 = (blockIdx.y - tl * nch) * SC_SH;
+  const int t = t_base + tl;
   if (g >= n_leaf) return;
   double a[SC_SH];
 #pragma unroll

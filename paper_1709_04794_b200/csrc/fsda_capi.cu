@@ -2906,9 +2906,12 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
   }
   CKL();
   if (nlN) {
-    dim3 g((unsigned)grid_for(nlN, WARPS_PER_BLOCK), (unsigned)(T * cdiv(ns, SC_SH)));
-    kb_orient_leaves<<<g, LEAF_THREADS, 0, st>>>(bb.labt.ptr, bb.SCORES.ptr, n, bb.opart.ptr, nlN, ns);
-    CKL();
+    const int nch = (int)cdiv(ns, SC_SH), t_per = std::max(1, 65535 / nch);  // grid.y <= 65535
+    for (int tb0 = 0; tb0 < T; tb0 += t_per) {
+      dim3 g((unsigned)grid_for(nlN, WARPS_PER_BLOCK), (unsigned)(std::min(t_per, T - tb0) * nch));
+      kb_orient_leaves<<<g, LEAF_THREADS, 0, st>>>(bb.labt.ptr, bb.SCORES.ptr, n, bb.opart.ptr, nlN, ns, tb0);
+      CKL();
+    }
     kb_orient_combine<<<T * ns, 256, 0, st>>>(bb.opart.ptr, nlN, B);
     CKL();
   }
@@ -2918,7 +2921,7 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
     CKL();
   }
   if (d > 0) {
-    dim3 g((unsigned)cdiv((long long)T * ns, 32), (unsigned)cdiv(d, 32));
+    dim3 g((unsigned)cdiv(d, 32), (unsigned)cdiv((long long)T * ns, 32));
     kb_directions_out<<<g, dim3(32, 8), 0, st>>>(bb.SOLS.ptr, bb.OUT.ptr, d, T, tp, ns, B.flip);
     CKL();
   }

@@ -145,6 +145,7 @@ struct TermPlain {
   static constexpr bool kSpecial = false;
   __device__ __forceinline__ bool special(int) const { return false; }
   __device__ __forceinline__ int special_row() const { return 0; }
+  __device__ __forceinline__ int map(int idx) const { return idx; }
   __device__ __forceinline__ double operator()(bool, double v) const { return v; }
 };
 struct TermLap {  // (L y)_i terms: d_i y_i on the diagonal, -y_j off it
@@ -153,7 +154,24 @@ struct TermLap {  // (L y)_i terms: d_i y_i on the diagonal, -y_j off it
   double dg;
   __device__ __forceinline__ bool special(int idx) const { return idx == row; }
   __device__ __forceinline__ int special_row() const { return row; }
+  __device__ __forceinline__ int map(int idx) const { return idx; }
   __device__ __forceinline__ double operator()(bool sp, double v) const { return sp ? dg * v : -v; }
+};
+// The same row sum with every term negated, so that no gather needs a select:
+// off-diagonal slots add +y_j, and the diagonal's slot is pointed (by the lane
+// that owns its index) at a second block of the table that holds
+// -(d_i y_i), written by the producer of y.  IEEE addition is symmetric under
+// negation, so the tree of negated terms is the negated tree: the caller
+// negates the result and has TermLap's sum bit for bit (a sum that is exactly
+// zero may differ in the sign of zero).
+struct TermLapNeg {
+  static constexpr bool kSpecial = false;
+  int row;
+  int yd_row0;  // first row of the -(d y) block in the table
+  __device__ __forceinline__ bool special(int) const { return false; }
+  __device__ __forceinline__ int special_row() const { return 0; }
+  __device__ __forceinline__ int map(int idx) const { return idx == row ? yd_row0 + idx : idx; }
+  __device__ __forceinline__ double operator()(bool, double v) const { return v; }
 };
 
 // Canonical leaf of a gathered index segment: ind[s0, s0 + len) (len <= 256)
@@ -179,7 +197,7 @@ __device__ __forceinline__ double emu_gather_leaf_ls(const int* __restrict__ ind
   const unsigned row_bytes = (unsigned)tp * (unsigned)sizeof(V);
 #pragma unroll
   for (int k = 0; k < NK; ++k)
-    my[k] = (32 * k + lane < len) ? (unsigned)__ldg(ind + s0 + 32 * k + lane) * row_bytes : zoff;
+    my[k] = (32 * k + lane < len) ? (unsigned)term.map(__ldg(ind + s0 + 32 * k + lane)) * row_bytes : zoff;
   // this lane's column of src as an opaque address, so that a gather is one
   // 64-bit add away (the compiler otherwise rebuilds (idx * tp + t) * 8 + src
   // for every load)
@@ -367,7 +385,9 @@ __global__ void kb_reset(BatchState B, int T, double tol) {
 
 // Row sums over a CSR pattern for every task: K1 (y = X p) and K2 (z = M y).
 // One warp per (row, task group).
-template <int KIND, typename V>
+// YD (fp64 storage, the loop's K1 / K2 pair): K1 also writes -(d_i y_i) into
+// rows yd_row0 + i of its output table, and K2 sums with TermLapNeg.
+template <int KIND, typename V, bool YD = false>
 __global__ void __launch_bounds__(256, (KIND == SEG_LROWS ? KB_LROWS_MINB : KB_XROWS_MINB) +
                                             (sizeof(V) == 4 ? KB_ROWS_F32_EXTRA : 0)) kb_rows(const int* __restrict__ rowptr,
                                                const int* __restrict__ cols,
@@ -375,7 +395,7 @@ __global__ void __launch_bounds__(256, (KIND == SEG_LROWS ? KB_LROWS_MINB : KB_X
                                                V* __restrict__ out, long long n_rows, int G,
                                                int tp, const double* __restrict__ ldiag,
                                                const signed char* __restrict__ lab, double alpha,
-                                               int alpha_mode, long long src_rows) {
+                                               int alpha_mode, long long src_rows, long long yd_row0) {
   const unsigned zoff = (unsigned)(src_rows * tp * (long long)sizeof(V));  // the zero row of src
   const int lane = threadIdx.x & 31;
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -386,13 +406,18 @@ __global__ void __launch_bounds__(256, (KIND == SEG_LROWS ? KB_LROWS_MINB : KB_X
   const int lo = __ldg(rowptr + i), n = __ldg(rowptr + i + 1) - lo;
   double s;
   if (KIND == SEG_LROWS) {
-    const double dg = __ldg(ldiag + i);
-    s = emu_segment(cols, lo, n, src, tp, t, lane, TermLap{(int)i, dg}, zoff);
+    if (YD) {
+      s = -emu_segment(cols, lo, n, src, tp, t, lane, TermLapNeg{(int)i, (int)yd_row0}, zoff);
+    } else {
+      const double dg = __ldg(ldiag + i);
+      s = emu_segment(cols, lo, n, src, tp, t, lane, TermLap{(int)i, dg}, zoff);
+    }
     const double masked = lab[i * tp + t] != 0 ? (double)src[i * tp + t] : 0.0;
     const double smoothed = alpha * s;
     s = (alpha_mode == 1) ? smoothed : (1.0 - alpha) * masked + smoothed;
   } else {
     s = emu_segment(cols, lo, n, src, tp, t, lane, TermPlain{}, zoff);
+    if (YD) out[(yd_row0 + i) * tp + t] = (V)(-(__ldg(ldiag + i) * (double)(V)s));
   }
   out[i * tp + t] = (V)s;
 }

@@ -2547,7 +2547,12 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
     bb.R0.ensure(std::max(1LL, d * ND));
     bb.R1.ensure(std::max(1LL, d * ND));
   }
-  bb.Y.ensure(std::max(1LL, (n + 1) * ND));
+  // fp64 storage: Y also holds -(d_i y_i) in rows n + 1 .. 2n + 1, the block the
+  // loop's K2 reads for its diagonal slot (TermLapNeg), when the 32-bit gather
+  // offsets reach it
+  const bool use_yd = !V32 && (2 * n + 2) * (long long)tp * 8 < (1LL << 32) &&
+                      !(std::getenv("FSDA_B200_BATCH_YD") && !std::atoi(std::getenv("FSDA_B200_BATCH_YD")));
+  bb.Y.ensure(std::max(1LL, (use_yd ? 2 * n + 2 : n + 1) * ND));
   bb.Z.ensure(std::max(1LL, (n + 1) * ND));
   bb.BIGP.ensure(basis ? 1LL : std::max(1LL, d * ND * ns));
   bb.SOLS.ensure(std::max(1LL, d * ND * ns));
@@ -2630,7 +2635,19 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
   auto rows_x = [&](auto* src, auto* out) {
     using U = std::remove_cv_t<std::remove_pointer_t<decltype(out)>>;
     kb_rows<SEG_XROWS, U><<<grid_w(n * G), 256, 0, st>>>(c->x_rowptr.ptr, c->x_cols.ptr, (const U*)src, out,
-                                                        n, G, tp, nullptr, nullptr, 0.0, 0, d);
+                                                        n, G, tp, nullptr, nullptr, 0.0, 0, d, 0);
+    CKL();
+  };
+  // the loop's K1 / K2 in fp64 storage: y and -(d y) out of K1, K2 without the diagonal select
+  auto rows_x_yd = [&](const double* src, double* out) {
+    kb_rows<SEG_XROWS, double, true><<<grid_w(n * G), 256, 0, st>>>(
+        c->x_rowptr.ptr, c->x_cols.ptr, src, out, n, G, tp, c->l_diag.ptr, nullptr, 0.0, 0, d, n + 1);
+    CKL();
+  };
+  auto smoother_yd = [&](const double* y, double* z) {
+    kb_rows<SEG_LROWS, double, true><<<grid_w(n * G), 256, 0, st>>>(
+        c->l_rowptr.ptr, c->l_cols.ptr, y, z, n, G, tp, c->l_diag.ptr, bb.lab.ptr, alpha, alpha_mode_of(alpha), n,
+        n + 1);
     CKL();
   };
   auto smoother = [&](auto* y, auto* z) {
@@ -2641,7 +2658,7 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
           (const U*)y, bb.lab.ptr, z, n * ND);
     else
       kb_rows<SEG_LROWS, U><<<grid_w(n * G), 256, 0, st>>>(c->l_rowptr.ptr, c->l_cols.ptr, (const U*)y, z, n,
-                                                          G, tp, c->l_diag.ptr, bb.lab.ptr, alpha, amode, n);
+                                                          G, tp, c->l_diag.ptr, bb.lab.ptr, alpha, amode, n, 0);
     CKL();
   };
   const SegPlan& pxc = c->plan_xc.pl;
@@ -2784,8 +2801,18 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
   CK(cudaMemsetAsync(loop_it, 0, sizeof(long long), st));
   CK(cudaMemsetAsync(n_live, 0, sizeof(int), st));
   auto body = [&](unsigned long long handle, int use_cond) {
-    rows_x(Pv, Yv);                                            // K1  y = X p
-    smoother(Yv, Zv);                                          // K2  z = M y
+    if constexpr (!V32) {
+      if (use_yd && alpha_mode_of(alpha) != 0) {
+        rows_x_yd(bb.P.ptr, bb.Y.ptr);                         // K1  y = X p and -(d y)
+        smoother_yd(bb.Y.ptr, bb.Z.ptr);                       // K2  z = M y
+      } else {
+        rows_x(Pv, Yv);
+        smoother(Yv, Zv);
+      }
+    } else {
+      rows_x(Pv, Yv);                                          // K1  y = X p
+      smoother(Yv, Zv);                                        // K2  z = M y
+    }
     xt(Zv, bb.Q.ptr, 0);                                       // K3  q = X^T z
     vec_sum(Zv, (V*)nullptr, 0, n, bb.partN.ptr, B.sum_v);     //     sum(z)
     if (nlD) {

@@ -11,6 +11,9 @@
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
 
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 #include <algorithm>
 #include <array>
 #include <chrono>
@@ -1408,6 +1411,65 @@ void h2d(fsda_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st)
   }
 }
 
+// One block of the host narrowing: int64 -> int32 with the range check, AVX2
+// when the CPU has it (8 indices per step, non-temporal stores: the staged
+// int32s are read next by the DMA engine, not by this core, so they need not
+// displace the cache or cost a read-for-ownership), scalar otherwise.
+// Returns 1 when an index lies outside [0, limit].
+int narrow_block_scalar(const int64_t* from, int* stage, long long len, long long limit) {
+  int bad = 0;
+  for (long long k = 0; k < len; ++k) {
+    const long long v = from[k];
+    bad |= (v < 0 || v > limit) ? 1 : 0;
+    stage[k] = (int)v;
+  }
+  return bad;
+}
+
+#if defined(__x86_64__) && defined(__GNUC__)
+__attribute__((target("avx2"))) int narrow_block_avx2(const int64_t* from, int* stage, long long len,
+                                                      long long limit) {
+  long long k = 0;
+  int bad = 0;
+  // scalar head up to a 32-byte boundary of the stage (stream stores need it)
+  while (k < len && (reinterpret_cast<uintptr_t>(stage + k) & 31u)) {
+    const long long v = from[k];
+    bad |= (v < 0 || v > limit) ? 1 : 0;
+    stage[k] = (int)v;
+    ++k;
+  }
+  const __m256i lim = _mm256_set1_epi64x(limit), zero = _mm256_setzero_si256();
+  const __m256i even = _mm256_setr_epi32(0, 2, 4, 6, 0, 2, 4, 6);
+  __m256i badv = zero;
+  for (; k + 8 <= len; k += 8) {
+    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(from + k));
+    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(from + k + 4));
+    badv = _mm256_or_si256(badv, _mm256_or_si256(_mm256_cmpgt_epi64(a, lim), _mm256_cmpgt_epi64(zero, a)));
+    badv = _mm256_or_si256(badv, _mm256_or_si256(_mm256_cmpgt_epi64(b, lim), _mm256_cmpgt_epi64(zero, b)));
+    const __m256i a32 = _mm256_permutevar8x32_epi32(a, even);  // low dwords of a in lanes 0..3
+    const __m256i b32 = _mm256_permutevar8x32_epi32(b, even);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(stage + k), _mm256_permute2x128_si256(a32, b32, 0x20));
+  }
+  bad |= _mm256_testz_si256(badv, badv) ? 0 : 1;
+  for (; k < len; ++k) {
+    const long long v = from[k];
+    bad |= (v < 0 || v > limit) ? 1 : 0;
+    stage[k] = (int)v;
+  }
+  _mm_sfence();
+  return bad;
+}
+#endif
+
+int narrow_block(const int64_t* from, int* stage, long long len, long long limit) {
+#if defined(__x86_64__) && defined(__GNUC__)
+  static const bool avx2 = __builtin_cpu_supports("avx2") &&
+                           !(std::getenv("FSDA_B200_NARROW_SCALAR") && std::atoi(std::getenv("FSDA_B200_NARROW_SCALAR")));
+  if (avx2) return narrow_block_avx2(from, stage, len, limit);
+#endif
+  return narrow_block_scalar(from, stage, len, limit);
+}
+
 // int64 host indices -> int32 device indices, narrowed (and range-checked)
 // on the host by all threads into the pinned ring, so only half the bytes
 // cross the link.  Returns 1 when an index lies outside [0, limit] (the
@@ -1428,11 +1490,12 @@ int h2d_narrow(fsda_ctx* c, DevBuf<int>& out, const int64_t* src, long long n, l
     CK(cudaEventSynchronize(c->h2d_ev[slot]));
     int* stage = reinterpret_cast<int*>(ring + (size_t)slot * CH);
     const int64_t* from = src + off;
+    constexpr long long NB = 1 << 16;  // indices per block: a few blocks per thread and chunk
+    const long long nblk = (len + NB - 1) / NB;
 #pragma omp parallel for schedule(static) reduction(max : bad)
-    for (long long k = 0; k < len; ++k) {
-      const long long v = from[k];
-      bad = std::max(bad, (v < 0 || v > limit) ? 1 : 0);
-      stage[k] = (int)v;
+    for (long long bk = 0; bk < nblk; ++bk) {
+      const long long k0 = bk * NB;
+      bad = std::max(bad, narrow_block(from + k0, stage + k0, std::min(NB, len - k0), limit));
     }
     CK(cudaMemcpyAsync(out.ptr + off, stage, sizeof(int) * len, cudaMemcpyHostToDevice, st));
     CK(cudaEventRecord(c->h2d_ev[slot], st));

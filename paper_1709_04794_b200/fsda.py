@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import importlib
+import threading
 import time
 import types as _pytypes
 from dataclasses import dataclass
@@ -415,8 +416,26 @@ def fsda_solve(p, *, device: Optional[Device] = None, storage: Optional[int] = N
     t0 = time.perf_counter()
     fam = _family(p)
     dev = device or default_device()
-    dev.load_problem(p, fam)
-    probe = np.random.default_rng(p.seed).uniform(-1.0, 1.0, size=int(p.x.n_cols))
+    # the probe draw (a few ms of one core at D ~ 10^5..10^6) runs beside the
+    # upload, which spends its time in C with the GIL released
+    drawn = {}
+
+    def _draw(quiet=True):
+        try:
+            drawn["probe"] = np.random.default_rng(p.seed).uniform(-1.0, 1.0, size=int(p.x.n_cols))
+        except Exception:
+            if not quiet:
+                raise
+
+    th = threading.Thread(target=_draw)
+    th.start()
+    try:
+        dev.load_problem(p, fam)
+    finally:
+        th.join()
+    if "probe" not in drawn:   # the draw failed (e.g. a bad seed): raise it here, as the reference does
+        _draw(quiet=False)
+    probe = drawn["probe"]
     prev = getattr(dev, "storage_bits", 64)
     if storage is not None and int(storage) != prev:
         dev.set_storage(int(storage))

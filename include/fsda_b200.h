@@ -61,6 +61,11 @@ int fsda_abi_version(void);
 /* Thread-local description of the last non-zero status. */
 const char* fsda_last_error(void);
 
+/* Host helper: 1 when every one of the n stored values equals 1.0 (the
+ * value-free device path needs a binary X; sparse.py:43-58 stores explicit
+ * float64 values), else 0.  All host threads; no device work. */
+int fsda_values_all_ones(const double* values, int64_t n);
+
 /* One context per device.  Calls on a context are serialized by a mutex and
  * are synchronous unless named *_async.  `stream` may be NULL (the context
  * creates its own) or a cudaStream_t owned by the caller (e.g. torch's

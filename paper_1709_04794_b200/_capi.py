@@ -31,6 +31,7 @@ _PI = C.POINTER(C.c_int)
 SIGNATURES = {
     "fsda_abi_version": [],
     "fsda_last_error": [],
+    "fsda_values_all_ones": [_PD, _I64],
     "fsda_ctx_create": [C.POINTER(_P), C.c_int, _P],
     "fsda_ctx_destroy": [_P],
     "fsda_ctx_set_stream": [_P, _P],

@@ -1575,6 +1575,15 @@ int fsda_set_storage(fsda_ctx* c, int bits) {
 
 const char* fsda_last_error(void) { return g_last_error.c_str(); }
 
+int fsda_values_all_ones(const double* values, int64_t n) {
+  if (n <= 0) return 1;
+  if (!values) return 0;
+  int ok = 1;
+#pragma omp parallel for schedule(static) reduction(min : ok) if (n > 65536)
+  for (int64_t k = 0; k < n; ++k) ok = std::min(ok, values[k] == 1.0 ? 1 : 0);
+  return ok;
+}
+
 int fsda_ctx_create(fsda_ctx** out, int device, void* stream) {
   if (!out) return fail(FSDA_EINVAL, "null output pointer");
   *out = nullptr;

@@ -93,6 +93,29 @@ class SweepResult:
     launches: int = 0
 
 
+_ONES_CACHE: dict = {}   # id(values array) -> (weakref, all-ones?) for read-only arrays
+
+
+def _all_ones(values) -> bool:
+    """Every stored value of X equals 1 (the reference's SparseMatrix keeps
+    explicit float64 values, sparse.py:43-58, and has no binary flag): checked
+    by all host threads in C, and remembered per read-only array — the
+    reference freezes its arrays, so the answer cannot change."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    frozen = v is values and not v.flags.writeable
+    if frozen:
+        hit = _ONES_CACHE.get(id(v))
+        if hit is not None and hit[0]() is v:
+            return hit[1]
+    ok = bool(_capi.lib().fsda_values_all_ones(_capi.dptr(v), int(v.size)))
+    if frozen:
+        import weakref
+
+        key = id(v)
+        _ONES_CACHE[key] = (weakref.ref(v, lambda _r, k=key: _ONES_CACHE.pop(k, None)), ok)
+    return ok
+
+
 def _pinned_empty(shape) -> np.ndarray:
     """A float64 host array in page-locked memory, from torch's caching host
     allocator, so the result copies (directions, scores) run at link speed
@@ -155,7 +178,7 @@ class Device:
 
     # ---- uploads
     def upload_x(self, x, fam=_OWN):
-        binary = x.is_binary if hasattr(x, "is_binary") else bool(np.all(np.asarray(x.values) == 1.0))
+        binary = x.is_binary if hasattr(x, "is_binary") else _all_ones(x.values)
         if not binary:
             raise ValueError("the B200 FSDA path needs a binary X (every stored value 1)")
         offs, cols = _i64(x.row_offsets), _i64(x.col_indices)
@@ -194,7 +217,7 @@ class Device:
         if not (reuse and (p.x is last_x or p.lap is last_l)):
             # all three travel: one call, L's copies overlapped with X's processing
             x, m = p.x, (p.lap.matrix if hasattr(p.lap, "matrix") else p.lap)
-            binary = x.is_binary if hasattr(x, "is_binary") else bool(np.all(np.asarray(x.values) == 1.0))
+            binary = x.is_binary if hasattr(x, "is_binary") else _all_ones(x.values)
             if not binary:
                 raise ValueError("the B200 FSDA path needs a binary X (every stored value 1)")
             if int(m.n_rows) != int(x.n_rows):

@@ -268,3 +268,27 @@ def test_workload_is_deterministic():
     np.testing.assert_array_equal(a.x_cols, b.x_cols)
     np.testing.assert_array_equal(a.l_cols, b.l_cols)
     np.testing.assert_array_equal(a.probe(), np.random.default_rng(0).uniform(-1, 1, 200))
+
+
+def test_values_all_ones_helper_and_cache():
+    """The binary-X precondition on an explicit values array (the reference's
+    SparseMatrix, sparse.py:43-58): checked in C by all host threads and
+    remembered per read-only array."""
+    from paper_1709_04794_b200 import fsda
+
+    ones = np.ones(300_000)
+    ones.setflags(write=False)
+    assert fsda._all_ones(ones) is True
+    assert id(ones) in fsda._ONES_CACHE and fsda._all_ones(ones) is True
+    bad = np.ones(300_000)
+    bad[-1] = 2.0
+    assert fsda._all_ones(bad) is False
+    assert id(bad) not in fsda._ONES_CACHE          # writable arrays are not remembered
+    assert fsda._all_ones(np.ones(0)) is True
+    assert fsda._all_ones(np.ones(7, dtype=np.float32)) is True
+    key = id(ones)
+    del ones
+    import gc
+
+    gc.collect()
+    assert key not in fsda._ONES_CACHE               # dropped with the array

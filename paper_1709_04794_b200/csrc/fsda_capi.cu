@@ -1510,16 +1510,19 @@ bool device_narrow() {
   return v;
 }
 
-void upload_narrow_async(fsda_ctx* c, const int64_t* host, long long n, long long limit,
-                         DevBuf<int>& out, long long* tmp) {
+// Returns 1 when the host narrowing already saw an index out of range (the
+// device flag is raised too); 0 otherwise, or when the device narrows.
+int upload_narrow_async(fsda_ctx* c, const int64_t* host, long long n, long long limit,
+                        DevBuf<int>& out, long long* tmp) {
   if (!device_narrow()) {
     static const int k_out_of_range = 1;  // check_err_flag's "index out of range"
-    if (h2d_narrow(c, out, host, n, limit, c->stream))
-      CK(cudaMemcpyAsync(c->err.ptr, &k_out_of_range, sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    return;
+    const int bad = h2d_narrow(c, out, host, n, limit, c->stream);
+    if (bad) CK(cudaMemcpyAsync(c->err.ptr, &k_out_of_range, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    return bad;
   }
   if (n > 0) h2d(c, tmp, host, sizeof(long long) * n, c->stream);
   narrow_async(c, tmp, n, limit, out);
+  return 0;
 }
 
 
@@ -1737,8 +1740,45 @@ static int upload_x_impl(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int6
   // H2D + narrowing run on the stream while the host builds the row plan
   // (it needs only the host offsets).
   c->scratch_i64.ensure(std::max<long long>(n_rows + 1 + nnz, 1));
-  upload_narrow_async(c, row_offsets, n_rows + 1, nnz, c->x_rowptr, c->scratch_i64.ptr);
-  upload_narrow_async(c, col_indices, nnz, n_cols - 1, c->x_cols, c->scratch_i64.ptr + n_rows + 1);
+  int bad_x = upload_narrow_async(c, row_offsets, n_rows + 1, nnz, c->x_rowptr, c->scratch_i64.ptr);
+  bad_x |= upload_narrow_async(c, col_indices, nnz, n_cols - 1, c->x_cols, c->scratch_i64.ptr + n_rows + 1);
+  // the hook's copies (the Laplacian, on the side stream) queue behind X's
+  // copies only, not behind the CSC build enqueued next
+  if (after_h2d) CK(cudaEventRecord(c->ev_lfork, c->stream));
+  // Row ids (with the in-row order check) and the CSC: a stable radix sort of
+  // (column, row) pairs, rows stay ascending.  Enqueued without host syncs.
+  DevBuf<int>& row_of = c->scratch_row_of;
+  DevBuf<int>& keys_out = c->scratch_keys;
+  auto enqueue_csc = [&] {
+    row_of.ensure(nnz);
+    c->csc_rows.ensure(nnz);
+    c->csc_colptr.ensure(n_cols + 1);
+    keys_out.ensure(nnz);
+    if (n_rows > 0) {
+      k_row_ids<<<grid_for(n_rows, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr,
+                                                              row_of.ptr, (int)n_rows, c->err.ptr);
+      CKL();
+    }
+    if (nnz > 0) {
+      int end_bit = 1;
+      while ((1LL << end_bit) < n_cols) ++end_bit;
+      size_t temp_bytes = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, c->x_cols.ptr, keys_out.ptr, row_of.ptr,
+                                         c->csc_rows.ptr, (int)nnz, 0, end_bit, c->stream));
+      c->scratch_sort.ensure(temp_bytes);
+      void* temp = c->scratch_sort.ptr;
+      CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, c->x_cols.ptr, keys_out.ptr, row_of.ptr,
+                                         c->csc_rows.ptr, (int)nnz, 0, end_bit, c->stream));
+    }
+    k_colptr_from_sorted<<<grid_for(n_cols + 1, 256), 256, 0, c->stream>>>(keys_out.ptr, nnz,
+                                                                            c->csc_colptr.ptr, (int)n_cols);
+    CKL();
+  };
+  // With the indices range-checked on the host, the device builds the CSC
+  // while the host runs the hook (the Laplacian's pass) and the row plan;
+  // otherwise it waits for the device-side range check first.
+  const bool early = !bad_x && !device_narrow();
+  if (early) enqueue_csc();
   if (after_h2d) after_h2d(hook_arg);
   build_seg_plan(c->plan_xr, c->stream, row_offsets, n_rows, c->x_cols.ptr);
   tr.mark("x: row plan (host)");
@@ -1746,39 +1786,12 @@ static int upload_x_impl(fsda_ctx* c, int64_t n_rows, int64_t n_cols, const int6
   int rc = check_err_flag(c, "X");
   if (rc) return rc;
   tr.mark("x: h2d + narrow");
-  // row ids + in-row order validation
-  DevBuf<int>& row_of = c->scratch_row_of;
-  row_of.ensure(nnz);
-  if (n_rows > 0) {
-    k_row_ids<<<grid_for(n_rows, 256), 256, 0, c->stream>>>(c->x_rowptr.ptr, c->x_cols.ptr,
-                                                            row_of.ptr, (int)n_rows, c->err.ptr);
-    CKL();
-  }
-  CK(cudaStreamSynchronize(c->stream));
-  rc = check_err_flag(c, "X");
-  if (rc) return rc;
-  tr.mark("x: row ids");
-  // CSC by a stable radix sort of (column, row) pairs: rows stay ascending.
-  c->csc_rows.ensure(nnz);
-  c->csc_colptr.ensure(n_cols + 1);
-  DevBuf<int>& keys_out = c->scratch_keys;
-  keys_out.ensure(nnz);
-  if (nnz > 0) {
-    int end_bit = 1;
-    while ((1LL << end_bit) < n_cols) ++end_bit;
-    size_t temp_bytes = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, c->x_cols.ptr, keys_out.ptr, row_of.ptr,
-                                       c->csc_rows.ptr, (int)nnz, 0, end_bit, c->stream));
-    c->scratch_sort.ensure(temp_bytes);
-    void* temp = c->scratch_sort.ptr;
-    CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, c->x_cols.ptr, keys_out.ptr, row_of.ptr,
-                                       c->csc_rows.ptr, (int)nnz, 0, end_bit, c->stream));
+  if (!early) {
+    enqueue_csc();
     CK(cudaStreamSynchronize(c->stream));
+    rc = check_err_flag(c, "X");
+    if (rc) return rc;
   }
-  k_colptr_from_sorted<<<grid_for(n_cols + 1, 256), 256, 0, c->stream>>>(keys_out.ptr, nnz,
-                                                                          c->csc_colptr.ptr, (int)n_cols);
-  CKL();
-  CK(cudaStreamSynchronize(c->stream));
   tr.mark("x: csc sort");
   {
     std::vector<int> colptr(n_cols + 1);
@@ -1888,8 +1901,7 @@ struct LPrefetch {
 void l_prefetch(void* arg) {
   LPrefetch* a = static_cast<LPrefetch*>(arg);
   fsda_ctx* c = a->c;
-  CK(cudaEventRecord(c->ev_lfork, c->stream));
-  CK(cudaStreamWaitEvent(c->side, c->ev_lfork, 0));
+  CK(cudaStreamWaitEvent(c->side, c->ev_lfork, 0));  // recorded behind X's copies by upload_x_impl
   int range_err = 0;
   if (device_narrow()) {
     c->scratch_l64.ensure(std::max<long long>(a->n + 1 + a->nnz, 1));

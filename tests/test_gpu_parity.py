@@ -625,3 +625,42 @@ def test_large_pageable_upload_narrowed_on_host():
     got = fb.matvec(x, v)
     np.testing.assert_array_equal(got, c_oracle.matvec(offs, cols, v))
 
+
+
+def test_scalar_host_narrowing_path_in_subprocess():
+    """FSDA_B200_NARROW_SCALAR=1 (read once per process) keeps the scalar host
+    narrowing instead of AVX2 + non-temporal stores: same device indices (X v
+    equals the oracle's), and the same out-of-range report, in the head of a
+    block, in its middle and at its end."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = r'''
+import numpy as np
+import paper_1709_04794_b200 as fb
+from paper_1709_04794_b200 import _capi
+from oracle import c_oracle
+rng = np.random.default_rng(3)
+n, d, per = 70_001, 9_000, 13            # 910,013 entries: 13 full 65,536-blocks and a ragged tail
+offs = np.arange(0, (n + 1) * per, per, dtype=np.int64)
+cols = np.sort(rng.integers(0, d - per, size=(n, per)), axis=1) + np.arange(per)
+cols = cols.astype(np.int64).ravel()
+dev = fb.Device(0)
+for pos in (0, 65_536 * 5 + 3, cols.size - 1):
+    bad = cols.copy()
+    bad[pos] = d + 1
+    rc = _capi.lib().fsda_upload_x(dev._h, n, d, _capi.i64ptr(offs), _capi.i64ptr(bad))
+    assert rc == _capi.FSDA_EINVAL and "out of range" in _capi.last_error(), (pos, rc, _capi.last_error())
+x = fb.SparseMatrix.binary(n, d, offs, cols)
+v = rng.standard_normal(d)
+np.testing.assert_array_equal(fb.matvec(x, v), c_oracle.matvec(offs, cols, v))
+print("NARROW-OK")
+'''
+    root = Path(__file__).resolve().parents[1]
+    for scalar in ("1", "0"):
+        env = dict(os.environ, FSDA_B200_NARROW_SCALAR=scalar, PYTHONPATH=str(root))
+        out = subprocess.run([sys.executable, "-c", code], env=env, cwd=str(root), capture_output=True,
+                             text=True, timeout=600)
+        assert out.returncode == 0 and "NARROW-OK" in out.stdout, out.stderr[-2000:]

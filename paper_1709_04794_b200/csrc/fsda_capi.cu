@@ -1090,7 +1090,7 @@ void build_seg_plan(HostPlan& hp, cudaStream_t stream, const OffT* offs, long lo
   };
   const int nch = (int)std::max<long long>(1, std::min<long long>(64, S / 8192));
   std::vector<Count> cc(nch);
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(dynamic, 1)
   for (int ch = 0; ch < nch; ++ch) {
     Count& q = cc[ch];
     for (long long sgi = S * ch / nch; sgi < S * (ch + 1) / nch; ++sgi) {
@@ -1150,7 +1150,7 @@ void build_seg_plan(HostPlan& hp, cudaStream_t stream, const OffT* offs, long lo
       run[8] += cc[ch].leaves;
     }
   }
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(dynamic, 1)
   for (int ch = 0; ch < nch; ++ch) {
     std::array<long long, 9> pos = start[ch];
     for (long long sgi = S * ch / nch; sgi < S * (ch + 1) / nch; ++sgi) {
@@ -1227,7 +1227,7 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   // max(1, ceil(n_hb / 256)) slots per block b — and each (h, b)'s first slot
   std::vector<long long> poff0((size_t)nh + 1, 0);
   std::vector<int> slot0((size_t)nh * nb);
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(dynamic, 64)
   for (long long h = 0; h < nh; ++h) {
     long long m = 0;
     const int* bp = bptr.data() + h * (nb + 1);
@@ -1251,7 +1251,7 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   // poff[nh] <= nnz / XT_DENSE_PER_BLOCK + nnz / LEAF < 2^31: int slots suffice
   // pass 2 (parallel over blocks): task counts per (block, class)
   std::vector<long long> cnt((size_t)nb * 6, 0);
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(dynamic, 1)
   for (int b = 0; b < nb; ++b)
     for (long long h = 0; h < nh; ++h) {
       const long long n = bptr[h * (nb + 1) + b + 1] - bptr[h * (nb + 1) + b];
@@ -1284,7 +1284,7 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   for (int k = 0; k < 7; ++k) boff[(size_t)nb * 7 + k] = t;
   // pass 3 (parallel over blocks): tasks by block, class, column (an empty
   // block's slot stays 0.0, see below)
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(dynamic, 1)
   for (int b = 0; b < nb; ++b) {
     long long* pb = pos.data() + (size_t)b * 6;
     for (long long h = 0; h < nh; ++h) {
@@ -1401,7 +1401,7 @@ void h2d(fsda_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st)
     char* stage = ring + (size_t)slot * CH;
     const char* from = static_cast<const char*>(src) + off;
     const long long parts = (long long)((len + (1 << 20) - 1) >> 20);
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(dynamic, 1)
     for (long long k = 0; k < parts; ++k) {
       const size_t a = (size_t)k << 20, b = std::min(len, a + ((size_t)1 << 20));
       memcpy(stage + a, from + a, b - a);
@@ -1492,7 +1492,7 @@ int h2d_narrow(fsda_ctx* c, DevBuf<int>& out, const int64_t* src, long long n, l
     const int64_t* from = src + off;
     constexpr long long NB = 1 << 16;  // indices per block: a few blocks per thread and chunk
     const long long nblk = (len + NB - 1) / NB;
-#pragma omp parallel for schedule(static) reduction(max : bad)
+#pragma omp parallel for schedule(dynamic, 1) reduction(max : bad)
     for (long long bk = 0; bk < nblk; ++bk) {
       const long long k0 = bk * NB;
       bad = std::max(bad, narrow_block(from + k0, stage + k0, std::min(NB, len - k0), limit));
@@ -1922,7 +1922,7 @@ void l_prefetch(void* arg) {
   const double* vals = a->vals;
   double* diag = static_cast<double*>(c->ldiag_stage.ensure(sizeof(double) * std::max<long long>(n, 1)));
   int err = 0;
-#pragma omp parallel for schedule(static, 4096) reduction(max : err)
+#pragma omp parallel for schedule(dynamic, 4096) reduction(max : err)
   for (long long i = 0; i < n; ++i) {
     const long long lo = offs[i], hi = offs[i + 1];
     double dv = 0.0;

@@ -1898,6 +1898,56 @@ struct LPrefetch {
 
 // The Laplacian's raw arrays to device scratch on the side stream, queued
 // behind X's copies, so they cross the link while X's CSC and plans build.
+// The Laplacian's columns in one host pass (offsets already checked):
+// narrowed to int32 into the pinned ring and copied on the side stream, and in
+// the same sweep the order check, the unit-weight check and the diagonal
+// split — cols is read once instead of twice.  Entries go ring chunk by ring
+// chunk; the rows overlapping a chunk are found by binary search in offs and
+// shared out over the host threads.  Returns the validation code (0, 3 or 4);
+// *range_bad = 1 when a column lies outside [0, n).
+int l_cols_fused(fsda_ctx* c, const LPrefetch* a, double* diag, int* range_bad) {
+  constexpr size_t CH = (size_t)16 << 20;  // bytes of int32 per ring slot (as h2d_narrow)
+  constexpr int SLOTS = 4;
+  const long long n = a->n, nnz = a->nnz;
+  const int64_t* offs = a->offs;
+  const int64_t* cols = a->cols;
+  const double* vals = a->vals;
+  cudaStream_t st = c->side;
+  c->l_cols.ensure(nnz + 8);  // tail padding: the row kernels stage indices with 16-byte loads
+  CK(cudaMemsetAsync(c->l_cols.ptr + nnz, 0, 8 * sizeof(int), st));
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < n; ++i) diag[i] = 0.0;
+  char* ring = static_cast<char*>(c->h2d_ring.ensure(CH * SLOTS));
+  const long long che = (long long)(CH / sizeof(int));
+  int err = 0, bad = 0;
+  for (long long off = 0; off < nnz; off += che) {
+    const long long len = std::min(che, nnz - off), end = off + len;
+    const int slot = (int)(c->h2d_next++ % SLOTS);
+    CK(cudaEventSynchronize(c->h2d_ev[slot]));
+    int* stage = reinterpret_cast<int*>(ring + (size_t)slot * CH);
+    // rows with entries in [off, end): from the last row starting at or before off
+    const long long r0 = std::max<long long>(0, (std::upper_bound(offs, offs + n + 1, (int64_t)off) - offs) - 1);
+    const long long r1 = std::min<long long>(n, std::lower_bound(offs, offs + n + 1, (int64_t)end) - offs);
+#pragma omp parallel for schedule(dynamic, 2048) reduction(max : err, bad)
+    for (long long i = r0; i < r1; ++i) {
+      const long long lo = offs[i], hi = offs[i + 1];
+      const long long jb = std::max(lo, off), je = std::min(hi, end);
+      for (long long jj = jb; jj < je; ++jj) {
+        const long long cc = cols[jj];
+        if (cc < 0 || cc > n - 1) bad = 1;
+        stage[jj - off] = (int)cc;
+        if (jj > lo && cc <= cols[jj - 1]) err = std::max(err, 3);
+        if (cc == i) diag[i] = vals[jj];
+        else if (vals[jj] != -1.0) err = std::max(err, 4);
+      }
+    }
+    CK(cudaMemcpyAsync(c->l_cols.ptr + off, stage, sizeof(int) * len, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(c->h2d_ev[slot], st));
+  }
+  *range_bad = bad;
+  return err;
+}
+
 void l_prefetch(void* arg) {
   LPrefetch* a = static_cast<LPrefetch*>(arg);
   fsda_ctx* c = a->c;
@@ -1909,6 +1959,25 @@ void l_prefetch(void* arg) {
     if (a->nnz > 0) h2d(c, c->scratch_l64.ptr + a->n + 1, a->cols, sizeof(long long) * a->nnz, c->side);
   } else {
     range_err |= h2d_narrow(c, c->l_rowptr, a->offs, a->n + 1, a->nnz, c->side);
+    // offsets that walk the entries exactly once let the columns go in one fused pass
+    static const bool fuse = !std::getenv("FSDA_B200_L_FUSED") || std::atoi(std::getenv("FSDA_B200_L_FUSED"));
+    int off_ok = fuse && !range_err && a->nnz > 0 && a->n > 0 && a->offs[0] == 0 && a->offs[a->n] == a->nnz;
+    if (off_ok) {
+      const int64_t* o = a->offs;
+      const long long nn = a->n;
+#pragma omp parallel for schedule(static) reduction(min : off_ok)
+      for (long long i = 0; i < nn; ++i) off_ok = std::min(off_ok, o[i + 1] >= o[i] ? 1 : 0);
+    }
+    if (off_ok) {
+      double* dg = static_cast<double*>(c->ldiag_stage.ensure(sizeof(double) * std::max<long long>(a->n, 1)));
+      int bad = 0;
+      const int err = l_cols_fused(c, a, dg, &bad);
+      c->l_host_err = bad ? 1 : err;
+      c->l_diag.ensure(std::max<long long>(a->n, 1));
+      CK(cudaMemcpyAsync(c->l_diag.ptr, dg, sizeof(double) * a->n, cudaMemcpyHostToDevice, c->side));
+      CK(cudaEventRecord(c->ev_lcopy, c->side));
+      return;
+    }
     range_err |= h2d_narrow(c, c->l_cols, a->cols, a->nnz, a->n - 1, c->side);
   }
   // L's values never cross the link: off-diagonals must be -1 (a unit-weight

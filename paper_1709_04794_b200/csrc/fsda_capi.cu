@@ -14,6 +14,7 @@
 #if defined(__x86_64__)
 #include <immintrin.h>
 #endif
+#include <omp.h>
 #include <algorithm>
 #include <array>
 #include <chrono>
@@ -66,6 +67,21 @@ struct Trace {
     t = now;
   }
 };
+
+// Host threads of the upload passes: two fewer than the machine has (unless
+// OMP_NUM_THREADS or FSDA_B200_HOST_THREADS says otherwise).  The CUDA driver's
+// own threads, the calling thread's copies and the Python side need cores too:
+// with every core in the OpenMP team, one drop-in call in ten took 20-50 ms
+// longer on a 16-vCPU box (mean 120-125 ms against 114-115 ms with 14 threads).
+int host_threads() {
+  static const int v = [] {
+    if (const char* e = std::getenv("FSDA_B200_HOST_THREADS")) return std::max(1, std::atoi(e));
+    if (std::getenv("OMP_NUM_THREADS")) return std::max(1, omp_get_max_threads());
+    const int procs = omp_get_num_procs();
+    return std::max(1, std::min(omp_get_max_threads(), procs > 4 ? procs - 2 : procs));
+  }();
+  return v;
+}
 
 struct CudaError {
   cudaError_t err;
@@ -1090,7 +1106,7 @@ void build_seg_plan(HostPlan& hp, cudaStream_t stream, const OffT* offs, long lo
   };
   const int nch = (int)std::max<long long>(1, std::min<long long>(64, S / 8192));
   std::vector<Count> cc(nch);
-#pragma omp parallel for schedule(dynamic, 1)
+#pragma omp parallel for schedule(dynamic, 1) num_threads(host_threads())
   for (int ch = 0; ch < nch; ++ch) {
     Count& q = cc[ch];
     for (long long sgi = S * ch / nch; sgi < S * (ch + 1) / nch; ++sgi) {
@@ -1150,7 +1166,7 @@ void build_seg_plan(HostPlan& hp, cudaStream_t stream, const OffT* offs, long lo
       run[8] += cc[ch].leaves;
     }
   }
-#pragma omp parallel for schedule(dynamic, 1)
+#pragma omp parallel for schedule(dynamic, 1) num_threads(host_threads())
   for (int ch = 0; ch < nch; ++ch) {
     std::array<long long, 9> pos = start[ch];
     for (long long sgi = S * ch / nch; sgi < S * (ch + 1) / nch; ++sgi) {
@@ -1227,7 +1243,7 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   // max(1, ceil(n_hb / 256)) slots per block b — and each (h, b)'s first slot
   std::vector<long long> poff0((size_t)nh + 1, 0);
   std::vector<int> slot0((size_t)nh * nb);
-#pragma omp parallel for schedule(dynamic, 64)
+#pragma omp parallel for schedule(dynamic, 64) num_threads(host_threads())
   for (long long h = 0; h < nh; ++h) {
     long long m = 0;
     const int* bp = bptr.data() + h * (nb + 1);
@@ -1251,7 +1267,7 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   // poff[nh] <= nnz / XT_DENSE_PER_BLOCK + nnz / LEAF < 2^31: int slots suffice
   // pass 2 (parallel over blocks): task counts per (block, class)
   std::vector<long long> cnt((size_t)nb * 6, 0);
-#pragma omp parallel for schedule(dynamic, 1)
+#pragma omp parallel for schedule(dynamic, 1) num_threads(host_threads())
   for (int b = 0; b < nb; ++b)
     for (long long h = 0; h < nh; ++h) {
       const long long n = bptr[h * (nb + 1) + b + 1] - bptr[h * (nb + 1) + b];
@@ -1284,7 +1300,7 @@ void build_dense_plan(fsda_ctx* c, const std::vector<int>& dense) {
   for (int k = 0; k < 7; ++k) boff[(size_t)nb * 7 + k] = t;
   // pass 3 (parallel over blocks): tasks by block, class, column (an empty
   // block's slot stays 0.0, see below)
-#pragma omp parallel for schedule(dynamic, 1)
+#pragma omp parallel for schedule(dynamic, 1) num_threads(host_threads())
   for (int b = 0; b < nb; ++b) {
     long long* pb = pos.data() + (size_t)b * 6;
     for (long long h = 0; h < nh; ++h) {
@@ -1401,7 +1417,7 @@ void h2d(fsda_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st)
     char* stage = ring + (size_t)slot * CH;
     const char* from = static_cast<const char*>(src) + off;
     const long long parts = (long long)((len + (1 << 20) - 1) >> 20);
-#pragma omp parallel for schedule(dynamic, 1)
+#pragma omp parallel for schedule(dynamic, 1) num_threads(host_threads())
     for (long long k = 0; k < parts; ++k) {
       const size_t a = (size_t)k << 20, b = std::min(len, a + ((size_t)1 << 20));
       memcpy(stage + a, from + a, b - a);
@@ -1492,7 +1508,7 @@ int h2d_narrow(fsda_ctx* c, DevBuf<int>& out, const int64_t* src, long long n, l
     const int64_t* from = src + off;
     constexpr long long NB = 1 << 16;  // indices per block: a few blocks per thread and chunk
     const long long nblk = (len + NB - 1) / NB;
-#pragma omp parallel for schedule(dynamic, 1) reduction(max : bad)
+#pragma omp parallel for schedule(dynamic, 1) reduction(max : bad) num_threads(host_threads())
     for (long long bk = 0; bk < nblk; ++bk) {
       const long long k0 = bk * NB;
       bad = std::max(bad, narrow_block(from + k0, stage + k0, std::min(NB, len - k0), limit));
@@ -1582,7 +1598,7 @@ int fsda_values_all_ones(const double* values, int64_t n) {
   if (n <= 0) return 1;
   if (!values) return 0;
   int ok = 1;
-#pragma omp parallel for schedule(static) reduction(min : ok) if (n > 65536)
+#pragma omp parallel for schedule(static) reduction(min : ok) if (n > 65536) num_threads(host_threads())
   for (int64_t k = 0; k < n; ++k) ok = std::min(ok, values[k] == 1.0 ? 1 : 0);
   return ok;
 }
@@ -1915,7 +1931,7 @@ int l_cols_fused(fsda_ctx* c, const LPrefetch* a, double* diag, int* range_bad) 
   cudaStream_t st = c->side;
   c->l_cols.ensure(nnz + 8);  // tail padding: the row kernels stage indices with 16-byte loads
   CK(cudaMemsetAsync(c->l_cols.ptr + nnz, 0, 8 * sizeof(int), st));
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) num_threads(host_threads())
   for (long long i = 0; i < n; ++i) diag[i] = 0.0;
   char* ring = static_cast<char*>(c->h2d_ring.ensure(CH * SLOTS));
   const long long che = (long long)(CH / sizeof(int));
@@ -1928,7 +1944,7 @@ int l_cols_fused(fsda_ctx* c, const LPrefetch* a, double* diag, int* range_bad) 
     // rows with entries in [off, end): from the last row starting at or before off
     const long long r0 = std::max<long long>(0, (std::upper_bound(offs, offs + n + 1, (int64_t)off) - offs) - 1);
     const long long r1 = std::min<long long>(n, std::lower_bound(offs, offs + n + 1, (int64_t)end) - offs);
-#pragma omp parallel for schedule(dynamic, 2048) reduction(max : err, bad)
+#pragma omp parallel for schedule(dynamic, 2048) reduction(max : err, bad) num_threads(host_threads())
     for (long long i = r0; i < r1; ++i) {
       const long long lo = offs[i], hi = offs[i + 1];
       const long long jb = std::max(lo, off), je = std::min(hi, end);
@@ -1965,7 +1981,7 @@ void l_prefetch(void* arg) {
     if (off_ok) {
       const int64_t* o = a->offs;
       const long long nn = a->n;
-#pragma omp parallel for schedule(static) reduction(min : off_ok)
+#pragma omp parallel for schedule(static) reduction(min : off_ok) num_threads(host_threads())
       for (long long i = 0; i < nn; ++i) off_ok = std::min(off_ok, o[i + 1] >= o[i] ? 1 : 0);
     }
     if (off_ok) {
@@ -1991,7 +2007,7 @@ void l_prefetch(void* arg) {
   const double* vals = a->vals;
   double* diag = static_cast<double*>(c->ldiag_stage.ensure(sizeof(double) * std::max<long long>(n, 1)));
   int err = 0;
-#pragma omp parallel for schedule(dynamic, 4096) reduction(max : err)
+#pragma omp parallel for schedule(dynamic, 4096) reduction(max : err) num_threads(host_threads())
   for (long long i = 0; i < n; ++i) {
     const long long lo = offs[i], hi = offs[i + 1];
     double dv = 0.0;
@@ -2024,7 +2040,7 @@ static int check_labels(const int8_t* labels, long long n, bool require_first, l
   // the first unlabeled / last labeled row (labeled-first <=> last < first)
   long long n1 = 0, n2 = 0, first_unlabeled = n, last_labeled = -1;
   int bad = 0;
-#pragma omp parallel for schedule(static) reduction(+ : n1, n2) reduction(max : bad, last_labeled) \
+#pragma omp parallel for schedule(static) reduction(+ : n1, n2) reduction(max : bad, last_labeled) num_threads(host_threads()) \
     reduction(min : first_unlabeled) if (n > 65536)
   for (long long i = 0; i < n; ++i) {
     const int8_t l = labels[i];
@@ -2641,7 +2657,7 @@ static int batch_solve_t(fsda_ctx* c, int T, const int8_t* labels, double alpha,
     return fail(FSDA_EINVAL, "fsda_solve_batch: a task-minor vector must stay below 4 GiB (32-bit gather offsets)");
   std::vector<double> ell(tp, 1.0), n1v(tp, 1.0), n2v(tp, 1.0);
   std::vector<int> bad(T, 0);
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) num_threads(host_threads())
   for (int t = 0; t < T; ++t) {
     long long a = 0, b = 0;
     int other = 0;
